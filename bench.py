@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""SPED hot-path benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl sped|reference]
+
+Workload (default, ``--config 4``): BASELINE configs[3] — Chung-Lu power-law
+graph, n = 10^7, Pareto(2.1) expected degrees (mean 16), normalized Laplacian
+fp32, k = 32, polynomial degree 12 (negexp-taylor, the literal degree).  One
+STEP = one mu-EigenGame solver step: MV = p(L)V (12 fused SpMM terms), Gram of
+[V | MV], k x k algebra, fused update.  ``value`` = 12*nnz*k per step / step
+time (p(L)V nnz*k/s, whole job).  Inputs (V: 1.28 GB, CSR: 1.4 GB) are far
+larger than the 126 MB L2, so no flush is needed between steps.
+
+N > 1 (torchrun): rows are sharded across ranks (strong scaling: the same
+graph), halo rows exchanged per term over NCCL, one Gram all-reduce per step.
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port:
+scipy csr_matvecs, fp64) on all host cores, on a bounded row sample of the
+same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "p(L)V nnz*k/s (mu-EG step incl. Gram+update)"
+UNIT = "nnz*k/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", choices=["sped", "reference"], default="sped")
+    ap.add_argument("--scale", type=float, default=1.0, help="node-count scale (debug only)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--stochastic", action="store_true", help="edge-minibatch mode (configs 3/5)")
+    return ap.parse_args()
+
+
+def cfg_spec(c):
+    from paper_2207_14589_b200 import generators as G
+    spec = dict(G.CONFIGS[c])
+    spec["index"] = c
+    return spec
+
+
+def transform_for(spec):
+    import paper_2207_14589_b200 as sp
+    return sp.SpectralTransform("negexp-taylor", spec["ell"])
+
+
+def bytes_per_term(n, nnz, k, stored_values, x_term, final_x):
+    """Algorithmic (compulsory) HBM bytes of one fused term:
+    indptr + indices (+ values) + read w + write w' (+ read x)."""
+    b = 4 * (n + 1) + (4 + (4 if stored_values else 0)) * nnz + 4 * n * k * 2
+    if x_term or final_x:
+        b += 4 * n * k
+    return b
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_term_sample(n, u, v, w, mode, k, seconds, threads, alpha=1.0, beta=1.0):
+    """One p(L)V term (``w' = alpha*x + beta*L w``, the Horner term of
+    transforms.py:249-254) over a row sample of the CSR, fp64, scipy
+    csr_matvecs split over ``threads`` row blocks.  Rows are grown until one
+    term takes ~seconds/4; returns (nnz*k/s, description)."""
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    rng = np.random.default_rng(0)
+    W = rng.standard_normal((n, k))
+    rows = max(1000, min(n, 200_000))
+    while True:
+        csr = O.laplacian_csr_rows(n, u, v, w, mode, 0, rows)
+        X = W[:rows]
+        bounds = np.linspace(0, rows, threads + 1).astype(np.int64)
+        blocks = [csr[bounds[i]:bounds[i + 1]] for i in range(threads)]
+        out = np.empty((rows, k))
+
+        def term():
+            def work(i):
+                a, b = bounds[i], bounds[i + 1]
+                out[a:b] = alpha * X[a:b] + beta * (blocks[i] @ W)
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(work, range(threads)))
+
+        t0 = time.perf_counter()
+        term()
+        dt = time.perf_counter() - t0
+        if dt > seconds / 4 or rows == n:
+            break
+        rows = min(n, int(rows * max(2.0, (seconds / 4) / max(dt, 1e-3))))
+    reps = max(1, int(seconds / max(dt, 1e-3)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        term()
+    dt = (time.perf_counter() - t0) / reps
+    rate = csr.nnz * k / dt
+    desc = (f"one Horner term w'=x+L w over rows [0,{rows}) = {csr.nnz} nnz of the same CSR, "
+            f"k={k}, fp64 scipy csr_matvecs on {threads} threads, {reps} reps")
+    return rate, desc, dt, csr.nnz
+
+
+# ------------------------------------------------------------------------------ sped arm
+
+def run_sped(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200 import generators as G
+    from paper_2207_14589_b200.solvers import StepWorkspace
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    spec = cfg_spec(args.config)
+    k, ell, mode = spec["k"], spec["ell"], spec["mode"]
+    t_setup = time.perf_counter()
+    n, u, v, w = G.config_graph(args.config, device=dev, scale=args.scale)
+    g = sp.Graph.from_canonical(n, u, v, w, validate=False)
+    t = transform_for(spec)
+    op = sp.make_reversed_operator(g, t, mode, device=dev)
+    lap = op.laplacian
+    nnz = lap.nnz
+    stored = lap.values is not None
+    al, be, ga, w0, lf, s = op.schedule
+    n_terms = len(al)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    if world > 1:
+        from paper_2207_14589_b200.distributed import ShardedLaplacian, ShardedOperator, sharded_mu_eg_step
+        shard = ShardedLaplacian(lap, rank, world)
+        sop = ShardedOperator(shard, t, op.lambda_star)
+        n_loc = shard.n_own
+    else:
+        n_loc = n
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    V = torch.randn((n_loc, k), device=dev, generator=gen)
+    V /= torch.linalg.norm(V, dim=0) * (world ** 0.5)
+    Vn = torch.empty_like(V)
+    MV = torch.empty_like(V)
+    ws = StepWorkspace(n_loc, k, dev)
+    eta = 0.1
+    stream = torch.cuda.current_stream(dev)
+
+    def step(Vin, Vout, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        if world > 1:
+            sop.apply_local(Vin, out=MV)
+        else:
+            op.apply_device(Vin, out=MV)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            ws.gram(Vin, MV)
+            dist.all_reduce(ws.G)
+            lib = sp._lib.load()
+            lib.sped_mueg_coeffs(k, ws.G.data_ptr(), eta, ws.A.data_ptr(), ws.scale.data_ptr(),
+                                 ws.flag.data_ptr(), stream.cuda_stream)
+            ws.update(Vin, ws.A, MV, None, eta, ws.scale, Vout)
+        else:
+            ws.mu_eg(Vin, MV, eta, Vout)
+        if ev is not None:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step(V, Vn)
+        V, Vn = Vn, V
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(args.steps):
+        step(V, Vn, evs[i])
+        V, Vn = Vn, V
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    apply_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    solve_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
+    if world > 1:
+        tt = torch.tensor([total_ms, apply_ms, solve_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, apply_ms, solve_ms = (float(x) for x in tt.tolist())
+    ms_per_step = total_ms / args.steps
+    work = n_terms * nnz * k
+    value = work * args.steps / (total_ms / 1e3)
+    t_term_s = apply_ms / 1e3 / (args.steps * n_terms)
+    bpt = bytes_per_term(n if world == 1 else n_loc, nnz if world == 1 else shard.nnz_local, k,
+                         stored, any(a != 0 for a in al), lf != 0.0)
+    peak, peak_src = measured_peak()
+    achieved = bpt / t_term_s / 1e9
+    launches_per_step = n_terms + 5
+    if world > 1:
+        launches_per_step = n_terms * 2 + 5
+
+    e2e = None
+    if not args.no_e2e:
+        # reference-facing call with HOST buffers: mu_eg_step(EigenState(host V), op, eta)
+        Vh = torch.empty((n_loc, k), dtype=torch.float32, pin_memory=True)
+        Vh.copy_(V)
+        if world == 1:
+            st = sp.EigenState(Vh)
+            st = sp.mu_eg_step(st, op, eta)  # warm
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                st = sp.mu_eg_step(sp.EigenState(Vh), op, eta)
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t0
+        else:
+            e2e_s = None
+            for it in range(args.e2e_steps + 1):
+                if it == 1:
+                    dist.barrier()
+                    t0 = time.perf_counter()
+                Vd = Vh.to(dev, non_blocking=True)
+                out = torch.empty_like(Vd)
+                sharded_mu_eg_step(sop, Vd, eta, ws, out, MV)
+                Vh.copy_(out, non_blocking=True)
+                torch.cuda.synchronize()
+            dist.barrier()
+            e2e_s = time.perf_counter() - t0
+            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": work * args.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(n * k * 4), "d2h_bytes_per_step": int(n * k * 4),
+               "ms_per_step": 1e3 * e2e_s / args.e2e_steps,
+               "api": "paper_2207_14589_b200.mu_eg_step(EigenState(pinned host V), op, eta)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        uh, vh, wh = g.u, g.v, g.w
+        thr = cpu_threads()
+        rate, desc, dt, snnz = cpu_term_sample(n, uh, vh, wh, mode, k, args.cpu_seconds, thr)
+        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port", "sample": desc,
+               "seconds_per_term": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, BASELINE shape)",
+            "config": {"workload": f"{spec['name']} (BASELINE configs[{args.config - 1}])",
+                       "n": n, "m": g.m, "nnz": nnz, "k": k, "mode": mode,
+                       "transform": f"negexp-taylor({ell})", "terms": n_terms,
+                       "solver": "mu-eg", "eta": eta,
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (V 4nk B, CSR) larger than the 126 MB L2; no flush",
+                       "setup_s": setup_s},
+            "breakdown_ms_per_step": {"p(L)V": apply_ms / args.steps,
+                                      "gram+coeffs+update": solve_ms / args.steps,
+                                      "per_term": 1e3 * t_term_s},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "spmm_term_kernel (one fused polynomial term)",
+                         "algorithmic_bytes_per_launch": bpt, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from paper_2207_14589_b200 import generators as G
+    spec = cfg_spec(args.config)
+    k, mode = spec["k"], spec["mode"]
+    device = "cuda" if torch.cuda.is_available() else "cpu"
+    n, u, v, w = G.config_graph(args.config, device=device, scale=args.scale)  # input synthesis
+    u, v, w = u.cpu().numpy(), v.cpu().numpy(), w.cpu().numpy()
+    thr = cpu_threads()
+    budget = max(10.0, min(60.0, 4.0 * (args.steps + args.warmup)))
+    rate, desc, dt, snnz = cpu_term_sample(n, u, v, w, mode, k, budget, thr)
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt * spec["ell"], "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, BASELINE shape)",
+            "config": {"workload": f"{spec['name']} (BASELINE configs[{args.config - 1}])",
+                       "n": n, "m": int(u.size), "k": k, "mode": mode},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_sped(args)
+
+
+if __name__ == "__main__":
+    main()

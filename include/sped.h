@@ -1,0 +1,166 @@
+/*
+ * sped.h — C ABI of the B200-native SPED hot path (libsped.so, sm_100a).
+ *
+ * Plain pointers and sizes only.  Every array argument is DEVICE memory
+ * (cudaMalloc / torch CUDA storage) unless its comment says "host".  Row-major
+ * n x k fp32 blocks.  Every entry point is stream-ordered on `stream`
+ * (a cudaStream_t passed as void*) and returns an sped_status; on error
+ * sped_last_error() describes it.  The Python host layer maps
+ * SPED_ERR_ARG / SPED_ERR_ZERO_DEGREE to the reference's ValueError.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/specgap/):
+ *   sped_laplacian_build       LaplacianOperator.__post_init__   graph.py:182-199
+ *                              (+ Graph.degrees graph.py:118-122)
+ *   sped_csr_poly_apply        TransformedOperator.apply         transforms.py:229-262
+ *                              (ell x LaplacianOperator.matvec   graph.py:205-211)
+ *   sped_edge_batch_poly_apply make_stochastic_oracle identity   solvers.py:166-178
+ *                              (+ restated per-term composition)
+ *   sped_gram / sped_mueg_coeffs / sped_block_update
+ *                              mu_eg_step                        solvers.py:121-144
+ *   sped_oja_coeffs (+ gram/update)  oja_step + _orthonormalize  solvers.py:84-118
+ *   sped_pcg64_integers        Generator(PCG64).integers(0,m,B)  solvers.py:171
+ *   sped_kmeans_*              kmeans_cluster                    metrics.py:143-176
+ *   sped_gather_rows/scatter   (new) halo exchange staging for row-sharded L
+ */
+#ifndef SPED_H_
+#define SPED_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* sped_stream_t;
+
+enum sped_status {
+  SPED_OK = 0,
+  SPED_ERR_ARG = 1,          /* invalid argument -> ValueError */
+  SPED_ERR_CUDA = 2,         /* CUDA runtime error -> RuntimeError */
+  SPED_ERR_ZERO_DEGREE = 3,  /* normalized Laplacian with an isolated node (graph.py:187-188) */
+  SPED_ERR_UNSUPPORTED = 4
+};
+
+const char* sped_last_error(void);
+int sped_abi_version(void);
+
+/* ---- graph -> Laplacian CSR (graph.py:182-199) --------------------------
+ * u, v, w: canonical edge list (u < v, lexsorted, unique; graph.py:64-88),
+ * int64/int64/fp64, m edges.  Outputs (caller-allocated, worst-case sizes):
+ *   indptr  int32[n+1]
+ *   indices int32[2m+n]      sorted columns, explicit diagonal (scipy layout)
+ *   values  fp32[2m+n]       fp32(scipy fp64 value); may be NULL when
+ *                            store_values == 0 (unweighted combinatorial:
+ *                            kernels synthesise -1 / row_len-1)
+ *   degrees fp64[n]          Graph.degrees() bit-exact (bincount order)
+ *   epos    int32[2m]        CSR position of edge e's (u,v) entry at [2e] and
+ *                            (v,u) entry at [2e+1] (stochastic path)
+ * *nnz_out (host) receives nnz.  Synchronises `stream`.  normalized=1 with a
+ * zero-degree node returns SPED_ERR_ZERO_DEGREE. */
+int sped_laplacian_build(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                         const double* w, int normalized, int store_values,
+                         int32_t* indptr, int32_t* indices, float* values,
+                         double* degrees, int32_t* epos, int64_t* nnz_out,
+                         sped_stream_t stream);
+
+/* ---- long-row split plan for the SpMM ----------------------------------
+ * Rows longer than long_threshold nonzeros are cut into chunks of chunk_len
+ * processed by separate warps and combined deterministically.  chunk_desc is
+ * int32[4*max_chunks] = {row, p_begin, p_end, first_chunk_of_row}.
+ * Synchronises `stream` (returns the counts to the host). */
+int64_t sped_spmm_plan_max_chunks(int64_t n, int64_t nnz, int32_t long_threshold,
+                                  int32_t chunk_len);
+int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_threshold,
+                   int32_t chunk_len, int32_t* chunk_desc, int64_t max_chunks,
+                   int64_t* n_chunks_out, int64_t* n_long_rows_out,
+                   sped_stream_t stream);
+
+/* ---- dilation-polynomial apply (transforms.py:229-262) -------------------
+ * w_0 = w0_scale * x;  for t < n_terms:
+ *     w_{t+1} = alpha[t]*x + beta[t]*(L w_t) + gamma[t]*w_t
+ * out = lam_f*x + s_final*w_{n_terms}.
+ * alpha/beta/gamma are HOST arrays of n_terms doubles.  w_a, w_b: n x k
+ * scratch (ping-pong; may be NULL when n_terms <= 1 / 2 respectively).
+ * long_threshold / chunk_len / chunk_desc / n_chunks: the sped_spmm_plan
+ * (rows longer than long_threshold are chunk-processed; n_chunks == 0 means
+ * no plan).  partials fp32[n_chunks*k] and tickets int32[n_chunks] (zero on
+ * entry, left zero) serve the plan (NULL when n_chunks == 0).  x must not alias
+ * out, w_a or w_b. */
+int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
+                        const int32_t* indices, const float* values,
+                        int32_t long_threshold, int32_t chunk_len,
+                        const int32_t* chunk_desc, int64_t n_chunks,
+                        float* partials, int32_t* tickets,
+                        const float* x, float* w_a, float* w_b, float* out,
+                        int32_t n_terms, const double* alpha, const double* beta,
+                        const double* gamma, double w0_scale, double lam_f,
+                        double s_final, sped_stream_t stream);
+
+/* ---- edge-minibatch apply (solvers.py:166-178, per term) ----------------
+ * Term t replaces L w by (m/B) * sum_{b<B} w_e x_e x_e^T w over the sampled
+ * edge ids batch[t*B .. t*B+B) (int32, the numpy rng.integers stream).
+ * edge_w fp32[m] (NULL = unit weights) are the RAW graph weights, exactly as
+ * the reference's identity oracle uses g.w (also in normalized mode).
+ * hitw fp32[nnz] must be zero on entry and is left zero. */
+int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indptr,
+                               const int32_t* indices, const float* edge_w,
+                               const int32_t* epos, const int32_t* batch, int64_t B,
+                               float* hitw, const float* x, float* w_a, float* w_b,
+                               float* out, int32_t n_terms, const double* alpha,
+                               const double* beta, const double* gamma,
+                               double w0_scale, double lam_f, double s_final,
+                               sped_stream_t stream);
+
+/* ---- solver step pieces (solvers.py:84-144) -----------------------------
+ * sped_gram: G fp64[3*k*k] = {S = V^T V, C = V^T M, Q = M^T M} (M may be
+ * NULL: only S).  workspace: sped_gram_workspace_bytes(n, k) bytes. */
+size_t sped_gram_workspace_bytes(int64_t n, int32_t k);
+int sped_gram(int64_t n, int32_t k, const float* V, const float* M, double* G,
+              void* workspace, size_t workspace_bytes, sped_stream_t stream);
+/* mu-EG k x k algebra: A = I - eta*(triu(C,1) + diag d),
+ * scale_i = 1/||W_i||.  flag int32[1]: set to 1 if a column norm < 1e-12
+ * (rank collapse, solvers.py:136-143); left unchanged otherwise. */
+int sped_mueg_coeffs(int32_t k, const double* G, double eta, float* A, float* scale,
+                     int32_t* flag, sped_stream_t stream);
+/* Oja/CholQR k x k algebra: with_m=1: Gram of W = V + eta*M from {S,C,Q};
+ * with_m=0: Gram = S.  T = R^{-1} for R = chol(Gram)^T (upper), fp32. */
+int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, float* T,
+                    int32_t* flag, sped_stream_t stream);
+/* out = (P*A + M*B) * diag(scale).  A k x k fp32; M may be NULL; B may be
+ * NULL meaning B = eta*I; scale may be NULL (ones). */
+int sped_block_update(int64_t n, int32_t k, const float* P, const float* A,
+                      const float* M, const float* B, double eta, const float* scale,
+                      float* out, sped_stream_t stream);
+/* out = a*x + b*y elementwise over count floats (y may be NULL). */
+int sped_axpby(int64_t count, double a, const float* x, double b, const float* y,
+               float* out, sped_stream_t stream);
+
+/* ---- bit-exact numpy PCG64 + Lemire (solvers.py:171) ---------------------
+ * Reproduces Generator(PCG64).integers(0, m, size=count) (m < 2^32) from the
+ * bit generator state (host scalars).  out int32[count].  On return
+ * *draws32_out (host) = number of 32-bit draws consumed, so the caller can
+ * advance its host generator.  workspace: sped_pcg64_workspace_bytes(count). */
+size_t sped_pcg64_workspace_bytes(int64_t count);
+int sped_pcg64_integers(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                        uint64_t inc_lo, int32_t has_uint32, uint32_t uinteger,
+                        uint64_t m, int64_t count, int32_t* out, int64_t* draws32_out,
+                        void* workspace, size_t workspace_bytes, sped_stream_t stream);
+
+/* ---- k-means on the embedding (metrics.py:143-176) ----------------------- */
+int sped_kmeans_assign(int64_t n, int32_t d, int32_t c, const float* X,
+                       const double* centers, int32_t* labels, double* sums,
+                       int64_t* counts, double* min_d2, sped_stream_t stream);
+int sped_row_dist2(int64_t n, int32_t d, const float* X, const double* center,
+                   double* dist, int32_t accumulate_min, sped_stream_t stream);
+
+/* ---- halo staging for row-sharded L (multi-GPU) ------------------------- */
+int sped_gather_rows(int64_t count, int32_t k, const int32_t* rows, const float* src,
+                     float* dst, sped_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPED_H_ */

@@ -1,0 +1,342 @@
+// Laplacian CSR construction on the device (replaces
+// LaplacianOperator.__post_init__, graph.py:182-199, and Graph.degrees,
+// graph.py:118-122).
+//
+// Input: the canonical edge list (u < v, lexsorted, unique) produced by
+// Graph.__post_init__ (graph.py:64-88).  Output: the scipy CSR layout
+// (sorted columns, explicit diagonal, isolated rows empty) with values equal
+// to fp32(scipy fp64 value):
+//   * off-diagonal  -w_e                              (graph.py:189-191)
+//   * diagonal      sum of w over incident edges, folded in scipy's
+//                   coo->csr input order: the (u,u) block entries in edge
+//                   order, then the (v,v) block entries in edge order
+//                   (graph.py:189-192; exact for unweighted graphs and for
+//                   weighted rows with <= 8 incident edges, where libstdc++'s
+//                   std::sort in csr_sort_indices is an insertion sort)
+//   * normalized    fl(fl(dinv_i * L_ij) * dinv_j), dinv = 1/sqrt(deg)
+//                   (graph.py:193-198, (D L) D evaluated left to right)
+// degrees reproduce np.bincount(u,w) + np.bincount(v,w) bit for bit.
+//
+// Layout choices (B200): one thread per row for the fill (each row's
+// diagonal must be a sequential fold to be bit-exact); the transposed
+// (lower-triangle) order comes from a stable radix sort of the edges by v,
+// which keeps edges with equal v in increasing u (= edge) order.
+
+#include <cub/cub.cuh>
+
+#include "sped_common.cuh"
+
+namespace sped {
+namespace {
+
+__global__ void count_kernel(int64_t m, const int64_t* __restrict__ u,
+                             const int64_t* __restrict__ v, int32_t* cnt_up,
+                             int32_t* cnt_lo, int32_t* vkey, int32_t* eval) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  int64_t a = u[e], b = v[e];
+  atomicAdd(&cnt_up[a], 1);
+  atomicAdd(&cnt_lo[b], 1);
+  vkey[e] = (int32_t)b;
+  eval[e] = (int32_t)e;
+}
+
+__global__ void rowlen_kernel(int64_t n, const int32_t* __restrict__ cnt_up,
+                              const int32_t* __restrict__ cnt_lo, int32_t* rowlen) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {
+    rowlen[n] = 0;
+    return;
+  }
+  int32_t d = cnt_up[i] + cnt_lo[i];
+  rowlen[i] = d + (d > 0 ? 1 : 0);
+}
+
+__global__ void degree_kernel(int64_t n, const int32_t* __restrict__ up_start,
+                              const int32_t* __restrict__ lo_start,
+                              const int32_t* __restrict__ sorted_e,
+                              const double* __restrict__ w, int normalized,
+                              double* __restrict__ degrees, double* __restrict__ dinv,
+                              int32_t* zero_flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // np.bincount(u, weights=w): sequential over edges with u == i in edge order
+  double su = 0.0;
+  for (int32_t e = up_start[i]; e < up_start[i + 1]; ++e) su += w[e];
+  // np.bincount(v, weights=w): edges with v == i, edge order == sorted order
+  double sv = 0.0;
+  for (int32_t j = lo_start[i]; j < lo_start[i + 1]; ++j) sv += w[sorted_e[j]];
+  double d = su + sv;
+  degrees[i] = d;
+  if (normalized) {
+    if (d == 0.0) {
+      atomicExch(zero_flag, 1);
+      dinv[i] = 0.0;
+    } else {
+      dinv[i] = 1.0 / sqrt(d);
+    }
+  }
+}
+
+__global__ void fill_kernel(int64_t n, const int64_t* __restrict__ u,
+                            const int64_t* __restrict__ v, const double* __restrict__ w,
+                            const int32_t* __restrict__ up_start,
+                            const int32_t* __restrict__ lo_start,
+                            const int32_t* __restrict__ sorted_e,
+                            const int32_t* __restrict__ indptr,
+                            const double* __restrict__ dinv, int normalized,
+                            int32_t* __restrict__ indices, float* __restrict__ values,
+                            int32_t* __restrict__ epos) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t p = indptr[i];
+  const double di = normalized ? dinv[i] : 1.0;
+  const int32_t lo0 = lo_start[i], lo1 = lo_start[i + 1];
+  const int32_t up0 = up_start[i], up1 = up_start[i + 1];
+  // lower triangle: columns u_e < i, increasing
+  for (int32_t j = lo0; j < lo1; ++j) {
+    int32_t e = sorted_e[j];
+    int32_t c = (int32_t)u[e];
+    indices[p] = c;
+    if (values) {
+      double val = -w[e];
+      if (normalized) val = (di * val) * dinv[c];
+      values[p] = (float)val;
+    }
+    epos[2 * (int64_t)e + 1] = p;
+    ++p;
+  }
+  if (lo1 > lo0 || up1 > up0) {
+    indices[p] = (int32_t)i;
+    if (values) {
+      // scipy duplicate fold: (u,u) block in edge order, then (v,v) block
+      double acc = 0.0;
+      bool first = true;
+      for (int32_t e = up0; e < up1; ++e) {
+        acc = first ? w[e] : acc + w[e];
+        first = false;
+      }
+      for (int32_t j = lo0; j < lo1; ++j) {
+        double x = w[sorted_e[j]];
+        acc = first ? x : acc + x;
+        first = false;
+      }
+      if (normalized) acc = (di * acc) * di;
+      values[p] = (float)acc;
+    }
+    ++p;
+  }
+  // upper triangle: columns v_e > i, increasing (edges are lexsorted)
+  for (int32_t e = up0; e < up1; ++e) {
+    int32_t c = (int32_t)v[e];
+    indices[p] = c;
+    if (values) {
+      double val = -w[e];
+      if (normalized) val = (di * val) * dinv[c];
+      values[p] = (float)val;
+    }
+    epos[2 * (int64_t)e] = p;
+    ++p;
+  }
+}
+
+struct AsyncBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit AsyncBuf(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 16, s); }
+  ~AsyncBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+}  // namespace
+}  // namespace sped
+
+using namespace sped;
+
+extern "C" int sped_laplacian_build(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                                    const double* w, int normalized, int store_values,
+                                    int32_t* indptr, int32_t* indices, float* values,
+                                    double* degrees, int32_t* epos, int64_t* nnz_out,
+                                    sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && m >= 0, "negative size");
+  SPED_CHECK_ARG(n < (int64_t)INT32_MAX && 2 * m + n < (int64_t)INT32_MAX,
+                 "graph too large for int32 CSR (n=%lld, m=%lld)", (long long)n, (long long)m);
+  SPED_CHECK_ARG(indptr && nnz_out, "null output");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) {
+    SPED_CUDA(cudaMemsetAsync(indptr, 0, sizeof(int32_t), s));
+    SPED_CUDA(cudaStreamSynchronize(s));
+    *nnz_out = 0;
+    return SPED_OK;
+  }
+  SPED_CHECK_ARG(m == 0 || (u && v && w && indices && epos && degrees), "null edge/output array");
+  SPED_CHECK_ARG(!store_values || values, "values requested but NULL");
+
+  AsyncBuf b_cnt(s), b_len(s), b_up(s), b_lo(s), b_keys(s), b_vals(s), b_keys2(s), b_vals2(s),
+      b_dinv(s), b_flag(s), b_tmp(s);
+  SPED_CUDA(b_cnt.alloc(sizeof(int32_t) * 2 * n));
+  int32_t* cnt_up = (int32_t*)b_cnt.p;
+  int32_t* cnt_lo = cnt_up + n;
+  SPED_CUDA(b_len.alloc(sizeof(int32_t) * (n + 1)));
+  SPED_CUDA(b_up.alloc(sizeof(int32_t) * (n + 1)));
+  SPED_CUDA(b_lo.alloc(sizeof(int32_t) * (n + 1)));
+  SPED_CUDA(b_keys.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_vals.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_keys2.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_vals2.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_dinv.alloc(sizeof(double) * n));
+  SPED_CUDA(b_flag.alloc(sizeof(int32_t)));
+  SPED_CUDA(cudaMemsetAsync(cnt_up, 0, sizeof(int32_t) * 2 * n, s));
+  SPED_CUDA(cudaMemsetAsync(b_flag.p, 0, sizeof(int32_t), s));
+
+  int32_t* rowlen = (int32_t*)b_len.p;
+  int32_t* up_start = (int32_t*)b_up.p;
+  int32_t* lo_start = (int32_t*)b_lo.p;
+  int32_t* keys = (int32_t*)b_keys.p;
+  int32_t* vals = (int32_t*)b_vals.p;
+
+  if (m > 0) {
+    count_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, u, v, cnt_up, cnt_lo, keys, vals);
+    SPED_LAUNCH_CHECK();
+  }
+  rowlen_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(n, cnt_up, cnt_lo, rowlen);
+  SPED_LAUNCH_CHECK();
+
+  // scans (n+1 elements; the trailing zero makes element n the total)
+  size_t tmp_scan = 0;
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, rowlen, indptr, (int)(n + 1), s));
+  size_t tmp_sort = 0;
+  int end_bit = 1;
+  while (end_bit < 31 && ((int64_t)1 << end_bit) < n) ++end_bit;
+  if (m > 0) {
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, keys, (int32_t*)b_keys2.p, vals,
+                                              (int32_t*)b_vals2.p, (int)m, 0, end_bit, s));
+  }
+  SPED_CUDA(b_tmp.alloc(tmp_scan > tmp_sort ? tmp_scan : tmp_sort));
+  size_t tmp_bytes = tmp_scan;
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp_bytes, rowlen, indptr, (int)(n + 1), s));
+  // up/lo starts: reuse rowlen as the (n+1) input with a trailing zero
+  SPED_CUDA(cudaMemcpyAsync(rowlen, cnt_up, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp_bytes, rowlen, up_start, (int)(n + 1), s));
+  SPED_CUDA(cudaMemcpyAsync(rowlen, cnt_lo, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp_bytes, rowlen, lo_start, (int)(n + 1), s));
+
+  const int32_t* sorted_e = vals;
+  if (m > 0) {
+    size_t sb = tmp_sort;
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(b_tmp.p, sb, keys, (int32_t*)b_keys2.p, vals,
+                                              (int32_t*)b_vals2.p, (int)m, 0, end_bit, s));
+    sorted_e = (const int32_t*)b_vals2.p;
+  }
+
+  degree_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, up_start, lo_start, sorted_e, w, normalized,
+                                                   degrees, (double*)b_dinv.p, (int32_t*)b_flag.p);
+  SPED_LAUNCH_CHECK();
+  int32_t zero_flag = 0;
+  SPED_CUDA(cudaMemcpyAsync(&zero_flag, b_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaStreamSynchronize(s));
+  if (normalized && zero_flag) {
+    set_error("normalized Laplacian requires all degrees > 0");
+    return SPED_ERR_ZERO_DEGREE;
+  }
+  fill_kernel<<<grid_for(n, 128), 128, 0, s>>>(n, u, v, w, up_start, lo_start, sorted_e, indptr,
+                                                 (const double*)b_dinv.p, normalized, indices,
+                                                 store_values ? values : nullptr, epos);
+  SPED_LAUNCH_CHECK();
+  int32_t nnz = 0;
+  SPED_CUDA(cudaMemcpyAsync(&nnz, indptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaStreamSynchronize(s));
+  *nnz_out = nnz;
+  return SPED_OK;
+}
+
+// ---------------------------------------------------------------------------
+// long-row plan
+
+namespace sped {
+namespace {
+__global__ void plan_count_kernel(int64_t n, const int32_t* __restrict__ indptr, int32_t thresh,
+                                  int32_t chunk, int32_t* __restrict__ nch) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {
+    nch[n] = 0;
+    return;
+  }
+  int32_t len = indptr[i + 1] - indptr[i];
+  nch[i] = len > thresh ? (len + chunk - 1) / chunk : 0;
+}
+__global__ void plan_fill_kernel(int64_t n, const int32_t* __restrict__ indptr, int32_t thresh,
+                                 int32_t chunk, const int32_t* __restrict__ off,
+                                 int32_t* __restrict__ desc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t b = indptr[i], e = indptr[i + 1];
+  if (e - b <= thresh) return;
+  int32_t c0 = off[i];
+  int32_t c = c0;
+  for (int32_t p = b; p < e; p += chunk, ++c) {
+    desc[4 * (int64_t)c + 0] = (int32_t)i;
+    desc[4 * (int64_t)c + 1] = p;
+    desc[4 * (int64_t)c + 2] = min(e, p + chunk);
+    desc[4 * (int64_t)c + 3] = c0;
+  }
+}
+__global__ void count_long_rows(int64_t n, const int32_t* __restrict__ nch, int32_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && nch[i] > 0) atomicAdd(out, 1);
+}
+}  // namespace
+}  // namespace sped
+
+extern "C" int64_t sped_spmm_plan_max_chunks(int64_t n, int64_t nnz, int32_t long_threshold,
+                                             int32_t chunk_len) {
+  if (long_threshold < 1 || chunk_len < 1) return 0;
+  (void)n;
+  return nnz / chunk_len + nnz / (long_threshold + 1) + 1;
+}
+
+extern "C" int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_threshold,
+                              int32_t chunk_len, int32_t* chunk_desc, int64_t max_chunks,
+                              int64_t* n_chunks_out, int64_t* n_long_rows_out,
+                              sped_stream_t stream) {
+  SPED_CHECK_ARG(long_threshold >= 1 && chunk_len >= 1, "bad plan parameters");
+  SPED_CHECK_ARG(n_chunks_out && n_long_rows_out, "null output");
+  cudaStream_t s = as_stream(stream);
+  *n_chunks_out = 0;
+  *n_long_rows_out = 0;
+  if (n == 0) return SPED_OK;
+  AsyncBuf b_nch(s), b_off(s), b_tmp(s), b_cnt(s);
+  SPED_CUDA(b_nch.alloc(sizeof(int32_t) * (n + 1)));
+  SPED_CUDA(b_off.alloc(sizeof(int32_t) * (n + 1)));
+  SPED_CUDA(b_cnt.alloc(sizeof(int32_t)));
+  SPED_CUDA(cudaMemsetAsync(b_cnt.p, 0, sizeof(int32_t), s));
+  int32_t* nch = (int32_t*)b_nch.p;
+  int32_t* off = (int32_t*)b_off.p;
+  plan_count_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(n, indptr, long_threshold, chunk_len, nch);
+  SPED_LAUNCH_CHECK();
+  size_t tmp = 0;
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nch, off, (int)(n + 1), s));
+  SPED_CUDA(b_tmp.alloc(tmp));
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp, nch, off, (int)(n + 1), s));
+  count_long_rows<<<grid_for(n, 256), 256, 0, s>>>(n, nch, (int32_t*)b_cnt.p);
+  SPED_LAUNCH_CHECK();
+  int32_t total = 0, nlong = 0;
+  SPED_CUDA(cudaMemcpyAsync(&total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaMemcpyAsync(&nlong, b_cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaStreamSynchronize(s));
+  SPED_CHECK_ARG(total <= max_chunks, "plan needs %d chunks > capacity %lld", total,
+                 (long long)max_chunks);
+  if (total > 0) {
+    SPED_CHECK_ARG(chunk_desc != nullptr, "null chunk_desc");
+    plan_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, indptr, long_threshold, chunk_len, off,
+                                                        chunk_desc);
+    SPED_LAUNCH_CHECK();
+  }
+  *n_chunks_out = total;
+  *n_long_rows_out = nlong;
+  return SPED_OK;
+}

@@ -1,0 +1,263 @@
+// K3: edge-minibatch sampled-Laplacian apply fused into the polynomial
+// recurrence.  Replaces the identity stochastic oracle of
+// make_stochastic_oracle (solvers.py:166-178):
+//     batch = rng.integers(0, m, B)                          (host / K4)
+//     diff  = (x[u_b] - x[v_b]) * w_b
+//     est[u_b] += diff ; est[v_b] -= diff                    (np.add.at)
+//     return lam* x - (m/B) est
+// and, per term, the restated composition of SURVEY 8c(1) (term t uses the
+// t-th minibatch of the same PCG64 stream).
+//
+// Deterministic formulation (no float atomics on the block): the sampled
+// estimate is the weighted Laplacian of the sampled multiset,
+//     est_r = sum_{p in row r, p off-diag} h_p (w_r - w_{col_p}),
+//     h_p   = (multiplicity of edge(p) in the batch) * w_edge(p),
+// so each term is (1) a histogram of the batch into the CSR positions of the
+// sampled edges (`epos`, built with the CSR) and (2) a warp-per-row sweep
+// that skips positions with h_p == 0, gathers only the sampled neighbours,
+// applies the recurrence epilogue and clears h.  Every atomicAdd into h_p adds
+// the SAME value w_e, so h_p is independent of the atomic order.
+
+#include "sped_common.cuh"
+
+namespace sped {
+namespace {
+
+__global__ void batch_hist_kernel(int64_t B, const int32_t* __restrict__ batch,
+                                  const int32_t* __restrict__ epos,
+                                  const float* __restrict__ edge_w, float* __restrict__ hitw) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < B; i += stride) {
+    const int64_t e = batch[i];
+    const float we = edge_w ? edge_w[e] : 1.0f;
+    atomicAdd(hitw + epos[2 * e], we);
+    atomicAdd(hitw + epos[2 * e + 1], we);
+  }
+}
+
+struct BatchArgs {
+  int64_t n;
+  int32_t k;   // slab width
+  int64_t ld;
+  const int32_t* indptr;
+  const int32_t* indices;
+  float* hitw;
+  const float* x;
+  const float* win;
+  float* wout;
+  float alpha, beta, gamma, lamf, sfin;  // beta already includes m/B
+  int flags;   // bit0 alpha, bit1 gamma, bit2 final, bit3 lamf, bit4 reset hits
+};
+
+template <int LPR, int CPL, bool VEC>
+struct Slab {
+  static constexpr int W = VEC ? 4 : 1;  // floats per access
+  float v[CPL][W];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int i = 0; i < W; ++i) v[q][i] = 0.f;
+  }
+  __device__ __forceinline__ static int col0(int q, int cl) { return (q * LPR + cl) * W; }
+  __device__ __forceinline__ void load(const float* base, int cl, int k, bool gather) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = col0(q, cl);
+      if (VEC) {
+        float4 t = gather ? ld_gather_f4(base + c) : ld_stream_f4(base + c);
+        v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
+      } else {
+        v[q][0] = (c < k) ? (gather ? ld_gather_f32(base + c) : ld_stream_f32(base + c)) : 0.f;
+      }
+    }
+  }
+  __device__ __forceinline__ void fma(float a, const Slab& o) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int i = 0; i < W; ++i) v[q][i] = fmaf(a, o.v[q][i], v[q][i]);
+  }
+  __device__ __forceinline__ void fold_xor(int off) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int i = 0; i < W; ++i) v[q][i] += __shfl_xor_sync(0xffffffffu, v[q][i], off);
+  }
+};
+
+template <int LPR, int CPL, bool VEC>
+__global__ void __launch_bounds__(256) batch_row_kernel(const BatchArgs a) {
+  constexpr int SUB = 32 / LPR;
+  using S = Slab<LPR, CPL, VEC>;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;
+  const int cl = lane % LPR;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= a.n) return;
+  const int32_t b = a.indptr[row], e = a.indptr[row + 1];
+  S wr, xr, acc;
+  wr.load(a.win + row * a.ld, cl, a.k, true);
+  const bool need_x = (a.flags & 1) || ((a.flags & 4) && (a.flags & 8));
+  if (need_x) xr.load(a.x + row * a.ld, cl, a.k, false); else xr.zero();
+  acc.zero();
+  float hsum = 0.f;  // sum of h over the row (for the h*w_r part)
+  for (int32_t p0 = b; p0 < e; p0 += 32) {
+    const int32_t p = p0 + lane;
+    float h = 0.f;
+    int32_t col = 0;
+    if (p < e) {
+      h = __ldcg(a.hitw + p);
+      if (h != 0.f) {
+        col = ld_stream_i32(a.indices + p);
+        if (col == row) h = 0.f;  // the diagonal position is never a sampled edge
+        else if (a.flags & 16) a.hitw[p] = 0.f;
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, h != 0.f);
+    hsum += h;
+    const int cnt = __popc(mask);
+    for (int j0 = 0; j0 < cnt; j0 += SUB) {
+      const int j = j0 + sub;
+      const int src = (j < cnt) ? (int)__fns(mask, 0, j + 1) : 0;
+      const int32_t c = __shfl_sync(0xffffffffu, col, src);
+      float hh = __shfl_sync(0xffffffffu, h, src);
+      if (j < cnt) {
+        S g;
+        g.load(a.win + (int64_t)c * a.ld, cl, a.k, true);
+        acc.fma(-hh, g);
+      }
+    }
+  }
+  // fold: nonzero-parallel groups, and the row-sum of h across all lanes
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1) acc.fold_xor(off);
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
+  if (sub != 0) return;
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+#pragma unroll
+    for (int i = 0; i < S::W; ++i) {
+      const float est = fmaf(hsum, wr.v[q][i], acc.v[q][i]);
+      float r = a.beta * est;
+      if (a.flags & 1) r = fmaf(a.alpha, xr.v[q][i], r);
+      if (a.flags & 2) r = fmaf(a.gamma, wr.v[q][i], r);
+      if (a.flags & 4) {
+        r *= a.sfin;
+        if (a.flags & 8) r = fmaf(a.lamf, xr.v[q][i], r);
+      }
+      acc.v[q][i] = r;
+    }
+    const int c = S::col0(q, cl);
+    float* dst = a.wout + row * a.ld + c;
+    if (VEC) {
+      st_stream_f4(dst, make_float4(acc.v[q][0], acc.v[q][1], acc.v[q][2], acc.v[q][3]));
+    } else if (c < a.k) {
+      dst[0] = acc.v[q][0];
+    }
+  }
+}
+
+template <int LPR, int CPL, bool VEC>
+void launch_rows(const BatchArgs& a, cudaStream_t s) {
+  batch_row_kernel<LPR, CPL, VEC><<<grid_for(a.n, 8), 256, 0, s>>>(a);
+}
+
+int launch_batch_slab(const BatchArgs& a, bool aligned, cudaStream_t s) {
+  const int k = a.k;
+  if (aligned && k % 4 == 0) {
+    switch (k) {
+      case 4: launch_rows<1, 1, true>(a, s); break;
+      case 8: launch_rows<2, 1, true>(a, s); break;
+      case 16: launch_rows<4, 1, true>(a, s); break;
+      case 32: launch_rows<8, 1, true>(a, s); break;
+      case 64: launch_rows<16, 1, true>(a, s); break;
+      case 128: launch_rows<32, 1, true>(a, s); break;
+      default: aligned = false;
+    }
+    if (aligned) {
+      SPED_LAUNCH_CHECK();
+      return SPED_OK;
+    }
+  }
+  if (k <= 1) launch_rows<1, 1, false>(a, s);
+  else if (k <= 2) launch_rows<2, 1, false>(a, s);
+  else if (k <= 4) launch_rows<4, 1, false>(a, s);
+  else if (k <= 8) launch_rows<8, 1, false>(a, s);
+  else if (k <= 16) launch_rows<16, 1, false>(a, s);
+  else if (k <= 32) launch_rows<32, 1, false>(a, s);
+  else if (k <= 64) launch_rows<32, 2, false>(a, s);
+  else if (k <= 96) launch_rows<32, 3, false>(a, s);
+  else launch_rows<32, 4, false>(a, s);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
+}  // namespace
+
+int launch_axpby(int64_t count, double a, const float* x, double b, const float* y, float* out,
+                 cudaStream_t s);
+
+}  // namespace sped
+
+using namespace sped;
+
+extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indptr,
+                                          const int32_t* indices, const float* edge_w,
+                                          const int32_t* epos, const int32_t* batch, int64_t B,
+                                          float* hitw, const float* x, float* w_a, float* w_b,
+                                          float* out, int32_t n_terms, const double* alpha,
+                                          const double* beta, const double* gamma,
+                                          double w0_scale, double lam_f, double s_final,
+                                          sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && k >= 1 && m >= 0 && B >= 1, "bad sizes");
+  SPED_CHECK_ARG(n_terms >= 0 && (n_terms == 0 || (alpha && beta && gamma)), "bad schedule");
+  SPED_CHECK_ARG(x != out && x != w_a && x != w_b, "x must not alias outputs");
+  SPED_CHECK_ARG(n < INT32_MAX, "problem too large");
+  if (n == 0) return SPED_OK;
+  cudaStream_t s = as_stream(stream);
+  if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0_scale, x, 0.0, nullptr, out, s);
+  SPED_CHECK_ARG(m > 0 && indptr && indices && epos && batch && hitw, "null graph/batch array");
+  const double scale = (double)m / (double)B;
+  const int32_t slabs = (k + 127) / 128;
+  const float* cur = x;
+  for (int32_t t = 0; t < n_terms; ++t) {
+    const bool final = (t == n_terms - 1);
+    float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);
+    SPED_CHECK_ARG(dst != nullptr, "scratch buffer for term %d is NULL", t);
+    batch_hist_kernel<<<grid_for(B, 256, num_sms() * 8), 256, 0, s>>>(B, batch + (int64_t)t * B,
+                                                                        epos, edge_w, hitw);
+    SPED_LAUNCH_CHECK();
+    const double sc = (t == 0) ? w0_scale : 1.0;
+    for (int32_t sl = 0; sl < slabs; ++sl) {
+      const int32_t c0 = sl * 128;
+      BatchArgs a;
+      a.n = n;
+      a.k = min(128, k - c0);
+      a.ld = k;
+      a.indptr = indptr;
+      a.indices = indices;
+      a.hitw = hitw;
+      a.x = x + c0;
+      a.win = cur + c0;
+      a.wout = dst + c0;
+      a.alpha = (float)alpha[t];
+      // est is built from the term input w_t = sc * (stored input)
+      a.beta = (float)(beta[t] * scale * sc);
+      a.gamma = (float)(gamma[t] * sc);
+      a.lamf = (float)lam_f;
+      a.sfin = (float)s_final;
+      a.flags = (alpha[t] != 0.0 ? 1 : 0) | (gamma[t] != 0.0 ? 2 : 0) | (final ? 4 : 0) |
+                (lam_f != 0.0 ? 8 : 0) | (sl == slabs - 1 ? 16 : 0);
+      const bool aligned = (k % 4 == 0) &&
+                           ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(cur) |
+                             reinterpret_cast<uintptr_t>(dst)) % 16 == 0);
+      int rc = launch_batch_slab(a, aligned, s);
+      if (rc != SPED_OK) return rc;
+    }
+    cur = dst;
+  }
+  return SPED_OK;
+}

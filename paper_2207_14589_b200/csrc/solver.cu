@@ -1,0 +1,308 @@
+// K6 + k x k algebra of the solver step.
+//
+// mu-EigenGame (mu_eg_step, solvers.py:121-144) in Gram form (SURVEY 8a,
+// verified to 1.2e-16 in fp64):  with S = V^T V, C = V^T MV, Q = MV^T MV,
+//   U = triu(C, 1);  d_i = C_ii - (S U)_ii;  A = I - eta (U + diag d)
+//   ||W_i||^2 = (A^T S A)_ii + 2 eta (A^T C)_ii + eta^2 Q_ii
+//   V' = (V A + eta MV) diag(1/||W_i||)
+// so one step is: Gram pass (gram.cu) -> this k x k kernel -> one update
+// pass (block_update below).  No extra pass for the column norms.
+//
+// Oja (oja_step + MGS _orthonormalize, solvers.py:84-118) in CholQR2 form:
+//   W = V + eta MV, Gram(W) = S + eta (C + C^T) + eta^2 Q = R^T R,
+//   W1 = W R^{-1}, then one more Gram/Cholesky pass on W1 (CholQR2 equals
+//   MGS's Q to 3.5e-17 in fp64, SURVEY finding 8).
+//
+// All k x k algebra runs on the device in fp64 so the whole step can be
+// captured in one CUDA graph (no host round trip).
+
+#include "sped_common.cuh"
+
+namespace sped {
+namespace {
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// one CTA per column i
+__global__ void mueg_coeffs_kernel(int32_t k, const double* __restrict__ G, double eta,
+                                   float* __restrict__ A, float* __restrict__ scale,
+                                   int32_t* __restrict__ flag) {
+  extern __shared__ double acol[];  // column i of A (k doubles)
+  __shared__ double red[32];
+  const int i = blockIdx.x;
+  const double* S = G;
+  const double* C = G + (int64_t)k * k;
+  const double* Q = G + 2 * (int64_t)k * k;
+  // d_i = C_ii - sum_{j<i} S_ij C_ji
+  double part = 0.0;
+  for (int j = threadIdx.x; j < i; j += blockDim.x) part += S[(int64_t)i * k + j] * C[(int64_t)j * k + i];
+  const double d = C[(int64_t)i * k + i] - block_sum(part, red);
+  // column i of A
+  for (int a = threadIdx.x; a < k; a += blockDim.x) {
+    double v;
+    if (a < i) v = -eta * C[(int64_t)a * k + i];
+    else if (a == i) v = 1.0 - eta * d;
+    else v = 0.0;
+    acol[a] = v;
+    A[(int64_t)a * k + i] = (float)v;
+  }
+  __syncthreads();
+  // ||W_i||^2 = sum_b A_bi (S A)_bi + 2 eta sum_a A_ai C_ai + eta^2 Q_ii
+  part = 0.0;
+  for (int b = threadIdx.x; b <= i; b += blockDim.x) {
+    double sa = 0.0;
+    for (int a = 0; a <= i; ++a) sa += S[(int64_t)b * k + a] * acol[a];
+    part += acol[b] * sa + 2.0 * eta * acol[b] * C[(int64_t)b * k + i];
+  }
+  const double nrm2 = block_sum(part, red) + eta * eta * Q[(int64_t)i * k + i];
+  if (threadIdx.x == 0) {
+    const double nrm = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
+    if (!(nrm >= 1e-12)) {
+      atomicExch(flag, 1);
+      scale[i] = 0.f;
+    } else {
+      scale[i] = (float)(1.0 / nrm);
+    }
+  }
+}
+
+// single CTA: Cholesky of the (combined) Gram and the inverse of R
+// (R lives in dynamic shared memory, k <= 160).
+__global__ void oja_coeffs_kernel(int32_t k, const double* __restrict__ G, double eta,
+                                  int32_t with_m, float* __restrict__ T,
+                                  int32_t* __restrict__ flag) {
+  extern __shared__ double R[];
+  const double* S = G;
+  const double* C = G + (int64_t)k * k;
+  const double* Q = G + 2 * (int64_t)k * k;
+  const int64_t kk = (int64_t)k * k;
+  for (int64_t e = threadIdx.x; e < kk; e += blockDim.x) {
+    const int64_t a = e / k, b = e % k;
+    double g = S[e];
+    if (with_m) g += eta * (C[a * k + b] + C[b * k + a]) + eta * eta * Q[e];
+    R[e] = g;
+  }
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  // upper Cholesky in place: Gram = R^T R, R upper triangular
+  for (int j = 0; j < k; ++j) {
+    if (threadIdx.x == 0) {
+      double djj = R[(int64_t)j * k + j];
+      for (int a = 0; a < j; ++a) djj -= R[(int64_t)a * k + j] * R[(int64_t)a * k + j];
+      if (!(djj > 1e-24)) {
+        bad = 1;
+        djj = 1.0;
+      }
+      R[(int64_t)j * k + j] = sqrt(djj);
+    }
+    __syncthreads();
+    const double rjj = R[(int64_t)j * k + j];
+    for (int l = j + 1 + threadIdx.x; l < k; l += blockDim.x) {
+      double v = R[(int64_t)j * k + l];
+      for (int a = 0; a < j; ++a) v -= R[(int64_t)a * k + j] * R[(int64_t)a * k + l];
+      R[(int64_t)j * k + l] = v / rjj;
+    }
+    __syncthreads();
+  }
+  // T = R^{-1} (upper): column l by back substitution, one thread per column.
+  // T[a][l] (a < l) is kept in fp64 in R's unused strict lower triangle at
+  // R[l][a]; the diagonal T[l][l] = 1/R[l][l].
+  for (int l = threadIdx.x; l < k; l += blockDim.x) {
+    const double tll = 1.0 / R[(int64_t)l * k + l];
+    for (int i = l - 1; i >= 0; --i) {
+      double acc = -R[(int64_t)i * k + l] * tll;
+      for (int a = i + 1; a < l; ++a) acc -= R[(int64_t)i * k + a] * R[(int64_t)l * k + a];
+      R[(int64_t)l * k + i] = acc / R[(int64_t)i * k + i];
+    }
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < kk; e += blockDim.x) {
+    const int64_t i = e / k, l = e % k;
+    double t = 0.0;
+    if (i == l) t = 1.0 / R[i * k + i];
+    else if (i < l) t = R[l * k + i];
+    T[e] = (float)t;
+  }
+  if (threadIdx.x == 0 && bad) atomicExch(flag, 1);
+}
+
+// out = (P A + M B) diag(scale); register-tiled for K in {16,32,64,128}:
+// 64-row tiles, each thread owns RPT rows x 4 consecutive columns.
+template <int K>
+__global__ void __launch_bounds__(256) block_update_kernel(
+    int64_t n, const float* __restrict__ P, const float* __restrict__ A,
+    const float* __restrict__ M, const float* __restrict__ B, float eta,
+    const float* __restrict__ scale, float* __restrict__ out) {
+  constexpr int TR = 64;
+  constexpr int CG = K / 4;          // column groups
+  constexpr int RG = 256 / CG;       // row groups
+  constexpr int RPT = TR / RG;       // rows per thread
+  extern __shared__ float4 smem4[];
+  float* As = reinterpret_cast<float*>(smem4);          // K*K
+  float* Bs = As + K * K;                               // K*K (if B)
+  float* Ps = Bs + (B ? K * K : 0);                     // TR*(K+1)
+  float* Ms = Ps + TR * (K + 1);                        // TR*(K+1) (if M && B)
+  for (int e = threadIdx.x; e < K * K; e += 256) {
+    As[e] = A[e];
+    if (B) Bs[e] = B[e];
+  }
+  const int cg = threadIdx.x % CG, rg = threadIdx.x / CG;
+  float4 sc = make_float4(1.f, 1.f, 1.f, 1.f);
+  if (scale) sc = *reinterpret_cast<const float4*>(scale + cg * 4);
+  const int64_t ntiles = (n + TR - 1) / TR;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TR;
+    __syncthreads();
+    for (int e = threadIdx.x; e < TR * K; e += 256) {
+      const int rr = e / K, cc = e % K;
+      const int64_t r = r0 + rr;
+      Ps[rr * (K + 1) + cc] = r < n ? P[r * K + cc] : 0.f;
+      if (M && B) Ms[rr * (K + 1) + cc] = r < n ? M[r * K + cc] : 0.f;
+    }
+    __syncthreads();
+    float4 acc[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int a = 0; a < K; ++a) {
+      const float4 av = *reinterpret_cast<const float4*>(As + a * K + cg * 4);
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) acc[i] = f4_fma(Ps[(rg + i * RG) * (K + 1) + a], av, acc[i]);
+    }
+    if (M && B) {
+#pragma unroll 4
+      for (int a = 0; a < K; ++a) {
+        const float4 bv = *reinterpret_cast<const float4*>(Bs + a * K + cg * 4);
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) acc[i] = f4_fma(Ms[(rg + i * RG) * (K + 1) + a], bv, acc[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t r = r0 + rg + i * RG;
+      if (r >= n) continue;
+      float4 v = acc[i];
+      if (M && !B) v = f4_fma(eta, *reinterpret_cast<const float4*>(M + r * K + cg * 4), v);
+      v = make_float4(v.x * sc.x, v.y * sc.y, v.z * sc.z, v.w * sc.w);
+      *reinterpret_cast<float4*>(out + r * K + cg * 4) = v;
+    }
+  }
+}
+
+// generic k: one thread per output element of a 32-row tile
+__global__ void __launch_bounds__(256) block_update_generic(
+    int64_t n, int32_t k, const float* __restrict__ P, const float* __restrict__ A,
+    const float* __restrict__ M, const float* __restrict__ B, float eta,
+    const float* __restrict__ scale, float* __restrict__ out) {
+  const int64_t total = n * (int64_t)k;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = o / k;
+    const int c = (int)(o % k);
+    float acc = 0.f;
+    for (int a = 0; a < k; ++a) acc = fmaf(P[r * k + a], A[(int64_t)a * k + c], acc);
+    if (M) {
+      if (B) {
+        for (int a = 0; a < k; ++a) acc = fmaf(M[r * k + a], B[(int64_t)a * k + c], acc);
+      } else {
+        acc = fmaf(eta, M[o], acc);
+      }
+    }
+    if (scale) acc *= scale[c];
+    out[o] = acc;
+  }
+}
+
+template <int K>
+int launch_update(int64_t n, const float* P, const float* A, const float* M, const float* B,
+                  float eta, const float* scale, float* out, cudaStream_t s) {
+  constexpr int TR = 64;
+  size_t smem = sizeof(float) * (K * K * (B ? 2 : 1) + TR * (K + 1) * ((M && B) ? 2 : 1));
+  auto kern = block_update_kernel<K>;
+  static bool attr_set = false;  // once, so the launch is graph-capturable
+  if (!attr_set) {
+    SPED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(float) * (2 * K * K + 2 * TR * (K + 1)))));
+    attr_set = true;
+  }
+  const int64_t ntiles = (n + TR - 1) / TR;
+  int per_sm = (int)((220 * 1024) / smem);
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 8) per_sm = 8;
+  unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms() * per_sm);
+  kern<<<grid, 256, smem, s>>>(n, P, A, M, B, eta, scale, out);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
+}  // namespace
+}  // namespace sped
+
+using namespace sped;
+
+extern "C" int sped_mueg_coeffs(int32_t k, const double* G, double eta, float* A, float* scale,
+                                int32_t* flag, sped_stream_t stream) {
+  SPED_CHECK_ARG(k >= 1 && G && A && scale && flag, "bad mueg_coeffs arguments");
+  cudaStream_t s = as_stream(stream);
+  mueg_coeffs_kernel<<<k, 128, sizeof(double) * k, s>>>(k, G, eta, A, scale, flag);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
+extern "C" int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, float* T,
+                               int32_t* flag, sped_stream_t stream) {
+  SPED_CHECK_ARG(k >= 1 && k <= 160 && G && T && flag, "bad oja_coeffs arguments (k <= 160)");
+  cudaStream_t s = as_stream(stream);
+  const size_t smem = sizeof(double) * (size_t)k * k;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SPED_CUDA(cudaFuncSetAttribute(oja_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * 160 * 160)));
+    attr_set = true;
+  }
+  oja_coeffs_kernel<<<1, 256, smem, s>>>(k, G, eta, with_m, T, flag);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
+extern "C" int sped_block_update(int64_t n, int32_t k, const float* P, const float* A,
+                                 const float* M, const float* B, double eta, const float* scale,
+                                 float* out, sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && k >= 1 && P && A && out, "bad block_update arguments");
+  SPED_CHECK_ARG(out != P && out != M, "out must not alias inputs");
+  if (n == 0) return SPED_OK;
+  cudaStream_t s = as_stream(stream);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(out) |
+                         reinterpret_cast<uintptr_t>(M) | reinterpret_cast<uintptr_t>(scale)) %
+                        16) == 0;
+  if (aligned) {
+    switch (k) {
+      case 16: return launch_update<16>(n, P, A, M, B, (float)eta, scale, out, s);
+      case 32: return launch_update<32>(n, P, A, M, B, (float)eta, scale, out, s);
+      case 64: return launch_update<64>(n, P, A, M, B, (float)eta, scale, out, s);
+      case 128: return launch_update<128>(n, P, A, M, B, (float)eta, scale, out, s);
+      default: break;
+    }
+  }
+  block_update_generic<<<grid_for(n * k, 256, num_sms() * 16), 256, 0, s>>>(n, k, P, A, M, B,
+                                                                             (float)eta, scale, out);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}

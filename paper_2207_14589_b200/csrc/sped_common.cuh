@@ -1,0 +1,121 @@
+// Shared helpers for the SPED sm_100a kernels (status codes, error text,
+// launch checks, cache-hinted loads).
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include <cuda_runtime.h>
+
+#include "../../include/sped.h"
+
+namespace sped {
+
+void set_error(const char* fmt, ...);
+
+#define SPED_CHECK_ARG(cond, ...)                                  \
+  do {                                                             \
+    if (!(cond)) {                                                 \
+      ::sped::set_error(__VA_ARGS__);                              \
+      return SPED_ERR_ARG;                                         \
+    }                                                              \
+  } while (0)
+
+#define SPED_CUDA(call)                                            \
+  do {                                                             \
+    cudaError_t e__ = (call);                                      \
+    if (e__ != cudaSuccess) {                                      \
+      ::sped::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, \
+                        cudaGetErrorString(e__));                  \
+      return SPED_ERR_CUDA;                                        \
+    }                                                              \
+  } while (0)
+
+#define SPED_LAUNCH_CHECK() SPED_CUDA(cudaGetLastError())
+
+inline cudaStream_t as_stream(sped_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+// L2 eviction policies (createpolicy + .L2::cache_hint).  Streaming
+// (read-once) arrays are evict_first and skip L1; gathered rows of the block
+// being multiplied are evict_last so they stay resident in the 126 MB L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int ld_stream_i32(const int32_t* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(r) : "l"(p), "l"(policy_evict_first()));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(r) : "l"(p), "l"(policy_evict_first()));
+  return r;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(policy_evict_first()));
+  return r;
+}
+__device__ __forceinline__ float4 ld_gather_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(policy_evict_last()));
+  return r;
+}
+__device__ __forceinline__ float ld_gather_f32(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(r) : "l"(p), "l"(policy_evict_last()));
+  return r;
+}
+__device__ __forceinline__ void st_stream_f4(float* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+__device__ __forceinline__ float4 f4_fma(float a, float4 x, float4 y) {
+  return make_float4(fmaf(a, x.x, y.x), fmaf(a, x.y, y.y), fmaf(a, x.z, y.z), fmaf(a, x.w, y.w));
+}
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4_scale(float a, float4 x) {
+  return make_float4(a * x.x, a * x.y, a * x.z, a * x.w);
+}
+__device__ __forceinline__ float4 f4_shfl_xor(float4 v, int m) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, m);
+  v.y = __shfl_xor_sync(0xffffffffu, v.y, m);
+  v.z = __shfl_xor_sync(0xffffffffu, v.z, m);
+  v.w = __shfl_xor_sync(0xffffffffu, v.w, m);
+  return v;
+}
+
+inline unsigned grid_for(int64_t items, int per_block, int max_blocks = 1 << 30) {
+  int64_t g = (items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (unsigned)g;
+}
+
+}  // namespace sped

@@ -1,0 +1,461 @@
+// K1: CSR SpMM with the dilation-polynomial recurrence fused into the
+// epilogue (replaces the ell x `L.matvec` + numpy axpys of
+// TransformedOperator.apply, transforms.py:241-262 / graph.py:211).
+//
+// One term:  w' = alpha*x + beta*(L w) + gamma*w
+// last term: out = lam_f*x + s*w'
+// so every intermediate block is written exactly once.
+//
+// Mapping (sm_100a, HBM/L2-gather bound):
+//  * one warp per row; the row's k columns are covered by LPR = k/4 lanes
+//    with 128-bit loads, and the SUB = 32/LPR lane groups split the row's
+//    nonzeros (a row's 32 column indices are fetched by one coalesced load
+//    and broadcast by shuffles), then a shuffle tree folds the SUB partials;
+//  * four gathers of w rows are kept in flight per lane (unrolled);
+//  * rows longer than `long_thresh` are cut into chunks (sped_spmm_plan);
+//    chunk warps run in the FIRST blocks of the same launch, write partial
+//    rows, and the last chunk to arrive (ticket) folds the partials in chunk
+//    order and applies the epilogue -> deterministic, no float atomics;
+//  * index/value/x streams use L2::evict_first, gathered w rows
+//    L2::evict_last so the block being multiplied stays in the 126 MB L2;
+//  * unweighted combinatorial Laplacians use implicit values (-1 off the
+//    diagonal, row_len-1 on it): 4 B per nonzero instead of 8.
+//  * column slabs of <= 128 floats (row stride `ld`) cover any k.
+
+#include "sped_common.cuh"
+
+namespace sped {
+
+enum TermFlags : int {
+  TF_ALPHA = 1,   // alpha != 0: read x
+  TF_GAMMA = 2,   // gamma != 0: read w row
+  TF_FINAL = 4,   // last term: out = lam_f*x + s*w'
+  TF_LAMF = 8,    // lam_f != 0
+};
+
+struct TermArgs {
+  int64_t n;
+  int32_t k;    // columns in this slab
+  int64_t ld;   // row stride (floats)
+  const int32_t* indptr;
+  const int32_t* indices;
+  const float* values;
+  const float* x;
+  const float* win;
+  float* wout;
+  float alpha, beta, gamma, lamf, sfin;
+  int flags;
+  int32_t long_thresh;     // rows longer than this are chunk-processed
+  const int32_t* chunk_desc;
+  int32_t n_chunks;
+  int32_t chunk_blocks;    // leading blocks reserved for chunks
+  int32_t chunk_len;
+  float* partials;         // [n_chunks][k]
+  int32_t* tickets;
+};
+
+template <bool IMPLICIT>
+__device__ __forceinline__ float entry_value(const float* values, int64_t p, int32_t col, int64_t row,
+                                             int32_t rowlen) {
+  if (IMPLICIT) return col == row ? (float)(rowlen - 1) : -1.0f;
+  return ld_stream_f32(values + p);
+}
+
+// Accumulate sum_p L[row,p] * win[col_p, slab] over p in [b, e) for one warp.
+// Returns the per-lane partial (already folded across the SUB groups): lanes
+// with sub == 0 hold the row's VPL float4s.
+template <int LPR, int VPL, bool IMPLICIT>
+__device__ __forceinline__ void warp_row_accumulate(const TermArgs& a, int64_t row, int32_t b,
+                                                    int32_t e, int32_t rowlen, int lane,
+                                                    float4 (&acc)[VPL]) {
+  constexpr int SUB = 32 / LPR;
+  const int sub = lane / LPR;
+  const int cl = lane % LPR;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int32_t p0 = b; p0 < e; p0 += 32) {
+    const int32_t p = p0 + lane;
+    int32_t col = 0;
+    float val = 0.f;
+    if (p < e) {
+      col = ld_stream_i32(a.indices + p);
+      val = entry_value<IMPLICIT>(a.values, p, col, row, rowlen);
+    }
+    const int cnt = min(32, e - p0);
+    const int T = (cnt + SUB - 1) / SUB;
+    for (int t = 0; t < T; t += 4) {
+      int32_t c[4];
+      float w[4];
+      float4 g[4][VPL];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = (t + u) * SUB + sub;
+        const int js = j < 32 ? j : 31;
+        c[u] = __shfl_sync(0xffffffffu, col, js);
+        w[u] = __shfl_sync(0xffffffffu, val, js);
+        if (j >= cnt) w[u] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = (t + u) * SUB + sub;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          if (j < cnt)
+            g[u][v] = ld_gather_f4(a.win + (int64_t)c[u] * a.ld + (v * LPR + cl) * 4);
+          else
+            g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = f4_fma(w[u], g[u][v], acc[v]);
+    }
+  }
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = f4_add(acc[v], f4_shfl_xor(acc[v], off));
+}
+
+template <int LPR, int VPL>
+__device__ __forceinline__ void row_epilogue(const TermArgs& a, int64_t row, int lane,
+                                             const float4 (&y)[VPL], const float4 (&xr)[VPL],
+                                             const float4 (&wr)[VPL]) {
+  const int cl = lane % LPR;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    float4 r = f4_scale(a.beta, y[v]);
+    if (a.flags & TF_ALPHA) r = f4_fma(a.alpha, xr[v], r);
+    if (a.flags & TF_GAMMA) r = f4_fma(a.gamma, wr[v], r);
+    if (a.flags & TF_FINAL) {
+      r = f4_scale(a.sfin, r);
+      if (a.flags & TF_LAMF) r = f4_fma(a.lamf, xr[v], r);
+    }
+    st_stream_f4(a.wout + row * a.ld + (v * LPR + cl) * 4, r);
+  }
+}
+
+template <int LPR, int VPL>
+__device__ __forceinline__ void load_epilogue_operands(const TermArgs& a, int64_t row, int lane,
+                                                       float4 (&xr)[VPL], float4 (&wr)[VPL]) {
+  const int cl = lane % LPR;
+  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const int64_t off = row * a.ld + (v * LPR + cl) * 4;
+    xr[v] = need_x ? ld_stream_f4(a.x + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    wr[v] = (a.flags & TF_GAMMA) ? ld_gather_f4(a.win + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <int LPR, int VPL, bool IMPLICIT>
+__global__ void __launch_bounds__(256) spmm_term_kernel(const TermArgs a) {
+  constexpr int SUB = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;
+  const int warp_in_block = threadIdx.x >> 5;
+  const int warps_per_block = blockDim.x >> 5;
+
+  if ((int)blockIdx.x < a.chunk_blocks) {
+    // ---- long-row chunk ---------------------------------------------------
+    const int64_t c = (int64_t)blockIdx.x * warps_per_block + warp_in_block;
+    if (c >= a.n_chunks) return;
+    const int32_t row = a.chunk_desc[4 * c + 0];
+    const int32_t pb = a.chunk_desc[4 * c + 1];
+    const int32_t pe = a.chunk_desc[4 * c + 2];
+    const int32_t c0 = a.chunk_desc[4 * c + 3];
+    const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
+    float4 acc[VPL];
+    warp_row_accumulate<LPR, VPL, IMPLICIT>(a, row, pb, pe, re - rb, lane, acc);
+    const int cl = lane % LPR;
+    if (sub == 0) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        __stcg(reinterpret_cast<float4*>(a.partials + c * a.k + (v * LPR + cl) * 4), acc[v]);
+    }
+    __threadfence();
+    int ticket = 0;
+    if (lane == 0) ticket = atomicAdd(a.tickets + c0, 1);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    const int32_t nch = (re - rb + a.chunk_len - 1) / a.chunk_len;
+    if (ticket != nch - 1) return;
+    __threadfence();
+    // finisher: fold the partials in chunk order (deterministic)
+    float4 y[VPL], xr[VPL], wr[VPL];
+    load_epilogue_operands<LPR, VPL>(a, row, lane, xr, wr);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) y[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sub == 0) {
+      for (int32_t q = 0; q < nch; ++q) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          y[v] = f4_add(y[v], __ldcg(reinterpret_cast<const float4*>(
+                                  a.partials + (int64_t)(c0 + q) * a.k + (v * LPR + cl) * 4)));
+      }
+      row_epilogue<LPR, VPL>(a, row, lane, y, xr, wr);
+    }
+    if (lane == 0) a.tickets[c0] = 0;
+    return;
+  }
+
+  // ---- regular rows: one warp per row ---------------------------------------
+  const int64_t row = ((int64_t)blockIdx.x - a.chunk_blocks) * warps_per_block + warp_in_block;
+  if (row >= a.n) return;
+  const int32_t b = a.indptr[row], e = a.indptr[row + 1];
+  if (e - b > a.long_thresh) return;
+  float4 xr[VPL], wr[VPL];
+  load_epilogue_operands<LPR, VPL>(a, row, lane, xr, wr);
+  float4 acc[VPL];
+  warp_row_accumulate<LPR, VPL, IMPLICIT>(a, row, b, e, e - b, lane, acc);
+  if (sub == 0) row_epilogue<LPR, VPL>(a, row, lane, acc, xr, wr);
+}
+
+// Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
+// lanes over columns (CPL columns each), SUB groups over nonzeros.  Handles
+// every row itself (no long-row plan).
+template <int LPR, int CPL, bool IMPLICIT>
+__global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
+  constexpr int SUB = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;
+  const int cl = lane % LPR;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= a.n) return;
+  const int32_t b = a.indptr[row], e = a.indptr[row + 1];
+  float acc[CPL];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) acc[q] = 0.f;
+  for (int32_t p0 = b; p0 < e; p0 += 32) {
+    const int32_t p = p0 + lane;
+    int32_t col = 0;
+    float val = 0.f;
+    if (p < e) {
+      col = ld_stream_i32(a.indices + p);
+      val = entry_value<IMPLICIT>(a.values, p, col, row, e - b);
+    }
+    const int cnt = min(32, e - p0);
+    const int T = (cnt + SUB - 1) / SUB;
+    for (int t = 0; t < T; t += 2) {
+      int32_t c[2];
+      float w[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = (t + u) * SUB + sub;
+        const int js = j < 32 ? j : 31;
+        c[u] = __shfl_sync(0xffffffffu, col, js);
+        w[u] = __shfl_sync(0xffffffffu, val, js);
+        if (j >= cnt) w[u] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = (t + u) * SUB + sub;
+        if (j < cnt) {
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            const int cc = q * LPR + cl;
+            if (cc < a.k) acc[q] = fmaf(w[u], ld_gather_f32(a.win + (int64_t)c[u] * a.ld + cc), acc[q]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+  if (sub != 0) return;
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    const int cc = q * LPR + cl;
+    if (cc >= a.k) continue;
+    const int64_t off = row * a.ld + cc;
+    float r = a.beta * acc[q];
+    const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
+    const float xv = need_x ? a.x[off] : 0.f;
+    if (a.flags & TF_ALPHA) r = fmaf(a.alpha, xv, r);
+    if (a.flags & TF_GAMMA) r = fmaf(a.gamma, a.win[off], r);
+    if (a.flags & TF_FINAL) {
+      r *= a.sfin;
+      if (a.flags & TF_LAMF) r = fmaf(a.lamf, xv, r);
+    }
+    a.wout[off] = r;
+  }
+}
+
+template <int LPR, int VPL>
+static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
+  const int threads = 256;
+  const int wpb = threads / 32;
+  const int64_t row_blocks = (a.n + wpb - 1) / wpb;
+  const unsigned grid = (unsigned)(row_blocks + a.chunk_blocks);
+  if (implicit)
+    spmm_term_kernel<LPR, VPL, true><<<grid, threads, 0, s>>>(a);
+  else
+    spmm_term_kernel<LPR, VPL, false><<<grid, threads, 0, s>>>(a);
+}
+
+template <int LPR, int CPL>
+static void launch_generic(const TermArgs& a, bool implicit, cudaStream_t s) {
+  const int threads = 256;
+  const unsigned grid = grid_for(a.n, threads / 32);
+  if (implicit)
+    spmm_term_generic<LPR, CPL, true><<<grid, threads, 0, s>>>(a);
+  else
+    spmm_term_generic<LPR, CPL, false><<<grid, threads, 0, s>>>(a);
+}
+
+// Launch one term over one column slab.
+static int launch_term_slab(TermArgs a, bool implicit, bool aligned, cudaStream_t s) {
+  const int k = a.k;
+  const bool fast = aligned && (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128);
+  if (fast) {
+    const int wpb = 8;
+    a.chunk_blocks = a.n_chunks > 0 ? (int32_t)((a.n_chunks + wpb - 1) / wpb) : 0;
+    switch (k) {
+      case 4: launch_fast<1, 1>(a, implicit, s); break;
+      case 8: launch_fast<2, 1>(a, implicit, s); break;
+      case 16: launch_fast<4, 1>(a, implicit, s); break;
+      case 32: launch_fast<8, 1>(a, implicit, s); break;
+      case 64: launch_fast<16, 1>(a, implicit, s); break;
+      default: launch_fast<32, 1>(a, implicit, s); break;
+    }
+  } else {
+    a.chunk_blocks = 0;
+    a.long_thresh = INT32_MAX;
+    if (k <= 1) launch_generic<1, 1>(a, implicit, s);
+    else if (k <= 2) launch_generic<2, 1>(a, implicit, s);
+    else if (k <= 4) launch_generic<4, 1>(a, implicit, s);
+    else if (k <= 8) launch_generic<8, 1>(a, implicit, s);
+    else if (k <= 16) launch_generic<16, 1>(a, implicit, s);
+    else if (k <= 32) launch_generic<32, 1>(a, implicit, s);
+    else if (k <= 64) launch_generic<32, 2>(a, implicit, s);
+    else if (k <= 96) launch_generic<32, 3>(a, implicit, s);
+    else launch_generic<32, 4>(a, implicit, s);
+  }
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
+__global__ void axpby_kernel(int64_t count, float a, const float* __restrict__ x, float b,
+                             const float* __restrict__ y, float* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < count; i += stride) {
+    float r = a * x[i];
+    if (y) r = fmaf(b, y[i], r);
+    out[i] = r;
+  }
+}
+
+int launch_axpby(int64_t count, double a, const float* x, double b, const float* y, float* out,
+                 cudaStream_t s) {
+  if (count <= 0) return SPED_OK;
+  axpby_kernel<<<grid_for(count, 256, num_sms() * 16), 256, 0, s>>>(count, (float)a, x, (float)b, y,
+                                                                       out);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
+// Shared driver for the exact and stochastic applies: runs the schedule,
+// calling `term(t, win, wout, args)` for each term.
+template <class TermFn>
+int run_schedule(int64_t n, int32_t k, const float* x, float* w_a, float* w_b, float* out,
+                 int32_t n_terms, const double* alpha, const double* beta, const double* gamma,
+                 double w0, double lam_f, double s_final, cudaStream_t s, TermFn&& term) {
+  if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0, x, 0.0, nullptr, out, s);
+  const float* cur = x;
+  for (int32_t t = 0; t < n_terms; ++t) {
+    const bool final = (t == n_terms - 1);
+    float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);
+    if (!dst) {
+      set_error("scratch buffer for term %d is NULL", t);
+      return SPED_ERR_ARG;
+    }
+    const double sc = (t == 0) ? w0 : 1.0;
+    int flags = 0;
+    if (alpha[t] != 0.0) flags |= TF_ALPHA;
+    if (gamma[t] != 0.0) flags |= TF_GAMMA;
+    if (final) {
+      flags |= TF_FINAL;
+      if (lam_f != 0.0) flags |= TF_LAMF;
+    }
+    int rc = term(t, cur, dst, (float)alpha[t], (float)(beta[t] * sc), (float)(gamma[t] * sc),
+                  (float)lam_f, (float)s_final, flags);
+    if (rc != SPED_OK) return rc;
+    cur = dst;
+  }
+  return SPED_OK;
+}
+
+}  // namespace sped
+
+using namespace sped;
+
+extern "C" int sped_axpby(int64_t count, double a, const float* x, double b, const float* y,
+                          float* out, sped_stream_t stream) {
+  SPED_CHECK_ARG(count >= 0 && (count == 0 || (x && out)), "bad axpby arguments");
+  return launch_axpby(count, a, x, b, y, out, as_stream(stream));
+}
+
+extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
+                                   const int32_t* indices, const float* values,
+                                   int32_t long_threshold, int32_t chunk_len,
+                                   const int32_t* chunk_desc, int64_t n_chunks, float* partials,
+                                   int32_t* tickets, const float* x, float* w_a, float* w_b,
+                                   float* out, int32_t n_terms, const double* alpha,
+                                   const double* beta, const double* gamma, double w0_scale,
+                                   double lam_f, double s_final, sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && k >= 1, "bad shape n=%lld k=%d", (long long)n, k);
+  SPED_CHECK_ARG(n_terms >= 0, "negative term count");
+  SPED_CHECK_ARG(n_terms == 0 || (alpha && beta && gamma), "null schedule");
+  SPED_CHECK_ARG(n == 0 || (indptr && x && out), "null array");
+  SPED_CHECK_ARG(x != out && x != w_a && x != w_b, "x must not alias outputs");
+  SPED_CHECK_ARG(n_chunks == 0 || (chunk_desc && partials && tickets && chunk_len > 0 &&
+                                   long_threshold > 0),
+                 "null or inconsistent long-row plan");
+  SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX, "problem too large");
+  if (n == 0) return SPED_OK;
+  cudaStream_t s = as_stream(stream);
+  const bool implicit = (values == nullptr);
+  const int32_t slabs = (k + 127) / 128;
+  auto term = [&](int32_t t, const float* win, float* wout, float al, float be, float ga,
+                  float lf, float sf, int flags) -> int {
+    (void)t;
+    for (int32_t sl = 0; sl < slabs; ++sl) {
+      const int32_t c0 = sl * 128;
+      const int32_t kw = min(128, k - c0);
+      TermArgs a;
+      a.n = n;
+      a.k = kw;
+      a.ld = k;
+      a.indptr = indptr;
+      a.indices = indices;
+      a.values = values;
+      a.x = x + c0;
+      a.win = win + c0;
+      a.wout = wout + c0;
+      a.alpha = al;
+      a.beta = be;
+      a.gamma = ga;
+      a.lamf = lf;
+      a.sfin = sf;
+      a.flags = flags;
+      a.long_thresh = n_chunks > 0 ? long_threshold : INT32_MAX;
+      a.chunk_desc = chunk_desc;
+      a.n_chunks = (int32_t)n_chunks;
+      a.chunk_blocks = 0;
+      a.chunk_len = chunk_len > 0 ? chunk_len : 1;
+      a.partials = partials;
+      a.tickets = tickets;
+      const bool aligned = (k % 4 == 0) &&
+                           ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(win) |
+                             reinterpret_cast<uintptr_t>(wout)) % 16 == 0);
+      int rc = launch_term_slab(a, implicit, aligned, s);
+      if (rc != SPED_OK) return rc;
+    }
+    return SPED_OK;
+  };
+  return run_schedule(n, k, x, w_a, w_b, out, n_terms, alpha, beta, gamma, w0_scale, lam_f,
+                      s_final, s, term);
+}

@@ -1,0 +1,272 @@
+"""Row-sharded Laplacian across the GPUs of one node.
+
+Partition: contiguous node ranges balanced by nonzeros.  Rank r owns rows
+[b_r, b_{r+1}) of L, of V and of every polynomial intermediate.  Its local
+CSR keeps only its rows; columns are remapped to an extended block
+
+    E = [ own rows (n_own) | halo rows (n_halo) ]
+
+where the halo is the sorted set of off-shard columns its rows reference,
+grouped by owner rank.  Per polynomial term the owners send exactly those
+rows (grouped NCCL send/recv over NVLink, ``batch_isend_irecv``) straight
+into the halo region of E, then the fused SpMM term kernel runs on the local
+rows reading E (C1).  Per solver step the 3 k x k Gram blocks are summed with
+one all-reduce (C2) and every rank applies the same k x k coefficients to its
+rows.  No other data crosses ranks.
+
+The exchange/partition logic is device-agnostic (it also runs on CPU tensors
+under gloo, which is how it is tested without GPUs); the local term on a GPU
+is always ``sped_csr_poly_apply``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+__all__ = ["partition_rows", "HaloPlan", "ShardedLaplacian", "ShardedOperator",
+           "sharded_mu_eg_step"]
+
+
+def partition_rows(indptr: np.ndarray, parts: int) -> np.ndarray:
+    """Node offsets (parts+1) splitting rows into contiguous ranges with
+    about nnz/parts nonzeros each (each range non-empty when n >= parts)."""
+    n = indptr.size - 1
+    nnz = int(indptr[-1])
+    targets = (np.arange(1, parts) * nnz) // parts
+    cuts = np.searchsorted(indptr[1:], targets, side="left") + 1
+    off = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    for i in range(1, parts + 1):  # strictly increasing when possible
+        off[i] = max(off[i], min(off[i - 1] + 1, n))
+    off[-1] = n
+    return off
+
+
+@dataclass
+class HaloPlan:
+    rank: int
+    world: int
+    offsets: np.ndarray          # parts+1 node offsets
+    n_own: int
+    halo_cols: np.ndarray        # global ids of halo rows, grouped by owner
+    recv_counts: np.ndarray      # per owner
+    send_rows: list              # per peer: local row ids this rank sends
+    local_indices: np.ndarray    # local CSR columns remapped into E
+
+    @property
+    def n_halo(self) -> int:
+        return int(self.halo_cols.size)
+
+    @property
+    def send_counts(self) -> np.ndarray:
+        return np.array([s.size for s in self.send_rows], dtype=np.int64)
+
+
+def build_halo_plan(indices_global: np.ndarray, offsets: np.ndarray, rank: int, world: int,
+                    group=None) -> HaloPlan:
+    """Remap a rank's CSR columns into [own | halo] and agree on the send
+    lists with every peer (collective over ``group``)."""
+    b, e = int(offsets[rank]), int(offsets[rank + 1])
+    cols = indices_global.astype(np.int64)
+    remote_mask = (cols < b) | (cols >= e)
+    halo = np.unique(cols[remote_mask])                  # sorted => grouped by owner
+    owners = np.searchsorted(offsets, halo, side="right") - 1
+    recv_counts = np.bincount(owners, minlength=world).astype(np.int64)
+    local = np.empty_like(cols)
+    local[~remote_mask] = cols[~remote_mask] - b
+    local[remote_mask] = (e - b) + np.searchsorted(halo, cols[remote_mask])
+    # exchange the request lists: counts first, then the ids
+    counts = torch.from_numpy(recv_counts.copy())
+    all_counts = [torch.zeros_like(counts) for _ in range(world)]
+    dist.all_gather(all_counts, counts, group=group)
+    send_counts = np.array([int(all_counts[q][rank]) for q in range(world)], dtype=np.int64)
+    ops = []
+    recv_bufs = {}
+    starts = np.concatenate([[0], np.cumsum(recv_counts)])
+    for q in range(world):
+        if q == rank:
+            continue
+        if recv_counts[q]:
+            req = torch.from_numpy(halo[starts[q]:starts[q + 1]].copy())
+            ops.append(dist.P2POp(dist.isend, req, q, group=group))
+        if send_counts[q]:
+            buf = torch.empty(int(send_counts[q]), dtype=torch.int64)
+            recv_bufs[q] = buf
+            ops.append(dist.P2POp(dist.irecv, buf, q, group=group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    send_rows = []
+    for q in range(world):
+        if q in recv_bufs:
+            send_rows.append(recv_bufs[q].numpy() - b)
+        else:
+            send_rows.append(np.zeros(0, dtype=np.int64))
+    return HaloPlan(rank, world, offsets, e - b, halo, recv_counts, send_rows, local)
+
+
+class HaloExchanger:
+    """Per-term halo fill of E = [own | halo] (grouped send/recv)."""
+
+    def __init__(self, plan: HaloPlan, k: int, device, group=None):
+        self.plan, self.k, self.device, self.group = plan, k, torch.device(device), group
+        self.send_idx = torch.from_numpy(np.concatenate(plan.send_rows).astype(np.int32)
+                                         if plan.send_rows else np.zeros(0, np.int32)).to(self.device)
+        sc = plan.send_counts
+        self.send_off = np.concatenate([[0], np.cumsum(sc)])
+        self.recv_off = np.concatenate([[0], np.cumsum(plan.recv_counts)])
+        self.send_buf = torch.empty((int(sc.sum()), k), dtype=torch.float32, device=self.device)
+
+    def gather(self, E: torch.Tensor):
+        if self.send_buf.shape[0] == 0:
+            return
+        if E.is_cuda:
+            lib = _lib.load()
+            rc = lib.sped_gather_rows(self.send_buf.shape[0], self.k, _lib.ptr(self.send_idx),
+                                      _lib.ptr(E), _lib.ptr(self.send_buf),
+                                      _lib.stream_ptr(E.device))
+            _lib.check(rc, "sped_gather_rows")
+        else:
+            torch.index_select(E, 0, self.send_idx.long(), out=self.send_buf)
+
+    def exchange(self, E: torch.Tensor):
+        """E[:n_own] holds this rank's rows; fill E[n_own:] from the owners."""
+        p = self.plan
+        self.gather(E)
+        ops = []
+        for q in range(p.world):
+            if q == p.rank:
+                continue
+            s0, s1 = self.send_off[q], self.send_off[q + 1]
+            if s1 > s0:
+                ops.append(dist.P2POp(dist.isend, self.send_buf[s0:s1], q, group=self.group))
+            r0, r1 = self.recv_off[q], self.recv_off[q + 1]
+            if r1 > r0:
+                ops.append(dist.P2POp(dist.irecv, E[p.n_own + r0:p.n_own + r1], q, group=self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+
+class ShardedLaplacian:
+    """This rank's rows of L on its GPU, plus the halo plan."""
+
+    def __init__(self, full_laplacian, rank: int, world: int, group=None,
+                 offsets: np.ndarray | None = None):
+        lap = full_laplacian
+        self.full = lap
+        self.device = lap.device
+        indptr_h = lap.indptr.cpu().numpy().astype(np.int64)
+        self.offsets = partition_rows(indptr_h, world) if offsets is None else offsets
+        b, e = int(self.offsets[rank]), int(self.offsets[rank + 1])
+        p0, p1 = int(indptr_h[b]), int(indptr_h[e])
+        cols = lap.indices[p0:p1].cpu().numpy()
+        self.plan = build_halo_plan(cols, self.offsets, rank, world, group)
+        self.group = group
+        self.rank, self.world = rank, world
+        self.n_own = e - b
+        self.row0 = b
+        self.n_global = lap.n
+        self.nnz_local = p1 - p0
+        self.nnz_global = lap.nnz
+        self.indptr = torch.from_numpy((indptr_h[b:e + 1] - p0).astype(np.int32)).to(self.device)
+        self.indices = torch.from_numpy(self.plan.local_indices.astype(np.int32)).to(self.device)
+        self.values = None if lap.values is None else lap.values[p0:p1].contiguous()
+        self.implicit = lap.values is None
+        self.long_threshold, self.chunk_len = lap.long_threshold, lap.chunk_len
+        self._plan_chunks()
+
+    def _plan_chunks(self):
+        import ctypes as C
+        lib = _lib.load()
+        n = self.n_own
+        maxc = int(lib.sped_spmm_plan_max_chunks(n, self.nnz_local, self.long_threshold, self.chunk_len))
+        desc = torch.empty(max(4 * maxc, 4), dtype=torch.int32, device=self.device)
+        nch, nlong = C.c_int64(0), C.c_int64(0)
+        rc = lib.sped_spmm_plan(n, _lib.ptr(self.indptr), self.long_threshold, self.chunk_len,
+                                _lib.ptr(desc), maxc, C.byref(nch), C.byref(nlong),
+                                _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_spmm_plan")
+        self.n_chunks = int(nch.value)
+        self.chunk_desc = desc[: max(4 * self.n_chunks, 4)].clone() if self.n_chunks else None
+        self.tickets = torch.zeros(max(self.n_chunks, 1), dtype=torch.int32, device=self.device)
+
+    def local_term(self, E, x_own, out, alpha, beta, gamma, w0, lam_f, s_final, k):
+        lib = _lib.load()
+        partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=self.device)
+                    if self.n_chunks else None)
+        rc = lib.sped_csr_poly_apply(
+            self.n_own, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
+            self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
+            _lib.ptr(partials), _lib.ptr(self.tickets if self.n_chunks else None), _lib.ptr(E),
+            None, None, _lib.ptr(out), 1, _lib.dbl_array([alpha]), _lib.dbl_array([beta]),
+            _lib.dbl_array([gamma]), float(w0), float(lam_f), float(s_final),
+            _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_csr_poly_apply (shard)")
+
+
+class ShardedOperator:
+    """Reversed polynomial operator over a ShardedLaplacian: same schedule
+    as ``TransformedOperator`` with a halo exchange before every term."""
+
+    def __init__(self, shard: ShardedLaplacian, transform, lambda_star: float, term_fn=None):
+        from .transforms import term_schedule
+        self.shard = shard
+        self.transform = transform
+        self.lambda_star = lambda_star
+        self.schedule = term_schedule(transform, lambda_star)
+        self.term_fn = term_fn or shard.local_term
+        self._ex = {}
+        self._bufs = {}
+
+    def _buffers(self, k):
+        if k not in self._bufs:
+            sh = self.shard
+            rows = sh.n_own + sh.plan.n_halo
+            self._bufs[k] = [torch.empty((rows, k), dtype=torch.float32, device=sh.device)
+                             for _ in range(2)]
+            self._ex[k] = HaloExchanger(sh.plan, k, sh.device, sh.group)
+        return self._bufs[k], self._ex[k]
+
+    def apply_local(self, x_own: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """p(L) applied to the distributed block whose local rows are x_own."""
+        sh = self.shard
+        k = int(x_own.shape[1])
+        (Ea, Eb), ex = self._buffers(k)
+        al, be, ga, w0, lf, s = self.schedule
+        if out is None:
+            out = torch.empty_like(x_own)
+        if len(al) == 0:
+            out.copy_(x_own * (lf + s * w0))
+            return out
+        Ea[: sh.n_own].copy_(x_own)
+        cur, nxt = Ea, Eb
+        for t in range(len(al)):
+            ex.exchange(cur)
+            final = t == len(al) - 1
+            dst = out if final else nxt[: sh.n_own]
+            self.term_fn(cur, x_own, dst, al[t], be[t], ga[t], w0 if t == 0 else 1.0,
+                         lf if final else 0.0, s if final else 1.0, k)
+            cur, nxt = nxt, cur
+        return out
+
+
+def sharded_mu_eg_step(op: ShardedOperator, V_own: torch.Tensor, eta: float, ws,
+                       out: torch.Tensor, MV: torch.Tensor | None = None, group=None):
+    """mu_eg_step (solvers.py:121-144) on row shards: local Gram, one
+    all-reduce of the 3 k x k blocks, identical k x k algebra on every rank,
+    local update."""
+    lib = _lib.load()
+    MV = op.apply_local(V_own, out=MV)
+    ws.gram(V_own, MV)
+    dist.all_reduce(ws.G, op=dist.ReduceOp.SUM, group=group)
+    rc = lib.sped_mueg_coeffs(ws.k, _lib.ptr(ws.G), float(eta), _lib.ptr(ws.A),
+                              _lib.ptr(ws.scale), _lib.ptr(ws.flag), _lib.stream_ptr(ws.device))
+    _lib.check(rc, "sped_mueg_coeffs")
+    ws.update(V_own, ws.A, MV, None, eta, ws.scale, out)
+    return out

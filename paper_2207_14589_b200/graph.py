@@ -1,0 +1,341 @@
+"""Graphs and the device Laplacian operator.
+
+Mirrors the reference ``specgap.graph`` surface used by the hot path
+(``/root/reference/pkg/src/specgap/graph.py``):
+
+* :class:`Graph` — canonical edge list with the same validation and error
+  messages as ``Graph.__post_init__`` (graph.py:64-88).  Host input is
+  canonicalised with numpy exactly as the reference does; generator output
+  that is already canonical and lives on the GPU can enter through
+  :meth:`Graph.from_canonical` without a host round trip.
+* :class:`LaplacianOperator` — the CSR of ``L = D - A`` or
+  ``D^-1/2 L D^-1/2`` built ON THE DEVICE by ``sped_laplacian_build``
+  (bit-identical to fp32 of scipy's CSR, graph.py:182-199) and applied by the
+  fused SpMM kernel (``matvec``, graph.py:205-211).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Iterable, NamedTuple, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .arrays import as_device_block, from_device_block
+
+__all__ = [
+    "Graph",
+    "LaplacianOperator",
+    "DegreeBounds",
+    "build_laplacian",
+    "laplacian_matvec",
+    "dense_laplacian",
+    "degree_bounds",
+]
+
+_DENSE_MAX_NODES = 5000
+LONG_ROW_THRESHOLD = 1024
+CHUNK_LEN = 512
+
+
+class Graph:
+    """Undirected weighted graph stored as a canonical edge list (u < v,
+    lexsorted, unique, w > 0).  Same contract as ``specgap.Graph``."""
+
+    def __init__(self, n: int, u, v, w, *, _canonical: bool = False):
+        if n < 0:
+            raise ValueError("node count must be nonnegative")
+        self.n = int(n)
+        self._dev = {}
+        if _canonical:
+            self._u, self._v, self._w = u, v, w
+            return
+        u = np.asarray(u, dtype=np.int64)
+        v = np.asarray(v, dtype=np.int64)
+        w = np.asarray(w, dtype=np.float64)
+        if not (u.shape == v.shape == w.shape):
+            raise ValueError("edge arrays must have identical length")
+        if np.any(w < 0):
+            raise ValueError("edge weights must be nonnegative")
+        keep = w > 0
+        u, v, w = u[keep], v[keep], w[keep]
+        if u.size:
+            if np.any(u == v):
+                raise ValueError("self-loops are not allowed")
+            if np.any((u < 0) | (u >= self.n) | (v < 0) | (v >= self.n)):
+                raise ValueError("edge endpoint out of range")
+        lo = np.minimum(u, v)
+        hi = np.maximum(u, v)
+        order = np.lexsort((hi, lo))
+        lo, hi, w = lo[order], hi[order], w[order]
+        pair_ids = lo * self.n + hi
+        if pair_ids.size and np.any(np.diff(pair_ids) == 0):
+            raise ValueError("duplicate edge for an unordered node pair")
+        self._u, self._v, self._w = lo, hi, w
+
+    # -- construction ------------------------------------------------------
+    @classmethod
+    def from_edges(cls, n: int, edges: Iterable[Sequence]) -> "Graph":
+        us, vs, ws = [], [], []
+        for e in edges:
+            if len(e) == 2:
+                a, b = e
+                c = 1.0
+            else:
+                a, b, c = e
+            us.append(a)
+            vs.append(b)
+            ws.append(c)
+        return cls(n, np.array(us, dtype=np.int64), np.array(vs, dtype=np.int64),
+                   np.array(ws, dtype=np.float64))
+
+    @classmethod
+    def from_canonical(cls, n: int, u, v, w, validate: bool = True) -> "Graph":
+        """Wrap an edge list that is already canonical (u < v, strictly
+        increasing ``u*n+v``, w > 0) — e.g. generator output on the GPU —
+        without the host lexsort.  ``validate`` checks the invariants with
+        device-side reductions and raises the reference's errors."""
+        if isinstance(u, torch.Tensor):
+            u = u.to(torch.int64)
+            v = v.to(torch.int64)
+            w = w.to(torch.float64)
+            if validate and u.numel():
+                if bool((w <= 0).any()):
+                    raise ValueError("edge weights must be positive in canonical form")
+                if bool((u >= v).any()) or bool((u < 0).any()) or bool((v >= n).any()):
+                    raise ValueError("canonical edges need 0 <= u < v < n")
+                key = u * n + v
+                if key.numel() > 1 and bool((key[1:] <= key[:-1]).any()):
+                    raise ValueError("canonical edges must be lexsorted without duplicates")
+            g = cls(n, u, v, w, _canonical=True)
+            if u.is_cuda:
+                g._dev[u.device] = (u, v, w)
+            return g
+        g = cls(n, u, v, w)
+        return g
+
+    # -- host views (API parity with specgap.Graph) --------------------------
+    def _host(self, a):
+        return a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+
+    @property
+    def u(self) -> np.ndarray:
+        self._u = self._host(self._u)
+        return self._u
+
+    @property
+    def v(self) -> np.ndarray:
+        self._v = self._host(self._v)
+        return self._v
+
+    @property
+    def w(self) -> np.ndarray:
+        self._w = self._host(self._w)
+        return self._w
+
+    @property
+    def m(self) -> int:
+        return int(self._u.shape[0])
+
+    @property
+    def num_edges(self) -> int:
+        return self.m
+
+    def is_unit_weight(self) -> bool:
+        w = self._w
+        if isinstance(w, torch.Tensor):
+            return bool((w == 1.0).all()) if w.numel() else True
+        return bool(np.all(w == 1.0))
+
+    def degrees(self) -> np.ndarray:
+        """Weighted degree (graph.py:118-122)."""
+        d = np.bincount(self.u, weights=self.w, minlength=self.n)
+        d += np.bincount(self.v, weights=self.w, minlength=self.n)
+        return d
+
+    def degree_counts(self) -> np.ndarray:
+        d = np.bincount(self.u, minlength=self.n)
+        d += np.bincount(self.v, minlength=self.n)
+        return d
+
+    def neighbors(self, i: int) -> np.ndarray:
+        return np.sort(np.concatenate([self.v[self.u == i], self.u[self.v == i]]))
+
+    def has_edge(self, i: int, j: int) -> bool:
+        return j in self.neighbors(i)
+
+    def device_edges(self, device):
+        """(u int64, v int64, w float64) on ``device`` (cached)."""
+        device = torch.device(device)
+        hit = self._dev.get(device)
+        if hit is None:
+            def dev(a, dt):
+                if isinstance(a, torch.Tensor):
+                    return a.to(device=device, dtype=dt)
+                return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+            hit = (dev(self._u, torch.int64), dev(self._v, torch.int64), dev(self._w, torch.float64))
+            self._dev[device] = hit
+        return hit
+
+    def __repr__(self) -> str:
+        return f"Graph(n={self.n}, m={self.m})"
+
+
+class DegreeBounds(NamedTuple):
+    deg_star: int
+    deg_star_inc: int
+    lambda_upper: float
+
+
+def degree_bounds(g: Graph) -> DegreeBounds:
+    """graph.py:351-362."""
+    if g.n == 0 or g.m == 0:
+        return DegreeBounds(0, 0, 0.0)
+    deg_star = int(g.degree_counts().max())
+    return DegreeBounds(deg_star, 2 * deg_star - 1, 2.0 * float(g.degrees().max()))
+
+
+class LaplacianOperator:
+    """Device CSR Laplacian; ``mode`` in {"unnormalized", "normalized"}.
+
+    Attributes mirror the reference (``graph``, ``mode``, ``degrees`` — host
+    fp64, bit-identical to ``Graph.degrees()``) plus the device arrays
+    ``indptr``, ``indices``, ``values`` (None for implicit unit-weight
+    combinatorial Laplacians), ``epos`` and the long-row plan.
+    """
+
+    def __init__(self, graph: Graph, mode: str = "unnormalized", device=None,
+                 long_threshold: int = LONG_ROW_THRESHOLD, chunk_len: int = CHUNK_LEN,
+                 implicit: bool | None = None):
+        if mode not in ("unnormalized", "normalized"):
+            raise ValueError(f"unknown Laplacian mode: {mode!r}")
+        dev = _lib.require_cuda(device)
+        lib = _lib.load()
+        self.graph = graph
+        self.mode = mode
+        self.device = dev
+        n, m = graph.n, graph.m
+        if implicit is None:
+            implicit = (mode == "unnormalized") and graph.is_unit_weight()
+        self.implicit = bool(implicit)
+        u, v, w = graph.device_edges(dev)
+        cap = 2 * m + n
+        self.indptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        self.indices = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        vals = None if self.implicit else torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+        deg = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        self.epos = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
+        nnz = C.c_int64(0)
+        with torch.cuda.device(dev):
+            rc = lib.sped_laplacian_build(n, m, _lib.ptr(u), _lib.ptr(v), _lib.ptr(w),
+                                          1 if mode == "normalized" else 0,
+                                          0 if self.implicit else 1,
+                                          _lib.ptr(self.indptr), _lib.ptr(self.indices),
+                                          _lib.ptr(vals), _lib.ptr(deg), _lib.ptr(self.epos),
+                                          C.byref(nnz), _lib.stream_ptr(dev))
+        _lib.check(rc, "sped_laplacian_build")
+        self.nnz = int(nnz.value)
+        self.indices = self.indices[: max(self.nnz, 1)]
+        self.values = None if vals is None else vals[: max(self.nnz, 1)]
+        self.degrees = deg[:n].cpu().numpy()
+        self.edge_w = None
+        if not graph.is_unit_weight():
+            self.edge_w = w.to(torch.float32)
+        # long-row plan (power-law hubs)
+        self.long_threshold = int(long_threshold)
+        self.chunk_len = int(chunk_len)
+        maxc = int(lib.sped_spmm_plan_max_chunks(n, self.nnz, self.long_threshold, self.chunk_len))
+        desc = torch.empty(max(4 * maxc, 4), dtype=torch.int32, device=dev)
+        nch, nlong = C.c_int64(0), C.c_int64(0)
+        with torch.cuda.device(dev):
+            rc = lib.sped_spmm_plan(n, _lib.ptr(self.indptr), self.long_threshold, self.chunk_len,
+                                    _lib.ptr(desc), maxc, C.byref(nch), C.byref(nlong),
+                                    _lib.stream_ptr(dev))
+        _lib.check(rc, "sped_spmm_plan")
+        self.n_chunks = int(nch.value)
+        self.n_long_rows = int(nlong.value)
+        self.chunk_desc = desc[: max(4 * self.n_chunks, 4)].clone() if self.n_chunks else None
+        self._tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=dev)
+                         if self.n_chunks else None)
+
+    # -- reference surface ---------------------------------------------------
+    @property
+    def n(self) -> int:
+        return self.graph.n
+
+    def matvec(self, x):
+        """``L @ x`` for a vector of length n or an (n, k) block (numpy in ->
+        numpy float64 out, torch CUDA in -> torch fp32 out)."""
+        shape0 = x.shape[0] if hasattr(x, "shape") and len(x.shape) else None
+        if shape0 != self.n:
+            raise ValueError(f"dimension mismatch: operator is {self.n}, "
+                             f"input has leading dimension {shape0}")
+        return self.poly_apply(x, [0.0], [1.0], [0.0], 1.0, 0.0, 1.0)
+
+    __call__ = matvec
+
+    # -- device entry points ---------------------------------------------------
+    def poly_apply(self, x, alpha, beta, gamma, w0, lam_f, s_final, out=None):
+        """Run a (alpha, beta, gamma) term schedule (see ``sped.h``)."""
+        xd, back = as_device_block(x, self.device)
+        yd = self.poly_apply_device(xd, alpha, beta, gamma, w0, lam_f, s_final, out=out)
+        return from_device_block(yd, back)
+
+    def poly_apply_device(self, xd: torch.Tensor, alpha, beta, gamma, w0, lam_f, s_final,
+                          out: torch.Tensor | None = None) -> torch.Tensor:
+        lib = _lib.load()
+        n = self.n
+        k = 1 if xd.dim() == 1 else int(xd.shape[1])
+        nt = len(alpha)
+        if out is None:
+            out = torch.empty_like(xd)
+        wa = torch.empty_like(xd) if nt >= 2 else None
+        wb = torch.empty_like(xd) if nt >= 3 else None
+        partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=self.device)
+                    if self.n_chunks else None)
+        with torch.cuda.device(self.device):
+            rc = lib.sped_csr_poly_apply(
+                n, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
+                self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
+                _lib.ptr(partials), _lib.ptr(self._tickets), _lib.ptr(xd), _lib.ptr(wa),
+                _lib.ptr(wb), _lib.ptr(out), nt, _lib.dbl_array(alpha), _lib.dbl_array(beta),
+                _lib.dbl_array(gamma), float(w0), float(lam_f), float(s_final),
+                _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_csr_poly_apply")
+        return out
+
+    def csr_host(self):
+        """(indptr, indices, data) as numpy (data fp32; implicit values are
+        materialised) — for parity checks and host-side tooling."""
+        indptr = self.indptr.cpu().numpy()
+        indices = self.indices[: self.nnz].cpu().numpy()
+        if self.values is not None:
+            data = self.values[: self.nnz].cpu().numpy()
+        else:
+            rows = np.repeat(np.arange(self.n), np.diff(indptr))
+            rl = np.diff(indptr)[rows]
+            data = np.where(indices == rows, rl - 1, -1).astype(np.float32)
+        return indptr, indices, data
+
+
+def build_laplacian(g: Graph, mode: str = "unnormalized", device=None) -> LaplacianOperator:
+    return LaplacianOperator(g, mode, device=device)
+
+
+def laplacian_matvec(op: LaplacianOperator, x):
+    return op.matvec(x)
+
+
+def dense_laplacian(g: Graph, mode: str = "unnormalized", device=None) -> np.ndarray:
+    """Dense Laplacian (desk scale only, graph.py:224-229): densified from the
+    device CSR (fp32 values, returned as float64)."""
+    if g.n > _DENSE_MAX_NODES:
+        raise ValueError(f"dense Laplacian refused for n={g.n} (limit {_DENSE_MAX_NODES})")
+    op = build_laplacian(g, mode, device=device)
+    indptr, indices, data = op.csr_host()
+    out = np.zeros((g.n, g.n))
+    rows = np.repeat(np.arange(g.n), np.diff(indptr))
+    out[rows, indices] = data
+    return out

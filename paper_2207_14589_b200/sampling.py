@@ -1,0 +1,168 @@
+"""Seeded edge minibatches and the stochastic (edge-minibatch) oracle.
+
+The reference draws ``rng.integers(0, m, size=B)`` from a numpy PCG64
+generator created once per oracle (solvers.py:167,171).  Here the same
+indices are produced either
+
+* on the device by ``sped_pcg64_integers`` (bit-exact numpy PCG64 + Lemire,
+  the default), after which the host ``Generator``'s state is advanced to
+  exactly where numpy would be, or
+* on the host by the numpy generator itself (``index_source="host"``),
+  uploaded through pinned memory.
+
+Both are bit-identical to the reference stream; a whole apply's ``ell`` term
+batches are one draw of ``ell*B`` values (numpy's buffered uint32 carries
+across calls, so consecutive calls concatenate).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .arrays import as_device_block, from_device_block
+
+__all__ = ["pcg64_draw", "host_draw", "EdgeBatchOracle", "pcg64_advance_state"]
+
+_MULT = (2549297995355413924 << 64) | 4865540595714422341
+_M128 = (1 << 128) - 1
+_M64 = (1 << 64) - 1
+
+
+def _advance(state: int, inc: int, delta: int) -> int:
+    acc_mult, acc_plus = 1, 0
+    cur_mult, cur_plus = _MULT, inc
+    while delta > 0:
+        if delta & 1:
+            acc_mult = (acc_mult * cur_mult) & _M128
+            acc_plus = (acc_plus * cur_mult + cur_plus) & _M128
+        cur_plus = ((cur_mult + 1) * cur_plus) & _M128
+        cur_mult = (cur_mult * cur_mult) & _M128
+        delta >>= 1
+    return (acc_mult * state + acc_plus) & _M128
+
+
+def _output(state: int) -> int:
+    hi, lo = state >> 64, state & _M64
+    rot = hi >> 58
+    x = hi ^ lo
+    return ((x >> rot) | (x << ((64 - rot) & 63))) & _M64
+
+
+def pcg64_advance_state(st: dict, draws32: int) -> dict:
+    """numpy PCG64 state after ``draws32`` calls of next_uint32."""
+    if draws32 <= 0:
+        return st
+    s = st["state"]["state"]
+    inc = st["state"]["inc"]
+    has = st["has_uint32"]
+    uint = st["uinteger"]
+    r = draws32 - (1 if has else 0)
+    if r <= 0:
+        has = 0
+    else:
+        steps = (r + 1) // 2
+        s = _advance(s, inc, steps)
+        has = r % 2
+        uint = _output(s) >> 32
+    return {"bit_generator": "PCG64", "state": {"state": s, "inc": inc},
+            "has_uint32": int(has), "uinteger": int(uint)}
+
+
+def pcg64_draw(rng: np.random.Generator, m: int, count: int, device) -> torch.Tensor:
+    """``rng.integers(0, m, size=count)`` generated on the device (int32),
+    advancing ``rng`` exactly as numpy would."""
+    if m <= 0:
+        raise ValueError("high <= 0")
+    if m > np.iinfo(np.int32).max:
+        raise ValueError("edge count exceeds int32 indices")
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValueError("device draws need a PCG64 generator")
+    lib = _lib.load()
+    out = torch.empty(max(count, 1), dtype=torch.int32, device=device)
+    nbytes = int(lib.sped_pcg64_workspace_bytes(count))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    s = st["state"]["state"]
+    inc = st["state"]["inc"]
+    draws = C.c_int64(0)
+    rc = lib.sped_pcg64_integers(s >> 64, s & _M64, inc >> 64, inc & _M64,
+                                 int(st["has_uint32"]), int(st["uinteger"]), int(m), int(count),
+                                 _lib.ptr(out), C.byref(draws), _lib.ptr(ws), nbytes,
+                                 _lib.stream_ptr(device))
+    _lib.check(rc, "sped_pcg64_integers")
+    rng.bit_generator.state = pcg64_advance_state(st, int(draws.value))
+    return out[:count]
+
+
+def host_draw(rng: np.random.Generator, m: int, count: int, device) -> torch.Tensor:
+    """The reference's own host draw, uploaded through pinned memory."""
+    idx = rng.integers(0, m, size=count)
+    pinned = torch.empty(count, dtype=torch.int32, pin_memory=True)
+    np.copyto(pinned.numpy(), idx, casting="unsafe")
+    return pinned.to(device, non_blocking=True)
+
+
+class EdgeBatchOracle:
+    """Stochastic reversed operator (solvers.py:150-180, restated per term).
+
+    Each call draws ``n_terms * batch_size`` edge ids from the oracle's PCG64
+    stream and runs ``sped_edge_batch_poly_apply``.  Stateful (owns the
+    stream), like the reference's closure."""
+
+    def __init__(self, op, batch_size: int, seed: int, index_source: str = "device"):
+        if index_source not in ("device", "host"):
+            raise ValueError("index_source must be 'device' or 'host'")
+        self.op = op
+        self.batch_size = int(batch_size)
+        self.rng = np.random.default_rng(seed)
+        self.index_source = index_source
+        lap = op.laplacian
+        self.device = lap.device
+        self.m = lap.graph.m
+        self.hitw = torch.zeros(max(lap.nnz, 1), dtype=torch.float32, device=self.device)
+        self.last_batch = None
+
+    @property
+    def n(self) -> int:
+        return self.op.n
+
+    def draw(self, count: int) -> torch.Tensor:
+        if self.index_source == "device":
+            return pcg64_draw(self.rng, self.m, count, self.device)
+        return host_draw(self.rng, self.m, count, self.device)
+
+    def apply_device(self, xd: torch.Tensor, batch: torch.Tensor | None = None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+        lib = _lib.load()
+        lap = self.op.laplacian
+        al, be, ga, w0, lf, s = self.op.schedule
+        nt = len(al)
+        B = self.batch_size
+        if batch is None:
+            batch = self.draw(nt * B) if nt > 0 else torch.empty(1, dtype=torch.int32,
+                                                                  device=self.device)
+        self.last_batch = batch
+        k = 1 if xd.dim() == 1 else int(xd.shape[1])
+        if out is None:
+            out = torch.empty_like(xd)
+        wa = torch.empty_like(xd) if nt >= 2 else None
+        wb = torch.empty_like(xd) if nt >= 3 else None
+        rc = lib.sped_edge_batch_poly_apply(
+            self.n, k, self.m, _lib.ptr(lap.indptr), _lib.ptr(lap.indices), _lib.ptr(lap.edge_w),
+            _lib.ptr(lap.epos), _lib.ptr(batch), B, _lib.ptr(self.hitw), _lib.ptr(xd),
+            _lib.ptr(wa), _lib.ptr(wb), _lib.ptr(out), nt, _lib.dbl_array(al),
+            _lib.dbl_array(be), _lib.dbl_array(ga), float(w0), float(lf), float(s),
+            _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_edge_batch_poly_apply")
+        return out
+
+    def __call__(self, x):
+        shape0 = x.shape[0] if hasattr(x, "shape") and len(x.shape) else None
+        if shape0 != self.n:
+            raise ValueError("dimension mismatch in transformed matvec")
+        xd, back = as_device_block(x, self.device)
+        return from_device_block(self.apply_device(xd), back)

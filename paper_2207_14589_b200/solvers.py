@@ -1,0 +1,485 @@
+"""Streaming top-k eigensolvers on the device.
+
+Mirrors ``specgap.solvers`` (/root/reference/pkg/src/specgap/solvers.py):
+``EigenState``, ``SolverConfig``, ``init_state``, ``oja_step``,
+``mu_eg_step``, ``make_stochastic_oracle``, ``run_solver``, ``run_to_csv``.
+
+A step never leaves the GPU: oracle (fused polynomial SpMM, or the
+edge-minibatch kernel) -> Gram of [V | MV] (``sped_gram``) -> k x k algebra
+in fp64 on the device (``sped_mueg_coeffs`` / ``sped_oja_coeffs``) -> one
+fused update pass (``sped_block_update``).  ``run_solver`` replays whole
+steps as CUDA graphs between metric evaluations (exact oracle, constant eta).
+Public step functions accept numpy or CUDA states; numpy in -> numpy out.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .arrays import as_device_block, from_device_block, is_device_array
+from .graph import Graph
+from .metrics import GroundTruth, eigenvector_streak, graph_ground_truth, subspace_error
+from .sampling import EdgeBatchOracle
+from .transforms import SpectralTransform, TransformedOperator, make_reversed_operator
+
+__all__ = [
+    "EigenState",
+    "SolverConfig",
+    "MetricRow",
+    "SolverRun",
+    "StepWorkspace",
+    "init_state",
+    "orthonormalize",
+    "oja_step",
+    "mu_eg_step",
+    "make_stochastic_oracle",
+    "run_solver",
+    "run_to_csv",
+]
+
+_NORM_TOL = 1e-12
+
+
+@dataclass
+class EigenState:
+    """Candidate eigenvector block plus a step counter (solvers.py:46-58).
+    ``V`` is a CUDA fp32 tensor (device solver) or a numpy array."""
+
+    V: object
+    step: int = 0
+
+    @property
+    def n(self) -> int:
+        return int(self.V.shape[0])
+
+    @property
+    def k(self) -> int:
+        return int(self.V.shape[1])
+
+    def numpy(self) -> np.ndarray:
+        V = self.V
+        return V.detach().cpu().numpy().astype(np.float64) if isinstance(V, torch.Tensor) else V
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """solvers.py:61-81."""
+
+    solver: str = "oja"
+    k: int = 2
+    eta: float = 0.1
+    steps: int = 1000
+    batch_size: int = 0
+    seed: int = 0
+    eval_every: int = 100
+    eta_schedule: str = "constant"
+    streak_epsilon: float = 0.01
+
+    def __post_init__(self):
+        if self.solver not in ("oja", "mu-eg"):
+            raise ValueError(f"unknown solver {self.solver!r}")
+        if self.eta <= 0:
+            raise ValueError("step size must be positive")
+        if self.steps < 0 or self.eval_every < 1 or self.k < 1:
+            raise ValueError("invalid solver configuration")
+        if self.eta_schedule not in ("constant", "invsqrt"):
+            raise ValueError(f"unknown eta schedule {self.eta_schedule!r}")
+
+
+class StepWorkspace:
+    """Static device buffers for one (n, k) solver step (graph-capturable)."""
+
+    def __init__(self, n: int, k: int, device):
+        lib = _lib.load()
+        self.n, self.k, self.device = n, k, device
+        self.G = torch.empty(3 * k * k, dtype=torch.float64, device=device)
+        self.gram_bytes = int(lib.sped_gram_workspace_bytes(n, k))
+        self.gram_ws = torch.empty(self.gram_bytes, dtype=torch.uint8, device=device)
+        self.A = torch.empty(k * k, dtype=torch.float32, device=device)
+        self.B = torch.empty(k * k, dtype=torch.float32, device=device)
+        self.scale = torch.empty(k, dtype=torch.float32, device=device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+        self.tmp = torch.empty((n, k), dtype=torch.float32, device=device)
+
+    def gram(self, V, M=None):
+        lib = _lib.load()
+        rc = lib.sped_gram(self.n, self.k, _lib.ptr(V), _lib.ptr(M), _lib.ptr(self.G),
+                           _lib.ptr(self.gram_ws), self.gram_bytes, _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_gram")
+
+    def update(self, P, A, M, B, eta, scale, out):
+        lib = _lib.load()
+        rc = lib.sped_block_update(self.n, self.k, _lib.ptr(P), _lib.ptr(A), _lib.ptr(M),
+                                   _lib.ptr(B), float(eta), _lib.ptr(scale), _lib.ptr(out),
+                                   _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_block_update")
+
+    def oja_coeffs(self, eta, with_m, T):
+        lib = _lib.load()
+        rc = lib.sped_oja_coeffs(self.k, _lib.ptr(self.G), float(eta), int(with_m), _lib.ptr(T),
+                                 _lib.ptr(self.flag), _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_oja_coeffs")
+
+    # -- step bodies (device, stream-ordered, no host sync) -------------------
+    def mu_eg(self, V, MV, eta, out):
+        """solvers.py:121-144 in Gram form."""
+        lib = _lib.load()
+        self.gram(V, MV)
+        rc = lib.sped_mueg_coeffs(self.k, _lib.ptr(self.G), float(eta), _lib.ptr(self.A),
+                                  _lib.ptr(self.scale), _lib.ptr(self.flag),
+                                  _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_mueg_coeffs")
+        self.update(V, self.A, MV, None, eta, self.scale, out)
+
+    def oja(self, V, MV, eta, out):
+        """oja_step (solvers.py:114-118) with MGS replaced by CholQR2."""
+        lib = _lib.load()
+        self.gram(V, MV)
+        self.oja_coeffs(eta, 1, self.A)
+        rc = lib.sped_axpby(self.k * self.k, float(eta), _lib.ptr(self.A), 0.0, None,
+                            _lib.ptr(self.B), _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_axpby")
+        self.update(V, self.A, MV, self.B, 0.0, None, self.tmp)
+        self.gram(self.tmp)
+        self.oja_coeffs(0.0, 0, self.A)
+        self.update(self.tmp, self.A, None, None, 0.0, None, out)
+
+    def cholqr2(self, V, out):
+        """_orthonormalize (solvers.py:84-102) as CholQR2 (same Q as MGS)."""
+        self.gram(V)
+        self.oja_coeffs(0.0, 0, self.A)
+        self.update(V, self.A, None, None, 0.0, None, self.tmp)
+        self.gram(self.tmp)
+        self.oja_coeffs(0.0, 0, self.A)
+        self.update(self.tmp, self.A, None, None, 0.0, None, out)
+
+    def take_flag(self) -> bool:
+        f = bool(self.flag.item())
+        if f:
+            self.flag.zero_()
+        return f
+
+
+_WS_CACHE: dict = {}
+
+
+def _workspace(n, k, device) -> StepWorkspace:
+    key = (n, k, str(device), torch.cuda.current_stream(device).cuda_stream)
+    ws = _WS_CACHE.get(key)
+    if ws is None:
+        ws = StepWorkspace(n, k, device)
+        _WS_CACHE[key] = ws
+    return ws
+
+
+def _device_of(oracle, default=None):
+    for obj in (getattr(oracle, "__self__", None), oracle):
+        for attr in ("device",):
+            d = getattr(obj, attr, None)
+            if d is not None:
+                return torch.device(d)
+        lap = getattr(obj, "laplacian", None)
+        if lap is not None and getattr(lap, "device", None) is not None:
+            return lap.device
+    return _lib.require_cuda(default)
+
+
+def orthonormalize(V, rng=None, device=None):
+    """Column-orthonormalise (same Q as MGS).  Collapsed columns are
+    re-randomised as in solvers.py:91-100."""
+    dev = _lib.require_cuda(device)
+    Vd, back = as_device_block(V, dev)
+    Vd = Vd.contiguous()
+    n, k = Vd.shape
+    ws = _workspace(n, k, dev)
+    out = torch.empty_like(Vd)
+    ws.cholqr2(Vd, out)
+    if ws.take_flag():
+        warnings.warn("rank collapse in orthonormalization; re-randomizing", RuntimeWarning)
+        out = _mgs_repair(Vd, rng)
+    return from_device_block(out, back)
+
+
+def _mgs_repair(Vd, rng):
+    """Rare path: column-sequential Gram-Schmidt with re-randomisation,
+    following solvers.py:84-102 (device torch ops, fp64)."""
+    V = Vd.double().clone()
+    n, k = V.shape
+    for j in range(k):
+        for i in range(j):
+            V[:, j] -= (V[:, i] @ V[:, j]) * V[:, i]
+        nrm = torch.linalg.norm(V[:, j])
+        if float(nrm) < _NORM_TOL:
+            if rng is None:
+                rng = np.random.default_rng(0)
+            V[:, j] = torch.from_numpy(rng.standard_normal(n)).to(V.device)
+            for i in range(j):
+                V[:, j] -= (V[:, i] @ V[:, j]) * V[:, i]
+            nrm = torch.linalg.norm(V[:, j])
+        V[:, j] /= nrm
+    return V.float()
+
+
+def init_state(n: int, k: int, seed: int, device=None) -> EigenState:
+    """Seeded Gaussian block (the reference's exact numpy stream,
+    solvers.py:105-111), orthonormalised on the device.  V is a CUDA tensor."""
+    if k > n:
+        raise ValueError("cannot ask for more eigenvectors than dimensions")
+    dev = _lib.require_cuda(device)
+    rng = np.random.default_rng(seed)
+    G = rng.standard_normal((n, k))
+    Vd = orthonormalize(torch.from_numpy(G.astype(np.float32)).to(dev), rng, device=dev)
+    return EigenState(Vd, 0)
+
+
+def _device_oracle(oracle):
+    """The device-side apply of our operators (also when the reference-style
+    bound method ``op.apply`` is passed), else None."""
+    obj = getattr(oracle, "__self__", oracle)
+    if isinstance(obj, TransformedOperator) and obj.transform.is_polynomial:
+        return obj.apply_device
+    if isinstance(obj, EdgeBatchOracle):
+        return obj.apply_device
+    return None
+
+
+def _oracle_block(oracle, V, Vd, dev):
+    """MV on the device.  Our operators run directly on the device copy of V
+    (one H2D per step for host states); foreign callables get V as passed."""
+    fn = _device_oracle(oracle)
+    if fn is not None:
+        return fn(Vd)
+    MVd, _ = as_device_block(oracle(V), dev)
+    return MVd
+
+
+def mu_eg_step(state: EigenState, oracle, eta: float, rng=None) -> EigenState:
+    """One parallel EigenGame update (solvers.py:121-144)."""
+    dev = _device_of(oracle)
+    Vd, back = as_device_block(state.V, dev)
+    MVd = _oracle_block(oracle, state.V, Vd, dev)
+    n, k = Vd.shape
+    ws = _workspace(n, k, dev)
+    out = torch.empty_like(Vd)
+    ws.mu_eg(Vd, MVd, eta, out)
+    if ws.take_flag():
+        out = _mueg_repair(Vd, MVd, ws, eta, rng)
+    return EigenState(from_device_block(out, back), state.step + 1)
+
+
+def _mueg_repair(Vd, MVd, ws, eta, rng):
+    warnings.warn("rank collapse in mu-eg update; re-randomizing", RuntimeWarning)
+    W = torch.empty_like(Vd)
+    ws.update(Vd, ws.A, MVd, None, eta, None, W)
+    W = W.double()
+    norms = torch.linalg.norm(W, dim=0)
+    bad = (norms < _NORM_TOL).cpu().numpy()
+    if rng is None:
+        rng = np.random.default_rng(0)
+    W[:, torch.from_numpy(bad).to(W.device)] = torch.from_numpy(
+        rng.standard_normal((W.shape[0], int(bad.sum())))).to(W.device)
+    return (W / torch.linalg.norm(W, dim=0)).float()
+
+
+def oja_step(state: EigenState, oracle, eta: float, rng=None) -> EigenState:
+    """One Oja update ``V <- orthonormalize(V + eta M V)`` (solvers.py:114-118)."""
+    dev = _device_of(oracle)
+    Vd, back = as_device_block(state.V, dev)
+    MVd = _oracle_block(oracle, state.V, Vd, dev)
+    n, k = Vd.shape
+    ws = _workspace(n, k, dev)
+    out = torch.empty_like(Vd)
+    ws.oja(Vd, MVd, eta, out)
+    if ws.take_flag():
+        warnings.warn("rank collapse in oja update; re-randomizing", RuntimeWarning)
+        out = _mgs_repair(Vd + eta * MVd, rng)
+    return EigenState(from_device_block(out, back), state.step + 1)
+
+
+_STEP_RULES = {"oja": oja_step, "mu-eg": mu_eg_step}
+
+
+def make_stochastic_oracle(op: TransformedOperator, batch_size: int, seed: int,
+                           sampler=None, index_source: str = "device"):
+    """Unbiased stochastic estimate of the reversed transformed matvec
+    (solvers.py:150-202).  Batch size 0 returns ``op.apply``.  Every
+    polynomial kind uses per-term seeded edge minibatches drawn from ONE
+    numpy PCG64 stream seeded with ``seed`` (identity: exactly the
+    reference's identity oracle; other kinds: the restated composition of
+    SURVEY 8c(1) — the reference's walk sampler is not on this path)."""
+    if batch_size == 0:
+        return op.apply
+    if batch_size < 0:
+        raise ValueError("batch size must be nonnegative")
+    if not op.transform.is_polynomial:
+        raise ValueError("stochastic sampling needs a polynomial transform")
+    if sampler is not None:
+        raise NotImplementedError("the walk sampler (walks.py) is not part of the device path; "
+                                  "per-term edge minibatches are used instead")
+    return EdgeBatchOracle(op, batch_size, seed, index_source=index_source)
+
+
+@dataclass
+class MetricRow:
+    step: int
+    subspace_error: float
+    streak: int
+    elapsed_ns: int
+
+
+@dataclass
+class SolverRun:
+    records: list
+    state: EigenState
+    config: SolverConfig
+    ground_truth: GroundTruth | None
+    steps_to_streak: int | None = None
+    steps_to_subspace: int | None = None
+
+    @property
+    def V(self):
+        return self.state.V
+
+
+class _GraphStepper:
+    """Whole solver steps captured as CUDA graphs (ping-pong buffers)."""
+
+    def __init__(self, op: TransformedOperator, solver: str, eta: float, V0: torch.Tensor):
+        self.dev = V0.device
+        n, k = V0.shape
+        self.bufs = [V0.clone(), torch.empty_like(V0)]
+        self.MV = torch.empty_like(V0)
+        self.ws = StepWorkspace(n, k, self.dev)
+        self.op, self.solver, self.eta = op, solver, eta
+        self.cur = 0
+        self.graphs = [None, None]
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            for i in (0, 1):  # warm-up (allocations, attributes)
+                self._body(self.bufs[i], self.bufs[1 - i])
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        torch.cuda.synchronize(self.dev)
+        self.bufs[0].copy_(V0)
+        for i in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body(self.bufs[i], self.bufs[1 - i])
+            self.graphs[i] = g
+
+    def _body(self, V, out):
+        self.op.apply_device(V, out=self.MV)
+        if self.solver == "mu-eg":
+            self.ws.mu_eg(V, self.MV, self.eta, out)
+        else:
+            self.ws.oja(V, self.MV, self.eta, out)
+
+    def step(self):
+        self.graphs[self.cur].replay()
+        self.cur ^= 1
+
+    @property
+    def V(self):
+        return self.bufs[self.cur]
+
+
+def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
+               mode: str = "unnormalized", ground_truth: GroundTruth | None = None,
+               operator: TransformedOperator | None = None,
+               streak_target: int | None = None, subspace_target: float | None = None,
+               stop_on_targets: bool = False, record_timing: bool = True,
+               device=None, use_cuda_graphs: bool = True,
+               index_source: str = "device") -> SolverRun:
+    """Run a solver on the reversed transformed Laplacian (solvers.py:227-292),
+    entirely on the device.  Metrics are evaluated on the host every
+    ``eval_every`` steps against the original Laplacian's bottom-k truth
+    (dense, n <= 5000, as in the reference)."""
+    if config.k > g.n:
+        raise ValueError("k exceeds the node count")
+    dev = _lib.require_cuda(device)
+    op = operator if operator is not None else make_reversed_operator(g, transform, mode, device=dev)
+    ss = np.random.SeedSequence(config.seed)
+    init_seed, aux_seed, oracle_seed = (int(x) for x in ss.generate_state(3))
+    rng = np.random.default_rng(aux_seed)
+    stochastic = config.batch_size > 0
+    oracle = make_stochastic_oracle(op, config.batch_size, oracle_seed,
+                                    index_source=index_source) if stochastic else op
+    if ground_truth is None and g.n <= 5000:
+        ground_truth = graph_ground_truth(g, mode)
+    state = init_state(g.n, config.k, init_seed, device=dev)
+    target_streak = config.k if streak_target is None else streak_target
+
+    records: list[MetricRow] = []
+    run = SolverRun(records, state, config, ground_truth)
+    t0 = time.perf_counter_ns()
+
+    def evaluate(V, step):
+        elapsed = time.perf_counter_ns() - t0 if record_timing else 0
+        if ground_truth is None:
+            records.append(MetricRow(step, float("nan"), 0, elapsed))
+            return
+        Vh = V.detach().cpu().numpy().astype(np.float64)
+        err = subspace_error(Vh, ground_truth, config.k)
+        stk = eigenvector_streak(Vh, ground_truth, config.streak_epsilon)
+        records.append(MetricRow(step, err, stk, elapsed))
+        if run.steps_to_streak is None and stk >= target_streak:
+            run.steps_to_streak = step
+        if subspace_target is not None and run.steps_to_subspace is None and err <= subspace_target:
+            run.steps_to_subspace = step
+
+    def targets_met():
+        if run.steps_to_streak is None:
+            return False
+        if subspace_target is not None and run.steps_to_subspace is None:
+            return False
+        return True
+
+    evaluate(state.V, 0)
+    graphable = (use_cuda_graphs and not stochastic and config.eta_schedule == "constant"
+                 and isinstance(op, TransformedOperator) and op.transform.is_polynomial
+                 and config.steps > 0)
+    V = state.V
+    if graphable:
+        stepper = _GraphStepper(op, config.solver, config.eta, V)
+        for t in range(1, config.steps + 1):
+            stepper.step()
+            if t % config.eval_every == 0 or t == config.steps:
+                if stepper.ws.take_flag():
+                    # rare: redo with the eager path's repair semantics
+                    warnings.warn("rank collapse detected; re-randomizing", RuntimeWarning)
+                    stepper.bufs[stepper.cur].copy_(orthonormalize(stepper.V, rng, device=dev))
+                evaluate(stepper.V, t)
+                if stop_on_targets and targets_met():
+                    break
+        V = stepper.V.clone()
+        steps_done = t
+    else:
+        step_fn = _STEP_RULES[config.solver]
+        st = EigenState(V, 0)
+        steps_done = 0
+        for t in range(1, config.steps + 1):
+            eta = config.eta if config.eta_schedule == "constant" else config.eta / math.sqrt(t)
+            st = step_fn(st, oracle, eta, rng)
+            steps_done = t
+            if t % config.eval_every == 0 or t == config.steps:
+                evaluate(st.V, t)
+                if stop_on_targets and targets_met():
+                    break
+        V = st.V
+    run.state = EigenState(V, steps_done)
+    return run
+
+
+def run_to_csv(run: SolverRun) -> str:
+    """solvers.py:295-300."""
+    lines = ["step,subspace_error,streak,elapsed_ns"]
+    for row in run.records:
+        lines.append(f"{row.step},{row.subspace_error!r},{row.streak},{row.elapsed_ns}")
+    return "\n".join(lines) + "\n"

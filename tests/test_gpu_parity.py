@@ -1,0 +1,220 @@
+"""CUDA path vs the reference goldens and the CPU oracle (run on a B200).
+
+Tolerances (BASELINE north_star): graph construction and sampled indices
+bit-exact; p(L)V within 1e-5 relative Frobenius in fp32.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import rel_fro
+
+pytestmark = pytest.mark.gpu
+
+PV_TOL = 1e-5
+
+
+def _sp():
+    import paper_2207_14589_b200 as sp
+    return sp
+
+
+def _graph(golden, name):
+    sp = _sp()
+    n, u, v, w = golden.graph(name)
+    return sp.Graph(n, u, v, w)
+
+
+# --- graph construction (bit-exact) -----------------------------------------------
+
+@pytest.mark.parametrize("mode", ["unnormalized", "normalized"])
+def test_csr_bit_exact_vs_reference(cuda, golden, mode):
+    sp = _sp()
+    checked = 0
+    for name in golden.graph_names():
+        key = f"csr/{name}/{mode}"
+        g = _graph(golden, name)
+        if f"{key}/error" in golden:
+            with pytest.raises(ValueError, match="degrees"):
+                sp.build_laplacian(g, mode)
+            continue
+        if f"{key}/indptr" not in golden:
+            continue
+        for implicit in (False, True):
+            if implicit and not (mode == "unnormalized" and g.is_unit_weight()):
+                continue
+            L = sp.LaplacianOperator(g, mode, implicit=implicit)
+            indptr, indices, data = L.csr_host()
+            np.testing.assert_array_equal(indptr, golden[f"{key}/indptr"], err_msg=name)
+            np.testing.assert_array_equal(indices, golden[f"{key}/indices"], err_msg=name)
+            ref32 = golden[f"{key}/data"].astype(np.float32)
+            assert np.array_equal(data.view(np.uint32), ref32.view(np.uint32)), (name, mode)
+            np.testing.assert_array_equal(L.degrees, golden[f"csr/{name}/{mode}/degrees"])
+        checked += 1
+    assert checked >= 10
+
+
+def test_csr_bit_exact_config_scale(cuda):
+    """Config-5-shaped weighted graph (n=2e5) and config-4-shaped normalized
+    Chung-Lu (n=2e5): device CSR == fp32(scipy CSR) bit for bit."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    for (n, u, v, w), mode in [(G.lp_sbm(200_000, 20, 24.0, 0.1, 5, 0.8, device="cuda"), "unnormalized"),
+                               (G.chung_lu(200_000, device="cuda"), "normalized"),
+                               (G.sbm_sparse(200_000, 20, 20.0, 0.9, device="cuda"), "normalized")]:
+        g = sp.Graph.from_canonical(n, u, v, w)
+        L = sp.LaplacianOperator(g, mode, implicit=False)
+        indptr, indices, data = L.csr_host()
+        ref = O.laplacian_csr(n, g.u, g.v, g.w, mode)
+        np.testing.assert_array_equal(indptr, ref.indptr)
+        np.testing.assert_array_equal(indices, ref.indices)
+        mism = np.flatnonzero(data.view(np.uint32) != ref.data.astype(np.float32).view(np.uint32))
+        assert mism.size == 0, (mode, mism[:10])
+        np.testing.assert_array_equal(L.degrees, O.degrees(n, g.u, g.v, g.w))
+
+
+# --- polynomial apply ----------------------------------------------------------------
+
+def test_apply_vs_reference_goldens(cuda, golden):
+    sp = _sp()
+    cases = sorted({k.rsplit("/", 1)[0] for k in golden.keys("apply/")})
+    worst = 0.0
+    ops = {}
+    for case in cases:
+        _, name, mode, kind, ell, eps, k = case.split("/")
+        ell = None if ell == "None" else int(ell)
+        key = (name, mode, kind, ell, eps)
+        if key not in ops:
+            import warnings
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                ops[key] = sp.make_reversed_operator(_graph(golden, name),
+                                                     sp.SpectralTransform(kind, ell, float(eps)), mode)
+        op = ops[key]
+        assert op.lambda_star == float(golden[case + "/lambda_star"])
+        x = golden[case + "/x"]
+        y = op.apply(x.astype(np.float64))          # numpy in -> numpy out (drop-in)
+        assert isinstance(y, np.ndarray) and y.dtype == np.float64 and y.shape == x.shape
+        err = rel_fro(y, golden[case + "/y"])
+        worst = max(worst, err)
+        assert err <= PV_TOL, (case, err)
+        # device tensors in -> device tensors out
+        yd = op.apply(torch.as_tensor(x, dtype=torch.float32, device="cuda"))
+        assert yd.is_cuda and yd.dtype == torch.float32
+        assert rel_fro(yd.cpu().numpy(), golden[case + "/y"]) <= PV_TOL
+    print("worst rel Frobenius vs reference:", worst)
+
+
+@pytest.mark.parametrize("k", [1, 3, 4, 8, 10, 16, 32, 64, 128, 130, 256])
+def test_apply_all_widths_vs_oracle(cuda, k):
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.lp_sbm(3000, 10, 24.0, 0.1, 5, 0.8)
+    g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
+    csr = O.laplacian_csr(n, g.u, g.v, g.w)
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((n, k)).astype(np.float32)
+    for kind, ell in (("negexp-limit", 9), ("negexp-taylor", 6), ("identity", None)):
+        op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell))
+        ref = O.apply_transform(csr, kind, ell, 1e-6, op.lambda_star, x.astype(np.float64))
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_fro(y, ref) <= PV_TOL, (k, kind)
+
+
+@pytest.mark.parametrize("k", [16, 32, 64, 128])
+def test_long_row_chunk_path(cuda, k):
+    """Power-law graph with hubs, tiny long-row threshold: every hub row is
+    split into chunks folded by the last-arriving warp (deterministic)."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.chung_lu(20000, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    L = sp.LaplacianOperator(g, "normalized", long_threshold=64, chunk_len=48)
+    assert L.n_long_rows > 10 and L.n_chunks > L.n_long_rows
+    csr = O.laplacian_csr(n, g.u, g.v, g.w, "normalized")
+    x = np.random.default_rng(0).standard_normal((n, k)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    y1 = L.matvec(xd)
+    y2 = L.matvec(xd)
+    assert torch.equal(y1, y2)  # deterministic
+    assert rel_fro(y1.cpu().numpy(), csr @ x.astype(np.float64)) <= PV_TOL
+    t = sp.SpectralTransform("negexp-limit", 13)
+    op = sp.TransformedOperator(L, t, 0.0, 2.0)
+    ref = O.apply_transform(csr, "negexp-limit", 13, 1e-6, 0.0, x.astype(np.float64))
+    assert rel_fro(op.apply(xd).cpu().numpy(), ref) <= PV_TOL
+
+
+def test_matvec_reference_cases(cuda, golden):
+    sp = _sp()
+    L = sp.build_laplacian(sp.Graph.from_edges(2, [(0, 1)]))
+    np.testing.assert_allclose(L.matvec(np.array([1.0, -1.0])), [2, -2])
+    L = sp.build_laplacian(_graph(golden, "two_triangles_bridge"))
+    np.testing.assert_allclose(L.matvec(np.ones(6)), 0, atol=1e-6)
+    with pytest.raises(ValueError, match="dimension"):
+        L.matvec(np.ones(5))
+    g = sp.Graph.from_edges(3, [])
+    np.testing.assert_allclose(sp.build_laplacian(g).matvec(np.ones(3)), 0)
+    op = sp.make_reversed_operator(_graph(golden, "k3"), sp.SpectralTransform("identity"))
+    with pytest.raises(ValueError, match="dimension"):
+        op.apply(np.ones(4))
+    op0 = sp.make_reversed_operator(_graph(golden, "k3"), sp.SpectralTransform("negexp-taylor", 0))
+    v = np.random.default_rng(1).standard_normal(3)
+    np.testing.assert_allclose(op0.apply(v), op0.lambda_star * v + v, atol=1e-6)
+
+
+def test_exact_kinds_dense_oracle(cuda, golden):
+    sp = _sp()
+    g = _graph(golden, "k3")
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 251))
+    dense = sp.exact_transform_dense(sp.SpectralTransform("negexp"), sp.dense_laplacian(g))
+    v = np.random.default_rng(0).standard_normal(3)
+    want = -dense @ v
+    assert np.linalg.norm(op.apply(v) - want) / np.linalg.norm(want) <= 1e-2
+    lap = sp.build_laplacian(g)
+    op2 = sp.TransformedOperator(lap, sp.SpectralTransform("negexp"), 0.0, 4.0, None)
+    with pytest.raises(ValueError, match="dense"):
+        op2.apply(np.ones(3))
+
+
+# --- full BASELINE sizes: size-independent properties ------------------------------------
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_full_size_properties(cuda, cfg):
+    """At BASELINE sizes (n = 1e6 / 1e7 / 2e6): exact-row parity on a random
+    row sample (oracle SpMM restricted to the sampled rows, fp64), linearity
+    of p(L), symmetry <y, Lx> = <Ly, x>, L 1 = 0 (combinatorial), and
+    run-to-run determinism."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    spec = G.CONFIGS[cfg]
+    n, u, v, w = G.config_graph(cfg, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    mode, k, ell = spec["mode"], spec["k"], spec["ell"]
+    L = sp.LaplacianOperator(g, mode)
+    gen = torch.Generator(device="cuda").manual_seed(cfg)
+    X = torch.randn((n, k), device="cuda", generator=gen)
+    Y = torch.randn((n, k), device="cuda", generator=gen)
+    LX = L.matvec(X)
+    # row-sample parity against the oracle (fp64 on host)
+    indptr, indices, data = L.csr_host()
+    rows = np.sort(np.random.default_rng(cfg).choice(n, 2000, replace=False))
+    Xh = X.cpu().numpy().astype(np.float64)
+    ref_rows = np.stack([data[indptr[r]:indptr[r + 1]].astype(np.float64)
+                         @ Xh[indices[indptr[r]:indptr[r + 1]]] for r in rows])
+    assert rel_fro(LX[rows].cpu().numpy(), ref_rows) <= PV_TOL
+    # symmetry
+    a = float((Y.double() * LX.double()).sum())
+    b = float((L.matvec(Y).double() * X.double()).sum())
+    assert abs(a - b) <= 1e-4 * max(abs(a), 1.0)
+    if mode == "unnormalized":
+        ones = torch.ones((n, k), device="cuda")
+        assert float(L.matvec(ones).abs().max()) <= 1e-3
+    # linearity of the full polynomial
+    t = sp.SpectralTransform("negexp-limit", ell + 1)
+    op = sp.TransformedOperator(L, t, 0.0, 2.0)
+    pX, pY = op.apply(X), op.apply(Y)
+    pZ = op.apply(2.0 * X - 0.5 * Y)
+    assert rel_fro(pZ.cpu().numpy(), (2.0 * pX - 0.5 * pY).cpu().numpy()) <= 1e-5
+    assert torch.equal(op.apply(X), pX)

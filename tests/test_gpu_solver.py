@@ -1,0 +1,254 @@
+"""Device solver steps, stochastic oracle and end-to-end runs vs the
+reference goldens / oracle (run on a B200)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+def _sp():
+    import paper_2207_14589_b200 as sp
+    return sp
+
+
+def _graph(golden, name):
+    sp = _sp()
+    n, u, v, w = golden.graph(name)
+    return sp.Graph(n, u, v, w)
+
+
+# --- solver steps --------------------------------------------------------------------
+
+def test_init_state_vs_reference(cuda, golden):
+    sp = _sp()
+    for key in golden.keys("init/"):
+        _, n, k, seed = key.split("/")
+        V = sp.init_state(int(n), int(k), int(seed)).V
+        assert V.is_cuda
+        np.testing.assert_allclose(V.cpu().numpy(), golden[key], atol=2e-5, err_msg=key)
+
+
+def test_steps_vs_reference(cuda, golden):
+    sp = _sp()
+    for key in golden.keys("step/"):
+        if not key.endswith("/V0"):
+            continue
+        base = key[: -len("/V0")]
+        _, name, mode, kind, ell, k = base.split("/")
+        ell = None if ell == "None" else int(ell)
+        op = sp.make_reversed_operator(_graph(golden, name), sp.SpectralTransform(kind, ell), mode)
+        V0 = golden[key]
+        for eta in (0.05, 0.5):
+            for rule, fn in (("mueg", sp.mu_eg_step), ("oja", sp.oja_step)):
+                ref = golden[f"{base}/{rule}/{eta}"]
+                # numpy state in -> numpy out (reference-facing)
+                out = fn(sp.EigenState(V0.copy()), op, eta)
+                assert isinstance(out.V, np.ndarray) and out.step == 1
+                assert rel_fro(out.V, ref) <= 1e-5, (base, rule, eta)
+                # device state in -> device state out
+                outd = fn(sp.EigenState(torch.as_tensor(V0, dtype=torch.float32, device="cuda")),
+                          op, eta)
+                assert outd.V.is_cuda
+                assert rel_fro(outd.V.cpu().numpy(), ref) <= 1e-5, (base, rule, eta)
+
+
+def test_mu_eg_reference_behaviours(cuda):
+    sp = _sp()
+    st = sp.init_state(5, 2, seed=9)
+    nxt = sp.mu_eg_step(st, lambda V: 2 * V, eta=0.0)
+    np.testing.assert_allclose(nxt.V.cpu().numpy(), st.V.cpu().numpy(), atol=1e-6)
+    st = sp.init_state(10, 3, seed=2)
+    nxt = sp.oja_step(st, lambda V: V, eta=0.7)
+    np.testing.assert_allclose(nxt.V.cpu().numpy(), st.V.cpu().numpy(), atol=1e-5)
+    # unit-norm columns every step
+    g = sp.Graph.from_edges(6, [(0, 1), (0, 2), (1, 2), (3, 4), (3, 5), (4, 5), (2, 3)])
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("identity"))
+    st = sp.init_state(6, 3, seed=20)
+    for _ in range(25):
+        st = sp.mu_eg_step(st, op, eta=0.05)
+        np.testing.assert_allclose(torch.linalg.norm(st.V, dim=0).cpu().numpy(), 1.0, atol=1e-5)
+
+
+def test_mu_eg_known_top_two(cuda):
+    sp = _sp()
+    rng = np.random.default_rng(7)
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    M = torch.as_tensor((q * np.array([3.0, 2.0, 1.0])) @ q.T, dtype=torch.float32, device="cuda")
+    st = sp.init_state(3, 2, seed=8)
+    for _ in range(2000):
+        st = sp.mu_eg_step(st, lambda V: M @ V, eta=0.1)
+    V = st.V.cpu().numpy()
+    for i in range(2):
+        assert abs(abs(V[:, i] @ q[:, i]) - 1) < 0.01
+
+
+# --- stochastic oracle ---------------------------------------------------------------
+
+def test_device_pcg64_bit_exact(cuda, golden):
+    from paper_2207_14589_b200.sampling import pcg64_draw
+    for case in sorted({k.rsplit("/", 1)[0] for k in golden.keys("pcg/")}):
+        _, m, seed = case.split("/")
+        rng = np.random.default_rng()
+        rng.bit_generator.state = golden.state(case + "/state0")
+        i = 0
+        while f"{case}/draw{i}" in golden:
+            ref = golden[f"{case}/draw{i}"]
+            got = pcg64_draw(rng, int(m), ref.size, "cuda").cpu().numpy()
+            np.testing.assert_array_equal(got, ref, err_msg=case)
+            assert rng.bit_generator.state == golden.state(f"{case}/state{i + 1}"), case
+            i += 1
+
+
+@pytest.mark.parametrize("m,count", [(10_000_000, 16_000_000), (31_600_000, 4_000_000),
+                                     (2**31 - 1, 1_000_000), (5, 100_000)])
+def test_device_pcg64_large_streams(cuda, m, count):
+    from paper_2207_14589_b200.sampling import pcg64_draw
+    rng = np.random.default_rng(123)
+    mirror = np.random.default_rng(123)
+    for _ in range(2):
+        got = pcg64_draw(rng, m, count, "cuda").cpu().numpy()
+        ref = mirror.integers(0, m, size=count)
+        np.testing.assert_array_equal(got, ref)
+        assert rng.bit_generator.state == mirror.bit_generator.state
+
+
+@pytest.mark.parametrize("source", ["device", "host"])
+def test_identity_stochastic_oracle_vs_reference(cuda, golden, source):
+    sp = _sp()
+    for case in sorted({k.rsplit("/", 1)[0] for k in golden.keys("sto/")}):
+        _, name, B, seed = case.split("/")
+        g = _graph(golden, name)
+        op = sp.make_reversed_operator(g, sp.SpectralTransform("identity"))
+        oracle = sp.make_stochastic_oracle(op, int(B), int(seed), index_source=source)
+        x = golden[case + "/x"]
+        for call in range(3):
+            y = oracle(x)
+            np.testing.assert_array_equal(oracle.last_batch.cpu().numpy(),
+                                          golden[f"{case}/batch{call}"])
+            assert rel_fro(y, golden[f"{case}/y{call}"]) <= 1e-5, (case, call)
+
+
+def test_stochastic_single_edge_is_exact(cuda):
+    sp = _sp()
+    g = sp.Graph.from_edges(2, [(0, 1)])
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("identity"))
+    oracle = sp.make_stochastic_oracle(op, 3, seed=1)
+    v = np.array([0.4, -1.2])
+    np.testing.assert_allclose(oracle(v), op.apply(v), atol=1e-6)
+    assert sp.make_stochastic_oracle(op, 0, seed=0) == op.apply
+    op2 = sp.make_reversed_operator(g, sp.SpectralTransform("negexp"))
+    with pytest.raises(ValueError, match="polynomial"):
+        sp.make_stochastic_oracle(op2, 4, seed=0)
+
+
+@pytest.mark.parametrize("kind,ell,k", [("negexp-limit", 9, 4), ("negexp-taylor", 6, 16),
+                                        ("log-taylor", 5, 64), ("negexp-limit", 3, 128),
+                                        ("negexp-limit", 5, 10)])
+def test_edge_batch_poly_vs_restated_oracle(cuda, kind, ell, k):
+    """Per-term minibatch composition: same batches -> oracle (fp64)."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.lp_sbm(2000, 10, 24.0, 0.1, 5, 0.8)
+    g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
+    eps = 0.5 if kind == "log-taylor" else 1e-6
+    op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell, eps))
+    oracle = sp.make_stochastic_oracle(op, 5000, seed=3)
+    x = np.random.default_rng(k).standard_normal((n, k)).astype(np.float32).astype(np.float64)
+    y = oracle(x)
+    B = 5000
+    batch = oracle.last_batch.cpu().numpy().astype(np.int64)
+    batches = [batch[t * B:(t + 1) * B] for t in range(op.n_terms)]
+    ref = O.edge_batch_poly_apply(g.u, g.v, g.w, kind, ell, eps, op.lambda_star, batches, x)
+    rng = np.random.default_rng(3)
+    np.testing.assert_array_equal(np.concatenate(O.draw_batches(rng, g.m, B, op.n_terms)), batch)
+    assert rel_fro(y, ref) <= 1e-5
+    # hitw scratch left zero; repeat draws advance the stream
+    assert float(oracle.hitw.abs().max()) == 0.0
+
+
+def test_edge_batch_unbiased_on_device(cuda):
+    sp = _sp()
+    g = sp.Graph.from_edges(3, [(0, 1), (1, 2)])
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 3))
+    oracle = sp.make_stochastic_oracle(op, 2, seed=3)
+    v = torch.tensor([0.2, -0.5, 0.9], device="cuda")
+    exact = op.apply(v).cpu().numpy()
+    draws = np.stack([oracle(v).cpu().numpy() for _ in range(4000)])
+    se = draws.std(axis=0, ddof=1) / np.sqrt(draws.shape[0])
+    assert np.all(np.abs(draws.mean(axis=0) - exact) <= 3.5 * se + 1e-6)
+
+
+# --- end to end ------------------------------------------------------------------------
+
+def test_run_solver_small_graphs(cuda, golden):
+    sp = _sp()
+    k3 = _graph(golden, "k3")
+    cfg = sp.SolverConfig(k=2, steps=0, seed=0)
+    run = sp.run_solver(k3, sp.SpectralTransform("identity"), cfg)
+    assert len(run.records) == 1 and run.records[0].step == 0
+    cfg = sp.SolverConfig(k=2, steps=120, eval_every=30, seed=5)
+    a = sp.run_to_csv(sp.run_solver(k3, sp.SpectralTransform("identity"), cfg, record_timing=False))
+    b = sp.run_to_csv(sp.run_solver(k3, sp.SpectralTransform("identity"), cfg, record_timing=False))
+    assert a == b
+    cfg = sp.SolverConfig(k=2, steps=50, eval_every=10, seed=5, batch_size=2)
+    a = sp.run_to_csv(sp.run_solver(k3, sp.SpectralTransform("identity"), cfg, record_timing=False))
+    b = sp.run_to_csv(sp.run_solver(k3, sp.SpectralTransform("identity"), cfg, record_timing=False))
+    assert a == b
+    with pytest.raises(ValueError):
+        sp.run_solver(k3, sp.SpectralTransform("identity"), sp.SolverConfig(k=4, steps=1))
+
+
+def test_run_solver_cfg1_matches_reference(cuda, golden):
+    """Config 1 (SBM 10x100), mu-EG, negexp-limit(13), 1500 steps: the
+    device run reaches the reference's subspace (max principal angle
+    <= 1e-3 between the two final blocks' spans and the truth), Ritz values
+    within 1e-4 relative, and k-means labels identical to the reference's."""
+    sp = _sp()
+    g = _graph(golden, "cfg1")
+    cfg = sp.SolverConfig(solver="mu-eg", k=10, eta=0.1, steps=1500, eval_every=50, seed=5)
+    run = sp.run_solver(g, sp.SpectralTransform("negexp-limit", 13), cfg, record_timing=False)
+    V = run.V.cpu().numpy().astype(np.float64)
+    Vref = golden["run/cfg1/mu-eg/V"]
+    gt = sp.graph_ground_truth(g)
+    U = gt.bottom(10)
+    assert sp.principal_angles(V, U) <= 1e-3
+    assert sp.principal_angles(V, Vref) <= 1e-3
+    L = sp.build_laplacian(g)
+    ritz = sp.ritz_values(L, V)
+    np.testing.assert_allclose(ritz[1:], gt.eigenvalues[1:10], rtol=1e-4)
+    assert abs(ritz[0]) <= 1e-4
+    labels = sp.kmeans_cluster(V, 10, seed=5)
+    assert sp.match_labels(labels, golden["run/cfg1/mu-eg/labels"]) == 1.0
+    assert sp.match_labels(labels, np.arange(1000) // 100) == 1.0
+
+
+def test_run_solver_cuda_graph_equals_eager(cuda, golden):
+    sp = _sp()
+    g = _graph(golden, "cfg1")
+    t = sp.SpectralTransform("negexp-limit", 13)
+    cfg = sp.SolverConfig(solver="mu-eg", k=10, eta=0.1, steps=40, eval_every=20, seed=1)
+    a = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=True)
+    b = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=False)
+    assert torch.equal(a.V, b.V)
+    cfg = sp.SolverConfig(solver="oja", k=10, eta=0.1, steps=40, eval_every=20, seed=1)
+    a = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=True)
+    b = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=False)
+    assert torch.equal(a.V, b.V)
+
+
+def test_reference_solver_accepts_device_operator(cuda, golden):
+    """The drop-in seam: the device operator satisfies the duck type the
+    reference's run_solver/oja_step consume (numpy in, numpy out)."""
+    sp = _sp()
+    g = _graph(golden, "two_triangles_bridge")
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("identity"))
+    V = O.init_state(6, 2, 3)
+    for _ in range(200):
+        V = O.oja_step(V, op.apply(V), 0.5)
+    gt = sp.graph_ground_truth(g)
+    assert sp.subspace_error(V, gt, 2) <= 1e-3
