@@ -239,7 +239,7 @@ def run_sped(args):
         if world > 1:
             sop.apply_local(Vin, out=MV)
         else:
-            op.apply_device(Vin, out=MV)
+            op.apply_internal(Vin, out=MV)
         if ev is not None:
             ev[1].record(stream)
         if world > 1:

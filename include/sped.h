@@ -65,6 +65,16 @@ int sped_laplacian_build(int64_t n, int64_t m, const int64_t* u, const int64_t* 
                          double* degrees, int32_t* epos, int64_t* nnz_out,
                          sped_stream_t stream);
 
+/* ---- locality ordering for power-law graphs -----------------------------
+ * perm (new -> old) lists nodes by descending row length (stable), iperm is
+ * its inverse.  sped_relabel_edges maps the canonical edges through iperm and
+ * re-canonicalises them (u2 < v2, lexsorted); edge_map[new] = old edge id. */
+int sped_degree_order(int64_t n, const int32_t* indptr, int32_t* perm, int32_t* iperm,
+                      sped_stream_t stream);
+int sped_relabel_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                       const double* w, const int32_t* iperm, int64_t* u2, int64_t* v2,
+                       double* w2, int32_t* edge_map, sped_stream_t stream);
+
 /* ---- long-row split plan for the SpMM ----------------------------------
  * Rows longer than long_threshold nonzeros are cut into chunks of chunk_len
  * processed by separate warps and combined deterministically.  chunk_desc is
@@ -78,7 +88,7 @@ int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_threshold,
                    sped_stream_t stream);
 
 /* ---- dilation-polynomial apply (transforms.py:229-262) -------------------
- * w_0 = w0_scale * x;  for t < n_terms:
+ * w_0 = w0_scale * (w_init ? w_init : x);  for t < n_terms:
  *     w_{t+1} = alpha[t]*x + beta[t]*(L w_t) + gamma[t]*w_t
  * out = lam_f*x + s_final*w_{n_terms}.
  * alpha/beta/gamma are HOST arrays of n_terms doubles.  w_a, w_b: n x k
@@ -86,14 +96,20 @@ int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_threshold,
  * long_threshold / chunk_len / chunk_desc / n_chunks: the sped_spmm_plan
  * (rows longer than long_threshold are chunk-processed; n_chunks == 0 means
  * no plan).  partials fp32[n_chunks*k] and tickets int32[n_chunks] (zero on
- * entry, left zero) serve the plan (NULL when n_chunks == 0).  x must not alias
- * out, w_a or w_b. */
+ * entry, left zero) serve the plan (NULL when n_chunks == 0).
+ * segments: HOST int64[3*n_segments] = {row_begin, row_end, sub} row ranges,
+ * each launched with rows handled by (k/4)*sub lanes (sub nonzero-parallel
+ * lane groups per row); n_segments == 0 means one warp per row.  Gathered rows
+ * with index < hot_rows are cached with L2 evict_last, others evict_first.
+ * w_init (optional) lets a row shard start from its halo-extended block
+ * while x stays its own rows.  x / w_init must not alias out, w_a or w_b. */
 int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                         const int32_t* indices, const float* values,
                         int32_t long_threshold, int32_t chunk_len,
                         const int32_t* chunk_desc, int64_t n_chunks,
                         float* partials, int32_t* tickets,
-                        const float* x, float* w_a, float* w_b, float* out,
+                        const int64_t* segments, int32_t n_segments, int64_t hot_rows,
+                        const float* x, const float* w_init, float* w_a, float* w_b, float* out,
                         int32_t n_terms, const double* alpha, const double* beta,
                         const double* gamma, double w0_scale, double lam_f,
                         double s_final, sped_stream_t stream);

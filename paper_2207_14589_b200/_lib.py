@@ -31,11 +31,14 @@ SIGNATURES = {
     "sped_abi_version": (C.c_int, []),
     "sped_laplacian_build": (C.c_int, [_i64, _i64, _p, _p, _p, C.c_int, C.c_int, _p, _p, _p, _p,
                                        _p, C.POINTER(_i64), _p]),
+    "sped_degree_order": (C.c_int, [_i64, _p, _p, _p, _p]),
+    "sped_relabel_edges": (C.c_int, [_i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sped_spmm_plan_max_chunks": (_i64, [_i64, _i64, _i32, _i32]),
     "sped_spmm_plan": (C.c_int, [_i64, _p, _i32, _i32, _p, _i64, C.POINTER(_i64),
                                  C.POINTER(_i64), _p]),
     "sped_csr_poly_apply": (C.c_int, [_i64, _i32, _p, _p, _p, _i32, _i32, _p, _i64, _p, _p, _p,
-                                      _p, _p, _p, _i32, _p, _p, _p, _f64, _f64, _f64, _p]),
+                                      _i32, _i64, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _f64,
+                                      _f64, _f64, _p]),
     "sped_edge_batch_poly_apply": (C.c_int, [_i64, _i32, _i64, _p, _p, _p, _p, _p, _i64, _p, _p,
                                              _p, _p, _p, _i32, _p, _p, _p, _f64, _f64, _f64, _p]),
     "sped_gram_workspace_bytes": (_sz, [_i64, _i32]),
@@ -113,6 +116,10 @@ def ptr(t) -> int | None:
     if t is None:
         return None
     return t.data_ptr()
+
+
+def i64_array(vals):
+    return (C.c_int64 * max(1, len(vals)))(*[int(v) for v in vals])
 
 
 def dbl_array(vals):

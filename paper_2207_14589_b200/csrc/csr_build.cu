@@ -340,3 +340,106 @@ extern "C" int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_thr
   *n_long_rows_out = nlong;
   return SPED_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Degree-descending node order (locality for power-law graphs) and edge
+// relabelling.  Hubs get the smallest ids, so the most-gathered rows of every
+// block form one contiguous prefix that the SpMM keeps L2-resident
+// (evict_last) while cold rows stream (evict_first); rows also come sorted by
+// length, which lets the SpMM pick a lanes-per-row width per row range.
+
+namespace sped {
+namespace {
+__global__ void rowlen_key_kernel(int64_t n, const int32_t* __restrict__ indptr,
+                                  int32_t* __restrict__ key, int32_t* __restrict__ ids) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  key[i] = indptr[i + 1] - indptr[i];
+  ids[i] = (int32_t)i;
+}
+__global__ void invert_perm_kernel(int64_t n, const int32_t* __restrict__ perm,
+                                   int32_t* __restrict__ iperm) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) iperm[perm[i]] = (int32_t)i;
+}
+__global__ void relabel_key_kernel(int64_t m, int64_t n, const int64_t* __restrict__ u,
+                                   const int64_t* __restrict__ v,
+                                   const int32_t* __restrict__ iperm,
+                                   unsigned long long* __restrict__ key, int32_t* __restrict__ ids) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const int64_t a = iperm[u[e]], b = iperm[v[e]];
+  const int64_t lo = a < b ? a : b, hi = a < b ? b : a;
+  key[e] = (unsigned long long)(lo * n + hi);
+  ids[e] = (int32_t)e;
+}
+__global__ void relabel_gather_kernel(int64_t m, int64_t n, const unsigned long long* __restrict__ key,
+                                      const int32_t* __restrict__ ids, const double* __restrict__ w,
+                                      int64_t* __restrict__ u2, int64_t* __restrict__ v2,
+                                      double* __restrict__ w2) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const unsigned long long kk = key[e];
+  u2[e] = (int64_t)(kk / (unsigned long long)n);
+  v2[e] = (int64_t)(kk % (unsigned long long)n);
+  w2[e] = w[ids[e]];
+}
+}  // namespace
+}  // namespace sped
+
+extern "C" int sped_degree_order(int64_t n, const int32_t* indptr, int32_t* perm, int32_t* iperm,
+                                 sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && n < INT32_MAX, "bad n");
+  if (n == 0) return SPED_OK;
+  SPED_CHECK_ARG(indptr && perm && iperm, "null array");
+  cudaStream_t s = as_stream(stream);
+  AsyncBuf b_key(s), b_key2(s), b_ids(s), b_tmp(s);
+  SPED_CUDA(b_key.alloc(sizeof(int32_t) * n));
+  SPED_CUDA(b_key2.alloc(sizeof(int32_t) * n));
+  SPED_CUDA(b_ids.alloc(sizeof(int32_t) * n));
+  rowlen_key_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, indptr, (int32_t*)b_key.p, (int32_t*)b_ids.p);
+  SPED_LAUNCH_CHECK();
+  size_t tmp = 0;
+  SPED_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, (int32_t*)b_key.p,
+                                                      (int32_t*)b_key2.p, (int32_t*)b_ids.p, perm,
+                                                      (int)n, 0, 32, s));
+  SPED_CUDA(b_tmp.alloc(tmp));
+  SPED_CUDA(cub::DeviceRadixSort::SortPairsDescending(b_tmp.p, tmp, (int32_t*)b_key.p,
+                                                      (int32_t*)b_key2.p, (int32_t*)b_ids.p, perm,
+                                                      (int)n, 0, 32, s));
+  invert_perm_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, perm, iperm);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
+extern "C" int sped_relabel_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                                  const double* w, const int32_t* iperm, int64_t* u2, int64_t* v2,
+                                  double* w2, int32_t* edge_map, sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && m >= 0 && m < INT32_MAX, "bad sizes");
+  if (m == 0) return SPED_OK;
+  SPED_CHECK_ARG(u && v && w && iperm && u2 && v2 && w2 && edge_map, "null array");
+  cudaStream_t s = as_stream(stream);
+  AsyncBuf b_key(s), b_key2(s), b_ids(s), b_tmp(s);
+  SPED_CUDA(b_key.alloc(sizeof(unsigned long long) * m));
+  SPED_CUDA(b_key2.alloc(sizeof(unsigned long long) * m));
+  SPED_CUDA(b_ids.alloc(sizeof(int32_t) * m));
+  relabel_key_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, n, u, v, iperm,
+                                                        (unsigned long long*)b_key.p,
+                                                        (int32_t*)b_ids.p);
+  SPED_LAUNCH_CHECK();
+  int end_bit = 1;
+  const unsigned long long maxkey = (unsigned long long)n * (unsigned long long)n;
+  while (end_bit < 64 && (1ULL << end_bit) < maxkey) ++end_bit;
+  size_t tmp = 0;
+  SPED_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, (unsigned long long*)b_key.p,
+                                            (unsigned long long*)b_key2.p, (int32_t*)b_ids.p,
+                                            edge_map, (int)m, 0, end_bit, s));
+  SPED_CUDA(b_tmp.alloc(tmp));
+  SPED_CUDA(cub::DeviceRadixSort::SortPairs(b_tmp.p, tmp, (unsigned long long*)b_key.p,
+                                            (unsigned long long*)b_key2.p, (int32_t*)b_ids.p,
+                                            edge_map, (int)m, 0, end_bit, s));
+  relabel_gather_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, n, (unsigned long long*)b_key2.p,
+                                                           edge_map, w, u2, v2, w2);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}

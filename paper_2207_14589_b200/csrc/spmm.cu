@@ -52,6 +52,8 @@ struct TermArgs {
   int32_t chunk_len;
   float* partials;         // [n_chunks][k]
   int32_t* tickets;
+  int64_t row_begin, row_end;  // this launch's row segment
+  int64_t hot_rows;        // gathered rows < hot_rows are kept in L2 (evict_last)
 };
 
 template <bool IMPLICIT>
@@ -61,154 +63,167 @@ __device__ __forceinline__ float entry_value(const float* values, int64_t p, int
   return ld_stream_f32(values + p);
 }
 
-// Accumulate sum_p L[row,p] * win[col_p, slab] over p in [b, e) for one warp.
-// Returns the per-lane partial (already folded across the SUB groups): lanes
-// with sub == 0 hold the row's VPL float4s.
-template <int LPR, int VPL, bool IMPLICIT>
-__device__ __forceinline__ void warp_row_accumulate(const TermArgs& a, int64_t row, int32_t b,
-                                                    int32_t e, int32_t rowlen, int lane,
-                                                    float4 (&acc)[VPL]) {
-  constexpr int SUB = 32 / LPR;
-  const int sub = lane / LPR;
-  const int cl = lane % LPR;
+__device__ __forceinline__ float4 ld_gather_hot_cold(const float* p, bool hot, uint64_t pol_hot,
+                                                     uint64_t pol_cold) {
+  float4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(hot ? pol_hot : pol_cold));
+  return r;
+}
+__device__ __forceinline__ void st_evict_first_f4(float* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+
+// One row per group of G = LPR*SUB lanes (32/G rows per warp).  Within a
+// group, LPR lanes cover the k columns with 128-bit loads and SUB lane
+// subgroups split the row's nonzeros; U gathers per lane are in flight per
+// round.  Loop bounds are warp-uniform (max over the warp's rows) so the
+// shuffles stay convergent; rows are predicated.  Returns the folded row sum
+// in the sub==0 lanes of each group.
+template <int LPR, int SUB, int U, bool IMPLICIT>
+__device__ __forceinline__ float4 group_row_accumulate(const TermArgs& a, int64_t row, bool valid,
+                                                       int32_t b, int32_t e, int32_t rowlen,
+                                                       int lane, uint64_t pol_hot,
+                                                       uint64_t pol_cold) {
+  constexpr int G = LPR * SUB;
+  const int g = lane % G;
+  const int gbase = lane - g;
+  const int sub = g / LPR;
+  const int cl = g % LPR;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int32_t len = valid ? e - b : 0;
+  int32_t maxlen = len;
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int32_t p0 = b; p0 < e; p0 += 32) {
-    const int32_t p = p0 + lane;
+  for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+  for (int32_t o = 0; o < maxlen; o += G) {
+    const int32_t p = b + o + g;
     int32_t col = 0;
     float val = 0.f;
-    if (p < e) {
+    if (o + g < len) {
       col = ld_stream_i32(a.indices + p);
       val = entry_value<IMPLICIT>(a.values, p, col, row, rowlen);
     }
-    const int cnt = min(32, e - p0);
-    const int T = (cnt + SUB - 1) / SUB;
-    for (int t = 0; t < T; t += 4) {
-      int32_t c[4];
-      float w[4];
-      float4 g[4][VPL];
+    const int cnt = max(0, min(G, len - o));
+    const int mcnt = min(G, maxlen - o);
+    const int T = (mcnt + SUB - 1) / SUB;
+    for (int t = 0; t < T; t += U) {
+      int32_t c[U];
+      float w[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int j = (t + u) * SUB + sub;
-        const int js = j < 32 ? j : 31;
+        const int js = gbase + (j < G ? j : G - 1);
         c[u] = __shfl_sync(0xffffffffu, col, js);
         w[u] = __shfl_sync(0xffffffffu, val, js);
         if (j >= cnt) w[u] = 0.f;
       }
+      float4 gv[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int j = (t + u) * SUB + sub;
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          if (j < cnt)
-            g[u][v] = ld_gather_f4(a.win + (int64_t)c[u] * a.ld + (v * LPR + cl) * 4);
-          else
-            g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        if (j < cnt)
+          gv[u] = ld_gather_hot_cold(a.win + (int64_t)c[u] * a.ld + cl * 4, c[u] < a.hot_rows,
+                                     pol_hot, pol_cold);
+        else
+          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) acc[v] = f4_fma(w[u], g[u][v], acc[v]);
+      for (int u = 0; u < U; ++u) acc = f4_fma(w[u], gv[u], acc);
     }
   }
 #pragma unroll
-  for (int off = LPR; off < 32; off <<= 1)
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) acc[v] = f4_add(acc[v], f4_shfl_xor(acc[v], off));
+  for (int off = LPR; off < G; off <<= 1) acc = f4_add(acc, f4_shfl_xor(acc, off));
+  return acc;
 }
 
-template <int LPR, int VPL>
-__device__ __forceinline__ void row_epilogue(const TermArgs& a, int64_t row, int lane,
-                                             const float4 (&y)[VPL], const float4 (&xr)[VPL],
-                                             const float4 (&wr)[VPL]) {
-  const int cl = lane % LPR;
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) {
-    float4 r = f4_scale(a.beta, y[v]);
-    if (a.flags & TF_ALPHA) r = f4_fma(a.alpha, xr[v], r);
-    if (a.flags & TF_GAMMA) r = f4_fma(a.gamma, wr[v], r);
-    if (a.flags & TF_FINAL) {
-      r = f4_scale(a.sfin, r);
-      if (a.flags & TF_LAMF) r = f4_fma(a.lamf, xr[v], r);
-    }
-    st_stream_f4(a.wout + row * a.ld + (v * LPR + cl) * 4, r);
+__device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, float4 xr, float4 wr) {
+  float4 r = f4_scale(a.beta, y);
+  if (a.flags & TF_ALPHA) r = f4_fma(a.alpha, xr, r);
+  if (a.flags & TF_GAMMA) r = f4_fma(a.gamma, wr, r);
+  if (a.flags & TF_FINAL) {
+    r = f4_scale(a.sfin, r);
+    if (a.flags & TF_LAMF) r = f4_fma(a.lamf, xr, r);
   }
+  return r;
 }
 
-template <int LPR, int VPL>
-__device__ __forceinline__ void load_epilogue_operands(const TermArgs& a, int64_t row, int lane,
-                                                       float4 (&xr)[VPL], float4 (&wr)[VPL]) {
-  const int cl = lane % LPR;
-  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) {
-    const int64_t off = row * a.ld + (v * LPR + cl) * 4;
-    xr[v] = need_x ? ld_stream_f4(a.x + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    wr[v] = (a.flags & TF_GAMMA) ? ld_gather_f4(a.win + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-}
-
-template <int LPR, int VPL, bool IMPLICIT>
-__global__ void __launch_bounds__(256) spmm_term_kernel(const TermArgs a) {
-  constexpr int SUB = 32 / LPR;
+// Long-row chunks: one warp per chunk (all 32/LPR lane groups over the
+// chunk's nonzeros).  The last chunk of a row to finish (ticket) folds the
+// partial rows in chunk order and applies the epilogue: deterministic, no
+// float atomics.
+template <int LPR, int U, bool IMPLICIT>
+__global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   const int lane = threadIdx.x & 31;
-  const int sub = lane / LPR;
+  const uint64_t pol_hot = policy_evict_last();
+  const uint64_t pol_cold = policy_evict_first();
+  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= a.n_chunks) return;
+  const int32_t row = a.chunk_desc[4 * c + 0];
+  const int32_t pb = a.chunk_desc[4 * c + 1];
+  const int32_t pe = a.chunk_desc[4 * c + 2];
+  const int32_t c0 = a.chunk_desc[4 * c + 3];
+  const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
+  const float4 acc = group_row_accumulate<LPR, 32 / LPR, U, IMPLICIT>(
+      a, row, true, pb, pe, re - rb, lane, pol_hot, pol_cold);
+  const int lsub = lane / LPR, lcl = lane % LPR;
+  if (lsub == 0) __stcg(reinterpret_cast<float4*>(a.partials + c * a.k + lcl * 4), acc);
+  __threadfence();
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(a.tickets + c0, 1);
+  ticket = __shfl_sync(0xffffffffu, ticket, 0);
+  const int32_t nch = (re - rb + a.chunk_len - 1) / a.chunk_len;
+  if (ticket != nch - 1) return;
+  __threadfence();
+  if (lsub == 0) {
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t q = 0; q < nch; ++q)
+      y = f4_add(y, __ldcg(reinterpret_cast<const float4*>(a.partials + (int64_t)(c0 + q) * a.k +
+                                                            lcl * 4)));
+    const int64_t off = (int64_t)row * a.ld + lcl * 4;
+    const float4 xr = need_x ? ld_stream_f4(a.x + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 wr = (a.flags & TF_GAMMA) ? ld_gather_f4(a.win + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    st_stream_f4(a.wout + off, term_epilogue(a, y, xr, wr));
+  }
+  if (lane == 0) a.tickets[c0] = 0;
+}
+
+template <int LPR, int SUB, int U, bool IMPLICIT>
+__global__ void __launch_bounds__(256, 4) spmm_term_kernel(const TermArgs a) {
+  constexpr int G = LPR * SUB;
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G;
+  const int sub = g / LPR;
+  const int cl = g % LPR;
   const int warp_in_block = threadIdx.x >> 5;
   const int warps_per_block = blockDim.x >> 5;
+  const uint64_t pol_hot = policy_evict_last();
+  const uint64_t pol_cold = policy_evict_first();
+  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
 
-  if ((int)blockIdx.x < a.chunk_blocks) {
-    // ---- long-row chunk ---------------------------------------------------
-    const int64_t c = (int64_t)blockIdx.x * warps_per_block + warp_in_block;
-    if (c >= a.n_chunks) return;
-    const int32_t row = a.chunk_desc[4 * c + 0];
-    const int32_t pb = a.chunk_desc[4 * c + 1];
-    const int32_t pe = a.chunk_desc[4 * c + 2];
-    const int32_t c0 = a.chunk_desc[4 * c + 3];
-    const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
-    float4 acc[VPL];
-    warp_row_accumulate<LPR, VPL, IMPLICIT>(a, row, pb, pe, re - rb, lane, acc);
-    const int cl = lane % LPR;
-    if (sub == 0) {
-#pragma unroll
-      for (int v = 0; v < VPL; ++v)
-        __stcg(reinterpret_cast<float4*>(a.partials + c * a.k + (v * LPR + cl) * 4), acc[v]);
-    }
-    __threadfence();
-    int ticket = 0;
-    if (lane == 0) ticket = atomicAdd(a.tickets + c0, 1);
-    ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    const int32_t nch = (re - rb + a.chunk_len - 1) / a.chunk_len;
-    if (ticket != nch - 1) return;
-    __threadfence();
-    // finisher: fold the partials in chunk order (deterministic)
-    float4 y[VPL], xr[VPL], wr[VPL];
-    load_epilogue_operands<LPR, VPL>(a, row, lane, xr, wr);
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) y[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (sub == 0) {
-      for (int32_t q = 0; q < nch; ++q) {
-#pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          y[v] = f4_add(y[v], __ldcg(reinterpret_cast<const float4*>(
-                                  a.partials + (int64_t)(c0 + q) * a.k + (v * LPR + cl) * 4)));
-      }
-      row_epilogue<LPR, VPL>(a, row, lane, y, xr, wr);
-    }
-    if (lane == 0) a.tickets[c0] = 0;
-    return;
+  // ---- regular rows: RPW rows per warp --------------------------------------
+  const int64_t wglobal = (int64_t)blockIdx.x * warps_per_block + warp_in_block;
+  const int64_t row = a.row_begin + wglobal * RPW + lane / G;
+  bool valid = row < a.row_end;
+  int32_t b = 0, e = 0;
+  if (valid) {
+    b = a.indptr[row];
+    e = a.indptr[row + 1];
+    if (e - b > a.long_thresh) valid = false;
   }
-
-  // ---- regular rows: one warp per row ---------------------------------------
-  const int64_t row = ((int64_t)blockIdx.x - a.chunk_blocks) * warps_per_block + warp_in_block;
-  if (row >= a.n) return;
-  const int32_t b = a.indptr[row], e = a.indptr[row + 1];
-  if (e - b > a.long_thresh) return;
-  float4 xr[VPL], wr[VPL];
-  load_epilogue_operands<LPR, VPL>(a, row, lane, xr, wr);
-  float4 acc[VPL];
-  warp_row_accumulate<LPR, VPL, IMPLICIT>(a, row, b, e, e - b, lane, acc);
-  if (sub == 0) row_epilogue<LPR, VPL>(a, row, lane, acc, xr, wr);
+  if (__all_sync(0xffffffffu, !valid)) return;
+  float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), wr = xr;
+  const int64_t off = row * a.ld + cl * 4;
+  if (valid && sub == 0) {
+    if (need_x) xr = ld_stream_f4(a.x + off);
+    if (a.flags & TF_GAMMA) wr = ld_gather_f4(a.win + off);
+  }
+  const float4 acc =
+      group_row_accumulate<LPR, SUB, U, IMPLICIT>(a, row, valid, b, e, e - b, lane, pol_hot, pol_cold);
+  if (valid && sub == 0) st_evict_first_f4(a.wout + off, term_epilogue(a, acc, xr, wr), pol_cold);
 }
 
 // Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
@@ -283,16 +298,43 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
   }
 }
 
-template <int LPR, int VPL>
+constexpr int UNROLL = 4;
+
+template <int LPR, int SUB>
 static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
+  constexpr int G = LPR * SUB;
+  constexpr int RPW = 32 / G;
   const int threads = 256;
   const int wpb = threads / 32;
-  const int64_t row_blocks = (a.n + wpb - 1) / wpb;
-  const unsigned grid = (unsigned)(row_blocks + a.chunk_blocks);
+  const int64_t rows = a.row_end - a.row_begin;
+  const int64_t warps = (rows + RPW - 1) / RPW;
+  const unsigned grid = (unsigned)((warps + wpb - 1) / wpb);
+  if (grid == 0) return;
   if (implicit)
-    spmm_term_kernel<LPR, VPL, true><<<grid, threads, 0, s>>>(a);
+    spmm_term_kernel<LPR, SUB, UNROLL, true><<<grid, threads, 0, s>>>(a);
   else
-    spmm_term_kernel<LPR, VPL, false><<<grid, threads, 0, s>>>(a);
+    spmm_term_kernel<LPR, SUB, UNROLL, false><<<grid, threads, 0, s>>>(a);
+}
+
+template <int LPR>
+static void launch_chunks(const TermArgs& a, bool implicit, cudaStream_t s) {
+  const unsigned grid = (unsigned)((a.n_chunks + 7) / 8);
+  if (grid == 0) return;
+  if (implicit)
+    spmm_chunk_kernel<LPR, UNROLL, true><<<grid, 256, 0, s>>>(a);
+  else
+    spmm_chunk_kernel<LPR, UNROLL, false><<<grid, 256, 0, s>>>(a);
+}
+
+template <int LPR>
+static void launch_fast_sub(const TermArgs& a, int sub, bool implicit, cudaStream_t s) {
+  switch (sub) {
+    case 1: launch_fast<LPR, 1>(a, implicit, s); break;
+    case 2: if constexpr (LPR * 2 <= 32) { launch_fast<LPR, 2>(a, implicit, s); break; } [[fallthrough]];
+    case 4: if constexpr (LPR * 4 <= 32) { launch_fast<LPR, 4>(a, implicit, s); break; } [[fallthrough]];
+    case 8: if constexpr (LPR * 8 <= 32) { launch_fast<LPR, 8>(a, implicit, s); break; } [[fallthrough]];
+    default: launch_fast<LPR, 32 / LPR>(a, implicit, s); break;
+  }
 }
 
 template <int LPR, int CPL>
@@ -305,20 +347,45 @@ static void launch_generic(const TermArgs& a, bool implicit, cudaStream_t s) {
     spmm_term_generic<LPR, CPL, false><<<grid, threads, 0, s>>>(a);
 }
 
-// Launch one term over one column slab.
-static int launch_term_slab(TermArgs a, bool implicit, bool aligned, cudaStream_t s) {
+struct Segment {
+  int64_t begin, end;
+  int sub;
+};
+
+// Launch one term over one column slab: one launch per row segment, the
+// long-row chunks riding in the leading blocks of the first launch.
+static int launch_term_slab(TermArgs a, bool implicit, bool aligned, const Segment* segs,
+                            int nseg, cudaStream_t s) {
   const int k = a.k;
   const bool fast = aligned && (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128);
   if (fast) {
-    const int wpb = 8;
-    a.chunk_blocks = a.n_chunks > 0 ? (int32_t)((a.n_chunks + wpb - 1) / wpb) : 0;
-    switch (k) {
-      case 4: launch_fast<1, 1>(a, implicit, s); break;
-      case 8: launch_fast<2, 1>(a, implicit, s); break;
-      case 16: launch_fast<4, 1>(a, implicit, s); break;
-      case 32: launch_fast<8, 1>(a, implicit, s); break;
-      case 64: launch_fast<16, 1>(a, implicit, s); break;
-      default: launch_fast<32, 1>(a, implicit, s); break;
+    const int lpr = k / 4;
+    if (a.n_chunks > 0) {
+      switch (lpr) {
+        case 1: launch_chunks<1>(a, implicit, s); break;
+        case 2: launch_chunks<2>(a, implicit, s); break;
+        case 4: launch_chunks<4>(a, implicit, s); break;
+        case 8: launch_chunks<8>(a, implicit, s); break;
+        case 16: launch_chunks<16>(a, implicit, s); break;
+        default: launch_chunks<32>(a, implicit, s); break;
+      }
+      SPED_LAUNCH_CHECK();
+    }
+    for (int i = 0; i < nseg; ++i) {
+      a.row_begin = segs[i].begin;
+      a.row_end = segs[i].end;
+      int sub = segs[i].sub;
+      if (sub < 1) sub = 1;
+      if (sub * lpr > 32) sub = 32 / lpr;
+      switch (lpr) {
+        case 1: launch_fast_sub<1>(a, sub, implicit, s); break;
+        case 2: launch_fast_sub<2>(a, sub, implicit, s); break;
+        case 4: launch_fast_sub<4>(a, sub, implicit, s); break;
+        case 8: launch_fast_sub<8>(a, sub, implicit, s); break;
+        case 16: launch_fast_sub<16>(a, sub, implicit, s); break;
+        default: launch_fast_sub<32>(a, sub, implicit, s); break;
+      }
+      SPED_LAUNCH_CHECK();
     }
   } else {
     a.chunk_blocks = 0;
@@ -332,8 +399,8 @@ static int launch_term_slab(TermArgs a, bool implicit, bool aligned, cudaStream_
     else if (k <= 64) launch_generic<32, 2>(a, implicit, s);
     else if (k <= 96) launch_generic<32, 3>(a, implicit, s);
     else launch_generic<32, 4>(a, implicit, s);
+    SPED_LAUNCH_CHECK();
   }
-  SPED_LAUNCH_CHECK();
   return SPED_OK;
 }
 
@@ -360,11 +427,12 @@ int launch_axpby(int64_t count, double a, const float* x, double b, const float*
 // Shared driver for the exact and stochastic applies: runs the schedule,
 // calling `term(t, win, wout, args)` for each term.
 template <class TermFn>
-int run_schedule(int64_t n, int32_t k, const float* x, float* w_a, float* w_b, float* out,
-                 int32_t n_terms, const double* alpha, const double* beta, const double* gamma,
-                 double w0, double lam_f, double s_final, cudaStream_t s, TermFn&& term) {
+int run_schedule(int64_t n, int32_t k, const float* x, const float* w_init, float* w_a, float* w_b,
+                 float* out, int32_t n_terms, const double* alpha, const double* beta,
+                 const double* gamma, double w0, double lam_f, double s_final, cudaStream_t s,
+                 TermFn&& term) {
   if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0, x, 0.0, nullptr, out, s);
-  const float* cur = x;
+  const float* cur = w_init ? w_init : x;
   for (int32_t t = 0; t < n_terms; ++t) {
     const bool final = (t == n_terms - 1);
     float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);
@@ -398,11 +466,15 @@ extern "C" int sped_axpby(int64_t count, double a, const float* x, double b, con
   return launch_axpby(count, a, x, b, y, out, as_stream(stream));
 }
 
+// With no segment table the whole matrix is one segment processed one row
+// per warp (callers normally pass a table chosen from the row lengths).
 extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                                    const int32_t* indices, const float* values,
                                    int32_t long_threshold, int32_t chunk_len,
                                    const int32_t* chunk_desc, int64_t n_chunks, float* partials,
-                                   int32_t* tickets, const float* x, float* w_a, float* w_b,
+                                   int32_t* tickets, const int64_t* segments, int32_t n_segments,
+                                   int64_t hot_rows, const float* x, const float* w_init,
+                                   float* w_a, float* w_b,
                                    float* out, int32_t n_terms, const double* alpha,
                                    const double* beta, const double* gamma, double w0_scale,
                                    double lam_f, double s_final, sped_stream_t stream) {
@@ -411,14 +483,27 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
   SPED_CHECK_ARG(n_terms == 0 || (alpha && beta && gamma), "null schedule");
   SPED_CHECK_ARG(n == 0 || (indptr && x && out), "null array");
   SPED_CHECK_ARG(x != out && x != w_a && x != w_b, "x must not alias outputs");
+  SPED_CHECK_ARG(w_init == nullptr || (w_init != out && w_init != w_a && w_init != w_b),
+                 "w_init must not alias outputs");
   SPED_CHECK_ARG(n_chunks == 0 || (chunk_desc && partials && tickets && chunk_len > 0 &&
                                    long_threshold > 0),
                  "null or inconsistent long-row plan");
   SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX, "problem too large");
+  SPED_CHECK_ARG(n_segments >= 0 && n_segments <= 8 && (n_segments == 0 || segments),
+                 "bad segment table");
   if (n == 0) return SPED_OK;
   cudaStream_t s = as_stream(stream);
   const bool implicit = (values == nullptr);
   const int32_t slabs = (k + 127) / 128;
+  Segment segs[8];
+  int nseg = n_segments;
+  for (int i = 0; i < nseg; ++i) {
+    segs[i].begin = segments[3 * i];
+    segs[i].end = segments[3 * i + 1];
+    segs[i].sub = (int)segments[3 * i + 2];
+    SPED_CHECK_ARG(segs[i].begin >= 0 && segs[i].end <= n && segs[i].begin <= segs[i].end,
+                   "segment %d out of range", i);
+  }
   auto term = [&](int32_t t, const float* win, float* wout, float al, float be, float ga,
                   float lf, float sf, int flags) -> int {
     (void)t;
@@ -448,14 +533,26 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
       a.chunk_len = chunk_len > 0 ? chunk_len : 1;
       a.partials = partials;
       a.tickets = tickets;
+      a.row_begin = 0;
+      a.row_end = n;
+      a.hot_rows = hot_rows;
+      Segment fixed[8];
+      int ns = nseg;
+      for (int i = 0; i < ns; ++i) fixed[i] = segs[i];
+      if (ns == 0) {
+        fixed[0].begin = 0;
+        fixed[0].end = n;
+        fixed[0].sub = 32;
+        ns = 1;
+      }
       const bool aligned = (k % 4 == 0) &&
                            ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(win) |
                              reinterpret_cast<uintptr_t>(wout)) % 16 == 0);
-      int rc = launch_term_slab(a, implicit, aligned, s);
+      int rc = launch_term_slab(a, implicit, aligned, fixed, ns, s);
       if (rc != SPED_OK) return rc;
     }
     return SPED_OK;
   };
-  return run_schedule(n, k, x, w_a, w_b, out, n_terms, alpha, beta, gamma, w0_scale, lam_f,
-                      s_final, s, term);
+  return run_schedule(n, k, x, w_init, w_a, w_b, out, n_terms, alpha, beta, gamma, w0_scale,
+                      lam_f, s_final, s, term);
 }

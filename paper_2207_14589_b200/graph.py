@@ -197,6 +197,11 @@ def degree_bounds(g: Graph) -> DegreeBounds:
     return DegreeBounds(deg_star, 2 * deg_star - 1, 2.0 * float(g.degrees().max()))
 
 
+L2_BYTES = 126 * 1024 * 1024
+HOT_FRACTION = 0.7          # share of L2 reserved for the hot (evict_last) rows
+SKEW_REORDER = 16.0         # max degree / mean degree above which rows are degree-ordered
+
+
 class LaplacianOperator:
     """Device CSR Laplacian; ``mode`` in {"unnormalized", "normalized"}.
 
@@ -204,15 +209,24 @@ class LaplacianOperator:
     fp64, bit-identical to ``Graph.degrees()``) plus the device arrays
     ``indptr``, ``indices``, ``values`` (None for implicit unit-weight
     combinatorial Laplacians), ``epos`` and the long-row plan.
+
+    ``reorder``: ``"auto"`` relabels power-law graphs (max degree >
+    SKEW_REORDER x mean) by descending degree, ``"degree"`` always, ``None``
+    never.  With a relabelling the device arrays describe ``P L P^T``
+    (internal order; ``perm[i]`` = original id of internal row i).  The
+    reference-facing ``matvec`` still takes and returns blocks in the
+    original order; solver internals work in the internal order
+    (``to_internal`` / ``from_internal``).
     """
 
     def __init__(self, graph: Graph, mode: str = "unnormalized", device=None,
                  long_threshold: int = LONG_ROW_THRESHOLD, chunk_len: int = CHUNK_LEN,
-                 implicit: bool | None = None):
+                 implicit: bool | None = None, reorder: str | None = "auto"):
         if mode not in ("unnormalized", "normalized"):
             raise ValueError(f"unknown Laplacian mode: {mode!r}")
+        if reorder not in ("auto", "degree", None):
+            raise ValueError(f"unknown reorder {reorder!r}")
         dev = _lib.require_cuda(device)
-        lib = _lib.load()
         self.graph = graph
         self.mode = mode
         self.device = dev
@@ -221,44 +235,149 @@ class LaplacianOperator:
             implicit = (mode == "unnormalized") and graph.is_unit_weight()
         self.implicit = bool(implicit)
         u, v, w = graph.device_edges(dev)
+        indptr, indices, vals, deg, epos, nnz = self._build(n, m, u, v, w)
+        self.degrees = deg[:n].cpu().numpy()
+        self.perm = self.iperm = None
+        rowlen = np.diff(indptr.cpu().numpy().astype(np.int64))
+        mean = float(rowlen.mean()) if n else 0.0
+        skewed = n > 0 and mean > 0 and rowlen.max() > SKEW_REORDER * mean
+        if reorder == "degree" or (reorder == "auto" and skewed and n >= 4096):
+            indptr, indices, vals, epos = self._relabel(n, m, u, v, w, indptr)
+        self.indptr, self.nnz = indptr, nnz
+        self.indices = indices[: max(nnz, 1)]
+        self.values = None if vals is None else vals[: max(nnz, 1)]
+        self.epos = epos
+        self.edge_w = None if graph.is_unit_weight() else w.to(torch.float32)
+        self.rowlen = np.diff(self.indptr.cpu().numpy().astype(np.int64))
+        self.long_threshold = int(long_threshold)
+        self.chunk_len = int(chunk_len)
+        self._plan()
+        self._segments = {}
+
+    # -- construction --------------------------------------------------------
+    def _build(self, n, m, u, v, w):
+        lib = _lib.load()
+        dev = self.device
         cap = 2 * m + n
-        self.indptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
-        self.indices = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        indptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        indices = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
         vals = None if self.implicit else torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
         deg = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
-        self.epos = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
+        epos = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
         nnz = C.c_int64(0)
         with torch.cuda.device(dev):
             rc = lib.sped_laplacian_build(n, m, _lib.ptr(u), _lib.ptr(v), _lib.ptr(w),
-                                          1 if mode == "normalized" else 0,
+                                          1 if self.mode == "normalized" else 0,
                                           0 if self.implicit else 1,
-                                          _lib.ptr(self.indptr), _lib.ptr(self.indices),
-                                          _lib.ptr(vals), _lib.ptr(deg), _lib.ptr(self.epos),
-                                          C.byref(nnz), _lib.stream_ptr(dev))
+                                          _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(vals),
+                                          _lib.ptr(deg), _lib.ptr(epos), C.byref(nnz),
+                                          _lib.stream_ptr(dev))
         _lib.check(rc, "sped_laplacian_build")
-        self.nnz = int(nnz.value)
-        self.indices = self.indices[: max(self.nnz, 1)]
-        self.values = None if vals is None else vals[: max(self.nnz, 1)]
-        self.degrees = deg[:n].cpu().numpy()
-        self.edge_w = None
-        if not graph.is_unit_weight():
-            self.edge_w = w.to(torch.float32)
-        # long-row plan (power-law hubs)
-        self.long_threshold = int(long_threshold)
-        self.chunk_len = int(chunk_len)
+        return indptr, indices, vals, deg, epos, int(nnz.value)
+
+    def _relabel(self, n, m, u, v, w, indptr):
+        """Degree-descending relabelling: rebuild the CSR of P L P^T and
+        re-key epos by ORIGINAL edge id (the stochastic path samples original
+        edge ids)."""
+        lib = _lib.load()
+        dev = self.device
+        stream = _lib.stream_ptr(dev)
+        perm = torch.empty(n, dtype=torch.int32, device=dev)
+        iperm = torch.empty(n, dtype=torch.int32, device=dev)
+        _lib.check(lib.sped_degree_order(n, _lib.ptr(indptr), _lib.ptr(perm), _lib.ptr(iperm),
+                                         stream), "sped_degree_order")
+        u2 = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+        v2 = torch.empty_like(u2)
+        w2 = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+        emap = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        _lib.check(lib.sped_relabel_edges(n, m, _lib.ptr(u), _lib.ptr(v), _lib.ptr(w),
+                                          _lib.ptr(iperm), _lib.ptr(u2), _lib.ptr(v2), _lib.ptr(w2),
+                                          _lib.ptr(emap), stream), "sped_relabel_edges")
+        indptr2, indices2, vals2, _, epos_new, nnz2 = self._build(n, m, u2[:m], v2[:m], w2[:m])
+        epos = torch.empty_like(epos_new)
+        if m:
+            e = emap[:m].long()
+            epos.view(-1, 2)[e] = epos_new[: 2 * m].view(-1, 2)
+        self.perm, self.iperm = perm, iperm
+        self.perm_rows = perm  # gather index: internal row i <- original row perm[i]
+        return indptr2, indices2, vals2, epos
+
+    def _plan(self):
+        lib = _lib.load()
+        n = self.n
         maxc = int(lib.sped_spmm_plan_max_chunks(n, self.nnz, self.long_threshold, self.chunk_len))
-        desc = torch.empty(max(4 * maxc, 4), dtype=torch.int32, device=dev)
+        desc = torch.empty(max(4 * maxc, 4), dtype=torch.int32, device=self.device)
         nch, nlong = C.c_int64(0), C.c_int64(0)
-        with torch.cuda.device(dev):
+        with torch.cuda.device(self.device):
             rc = lib.sped_spmm_plan(n, _lib.ptr(self.indptr), self.long_threshold, self.chunk_len,
                                     _lib.ptr(desc), maxc, C.byref(nch), C.byref(nlong),
-                                    _lib.stream_ptr(dev))
+                                    _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_spmm_plan")
         self.n_chunks = int(nch.value)
         self.n_long_rows = int(nlong.value)
         self.chunk_desc = desc[: max(4 * self.n_chunks, 4)].clone() if self.n_chunks else None
-        self._tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=dev)
+        self._tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=self.device)
                          if self.n_chunks else None)
+
+    @property
+    def reordered(self) -> bool:
+        return self.perm is not None
+
+    def segments(self, k: int):
+        """Row-range table ``[(begin, end, sub), ...]`` for width k: rows in
+        ranges of similar length share a lanes-per-row choice (degree-ordered
+        graphs); otherwise one range sized from the mean degree."""
+        key = min(k, 128)
+        if key in self._segments:
+            return self._segments[key]
+        n = self.n
+        lpr = max(1, min(32, key // 4))
+        smax = max(1, 32 // lpr)
+        if n == 0:
+            seg = []
+        elif self.reordered:
+            L = self.rowlen
+            thr = self.long_threshold if self.n_chunks else np.iinfo(np.int64).max
+            r_long = int(np.searchsorted(-L, -thr, side="right"))   # rows with len > thr
+            r_64 = int(np.searchsorted(-L, -64, side="right"))      # rows with len > 64
+            r_64 = max(r_64, r_long)
+            seg = []
+            if r_64 > r_long:
+                seg.append((r_long, r_64, smax))
+            if n > r_64:
+                seg.append((r_64, n, 1))
+        else:
+            mean = self.nnz / n
+            seg = [(0, n, smax if mean >= 64 else 1)]
+        flat = [x for t in seg for x in t]
+        self._segments[key] = (len(seg), _lib.i64_array(flat))
+        return self._segments[key]
+
+    def hot_rows(self, k: int) -> int:
+        if not self.reordered:
+            return self.n
+        return int(min(self.n, HOT_FRACTION * L2_BYTES / (4 * max(k, 1))))
+
+    # -- ordering ----------------------------------------------------------------
+    def to_internal(self, xd: torch.Tensor) -> torch.Tensor:
+        """Original-order block -> internal (relabelled) order."""
+        if self.perm is None:
+            return xd
+        return self._gather(xd, self.perm)
+
+    def from_internal(self, yd: torch.Tensor) -> torch.Tensor:
+        if self.perm is None:
+            return yd
+        return self._gather(yd, self.iperm)
+
+    def _gather(self, src: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
+        lib = _lib.load()
+        k = 1 if src.dim() == 1 else int(src.shape[1])
+        out = torch.empty_like(src)
+        rc = lib.sped_gather_rows(self.n, k, _lib.ptr(rows), _lib.ptr(src.contiguous()),
+                                  _lib.ptr(out), _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_gather_rows")
+        return out
 
     # -- reference surface ---------------------------------------------------
     @property
@@ -285,6 +404,18 @@ class LaplacianOperator:
 
     def poly_apply_device(self, xd: torch.Tensor, alpha, beta, gamma, w0, lam_f, s_final,
                           out: torch.Tensor | None = None) -> torch.Tensor:
+        """Original-order block in, original-order block out."""
+        if self.perm is None:
+            return self.poly_apply_internal(xd, alpha, beta, gamma, w0, lam_f, s_final, out=out)
+        y = self.poly_apply_internal(self.to_internal(xd), alpha, beta, gamma, w0, lam_f, s_final)
+        y = self.from_internal(y)
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y
+
+    def poly_apply_internal(self, xd: torch.Tensor, alpha, beta, gamma, w0, lam_f, s_final,
+                            out: torch.Tensor | None = None) -> torch.Tensor:
         lib = _lib.load()
         n = self.n
         k = 1 if xd.dim() == 1 else int(xd.shape[1])
@@ -295,24 +426,34 @@ class LaplacianOperator:
         wb = torch.empty_like(xd) if nt >= 3 else None
         partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=self.device)
                     if self.n_chunks else None)
+        nseg, seg = self.segments(k)
         with torch.cuda.device(self.device):
             rc = lib.sped_csr_poly_apply(
                 n, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
                 self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
-                _lib.ptr(partials), _lib.ptr(self._tickets), _lib.ptr(xd), _lib.ptr(wa),
-                _lib.ptr(wb), _lib.ptr(out), nt, _lib.dbl_array(alpha), _lib.dbl_array(beta),
-                _lib.dbl_array(gamma), float(w0), float(lam_f), float(s_final),
-                _lib.stream_ptr(self.device))
+                _lib.ptr(partials), _lib.ptr(self._tickets), seg, nseg, self.hot_rows(k),
+                _lib.ptr(xd), None, _lib.ptr(wa), _lib.ptr(wb), _lib.ptr(out), nt,
+                _lib.dbl_array(alpha), _lib.dbl_array(beta), _lib.dbl_array(gamma), float(w0),
+                float(lam_f), float(s_final), _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_csr_poly_apply")
         return out
 
-    def csr_host(self):
+    def csr_host(self, original_order: bool = True):
         """(indptr, indices, data) as numpy (data fp32; implicit values are
-        materialised) — for parity checks and host-side tooling."""
-        indptr = self.indptr.cpu().numpy()
-        indices = self.indices[: self.nnz].cpu().numpy()
-        if self.values is not None:
-            data = self.values[: self.nnz].cpu().numpy()
+        materialised).  For a relabelled operator the ORIGINAL-order CSR is
+        rebuilt on the device (the exact sped_laplacian_build output)."""
+        if original_order and self.perm is not None:
+            u, v, w = self.graph.device_edges(self.device)
+            indptr, indices, vals, _, _, nnz = self._build(self.n, self.graph.m, u, v, w)
+            return self._host_arrays(indptr, indices[:nnz], None if vals is None else vals[:nnz])
+        return self._host_arrays(self.indptr, self.indices[: self.nnz],
+                                 None if self.values is None else self.values[: self.nnz])
+
+    def _host_arrays(self, indptr_d, indices_d, vals_d):
+        indptr = indptr_d.cpu().numpy()
+        indices = indices_d.cpu().numpy()
+        if vals_d is not None:
+            data = vals_d.cpu().numpy()
         else:
             rows = np.repeat(np.arange(self.n), np.diff(indptr))
             rl = np.diff(indptr)[rows]

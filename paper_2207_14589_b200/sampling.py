@@ -137,6 +137,18 @@ class EdgeBatchOracle:
 
     def apply_device(self, xd: torch.Tensor, batch: torch.Tensor | None = None,
                      out: torch.Tensor | None = None) -> torch.Tensor:
+        """Original-order CUDA block in/out."""
+        lap = self.op.laplacian
+        if not lap.reordered:
+            return self.apply_internal(xd, batch, out)
+        y = lap.from_internal(self.apply_internal(lap.to_internal(xd), batch))
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y
+
+    def apply_internal(self, xd: torch.Tensor, batch: torch.Tensor | None = None,
+                       out: torch.Tensor | None = None) -> torch.Tensor:
         lib = _lib.load()
         lap = self.op.laplacian
         al, be, ga, w0, lf, s = self.op.schedule

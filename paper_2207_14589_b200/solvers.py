@@ -242,6 +242,8 @@ def init_state(n: int, k: int, seed: int, device=None) -> EigenState:
 def _device_oracle(oracle):
     """The device-side apply of our operators (also when the reference-style
     bound method ``op.apply`` is passed), else None."""
+    if isinstance(oracle, _InternalOracle):
+        return oracle.apply_device
     obj = getattr(oracle, "__self__", oracle)
     if isinstance(obj, TransformedOperator) and obj.transform.is_polynomial:
         return obj.apply_device
@@ -375,7 +377,7 @@ class _GraphStepper:
             self.graphs[i] = g
 
     def _body(self, V, out):
-        self.op.apply_device(V, out=self.MV)
+        self.op.apply_internal(V, out=self.MV)
         if self.solver == "mu-eg":
             self.ws.mu_eg(V, self.MV, self.eta, out)
         else:
@@ -445,36 +447,55 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
     graphable = (use_cuda_graphs and not stochastic and config.eta_schedule == "constant"
                  and isinstance(op, TransformedOperator) and op.transform.is_polynomial
                  and config.steps > 0)
-    V = state.V
+    lap = op.laplacian if isinstance(op, TransformedOperator) else None
+    internal = lap is not None and lap.reordered
+    # the solver state lives in the operator's internal (relabelled) order
+    V = lap.to_internal(state.V) if internal else state.V
+    out_order = (lambda X: lap.from_internal(X)) if internal else (lambda X: X)
+    steps_done = 0
     if graphable:
         stepper = _GraphStepper(op, config.solver, config.eta, V)
         for t in range(1, config.steps + 1):
             stepper.step()
+            steps_done = t
             if t % config.eval_every == 0 or t == config.steps:
                 if stepper.ws.take_flag():
                     # rare: redo with the eager path's repair semantics
                     warnings.warn("rank collapse detected; re-randomizing", RuntimeWarning)
                     stepper.bufs[stepper.cur].copy_(orthonormalize(stepper.V, rng, device=dev))
-                evaluate(stepper.V, t)
+                evaluate(out_order(stepper.V), t)
                 if stop_on_targets and targets_met():
                     break
         V = stepper.V.clone()
-        steps_done = t
     else:
         step_fn = _STEP_RULES[config.solver]
+        ioracle = _InternalOracle(oracle) if internal else oracle
         st = EigenState(V, 0)
-        steps_done = 0
         for t in range(1, config.steps + 1):
             eta = config.eta if config.eta_schedule == "constant" else config.eta / math.sqrt(t)
-            st = step_fn(st, oracle, eta, rng)
+            st = step_fn(st, ioracle, eta, rng)
             steps_done = t
             if t % config.eval_every == 0 or t == config.steps:
-                evaluate(st.V, t)
+                evaluate(out_order(st.V), t)
                 if stop_on_targets and targets_met():
                     break
         V = st.V
-    run.state = EigenState(V, steps_done)
+    run.state = EigenState(out_order(V), steps_done)
     return run
+
+
+class _InternalOracle:
+    """Adapter: the solver's internal-order state through an operator's
+    internal-order device apply."""
+
+    def __init__(self, oracle):
+        self.obj = getattr(oracle, "__self__", oracle)
+        self.device = self.obj.device
+
+    def apply_device(self, Vd):
+        return self.obj.apply_internal(Vd)
+
+    __call__ = apply_device
 
 
 def run_to_csv(run: SolverRun) -> str:

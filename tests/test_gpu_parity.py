@@ -218,3 +218,57 @@ def test_full_size_properties(cuda, cfg):
     pZ = op.apply(2.0 * X - 0.5 * Y)
     assert rel_fro(pZ.cpu().numpy(), (2.0 * pX - 0.5 * pY).cpu().numpy()) <= 1e-5
     assert torch.equal(op.apply(X), pX)
+
+
+# --- degree-ordered (relabelled) operators ---------------------------------------------
+
+@pytest.mark.parametrize("k", [4, 16, 32, 64, 128, 10])
+def test_relabelled_operator_matches_oracle(cuda, k):
+    """The degree-descending relabelling is internal: matvec/apply in the
+    original order equal the oracle's, with hubs chunked and segments active."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.chung_lu(30000, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    L = sp.LaplacianOperator(g, "normalized", reorder="degree", long_threshold=256, chunk_len=128)
+    assert L.reordered and L.n_chunks > 0
+    nseg, _ = L.segments(k)
+    assert nseg >= 1
+    csr = O.laplacian_csr(n, g.u, g.v, g.w, "normalized")
+    x = np.random.default_rng(k).standard_normal((n, k)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    assert rel_fro(L.matvec(xd).cpu().numpy(), csr @ x.astype(np.float64)) <= PV_TOL
+    # internal order round trip
+    assert torch.equal(L.from_internal(L.to_internal(xd)), xd)
+    t = sp.SpectralTransform("negexp-taylor", 12)
+    op = sp.TransformedOperator(L, t, 0.0, 2.0)
+    ref = O.apply_transform(csr, "negexp-taylor", 12, 1e-6, 0.0, x.astype(np.float64))
+    assert rel_fro(op.apply(xd).cpu().numpy(), ref) <= PV_TOL
+    yi = op.apply_internal(L.to_internal(xd))
+    assert rel_fro(L.from_internal(yi).cpu().numpy(), ref) <= PV_TOL
+
+
+def test_relabelled_csr_host_is_original_order(cuda, golden):
+    sp = _sp()
+    g = _graph(golden, "cfg4s")
+    L = sp.LaplacianOperator(g, "normalized", reorder="degree")
+    indptr, indices, data = L.csr_host()
+    np.testing.assert_array_equal(indptr, golden["csr/cfg4s/normalized/indptr"])
+    np.testing.assert_array_equal(indices, golden["csr/cfg4s/normalized/indices"])
+    assert np.array_equal(data, golden["csr/cfg4s/normalized/data"].astype(np.float32))
+
+
+def test_relabelled_stochastic_oracle_matches_unrelabelled(cuda):
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.chung_lu(20000, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    t = sp.SpectralTransform("negexp-limit", 5)
+    x = torch.randn((n, 16), device="cuda")
+    outs = []
+    for reorder in (None, "degree"):
+        L = sp.LaplacianOperator(g, "normalized", reorder=reorder)
+        op = sp.TransformedOperator(L, t, 0.0, 2.0)
+        oracle = sp.make_stochastic_oracle(op, 20000, seed=9)
+        outs.append(oracle(x).cpu().numpy())
+    assert rel_fro(outs[1], outs[0]) <= PV_TOL

@@ -224,7 +224,9 @@ def test_run_solver_cfg1_matches_reference(cuda, golden):
     assert abs(ritz[0]) <= 1e-4
     labels = sp.kmeans_cluster(V, 10, seed=5)
     assert sp.match_labels(labels, golden["run/cfg1/mu-eg/labels"]) == 1.0
-    assert sp.match_labels(labels, np.arange(1000) // 100) == 1.0
+    # the planted blocks themselves are recovered as well as by the reference
+    ref_acc = sp.match_labels(golden["run/cfg1/mu-eg/labels"], np.arange(1000) // 100)
+    assert sp.match_labels(labels, np.arange(1000) // 100) >= ref_acc
 
 
 def test_run_solver_cuda_graph_equals_eager(cuda, golden):
@@ -252,3 +254,21 @@ def test_reference_solver_accepts_device_operator(cuda, golden):
         V = O.oja_step(V, op.apply(V), 0.5)
     gt = sp.graph_ground_truth(g)
     assert sp.subspace_error(V, gt, 2) <= 1e-3
+
+
+def test_run_solver_relabelled_operator(cuda):
+    """run_solver keeps its state in the operator's internal order; the
+    result (original order) matches the unrelabelled run."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.chung_lu(6000, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    t = sp.SpectralTransform("negexp-limit", 7)
+    runs = []
+    for reorder in (None, "degree"):
+        L = sp.LaplacianOperator(g, "normalized", reorder=reorder)
+        op = sp.TransformedOperator(L, t, 0.0, 2.0)
+        cfg = sp.SolverConfig(solver="mu-eg", k=8, eta=0.5, steps=30, eval_every=10, seed=2)
+        runs.append(sp.run_solver(g, t, cfg, mode="normalized", operator=op,
+                                  record_timing=False).V.cpu().numpy())
+    assert rel_fro(runs[1], runs[0]) <= 1e-4
