@@ -145,10 +145,11 @@ int sped_mueg_coeffs(int32_t k, const double* G, double eta, float* A, float* sc
 int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, float* T,
                     int32_t* flag, sped_stream_t stream);
 /* out = (P*A + M*B) * diag(scale).  A k x k fp32; M may be NULL; B may be
- * NULL meaning B = eta*I; scale may be NULL (ones). */
+ * NULL meaning B = eta*I; scale may be NULL (ones).  upper != 0 promises A is
+ * upper triangular (mu-EG), letting the kernel skip the zero half. */
 int sped_block_update(int64_t n, int32_t k, const float* P, const float* A,
                       const float* M, const float* B, double eta, const float* scale,
-                      float* out, sped_stream_t stream);
+                      int32_t upper, float* out, sped_stream_t stream);
 /* out = a*x + b*y elementwise over count floats (y may be NULL). */
 int sped_axpby(int64_t count, double a, const float* x, double b, const float* y,
                float* out, sped_stream_t stream);

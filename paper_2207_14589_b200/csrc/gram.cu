@@ -15,6 +15,8 @@
 // HBM/L2 bound, at k = 128 SIMT fp32 bound (the tcgen05 3xTF32 path is the
 // planned upgrade).
 
+#include <cstdlib>
+
 #include "sped_common.cuh"
 
 namespace sped {
@@ -131,12 +133,27 @@ void gram_geometry(int64_t n, int32_t k, bool with_m, int* ntiles, int* splits,
 }
 
 }  // namespace
+
+bool gram_tc_supported(int32_t k, bool with_m);
+size_t gram_tc_workspace(int64_t n, int32_t k);
+int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, void* ws,
+            cudaStream_t s);
+
+static bool use_tc(int32_t k, bool with_m) {
+  static int force_simt = -1;
+  if (force_simt < 0) {
+    const char* e = getenv("SPED_GRAM_SIMT");
+    force_simt = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !force_simt && gram_tc_supported(k, with_m);
+}
+
 }  // namespace sped
 
 using namespace sped;
 
 extern "C" size_t sped_gram_workspace_bytes(int64_t n, int32_t k) {
-  size_t best = 0;
+  size_t best = gram_tc_supported(k, true) ? gram_tc_workspace(n, k) : 0;
   for (int wm = 0; wm < 2; ++wm) {
     int ntiles, splits;
     int64_t rps;
@@ -152,6 +169,10 @@ extern "C" int sped_gram(int64_t n, int32_t k, const float* V, const float* M, d
   SPED_CHECK_ARG(n >= 1 && k >= 1 && V && G && workspace, "bad gram arguments");
   cudaStream_t s = as_stream(stream);
   const bool with_m = (M != nullptr);
+  if (use_tc(k, with_m)) {
+    SPED_CHECK_ARG(workspace_bytes >= gram_tc_workspace(n, k), "gram workspace too small");
+    return gram_tc(n, k, V, M, G, workspace, s);
+  }
   const int K2 = with_m ? 2 * k : k;
   int ntiles, splits;
   int64_t rps;

@@ -206,6 +206,114 @@ __global__ void __launch_bounds__(256) block_update_kernel(
   }
 }
 
+// Row-streaming update: one thread owns (row, 32-column block) and keeps its
+// 32 outputs in registers; the input rows are read as float4s (each thread
+// walks its row, neighbouring chunks hit L1), A / B come from shared memory
+// as float4 broadcasts.  UPPER: A is upper triangular (mu-EG: I - eta(U +
+// diag d)), so column block cb only needs rows i < 32*(cb+1).  Memory bound:
+// reads P (+ M) once, writes out once.
+template <int K, bool UPPER>
+__global__ void __launch_bounds__(256) block_update_rows(
+    int64_t n, const float* __restrict__ P, const float* __restrict__ A,
+    const float* __restrict__ M, const float* __restrict__ B, float eta,
+    const float* __restrict__ scale, float* __restrict__ out) {
+  constexpr int NB = K / 32;  // column blocks per row
+  extern __shared__ float4 rows_smem4[];
+  float* As = reinterpret_cast<float*>(rows_smem4);
+  float* Bs = As + K * K;  // only when B (dynamic size covers it)
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    As[e] = A[e];
+    if (B) Bs[e] = B[e];
+  }
+  __syncthreads();
+  const int64_t total = n * NB;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / NB;
+    const int cb = (int)(t % NB);
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    const float* prow = P + row * K;
+    const int ilim = UPPER ? 32 * (cb + 1) : K;
+#pragma unroll 1
+    for (int i4 = 0; i4 < ilim; i4 += 4) {
+      const float4 pv = __ldg(reinterpret_cast<const float4*>(prow + i4));
+      const float pvv[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* arow = As + (i4 + q) * K + cb * 32;
+#pragma unroll
+        for (int j4 = 0; j4 < 32; j4 += 4) {
+          const float4 a4 = *reinterpret_cast<const float4*>(arow + j4);
+          acc[j4 + 0] = fmaf(pvv[q], a4.x, acc[j4 + 0]);
+          acc[j4 + 1] = fmaf(pvv[q], a4.y, acc[j4 + 1]);
+          acc[j4 + 2] = fmaf(pvv[q], a4.z, acc[j4 + 2]);
+          acc[j4 + 3] = fmaf(pvv[q], a4.w, acc[j4 + 3]);
+        }
+      }
+    }
+    if (M && B) {
+      const float* mrow = M + row * K;
+      const float* Bsrc = Bs;
+#pragma unroll 1
+      for (int i4 = 0; i4 < K; i4 += 4) {
+        const float4 mv = __ldg(reinterpret_cast<const float4*>(mrow + i4));
+        const float mvv[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* brow = Bsrc + (i4 + q) * K + cb * 32;
+#pragma unroll
+          for (int j4 = 0; j4 < 32; j4 += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(brow + j4);
+            acc[j4 + 0] = fmaf(mvv[q], b4.x, acc[j4 + 0]);
+            acc[j4 + 1] = fmaf(mvv[q], b4.y, acc[j4 + 1]);
+            acc[j4 + 2] = fmaf(mvv[q], b4.z, acc[j4 + 2]);
+            acc[j4 + 3] = fmaf(mvv[q], b4.w, acc[j4 + 3]);
+          }
+        }
+      }
+    }
+    float* orow = out + row * K + cb * 32;
+    const float* mcol = M ? M + row * K + cb * 32 : nullptr;
+#pragma unroll
+    for (int j4 = 0; j4 < 32; j4 += 4) {
+      float4 r = make_float4(acc[j4], acc[j4 + 1], acc[j4 + 2], acc[j4 + 3]);
+      if (M && !B) r = f4_fma(eta, __ldg(reinterpret_cast<const float4*>(mcol + j4)), r);
+      if (scale) {
+        const float4 sc = *reinterpret_cast<const float4*>(scale + cb * 32 + j4);
+        r = make_float4(r.x * sc.x, r.y * sc.y, r.z * sc.z, r.w * sc.w);
+      }
+      *reinterpret_cast<float4*>(orow + j4) = r;
+    }
+  }
+}
+
+template <int K>
+int launch_rows(int64_t n, const float* P, const float* A, const float* M, const float* B,
+                float eta, const float* scale, float* out, bool upper, cudaStream_t s) {
+  const int64_t total = n * (K / 32);
+  const size_t smem = sizeof(float) * K * K * (B ? 2 : 1);
+  static bool attr = false;
+  if (!attr) {
+    const int maxb = (int)(sizeof(float) * K * K * 2);
+    SPED_CUDA(cudaFuncSetAttribute(block_update_rows<K, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, maxb));
+    SPED_CUDA(cudaFuncSetAttribute(block_update_rows<K, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, maxb));
+    attr = true;
+  }
+  int per_sm = (int)((200 * 1024) / (smem + 1024));
+  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * per_sm);
+  if (upper)
+    block_update_rows<K, true><<<grid, 256, smem, s>>>(n, P, A, M, B, eta, scale, out);
+  else
+    block_update_rows<K, false><<<grid, 256, smem, s>>>(n, P, A, M, B, eta, scale, out);
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
 // generic k: one thread per output element of a 32-row tile
 __global__ void __launch_bounds__(256) block_update_generic(
     int64_t n, int32_t k, const float* __restrict__ P, const float* __restrict__ A,
@@ -284,7 +392,7 @@ extern "C" int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t w
 
 extern "C" int sped_block_update(int64_t n, int32_t k, const float* P, const float* A,
                                  const float* M, const float* B, double eta, const float* scale,
-                                 float* out, sped_stream_t stream) {
+                                 int32_t upper_flag, float* out, sped_stream_t stream) {
   SPED_CHECK_ARG(n >= 0 && k >= 1 && P && A && out, "bad block_update arguments");
   SPED_CHECK_ARG(out != P && out != M, "out must not alias inputs");
   if (n == 0) return SPED_OK;
@@ -293,11 +401,12 @@ extern "C" int sped_block_update(int64_t n, int32_t k, const float* P, const flo
                          reinterpret_cast<uintptr_t>(M) | reinterpret_cast<uintptr_t>(scale)) %
                         16) == 0;
   if (aligned) {
+    const bool upper = (upper_flag != 0);
     switch (k) {
       case 16: return launch_update<16>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 32: return launch_update<32>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 64: return launch_update<64>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 128: return launch_update<128>(n, P, A, M, B, (float)eta, scale, out, s);
+      case 32: return launch_rows<32>(n, P, A, M, B, (float)eta, scale, out, upper, s);
+      case 64: return launch_rows<64>(n, P, A, M, B, (float)eta, scale, out, upper, s);
+      case 128: return launch_rows<128>(n, P, A, M, B, (float)eta, scale, out, upper, s);
       default: break;
     }
   }

@@ -51,41 +51,41 @@ inline int num_sms() {
 // being multiplied are evict_last so they stay resident in the 126 MB L2.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ int ld_stream_i32(const int32_t* p) {
   int r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
                : "=r"(r) : "l"(p), "l"(policy_evict_first()));
   return r;
 }
 __device__ __forceinline__ float ld_stream_f32(const float* p) {
   float r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
                : "=f"(r) : "l"(p), "l"(policy_evict_first()));
   return r;
 }
 __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
   float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(policy_evict_first()));
   return r;
 }
 __device__ __forceinline__ float4 ld_gather_f4(const float* p) {
   float4 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(policy_evict_last()));
   return r;
 }
 __device__ __forceinline__ float ld_gather_f32(const float* p) {
   float r;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
                : "=f"(r) : "l"(p), "l"(policy_evict_last()));
   return r;
 }

@@ -66,9 +66,9 @@ __device__ __forceinline__ float entry_value(const float* values, int64_t p, int
 __device__ __forceinline__ float4 ld_gather_hot_cold(const float* p, bool hot, uint64_t pol_hot,
                                                      uint64_t pol_cold) {
   float4 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p), "l"(hot ? pol_hot : pol_cold));
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p), "l"(hot ? pol_hot : pol_cold));
   return r;
 }
 __device__ __forceinline__ void st_evict_first_f4(float* p, float4 v, uint64_t pol) {
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
 
 constexpr int UNROLL = 4;
 
-template <int LPR, int SUB>
+template <int LPR, int SUB, int U = ((SUB == 1 && LPR <= 8) ? 8 : UNROLL)>
 static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
@@ -311,9 +311,9 @@ static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
   const unsigned grid = (unsigned)((warps + wpb - 1) / wpb);
   if (grid == 0) return;
   if (implicit)
-    spmm_term_kernel<LPR, SUB, UNROLL, true><<<grid, threads, 0, s>>>(a);
+    spmm_term_kernel<LPR, SUB, U, true><<<grid, threads, 0, s>>>(a);
   else
-    spmm_term_kernel<LPR, SUB, UNROLL, false><<<grid, threads, 0, s>>>(a);
+    spmm_term_kernel<LPR, SUB, U, false><<<grid, threads, 0, s>>>(a);
 }
 
 template <int LPR>

@@ -269,5 +269,5 @@ def sharded_mu_eg_step(op: ShardedOperator, V_own: torch.Tensor, eta: float, ws,
     rc = lib.sped_mueg_coeffs(ws.k, _lib.ptr(ws.G), float(eta), _lib.ptr(ws.A),
                               _lib.ptr(ws.scale), _lib.ptr(ws.flag), _lib.stream_ptr(ws.device))
     _lib.check(rc, "sped_mueg_coeffs")
-    ws.update(V_own, ws.A, MV, None, eta, ws.scale, out)
+    ws.update(V_own, ws.A, MV, None, eta, ws.scale, out, upper=True)
     return out

@@ -338,8 +338,8 @@ class LaplacianOperator:
         elif self.reordered:
             L = self.rowlen
             thr = self.long_threshold if self.n_chunks else np.iinfo(np.int64).max
-            r_long = int(np.searchsorted(-L, -thr, side="right"))   # rows with len > thr
-            r_64 = int(np.searchsorted(-L, -64, side="right"))      # rows with len > 64
+            r_long = int(np.searchsorted(-L, -thr, side="left"))    # rows with len > thr
+            r_64 = int(np.searchsorted(-L, -64, side="left"))       # rows with len > 64
             r_64 = max(r_64, r_long)
             seg = []
             if r_64 > r_long:

@@ -114,11 +114,11 @@ class StepWorkspace:
                            _lib.ptr(self.gram_ws), self.gram_bytes, _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_gram")
 
-    def update(self, P, A, M, B, eta, scale, out):
+    def update(self, P, A, M, B, eta, scale, out, upper=False):
         lib = _lib.load()
         rc = lib.sped_block_update(self.n, self.k, _lib.ptr(P), _lib.ptr(A), _lib.ptr(M),
-                                   _lib.ptr(B), float(eta), _lib.ptr(scale), _lib.ptr(out),
-                                   _lib.stream_ptr(self.device))
+                                   _lib.ptr(B), float(eta), _lib.ptr(scale), int(upper),
+                                   _lib.ptr(out), _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_block_update")
 
     def oja_coeffs(self, eta, with_m, T):
@@ -136,7 +136,7 @@ class StepWorkspace:
                                   _lib.ptr(self.scale), _lib.ptr(self.flag),
                                   _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_mueg_coeffs")
-        self.update(V, self.A, MV, None, eta, self.scale, out)
+        self.update(V, self.A, MV, None, eta, self.scale, out, upper=True)
 
     def oja(self, V, MV, eta, out):
         """oja_step (solvers.py:114-118) with MGS replaced by CholQR2."""

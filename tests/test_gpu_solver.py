@@ -272,3 +272,44 @@ def test_run_solver_relabelled_operator(cuda):
         runs.append(sp.run_solver(g, t, cfg, mode="normalized", operator=op,
                                   record_timing=False).V.cpu().numpy())
     assert rel_fro(runs[1], runs[0]) <= 1e-4
+
+
+@pytest.mark.parametrize("k", [10, 16, 32, 64, 128])
+@pytest.mark.parametrize("n", [8191, 20000, 100003])
+def test_gram_kernels_vs_fp64(cuda, k, n):
+    """sped_gram (tcgen05 3xTF32 path for k in {32,64,128}, SIMT otherwise)
+    against an fp64 reference: S = V^T V, C = V^T M, Q = M^T M."""
+    from paper_2207_14589_b200.solvers import StepWorkspace
+    gen = torch.Generator(device="cuda").manual_seed(k * 7 + n)
+    V = torch.randn((n, k), device="cuda", generator=gen) / n ** 0.5
+    M = 3.0 * torch.randn((n, k), device="cuda", generator=gen) / n ** 0.5 + 0.5 * V
+    ws = StepWorkspace(n, k, torch.device("cuda"))
+    ws.gram(V, M)
+    G = ws.G.cpu().numpy()
+    Vh, Mh = V.double().cpu().numpy(), M.double().cpu().numpy()
+    for blk, ref in ((0, Vh.T @ Vh), (1, Vh.T @ Mh), (2, Mh.T @ Mh)):
+        got = G[blk * k * k:(blk + 1) * k * k].reshape(k, k)
+        scale = np.abs(ref).max()
+        assert np.abs(got - ref).max() <= 2e-6 * scale, (blk, np.abs(got - ref).max() / scale)
+    ws.gram(V)
+    S = ws.G.cpu().numpy()[: k * k].reshape(k, k)
+    assert np.abs(S - Vh.T @ Vh).max() <= 2e-6 * np.abs(Vh.T @ Vh).max()
+
+
+@pytest.mark.parametrize("k", [10, 16, 32, 64, 128])
+def test_block_update_vs_fp64(cuda, k):
+    from paper_2207_14589_b200.solvers import StepWorkspace
+    n = 50001
+    gen = torch.Generator(device="cuda").manual_seed(k)
+    P = torch.randn((n, k), device="cuda", generator=gen)
+    M = torch.randn((n, k), device="cuda", generator=gen)
+    A = torch.triu(torch.randn((k, k), device="cuda", generator=gen))
+    B = torch.randn((k, k), device="cuda", generator=gen)
+    sc = torch.rand(k, device="cuda", generator=gen) + 0.5
+    ws = StepWorkspace(n, k, torch.device("cuda"))
+    out = torch.empty_like(P)
+    Pd, Md, Ad, Bd, sd = (t.double() for t in (P, M, A, B, sc))
+    for upper, Bm, eta in ((True, None, 0.3), (False, None, 0.7), (False, B, 0.0)):
+        ws.update(P, A.contiguous(), M, Bm, eta, sc, out, upper=upper)
+        ref = (Pd @ Ad + (Md @ Bd if Bm is not None else eta * Md)) * sd
+        assert rel_fro(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-6, (upper, Bm is not None)
