@@ -5,17 +5,27 @@
 //   G = Z^T Z  (K2 x K2), contraction over the n rows.
 //
 // Operands come from ONE shared-memory tile per stage: the MMA's A = Z^T
-// (M = K2 columns of Z, MN-major) and B = Z (N = K2 columns, MN-major) read
-// the same canonical "interleaved" (no-swizzle) layout: element (row r, col
-// c) at float offset ((c/4)*KC + r)*4 + c%4, i.e. 16-byte column groups of KC
-// rows (SBO = 16*KC bytes, one K=8 block = 128 bytes).  Each thread loads
+// (M = K2 columns of Z) and B (N = K2 columns of Z) are both K-major (the
+// n-row contraction is contiguous) and read the same canonical no-swizzle
+// layout.  Per 8-row K step: 128-byte core matrices (8 columns x 4 rows),
+// the two 4-row halves of a column group 144 B apart (LBO) and column groups
+// 288 B apart (SBO), K steps padded by 32 B: the padding makes the
+// transposing stores from registers bank-conflict free (32 consecutive rows
+// of one column land in 32 different banks).  (MN-major tf32 operands read
+// back as zeros on sm_100a in our probes, tools/probe/tc_probe.cu.)  Each thread loads
 // float4s of V / M rows, splits them into tf32 hi/lo parts (cvt.rna.tf32)
 // and stores both tiles; one elected thread issues the MMAs and commits them
 // to the stage's mbarrier, which the loaders wait on before refilling it
-// (double buffering).  Rows are processed in SPLIT-row slices; each slice's
-// TMEM accumulator is drained with tcgen05.ld into an fp32 partial Gram, and
-// the partials are summed in fp64 in slice order by sped_gram's reduce
-// kernel (deterministic, and no fp32 sum spans more than SPLIT rows).
+// (double buffering).
+//
+// Precision: the tensor core accumulates in fp32 with a directed (toward
+// zero) rounding per MMA, so the error grows with the number of MMAs folded
+// into one accumulator (measured: ~8.5e-5 relative after 8192 rows).  K steps
+// are therefore spread round-robin over NACC TMEM accumulators and every
+// SPLIT rows the accumulators are drained (tcgen05.ld), summed and added in
+// fp64 into the CTA's private fp64 partial Gram; the partials are summed in
+// CTA order by the reduce kernel (deterministic).  Each fp32 accumulator then
+// folds at most 3*SPLIT/(8*NACC) MMAs (96 at k=32).
 //
 // K2 = 256 is computed as two M=128 tiles over the upper triangle:
 // rows 0..127 x cols 0..255 (TMEM cols 0..255) and rows 128..255 x cols
@@ -27,7 +37,6 @@ namespace sped {
 namespace tc {
 
 constexpr int THREADS = 128;
-constexpr int SPLIT = 8192;  // rows per accumulator slice
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -45,10 +54,10 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t sbo_bytes,
 }
 
 __host__ __device__ constexpr uint32_t instr_desc_tf32(int M, int N) {
-  // c_format F32 (1) @4, a/b format TF32 (2) @7/@10, a/b major MN (1) @15/@16,
+  // c_format F32 (1) @4, a/b format TF32 (2) @7/@10, a/b K-major (0) @15/@16,
   // n_dim = N>>3 @17, m_dim = M>>4 @24
-  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
@@ -100,22 +109,34 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+constexpr int SBO_B = 288;   // column-group (8 MN) stride, bytes
+constexpr int LBO_B = 144;   // second 4-row K half, bytes
+
 template <int K2>
 struct Cfg {
-  static constexpr int KC = (K2 == 256) ? 32 : 64;             // rows per stage
-  static constexpr int TILE_FLOATS = K2 * KC;                   // one of hi / lo
-  static constexpr int STAGE_BYTES = 2 * TILE_FLOATS * 4;       // hi + lo
-  static constexpr int TMEM_COLS = (K2 == 64) ? 64 : (K2 == 128) ? 128 : 512;
+  static constexpr int NACC = (K2 == 64) ? 4 : (K2 == 128) ? 2 : 1;  // accumulator sets
+  static constexpr int SPLIT = (K2 == 64) ? 1024 : 512;              // rows per drain
+  static constexpr int KC = (K2 == 256) ? 32 : 64;              // rows per stage
+  static constexpr int KSTEP_FLOATS = (K2 / 8) * (SBO_B / 4) + 8;  // one 8-row K step
+  static constexpr int TILE_FLOATS = (KC / 8) * KSTEP_FLOATS;    // one of hi / lo
+  static constexpr int STAGE_BYTES = 2 * TILE_FLOATS * 4;        // hi + lo
+  static constexpr int TMEM_COLS = (K2 == 64) ? 256 : (K2 == 128) ? 256 : 512;
   static constexpr int SMEM = 2 * STAGE_BYTES + 1024;
 };
 
-// Gram partials: one fp32 K2 x K2 block (upper triangle meaningful) per
-// SPLIT-row slice.
+template <int K2>
+__device__ __forceinline__ int kmaj_offset(int r, int c) {
+  // float offset of element (row r of the stage, column c)
+  return (r >> 3) * Cfg<K2>::KSTEP_FLOATS + ((r >> 2) & 1) * (LBO_B / 4) + (c >> 3) * (SBO_B / 4) +
+         (c & 7) * 4 + (r & 3);
+}
+
+// Gram partials: one fp64 K2 x K2 block (upper triangle meaningful) per CTA.
 template <int K2>
 __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(int64_t n, int32_t k,
                                                              const float* __restrict__ V,
                                                              const float* __restrict__ M,
-                                                             float* __restrict__ partial,
+                                                             double* __restrict__ partial,
                                                              int64_t nslices) {
   using C = Cfg<K2>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -145,10 +166,12 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(int64_t n, int32_t 
 
   uint32_t stage_uses[2] = {0, 0};
   uint32_t done_uses = 0;
-  const uint32_t sbo = 16u * C::KC;
+  constexpr uint32_t KSTEP_B = C::KSTEP_FLOATS * 4;
+  double* out = partial + (int64_t)blockIdx.x * K2 * K2;
+  for (int e = tid; e < K2 * K2; e += THREADS) out[e] = 0.0;
   for (int64_t slice = blockIdx.x; slice < nslices; slice += gridDim.x) {
-    const int64_t r_begin = slice * SPLIT;
-    const int64_t r_end = min(n, r_begin + SPLIT);
+    const int64_t r_begin = slice * C::SPLIT;
+    const int64_t r_end = min(n, r_begin + (int64_t)C::SPLIT);
     const int nchunks = (int)((r_end - r_begin + C::KC - 1) / C::KC);
     for (int ch = 0; ch < nchunks; ++ch) {
       const int s = ch & 1;
@@ -177,9 +200,15 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(int64_t n, int32_t 
         l.y = to_tf32(z.y - __uint_as_float(h.y));
         l.z = to_tf32(z.z - __uint_as_float(h.z));
         l.w = to_tf32(z.w - __uint_as_float(h.w));
-        const int off = (g * C::KC + r) * 4;
-        *reinterpret_cast<uint4*>(hi + off) = h;
-        *reinterpret_cast<uint4*>(lo + off) = l;
+        const int off = kmaj_offset<K2>(r, c);
+        hi[off] = __uint_as_float(h.x);
+        hi[off + 4] = __uint_as_float(h.y);
+        hi[off + 8] = __uint_as_float(h.z);
+        hi[off + 12] = __uint_as_float(h.w);
+        lo[off] = __uint_as_float(l.x);
+        lo[off + 4] = __uint_as_float(l.y);
+        lo[off + 8] = __uint_as_float(l.z);
+        lo[off + 12] = __uint_as_float(l.w);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
@@ -188,28 +217,30 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(int64_t n, int32_t 
         const uint32_t hi_a = smem_u32(hi), lo_a = smem_u32(lo);
 #pragma unroll
         for (int kb = 0; kb < C::KC / 8; ++kb) {
-          const uint32_t acc0 = (ch > 0 || kb > 0) ? 1u : 0u;
+          const int gk = ch * (C::KC / 8) + kb;              // K step within the slice
+          const uint32_t acc0 = (gk >= C::NACC) ? 1u : 0u;   // first use of this accumulator
+          const uint32_t tacc = tmem + (uint32_t)((gk % C::NACC) * K2);
           if (K2 <= 128) {
             constexpr int MM = K2;
             constexpr uint32_t idesc = instr_desc_tf32(MM, K2);
-            const uint64_t dh = smem_desc(hi_a + kb * 128, sbo, 128);
-            const uint64_t dl = smem_desc(lo_a + kb * 128, sbo, 128);
-            mma_tf32(tmem, dh, dh, idesc, acc0);
-            mma_tf32(tmem, dh, dl, idesc, 1u);
-            mma_tf32(tmem, dl, dh, idesc, 1u);
+            const uint64_t dh = smem_desc(hi_a + kb * KSTEP_B, SBO_B, LBO_B);
+            const uint64_t dl = smem_desc(lo_a + kb * KSTEP_B, SBO_B, LBO_B);
+            mma_tf32(tacc, dh, dh, idesc, acc0);
+            mma_tf32(tacc, dh, dl, idesc, 1u);
+            mma_tf32(tacc, dl, dh, idesc, 1u);
           } else {
             // tile 0: rows 0..127 x cols 0..255
             constexpr uint32_t id0 = instr_desc_tf32(128, 256);
-            const uint64_t ah0 = smem_desc(hi_a + kb * 128, sbo, 128);
-            const uint64_t al0 = smem_desc(lo_a + kb * 128, sbo, 128);
+            const uint64_t ah0 = smem_desc(hi_a + kb * KSTEP_B, SBO_B, LBO_B);
+            const uint64_t al0 = smem_desc(lo_a + kb * KSTEP_B, SBO_B, LBO_B);
             mma_tf32(tmem, ah0, ah0, id0, acc0);
             mma_tf32(tmem, ah0, al0, id0, 1u);
             mma_tf32(tmem, al0, ah0, id0, 1u);
-            // tile 1: rows 128..255 x cols 128..255 (column groups 32..63)
+            // tile 1: rows 128..255 x cols 128..255 (column groups 16..31)
             constexpr uint32_t id1 = instr_desc_tf32(128, 128);
-            const uint32_t goff = 32u * sbo;
-            const uint64_t ah1 = smem_desc(hi_a + goff + kb * 128, sbo, 128);
-            const uint64_t al1 = smem_desc(lo_a + goff + kb * 128, sbo, 128);
+            const uint32_t goff = 16u * SBO_B;
+            const uint64_t ah1 = smem_desc(hi_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
+            const uint64_t al1 = smem_desc(lo_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
             mma_tf32(tmem + 256, ah1, ah1, id1, acc0);
             mma_tf32(tmem + 256, ah1, al1, id1, 1u);
             mma_tf32(tmem + 256, al1, ah1, id1, 1u);
@@ -224,41 +255,34 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(int64_t n, int32_t 
     mbar_wait(&done_bar, done_uses & 1);
     done_uses += 1;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float* out = partial + slice * (int64_t)K2 * K2;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    if (K2 == 64) {
-      // M = 64: row m lives in lane (m % 16) + 32 * (m / 16)
-      const int m = warp * 16 + lane;
-      for (int c0 = 0; c0 < K2; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + lane_base + c0, v);
-        if (lane < 16) {
+    // sum the NACC accumulators (fp64) and add into this CTA's fp64 partial
+    const int nk = min(C::NACC, (int)((r_end - r_begin + 7) / 8));
+    auto drain = [&](uint32_t tcol, int row, int col0, int ncols, bool valid) {
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
+        double acc[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) out[m * K2 + c0 + i] = v[i];
+        for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+        for (int a = 0; a < nk; ++a) {
+          float v[16];
+          tmem_ld16(tmem + tcol + (uint32_t)(a * K2) + lane_base + c0, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] += (double)v[i];
+        }
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) out[row * K2 + col0 + c0 + i] += acc[i];
         }
       }
+    };
+    if (K2 == 64) {
+      // M = 64: row m lives in lane (m % 16) + 32 * (m / 16)
+      drain(0, warp * 16 + lane, 0, K2, lane < 16);
     } else if (K2 == 128) {
-      const int m = warp * 32 + lane;
-      for (int c0 = 0; c0 < K2; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + lane_base + c0, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) out[m * K2 + c0 + i] = v[i];
-      }
+      drain(0, warp * 32 + lane, 0, K2, true);
     } else {
-      const int m = warp * 32 + lane;
-      for (int c0 = 0; c0 < 256; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + lane_base + c0, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) out[m * K2 + c0 + i] = v[i];
-      }
-      for (int c0 = 0; c0 < 128; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + 256 + lane_base + c0, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) out[(128 + m) * K2 + 128 + c0 + i] = v[i];
-      }
+      drain(0, warp * 32 + lane, 0, 256, true);
+      drain(256, 128 + warp * 32 + lane, 128, 128, true);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -272,15 +296,15 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(int64_t n, int32_t 
   }
 }
 
-// Sum slice partials in fp64 (slice order) and scatter into S / C / Q.
+// Sum the per-CTA fp64 partials (CTA order) and scatter into S / C / Q.
 __global__ void gram_tc_reduce(int32_t k, int32_t K2, int64_t nslices,
-                               const float* __restrict__ partial, double* __restrict__ G) {
+                               const double* __restrict__ partial, double* __restrict__ G) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= K2 * K2) return;
   const int i = e / K2, j = e % K2;
   if (j < i) return;
   double s = 0.0;
-  for (int64_t sl = 0; sl < nslices; ++sl) s += (double)partial[sl * K2 * K2 + e];
+  for (int64_t sl = 0; sl < nslices; ++sl) s += partial[sl * K2 * K2 + e];
   auto put = [&](int a, int b) {
     if (a < k && b < k) G[a * k + b] = s;
     else if (a < k) G[k * k + a * k + (b - k)] = s;
@@ -291,7 +315,10 @@ __global__ void gram_tc_reduce(int32_t k, int32_t K2, int64_t nslices,
 }
 
 template <int K2>
-int launch(int64_t n, int32_t k, const float* V, const float* M, double* G, float* partial,
+constexpr int grid_per_sm() { return K2 == 64 ? 2 : 1; }
+
+template <int K2>
+int launch(int64_t n, int32_t k, const float* V, const float* M, double* G, double* partial,
            cudaStream_t s) {
   using C = Cfg<K2>;
   static bool attr = false;
@@ -300,12 +327,11 @@ int launch(int64_t n, int32_t k, const float* V, const float* M, double* G, floa
                                    C::SMEM));
     attr = true;
   }
-  const int64_t nslices = (n + SPLIT - 1) / SPLIT;
-  const int per_sm = (K2 == 256) ? 1 : (K2 == 128 ? 2 : 3);
-  const unsigned grid = (unsigned)std::min<int64_t>(nslices, (int64_t)num_sms() * per_sm);
+  const int64_t nslices = (n + C::SPLIT - 1) / C::SPLIT;
+  const unsigned grid = (unsigned)std::min<int64_t>(nslices, (int64_t)num_sms() * grid_per_sm<K2>());
   gram_tc_kernel<K2><<<grid, THREADS, C::SMEM, s>>>(n, k, V, M, partial, nslices);
   SPED_LAUNCH_CHECK();
-  gram_tc_reduce<<<(K2 * K2 + 255) / 256, 256, 0, s>>>(k, K2, nslices, partial, G);
+  gram_tc_reduce<<<(K2 * K2 + 255) / 256, 256, 0, s>>>(k, K2, (int64_t)grid, partial, G);
   SPED_LAUNCH_CHECK();
   return SPED_OK;
 }
@@ -315,14 +341,14 @@ int launch(int64_t n, int32_t k, const float* V, const float* M, double* G, floa
 bool gram_tc_supported(int32_t k, bool with_m) { return with_m && (k == 32 || k == 64 || k == 128); }
 
 size_t gram_tc_workspace(int64_t n, int32_t k) {
+  (void)n;
   const int K2 = 2 * k;
-  const int64_t nslices = (n + tc::SPLIT - 1) / tc::SPLIT;
-  return sizeof(float) * (size_t)nslices * K2 * K2 + 256;
+  return sizeof(double) * (size_t)num_sms() * 2 * K2 * K2 + 256;
 }
 
 int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, void* ws,
             cudaStream_t s) {
-  float* partial = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  double* partial = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   switch (k) {
     case 32: return tc::launch<64>(n, k, V, M, G, partial, s);
     case 64: return tc::launch<128>(n, k, V, M, G, partial, s);
