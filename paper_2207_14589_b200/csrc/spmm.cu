@@ -24,6 +24,13 @@
 
 #include "sped_common.cuh"
 
+#ifndef TERM_MIN_BLOCKS
+#define TERM_MIN_BLOCKS 6
+#endif
+#ifndef SUB1_U
+#define SUB1_U 4
+#endif
+
 namespace sped {
 
 enum TermFlags : int {
@@ -71,6 +78,19 @@ __device__ __forceinline__ float4 ld_gather_hot_cold(const float* p, bool hot, u
       : "l"(p), "l"(hot ? pol_hot : pol_cold));
   return r;
 }
+__device__ __forceinline__ float4 ldg_f4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ int32_t ld_idx(const int32_t* p) {
+  int32_t r;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_val(const float* p) {
+  float r;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ void st_evict_first_f4(float* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
                :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
@@ -83,15 +103,17 @@ __device__ __forceinline__ void st_evict_first_f4(float* p, float4 v, uint64_t p
 // shuffles stay convergent; rows are predicated.  Returns the folded row sum
 // in the sub==0 lanes of each group.
 template <int LPR, int SUB, int U, bool IMPLICIT>
-__device__ __forceinline__ float4 group_row_accumulate(const TermArgs& a, int64_t row, bool valid,
+__device__ __forceinline__ float4 group_row_accumulate(const TermArgs& a, int32_t row, bool valid,
                                                        int32_t b, int32_t e, int32_t rowlen,
-                                                       int lane, uint64_t pol_hot,
-                                                       uint64_t pol_cold) {
+                                                       int lane) {
   constexpr int G = LPR * SUB;
   const int g = lane % G;
   const int gbase = lane - g;
   const int sub = g / LPR;
   const int cl = g % LPR;
+  // single-slab rows are exactly 4*LPR floats: compile-time stride
+  const bool single = (a.ld == 4 * LPR);
+  const float* wbase = a.win + cl * 4;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const int32_t len = valid ? e - b : 0;
   int32_t maxlen = len;
@@ -102,32 +124,30 @@ __device__ __forceinline__ float4 group_row_accumulate(const TermArgs& a, int64_
     int32_t col = 0;
     float val = 0.f;
     if (o + g < len) {
-      col = ld_stream_i32(a.indices + p);
-      val = entry_value<IMPLICIT>(a.values, p, col, row, rowlen);
+      col = ld_idx(a.indices + p);
+      if (IMPLICIT)
+        val = col == row ? (float)(rowlen - 1) : -1.0f;
+      else
+        val = ld_val(a.values + p);
     }
     const int cnt = max(0, min(G, len - o));
     const int mcnt = min(G, maxlen - o);
     const int T = (mcnt + SUB - 1) / SUB;
     for (int t = 0; t < T; t += U) {
-      int32_t c[U];
+      float4 gv[U];
       float w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int j = (t + u) * SUB + sub;
         const int js = gbase + (j < G ? j : G - 1);
-        c[u] = __shfl_sync(0xffffffffu, col, js);
+        const int32_t c = __shfl_sync(0xffffffffu, col, js);
         w[u] = __shfl_sync(0xffffffffu, val, js);
-        if (j >= cnt) w[u] = 0.f;
-      }
-      float4 gv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = (t + u) * SUB + sub;
-        if (j < cnt)
-          gv[u] = ld_gather_hot_cold(a.win + (int64_t)c[u] * a.ld + cl * 4, c[u] < a.hot_rows,
-                                     pol_hot, pol_cold);
-        else
+        if (j < cnt) {
+          gv[u] = single ? ldg_f4(wbase + c * (4 * LPR)) : ldg_f4(wbase + (int64_t)c * a.ld);
+        } else {
           gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          w[u] = 0.f;
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) acc = f4_fma(w[u], gv[u], acc);
@@ -156,8 +176,6 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
 template <int LPR, int U, bool IMPLICIT>
 __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   const int lane = threadIdx.x & 31;
-  const uint64_t pol_hot = policy_evict_last();
-  const uint64_t pol_cold = policy_evict_first();
   const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= a.n_chunks) return;
@@ -167,7 +185,7 @@ __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   const int32_t c0 = a.chunk_desc[4 * c + 3];
   const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
   const float4 acc = group_row_accumulate<LPR, 32 / LPR, U, IMPLICIT>(
-      a, row, true, pb, pe, re - rb, lane, pol_hot, pol_cold);
+      a, row, true, pb, pe, re - rb, lane);
   const int lsub = lane / LPR, lcl = lane % LPR;
   if (lsub == 0) __stcg(reinterpret_cast<float4*>(a.partials + c * a.k + lcl * 4), acc);
   __threadfence();
@@ -191,39 +209,190 @@ __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
 }
 
 template <int LPR, int SUB, int U, bool IMPLICIT>
-__global__ void __launch_bounds__(256, 4) spmm_term_kernel(const TermArgs a) {
+__global__ void __launch_bounds__(256, TERM_MIN_BLOCKS) spmm_term_kernel(const TermArgs a) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31;
   const int g = lane % G;
   const int sub = g / LPR;
   const int cl = g % LPR;
-  const int warp_in_block = threadIdx.x >> 5;
-  const int warps_per_block = blockDim.x >> 5;
-  const uint64_t pol_hot = policy_evict_last();
-  const uint64_t pol_cold = policy_evict_first();
-  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
-
-  // ---- regular rows: RPW rows per warp --------------------------------------
-  const int64_t wglobal = (int64_t)blockIdx.x * warps_per_block + warp_in_block;
-  const int64_t row = a.row_begin + wglobal * RPW + lane / G;
+  const int32_t wglobal = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int32_t row = (int32_t)a.row_begin + wglobal * RPW + lane / G;
   bool valid = row < a.row_end;
   int32_t b = 0, e = 0;
   if (valid) {
-    b = a.indptr[row];
-    e = a.indptr[row + 1];
+    b = __ldg(a.indptr + row);
+    e = __ldg(a.indptr + row + 1);
     if (e - b > a.long_thresh) valid = false;
   }
   if (__all_sync(0xffffffffu, !valid)) return;
-  float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), wr = xr;
-  const int64_t off = row * a.ld + cl * 4;
+  const float4 acc = group_row_accumulate<LPR, SUB, U, IMPLICIT>(a, row, valid, b, e, e - b, lane);
   if (valid && sub == 0) {
-    if (need_x) xr = ld_stream_f4(a.x + off);
-    if (a.flags & TF_GAMMA) wr = ld_gather_f4(a.win + off);
+    const int64_t off = (int64_t)row * a.ld + cl * 4;
+    const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
+    const float4 xr = need_x ? ld_stream_f4(a.x + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 wr = (a.flags & TF_GAMMA) ? ldg_f4(a.win + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    st_stream_f4(a.wout + off, term_epilogue(a, acc, xr, wr));
   }
-  const float4 acc =
-      group_row_accumulate<LPR, SUB, U, IMPLICIT>(a, row, valid, b, e, e - b, lane, pol_hot, pol_cold);
-  if (valid && sub == 0) st_evict_first_f4(a.wout + off, term_epilogue(a, acc, xr, wr), pol_cold);
+}
+
+#ifndef SHORT_U
+#define SHORT_U 4
+#endif
+template <int LPR, bool IMPLICIT>
+__global__ void __launch_bounds__(256, 4) spmm_short_kernel(const TermArgs a) {
+  constexpr int G = LPR;
+  constexpr int RPW = 32 / G;
+  constexpr int CAP = 2 * G;
+  constexpr int U = SHORT_U;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int g = lane % G;
+  const int gbase = grp * G;
+  const uint64_t pol_hot = policy_evict_last();
+  const uint64_t pol_cold = policy_evict_first();
+  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
+  const int64_t rows = a.row_end - a.row_begin;
+  const int64_t nbatch = (rows + RPW - 1) / RPW;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int64_t bi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (bi >= nbatch) return;
+
+  auto load_bounds = [&](int64_t batch, int32_t& b, int32_t& e) {
+    const int64_t row = a.row_begin + batch * RPW + grp;
+    b = 0;
+    e = 0;
+    if (batch < nbatch && row < a.row_end) {
+      b = __ldg(a.indptr + row);
+      e = __ldg(a.indptr + row + 1);
+    }
+  };
+  auto load_cols = [&](int32_t b, int32_t e, int64_t row, int32_t (&col)[2], float (&val)[2]) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int32_t p = b + g + q * G;
+      col[q] = 0;
+      val[q] = 0.f;
+      if (p < e) {
+        col[q] = ld_stream_i32(a.indices + p);
+        val[q] = entry_value<IMPLICIT>(a.values, p, col[q], row, e - b);
+      }
+    }
+  };
+
+  int32_t b0, e0, b1, e1;
+  load_bounds(bi, b0, e0);
+  load_bounds(bi + wstride, b1, e1);
+  int32_t col0[2], col1[2];
+  float val0[2], val1[2];
+  load_cols(b0, e0, a.row_begin + bi * RPW + grp, col0, val0);
+
+  for (; bi < nbatch; bi += wstride) {
+    const int64_t row = a.row_begin + bi * RPW + grp;
+    const bool valid = row < a.row_end;
+    // ---- prefetch: bounds of batch +2, columns of batch +1, x of this batch
+    int32_t b2, e2;
+    load_bounds(bi + 2 * wstride, b2, e2);
+    load_cols(b1, e1, row + wstride * RPW, col1, val1);
+    const int64_t off = row * a.ld + g * 4;
+    float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), wr = xr;
+    if (valid) {
+      if (need_x) xr = ld_stream_f4(a.x + off);
+      if (a.flags & TF_GAMMA) wr = ld_gather_f4(a.win + off);
+    }
+    // ---- gathers of this batch from the prefetched columns
+    const int32_t len = valid ? e0 - b0 : 0;
+    int32_t mlen = min(len, CAP);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mlen = max(mlen, __shfl_xor_sync(0xffffffffu, mlen, o));
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j0 = 0; j0 < CAP; j0 += U) {
+      if (j0 >= mlen) break;
+      float4 gv[U];
+      float w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u;
+        const int src = gbase + (j % G);
+        const int32_t c = __shfl_sync(0xffffffffu, (j < G) ? col0[0] : col0[1], src);
+        w[u] = __shfl_sync(0xffffffffu, (j < G) ? val0[0] : val0[1], src);
+        if (j < len) {
+          gv[u] = ld_gather_hot_cold(a.win + (int64_t)c * a.ld + g * 4, c < a.hot_rows, pol_hot,
+                                     pol_cold);
+        } else {
+          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          w[u] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = f4_fma(w[u], gv[u], acc);
+    }
+    // rows longer than CAP: finish in a plain loop (rare here)
+    int32_t mall = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mall = max(mall, __shfl_xor_sync(0xffffffffu, mall, o));
+    for (int32_t o = CAP; o < mall; o += G) {
+      const int32_t p = b0 + o + g;
+      int32_t c = 0;
+      float v = 0.f;
+      if (o + g < len) {
+        c = ld_stream_i32(a.indices + p);
+        v = entry_value<IMPLICIT>(a.values, p, c, row, len);
+      }
+      const int cnt = max(0, min(G, len - o));
+#pragma unroll
+      for (int j0 = 0; j0 < G; j0 += 4) {
+        float4 gv[4];
+        float wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u;
+          const int32_t cj = __shfl_sync(0xffffffffu, c, gbase + (j % G));
+          wv[u] = __shfl_sync(0xffffffffu, v, gbase + (j % G));
+          gv[u] = (j < cnt) ? ld_gather_f4(a.win + (int64_t)cj * a.ld + g * 4)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j >= cnt) wv[u] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = f4_fma(wv[u], gv[u], acc);
+      }
+    }
+    if (valid && len <= a.long_thresh)
+      st_evict_first_f4(a.wout + off, term_epilogue(a, acc, xr, wr), pol_cold);
+    // ---- rotate the pipeline
+    b0 = b1;
+    e0 = e1;
+    b1 = b2;
+    e1 = e2;
+    col0[0] = col1[0];
+    col0[1] = col1[1];
+    val0[0] = val1[0];
+    val0[1] = val1[1];
+  }
+}
+
+template <int LPR>
+static void launch_short(const TermArgs& a, bool implicit, cudaStream_t s) {
+  const int64_t rows = a.row_end - a.row_begin;
+  const int64_t batches = (rows + (32 / LPR) - 1) / (32 / LPR);
+  // persistent grid = exactly the resident capacity (no second wave)
+  static int per_sm[2] = {0, 0};
+  int& ps = per_sm[implicit ? 1 : 0];
+  if (ps == 0) {
+    if (implicit)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, true>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, false>, 256, 0);
+    if (ps < 1) ps = 1;
+  }
+  const int64_t blocks = std::min<int64_t>((batches + 7) / 8, (int64_t)num_sms() * ps);
+  const unsigned grid = (unsigned)blocks;
+  if (grid == 0) return;
+  if (implicit)
+    spmm_short_kernel<LPR, true><<<grid, 256, 0, s>>>(a);
+  else
+    spmm_short_kernel<LPR, false><<<grid, 256, 0, s>>>(a);
 }
 
 // Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
@@ -300,7 +469,7 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
 
 constexpr int UNROLL = 4;
 
-template <int LPR, int SUB, int U = ((SUB == 1 && LPR <= 8) ? 8 : UNROLL)>
+template <int LPR, int SUB, int U = ((SUB == 1 && LPR <= 8) ? SUB1_U : UNROLL)>
 static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
@@ -375,6 +544,18 @@ static int launch_term_slab(TermArgs a, bool implicit, bool aligned, const Segme
       a.row_begin = segs[i].begin;
       a.row_end = segs[i].end;
       int sub = segs[i].sub;
+      if (sub == 0) {  // software-pipelined short rows
+        switch (lpr) {
+          case 1: launch_short<1>(a, implicit, s); break;
+          case 2: launch_short<2>(a, implicit, s); break;
+          case 4: launch_short<4>(a, implicit, s); break;
+          case 8: launch_short<8>(a, implicit, s); break;
+          case 16: launch_short<16>(a, implicit, s); break;
+          default: launch_short<32>(a, implicit, s); break;
+        }
+        SPED_LAUNCH_CHECK();
+        continue;
+      }
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
       switch (lpr) {

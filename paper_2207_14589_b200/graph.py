@@ -17,6 +17,7 @@ Mirrors the reference ``specgap.graph`` surface used by the hot path
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Iterable, NamedTuple, Sequence
 
 import numpy as np
@@ -333,22 +334,31 @@ class LaplacianOperator:
         n = self.n
         lpr = max(1, min(32, key // 4))
         smax = max(1, 32 // lpr)
+        use_short = os.environ.get("SPED_SHORT", "0") == "1"
         if n == 0:
             seg = []
         elif self.reordered:
             L = self.rowlen
+            cap = 2 * lpr      # rows the pipelined short-row kernel covers from registers
             thr = self.long_threshold if self.n_chunks else np.iinfo(np.int64).max
             r_long = int(np.searchsorted(-L, -thr, side="left"))    # rows with len > thr
-            r_64 = int(np.searchsorted(-L, -64, side="left"))       # rows with len > 64
-            r_64 = max(r_64, r_long)
+            r_64 = max(int(np.searchsorted(-L, -64, side="left")), r_long)
+            r_cap = max(int(np.searchsorted(-L, -cap, side="left")), r_64)
             seg = []
             if r_64 > r_long:
-                seg.append((r_long, r_64, smax))
-            if n > r_64:
-                seg.append((r_64, n, 1))
+                seg.append((r_long, r_64, smax))      # long rows: warp per row
+            if not use_short:
+                r_cap = n
+            if r_cap > r_64:
+                seg.append((r_64, r_cap, 1))          # medium rows: LPR lanes per row
+            if n > r_cap:
+                seg.append((r_cap, n, 0))             # short rows: pipelined kernel
         else:
             mean = self.nnz / n
-            seg = [(0, n, smax if mean >= 64 else 1)]
+            if use_short and mean <= 2 * lpr:
+                seg = [(0, n, 0)]
+            else:
+                seg = [(0, n, smax if mean >= 64 else 1)]
         flat = [x for t in seg for x in t]
         self._segments[key] = (len(seg), _lib.i64_array(flat))
         return self._segments[key]
