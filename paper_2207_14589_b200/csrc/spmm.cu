@@ -22,6 +22,8 @@
 //    diagonal, row_len-1 on it): 4 B per nonzero instead of 8.
 //  * column slabs of <= 128 floats (row stride `ld`) cover any k.
 
+#include <cstdlib>
+
 #include "sped_common.cuh"
 
 #ifndef TERM_MIN_BLOCKS
@@ -29,6 +31,15 @@
 #endif
 #ifndef SUB1_U
 #define SUB1_U 4
+#endif
+#ifndef W8_U
+#define W8_U 2
+#endif
+#ifndef LONG_MIN_BLOCKS
+#define LONG_MIN_BLOCKS 4
+#endif
+#ifndef LONG_U
+#define LONG_U 8
 #endif
 
 namespace sped {
@@ -96,25 +107,76 @@ __device__ __forceinline__ void st_evict_first_f4(float* p, float4 v, uint64_t p
                :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
 }
 
+// W-float lane vectors: W = 4 (128-bit loads) or W = 8 (256-bit loads,
+// LDG.E.256 on sm_100a).
+template <int W>
+struct Vf {
+  float v[W];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < W; ++i) v[i] = 0.f;
+  }
+  __device__ __forceinline__ void fma(float s, const Vf& x) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) v[i] = fmaf(s, x.v[i], v[i]);
+  }
+  __device__ __forceinline__ void add_xor(int off) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+  }
+};
+
+template <int W>
+__device__ __forceinline__ Vf<W> ldg_vec(const float* p) {
+  Vf<W> r;
+  if constexpr (W == 8) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+          "=f"(r.v[6]), "=f"(r.v[7])
+        : "l"(p));
+  } else {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w;
+  }
+  return r;
+}
+template <int W>
+__device__ __forceinline__ Vf<W> ld_stream_vec(const float* p) {
+  Vf<W> r;
+#pragma unroll
+  for (int h = 0; h < W / 4; ++h) {
+    const float4 t = ld_stream_f4(p + 4 * h);
+    r.v[4 * h] = t.x; r.v[4 * h + 1] = t.y; r.v[4 * h + 2] = t.z; r.v[4 * h + 3] = t.w;
+  }
+  return r;
+}
+template <int W>
+__device__ __forceinline__ void st_stream_vec(float* p, const Vf<W>& x) {
+#pragma unroll
+  for (int h = 0; h < W / 4; ++h)
+    st_stream_f4(p + 4 * h, make_float4(x.v[4 * h], x.v[4 * h + 1], x.v[4 * h + 2], x.v[4 * h + 3]));
+}
+
 // One row per group of G = LPR*SUB lanes (32/G rows per warp).  Within a
-// group, LPR lanes cover the k columns with 128-bit loads and SUB lane
-// subgroups split the row's nonzeros; U gathers per lane are in flight per
-// round.  Loop bounds are warp-uniform (max over the warp's rows) so the
+// group, LPR lanes cover the k = W*LPR columns with W-float loads and SUB
+// lane subgroups split the row's nonzeros; U gathers per lane are in flight
+// per round.  Loop bounds are warp-uniform (max over the warp's rows) so the
 // shuffles stay convergent; rows are predicated.  Returns the folded row sum
 // in the sub==0 lanes of each group.
-template <int LPR, int SUB, int U, bool IMPLICIT>
-__device__ __forceinline__ float4 group_row_accumulate(const TermArgs& a, int32_t row, bool valid,
-                                                       int32_t b, int32_t e, int32_t rowlen,
-                                                       int lane) {
+template <int W, int LPR, int SUB, int U, bool IMPLICIT>
+__device__ __forceinline__ Vf<W> group_row_accumulate(const TermArgs& a, int32_t row, bool valid,
+                                                      int32_t b, int32_t e, int32_t rowlen,
+                                                      int lane) {
   constexpr int G = LPR * SUB;
   const int g = lane % G;
   const int gbase = lane - g;
   const int sub = g / LPR;
   const int cl = g % LPR;
-  // single-slab rows are exactly 4*LPR floats: compile-time stride
-  const bool single = (a.ld == 4 * LPR);
-  const float* wbase = a.win + cl * 4;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  // single-slab rows are exactly W*LPR floats: compile-time stride
+  const bool single = (a.ld == W * LPR);
+  const float* wbase = a.win + cl * W;
+  Vf<W> acc;
+  acc.zero();
   const int32_t len = valid ? e - b : 0;
   int32_t maxlen = len;
 #pragma unroll
@@ -134,7 +196,7 @@ __device__ __forceinline__ float4 group_row_accumulate(const TermArgs& a, int32_
     const int mcnt = min(G, maxlen - o);
     const int T = (mcnt + SUB - 1) / SUB;
     for (int t = 0; t < T; t += U) {
-      float4 gv[U];
+      Vf<W> gv[U];
       float w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -143,37 +205,53 @@ __device__ __forceinline__ float4 group_row_accumulate(const TermArgs& a, int32_
         const int32_t c = __shfl_sync(0xffffffffu, col, js);
         w[u] = __shfl_sync(0xffffffffu, val, js);
         if (j < cnt) {
-          gv[u] = single ? ldg_f4(wbase + c * (4 * LPR)) : ldg_f4(wbase + (int64_t)c * a.ld);
+          gv[u] = single ? ldg_vec<W>(wbase + c * (W * LPR)) : ldg_vec<W>(wbase + (int64_t)c * a.ld);
         } else {
-          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          gv[u].zero();
           w[u] = 0.f;
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc = f4_fma(w[u], gv[u], acc);
+      for (int u = 0; u < U; ++u) acc.fma(w[u], gv[u]);
     }
   }
 #pragma unroll
-  for (int off = LPR; off < G; off <<= 1) acc = f4_add(acc, f4_shfl_xor(acc, off));
+  for (int off = LPR; off < G; off <<= 1) acc.add_xor(off);
   return acc;
 }
 
-__device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, float4 xr, float4 wr) {
-  float4 r = f4_scale(a.beta, y);
-  if (a.flags & TF_ALPHA) r = f4_fma(a.alpha, xr, r);
-  if (a.flags & TF_GAMMA) r = f4_fma(a.gamma, wr, r);
-  if (a.flags & TF_FINAL) {
-    r = f4_scale(a.sfin, r);
-    if (a.flags & TF_LAMF) r = f4_fma(a.lamf, xr, r);
+template <int W>
+__device__ __forceinline__ Vf<W> term_epilogue(const TermArgs& a, const Vf<W>& y, const Vf<W>& xr,
+                                               const Vf<W>& wr) {
+  Vf<W> r;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    float t = a.beta * y.v[i];
+    if (a.flags & TF_ALPHA) t = fmaf(a.alpha, xr.v[i], t);
+    if (a.flags & TF_GAMMA) t = fmaf(a.gamma, wr.v[i], t);
+    if (a.flags & TF_FINAL) {
+      t *= a.sfin;
+      if (a.flags & TF_LAMF) t = fmaf(a.lamf, xr.v[i], t);
+    }
+    r.v[i] = t;
   }
   return r;
+}
+
+__device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, float4 xr, float4 wr) {
+  Vf<4> Y, X, R;
+  Y.v[0] = y.x; Y.v[1] = y.y; Y.v[2] = y.z; Y.v[3] = y.w;
+  X.v[0] = xr.x; X.v[1] = xr.y; X.v[2] = xr.z; X.v[3] = xr.w;
+  R.v[0] = wr.x; R.v[1] = wr.y; R.v[2] = wr.z; R.v[3] = wr.w;
+  const Vf<4> o = term_epilogue<4>(a, Y, X, R);
+  return make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
 }
 
 // Long-row chunks: one warp per chunk (all 32/LPR lane groups over the
 // chunk's nonzeros).  The last chunk of a row to finish (ticket) folds the
 // partial rows in chunk order and applies the epilogue: deterministic, no
 // float atomics.
-template <int LPR, int U, bool IMPLICIT>
+template <int W, int LPR, int U, bool IMPLICIT>
 __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   const int lane = threadIdx.x & 31;
   const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
@@ -184,10 +262,15 @@ __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   const int32_t pe = a.chunk_desc[4 * c + 2];
   const int32_t c0 = a.chunk_desc[4 * c + 3];
   const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
-  const float4 acc = group_row_accumulate<LPR, 32 / LPR, U, IMPLICIT>(
+  const Vf<W> acc = group_row_accumulate<W, LPR, 32 / LPR, U, IMPLICIT>(
       a, row, true, pb, pe, re - rb, lane);
   const int lsub = lane / LPR, lcl = lane % LPR;
-  if (lsub == 0) __stcg(reinterpret_cast<float4*>(a.partials + c * a.k + lcl * 4), acc);
+  if (lsub == 0) {
+#pragma unroll
+    for (int h = 0; h < W / 4; ++h)
+      __stcg(reinterpret_cast<float4*>(a.partials + c * a.k + lcl * W + 4 * h),
+             make_float4(acc.v[4 * h], acc.v[4 * h + 1], acc.v[4 * h + 2], acc.v[4 * h + 3]));
+  }
   __threadfence();
   int ticket = 0;
   if (lane == 0) ticket = atomicAdd(a.tickets + c0, 1);
@@ -196,20 +279,29 @@ __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   if (ticket != nch - 1) return;
   __threadfence();
   if (lsub == 0) {
-    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int32_t q = 0; q < nch; ++q)
-      y = f4_add(y, __ldcg(reinterpret_cast<const float4*>(a.partials + (int64_t)(c0 + q) * a.k +
-                                                            lcl * 4)));
-    const int64_t off = (int64_t)row * a.ld + lcl * 4;
-    const float4 xr = need_x ? ld_stream_f4(a.x + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 wr = (a.flags & TF_GAMMA) ? ld_gather_f4(a.win + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    st_stream_f4(a.wout + off, term_epilogue(a, y, xr, wr));
+    Vf<W> y;
+    y.zero();
+    for (int32_t q = 0; q < nch; ++q) {
+#pragma unroll
+      for (int h = 0; h < W / 4; ++h) {
+        const float4 t = __ldcg(reinterpret_cast<const float4*>(
+            a.partials + (int64_t)(c0 + q) * a.k + lcl * W + 4 * h));
+        y.v[4 * h] += t.x; y.v[4 * h + 1] += t.y; y.v[4 * h + 2] += t.z; y.v[4 * h + 3] += t.w;
+      }
+    }
+    const int64_t off = (int64_t)row * a.ld + lcl * W;
+    Vf<W> xr, wr;
+    xr.zero();
+    wr.zero();
+    if (need_x) xr = ld_stream_vec<W>(a.x + off);
+    if (a.flags & TF_GAMMA) wr = ldg_vec<W>(a.win + off);
+    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, y, xr, wr));
   }
   if (lane == 0) a.tickets[c0] = 0;
 }
 
-template <int LPR, int SUB, int U, bool IMPLICIT>
-__global__ void __launch_bounds__(256, TERM_MIN_BLOCKS) spmm_term_kernel(const TermArgs a) {
+template <int W, int LPR, int SUB, int U, bool IMPLICIT>
+__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : TERM_MIN_BLOCKS)) spmm_term_kernel(const TermArgs a) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -226,13 +318,16 @@ __global__ void __launch_bounds__(256, TERM_MIN_BLOCKS) spmm_term_kernel(const T
     if (e - b > a.long_thresh) valid = false;
   }
   if (__all_sync(0xffffffffu, !valid)) return;
-  const float4 acc = group_row_accumulate<LPR, SUB, U, IMPLICIT>(a, row, valid, b, e, e - b, lane);
+  const Vf<W> acc = group_row_accumulate<W, LPR, SUB, U, IMPLICIT>(a, row, valid, b, e, e - b, lane);
   if (valid && sub == 0) {
-    const int64_t off = (int64_t)row * a.ld + cl * 4;
+    const int64_t off = (int64_t)row * a.ld + cl * W;
     const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
-    const float4 xr = need_x ? ld_stream_f4(a.x + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 wr = (a.flags & TF_GAMMA) ? ldg_f4(a.win + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-    st_stream_f4(a.wout + off, term_epilogue(a, acc, xr, wr));
+    Vf<W> xr, wr;
+    xr.zero();
+    wr.zero();
+    if (need_x) xr = ld_stream_vec<W>(a.x + off);
+    if (a.flags & TF_GAMMA) wr = ldg_vec<W>(a.win + off);
+    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, acc, xr, wr));
   }
 }
 
@@ -469,7 +564,8 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
 
 constexpr int UNROLL = 4;
 
-template <int LPR, int SUB, int U = ((SUB == 1 && LPR <= 8) ? SUB1_U : UNROLL)>
+template <int W, int LPR, int SUB,
+          int U = (SUB > 1 ? (W == 8 ? 4 : LONG_U) : (W == 8 ? W8_U : SUB1_U))>
 static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
@@ -480,29 +576,54 @@ static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
   const unsigned grid = (unsigned)((warps + wpb - 1) / wpb);
   if (grid == 0) return;
   if (implicit)
-    spmm_term_kernel<LPR, SUB, U, true><<<grid, threads, 0, s>>>(a);
+    spmm_term_kernel<W, LPR, SUB, U, true><<<grid, threads, 0, s>>>(a);
   else
-    spmm_term_kernel<LPR, SUB, U, false><<<grid, threads, 0, s>>>(a);
+    spmm_term_kernel<W, LPR, SUB, U, false><<<grid, threads, 0, s>>>(a);
 }
 
-template <int LPR>
+template <int W, int LPR>
 static void launch_chunks(const TermArgs& a, bool implicit, cudaStream_t s) {
   const unsigned grid = (unsigned)((a.n_chunks + 7) / 8);
   if (grid == 0) return;
   if (implicit)
-    spmm_chunk_kernel<LPR, UNROLL, true><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), true><<<grid, 256, 0, s>>>(a);
   else
-    spmm_chunk_kernel<LPR, UNROLL, false><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), false><<<grid, 256, 0, s>>>(a);
 }
 
-template <int LPR>
+template <int W, int LPR>
 static void launch_fast_sub(const TermArgs& a, int sub, bool implicit, cudaStream_t s) {
   switch (sub) {
-    case 1: launch_fast<LPR, 1>(a, implicit, s); break;
-    case 2: if constexpr (LPR * 2 <= 32) { launch_fast<LPR, 2>(a, implicit, s); break; } [[fallthrough]];
-    case 4: if constexpr (LPR * 4 <= 32) { launch_fast<LPR, 4>(a, implicit, s); break; } [[fallthrough]];
-    case 8: if constexpr (LPR * 8 <= 32) { launch_fast<LPR, 8>(a, implicit, s); break; } [[fallthrough]];
-    default: launch_fast<LPR, 32 / LPR>(a, implicit, s); break;
+    case 1: launch_fast<W, LPR, 1>(a, implicit, s); break;
+    case 2: if constexpr (LPR * 2 <= 32) { launch_fast<W, LPR, 2>(a, implicit, s); break; } [[fallthrough]];
+    case 4: if constexpr (LPR * 4 <= 32) { launch_fast<W, LPR, 4>(a, implicit, s); break; } [[fallthrough]];
+    case 8: if constexpr (LPR * 8 <= 32) { launch_fast<W, LPR, 8>(a, implicit, s); break; } [[fallthrough]];
+    default: launch_fast<W, LPR, 32 / LPR>(a, implicit, s); break;
+  }
+}
+
+// width dispatch: W = 8 (256-bit gathers) when k % 8 == 0 and rows are 32 B
+// aligned, else W = 4.  lpr = k / W.
+template <int W>
+static void launch_chunks_w(int lpr, const TermArgs& a, bool implicit, cudaStream_t s) {
+  switch (lpr) {
+    case 1: launch_chunks<W, 1>(a, implicit, s); break;
+    case 2: launch_chunks<W, 2>(a, implicit, s); break;
+    case 4: launch_chunks<W, 4>(a, implicit, s); break;
+    case 8: launch_chunks<W, 8>(a, implicit, s); break;
+    case 16: launch_chunks<W, 16>(a, implicit, s); break;
+    default: if constexpr (W == 4) launch_chunks<W, 32>(a, implicit, s); break;
+  }
+}
+template <int W>
+static void launch_rows_w(int lpr, int sub, const TermArgs& a, bool implicit, cudaStream_t s) {
+  switch (lpr) {
+    case 1: launch_fast_sub<W, 1>(a, sub, implicit, s); break;
+    case 2: launch_fast_sub<W, 2>(a, sub, implicit, s); break;
+    case 4: launch_fast_sub<W, 4>(a, sub, implicit, s); break;
+    case 8: launch_fast_sub<W, 8>(a, sub, implicit, s); break;
+    case 16: launch_fast_sub<W, 16>(a, sub, implicit, s); break;
+    default: if constexpr (W == 4) launch_fast_sub<W, 32>(a, sub, implicit, s); break;
   }
 }
 
@@ -523,28 +644,28 @@ struct Segment {
 
 // Launch one term over one column slab: one launch per row segment, the
 // long-row chunks riding in the leading blocks of the first launch.
-static int launch_term_slab(TermArgs a, bool implicit, bool aligned, const Segment* segs,
-                            int nseg, cudaStream_t s) {
+static int launch_term_slab(TermArgs a, bool implicit, bool aligned, bool aligned32,
+                            const Segment* segs, int nseg, cudaStream_t s) {
   const int k = a.k;
   const bool fast = aligned && (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128);
   if (fast) {
-    const int lpr = k / 4;
+    static int wide = -1;  // SPED_VEC=4 forces 128-bit gathers
+    if (wide < 0) {
+      const char* e = getenv("SPED_VEC");
+      wide = (e && e[0] == '4') ? 0 : 1;
+    }
+    const bool w8 = wide && (k % 8 == 0) && aligned32 && k >= 64;
+    const int lpr = k / (w8 ? 8 : 4);
     if (a.n_chunks > 0) {
-      switch (lpr) {
-        case 1: launch_chunks<1>(a, implicit, s); break;
-        case 2: launch_chunks<2>(a, implicit, s); break;
-        case 4: launch_chunks<4>(a, implicit, s); break;
-        case 8: launch_chunks<8>(a, implicit, s); break;
-        case 16: launch_chunks<16>(a, implicit, s); break;
-        default: launch_chunks<32>(a, implicit, s); break;
-      }
+      if (w8) launch_chunks_w<8>(lpr, a, implicit, s);
+      else launch_chunks_w<4>(lpr, a, implicit, s);
       SPED_LAUNCH_CHECK();
     }
     for (int i = 0; i < nseg; ++i) {
       a.row_begin = segs[i].begin;
       a.row_end = segs[i].end;
       int sub = segs[i].sub;
-      if (sub == 0) {  // software-pipelined short rows
+      if (sub == 0 && !w8) {  // software-pipelined short rows (128-bit path only)
         switch (lpr) {
           case 1: launch_short<1>(a, implicit, s); break;
           case 2: launch_short<2>(a, implicit, s); break;
@@ -558,14 +679,8 @@ static int launch_term_slab(TermArgs a, bool implicit, bool aligned, const Segme
       }
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
-      switch (lpr) {
-        case 1: launch_fast_sub<1>(a, sub, implicit, s); break;
-        case 2: launch_fast_sub<2>(a, sub, implicit, s); break;
-        case 4: launch_fast_sub<4>(a, sub, implicit, s); break;
-        case 8: launch_fast_sub<8>(a, sub, implicit, s); break;
-        case 16: launch_fast_sub<16>(a, sub, implicit, s); break;
-        default: launch_fast_sub<32>(a, sub, implicit, s); break;
-      }
+      if (w8) launch_rows_w<8>(lpr, sub, a, implicit, s);
+      else launch_rows_w<4>(lpr, sub, a, implicit, s);
       SPED_LAUNCH_CHECK();
     }
   } else {
@@ -726,10 +841,11 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
         fixed[0].sub = 32;
         ns = 1;
       }
-      const bool aligned = (k % 4 == 0) &&
-                           ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(win) |
-                             reinterpret_cast<uintptr_t>(wout)) % 16 == 0);
-      int rc = launch_term_slab(a, implicit, aligned, fixed, ns, s);
+      const uintptr_t pbits = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(win) |
+                              reinterpret_cast<uintptr_t>(wout);
+      const bool aligned = (k % 4 == 0) && (pbits % 16 == 0);
+      const bool aligned32 = (k % 8 == 0) && (pbits % 32 == 0);
+      int rc = launch_term_slab(a, implicit, aligned, aligned32, fixed, ns, s);
       if (rc != SPED_OK) return rc;
     }
     return SPED_OK;
