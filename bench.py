@@ -186,6 +186,62 @@ def cpu_term_sample(n, u, v, w, mode, k, seconds, threads, alpha=1.0, beta=1.0):
     return rate, desc, dt, csr.nnz
 
 
+def time_to_angle(cfg=1, target=1e-3, eval_every=50, max_steps=20000, cpu=True):
+    """Time to max principal angle <= target between span(V) and the true
+    bottom-k eigenvectors (BASELINE metric, part 3), GPU solver vs the CPU
+    reference algorithm (oracle port), same graph / transform / seeds.
+    Config 1: SBM 10x100, mu-EG, eta = 0.1, negexp-limit(13) (the smallest
+    odd degree covering the spectrum, SURVEY 8d note (ii))."""
+    import torch
+    import oracle as O
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200 import generators as G
+    from paper_2207_14589_b200.solvers import _GraphStepper, _SmallStepper, small_solver_eligible
+    spec = G.CONFIGS[cfg]
+    k = spec["k"]
+    kind, ell, eta = "negexp-limit", 13, 0.1
+    n, u, v, w = G.config_graph(cfg)
+    g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
+    gt = sp.graph_ground_truth(g, spec["mode"])
+    U = gt.bottom(k)
+    init_seed, _, _ = O.solver_seeds(0)
+    op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell), spec["mode"])
+    V0 = sp.init_state(n, k, init_seed).V
+    small = False  # the multi-SM CUDA-graph path is faster than the single-block K2 kernel
+    Vi = op.laplacian.to_internal(V0)
+    stepper = _SmallStepper(op, eta, Vi) if small else _GraphStepper(op, "mu-eg", eta, Vi)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    gpu_steps = None
+    for t in range(eval_every, max_steps + 1, eval_every):
+        stepper.advance(eval_every)
+        Vh = op.laplacian.from_internal(stepper.V).cpu().numpy().astype(np.float64)
+        if sp.principal_angles(Vh, U) <= target:
+            gpu_steps = t
+            break
+    gpu_s = time.perf_counter() - t0
+    out = {"config": spec["name"], "transform": f"{kind}({ell})", "eta": eta, "k": k,
+           "gpu_path": "single-block K2 kernel (sped_small_mueg)" if small else "CUDA-graph steps",
+           "target_angle": target, "eval_every": eval_every,
+           "gpu_steps": gpu_steps, "gpu_s": gpu_s}
+    if cpu:
+        csr = O.laplacian_csr(n, g.u, g.v, g.w, spec["mode"])
+        lam = O.choose_lambda_star(kind, O.lambda_upper(n, g.u, g.v, g.w, spec["mode"]))
+        V = O.init_state(n, k, init_seed)
+        t0 = time.perf_counter()
+        cpu_steps = None
+        for t in range(1, max_steps + 1):
+            V = O.mu_eg_step(V, O.apply_transform(csr, kind, ell, 1e-6, lam, V), eta)
+            if t % eval_every == 0 and O.principal_angles(V, U) <= target:
+                cpu_steps = t
+                break
+        out.update(cpu_steps=cpu_steps, cpu_s=time.perf_counter() - t0, cpu_cores=1,
+                   cpu_kind="port (scipy csr @ dense, fp64; the reference path)")
+        if gpu_steps and cpu_steps:
+            out["speedup"] = out["cpu_s"] / gpu_s
+    return out
+
+
 # ------------------------------------------------------------------------------ sped arm
 
 def run_sped(args):
@@ -339,6 +395,10 @@ def run_sped(args):
         cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port", "sample": desc,
                "seconds_per_term": dt}
 
+    conv = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        conv = time_to_angle(1)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -360,6 +420,7 @@ def run_sped(args):
                          "kernel": "spmm_term_kernel (one fused polynomial term)",
                          "algorithmic_bytes_per_launch": bpt, "peak_source": peak_src},
             "cpu_baseline": cpu,
+            "time_to_angle": conv,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,

@@ -144,6 +144,15 @@ int sped_mueg_coeffs(int32_t k, const double* G, double eta, float* A, float* sc
  * with_m=0: Gram = S.  T = R^{-1} for R = chol(Gram)^T (upper), fp32. */
 int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, float* T,
                     int32_t* flag, sped_stream_t stream);
+/* Desk-scale fast path (n*k <= 12288, k <= 32): `steps` whole mu-EG steps
+ * (polynomial apply, Gram, k x k algebra, update) in one thread block with
+ * the state in shared memory.  V (n x k) is updated in place; flag as above;
+ * returns SPED_ERR_UNSUPPORTED when the graph is too large. */
+int sped_small_mueg(int32_t n, int32_t k, const int32_t* indptr, const int32_t* indices,
+                    const float* values, int32_t n_terms, const double* alpha,
+                    const double* beta, const double* gamma, double w0_scale, double lam_f,
+                    double s_final, double eta, int32_t steps, float* V, int32_t* flag,
+                    sped_stream_t stream);
 /* out = (P*A + M*B) * diag(scale).  A k x k fp32; M may be NULL; B may be
  * NULL meaning B = eta*I; scale may be NULL (ones).  upper != 0 promises A is
  * upper triangular (mu-EG), letting the kernel skip the zero half. */
