@@ -256,7 +256,13 @@ def run_sped(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # SPED_FORCE_SHARD=1 runs the row-sharded NCCL path even on one rank
+    sharded = world > 1 or os.environ.get("SPED_FORCE_SHARD") == "1"
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     spec = cfg_spec(args.config)
     k, ell, mode = spec["k"], spec["ell"], spec["mode"]
@@ -273,7 +279,7 @@ def run_sped(args):
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
 
-    if world > 1:
+    if sharded:
         from paper_2207_14589_b200.distributed import ShardedLaplacian, ShardedOperator, sharded_mu_eg_step
         shard = ShardedLaplacian(lap, rank, world)
         sop = ShardedOperator(shard, t, op.lambda_star)
@@ -292,13 +298,13 @@ def run_sped(args):
     def step(Vin, Vout, ev=None):
         if ev is not None:
             ev[0].record(stream)
-        if world > 1:
+        if sharded:
             sop.apply_local(Vin, out=MV)
         else:
             op.apply_internal(Vin, out=MV)
         if ev is not None:
             ev[1].record(stream)
-        if world > 1:
+        if sharded:
             ws.gram(Vin, MV)
             dist.all_reduce(ws.G)
             lib = sp._lib.load()
@@ -314,7 +320,7 @@ def run_sped(args):
         step(V, Vn)
         V, Vn = Vn, V
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -328,14 +334,14 @@ def run_sped(args):
         V, Vn = Vn, V
     end.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = start.elapsed_time(end)
     apply_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     solve_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
-    if world > 1:
+    if sharded:
         tt = torch.tensor([total_ms, apply_ms, solve_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms, apply_ms, solve_ms = (float(x) for x in tt.tolist())
@@ -343,12 +349,12 @@ def run_sped(args):
     work = n_terms * nnz * k
     value = work * args.steps / (total_ms / 1e3)
     t_term_s = apply_ms / 1e3 / (args.steps * n_terms)
-    bpt = bytes_per_term(n if world == 1 else n_loc, nnz if world == 1 else shard.nnz_local, k,
+    bpt = bytes_per_term(n if not sharded else n_loc, nnz if not sharded else shard.nnz_local, k,
                          stored, any(a != 0 for a in al), lf != 0.0)
     peak, peak_src = measured_peak()
     achieved = bpt / t_term_s / 1e9
     launches_per_step = n_terms + 5
-    if world > 1:
+    if sharded:
         launches_per_step = n_terms * 2 + 5
 
     e2e = None
@@ -356,7 +362,7 @@ def run_sped(args):
         # reference-facing call with HOST buffers: mu_eg_step(EigenState(host V), op, eta)
         Vh = torch.empty((n_loc, k), dtype=torch.float32, pin_memory=True)
         Vh.copy_(V)
-        if world == 1:
+        if not sharded:
             # two warm-up calls populate the pinned-host cache (result + input)
             for _ in range(2):
                 st = sp.mu_eg_step(sp.EigenState(Vh), op, eta)
@@ -388,7 +394,7 @@ def run_sped(args):
                "api": "paper_2207_14589_b200.mu_eg_step(EigenState(pinned host V), op, eta)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not sharded and not args.no_cpu:
         uh, vh, wh = g.u, g.v, g.w
         thr = cpu_threads()
         rate, desc, dt, snnz = cpu_term_sample(n, uh, vh, wh, mode, k, args.cpu_seconds, thr)
@@ -396,7 +402,7 @@ def run_sped(args):
                "seconds_per_term": dt}
 
     conv = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not sharded and not args.no_cpu:
         conv = time_to_angle(1)
 
     if rank == 0:
@@ -409,7 +415,7 @@ def run_sped(args):
                        "n": n, "m": g.m, "nnz": nnz, "k": k, "mode": mode,
                        "transform": f"negexp-taylor({ell})", "terms": n_terms,
                        "solver": "mu-eg", "eta": eta,
-                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "parallelism": f"row-shard x{world}" if sharded else "single GPU",
                        "l2": "inputs (V 4nk B, CSR) larger than the 126 MB L2; no flush",
                        "setup_s": setup_s},
             "breakdown_ms_per_step": {"p(L)V": apply_ms / args.steps,
@@ -426,7 +432,7 @@ def run_sped(args):
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

@@ -67,10 +67,7 @@ class HaloPlan:
         return np.array([s.size for s in self.send_rows], dtype=np.int64)
 
 
-def build_halo_plan(indices_global: np.ndarray, offsets: np.ndarray, rank: int, world: int,
-                    group=None) -> HaloPlan:
-    """Remap a rank's CSR columns into [own | halo] and agree on the send
-    lists with every peer (collective over ``group``)."""
+def _local_view(indices_global: np.ndarray, offsets: np.ndarray, rank: int, world: int):
     b, e = int(offsets[rank]), int(offsets[rank + 1])
     cols = indices_global.astype(np.int64)
     remote_mask = (cols < b) | (cols >= e)
@@ -80,8 +77,50 @@ def build_halo_plan(indices_global: np.ndarray, offsets: np.ndarray, rank: int, 
     local = np.empty_like(cols)
     local[~remote_mask] = cols[~remote_mask] - b
     local[remote_mask] = (e - b) + np.searchsorted(halo, cols[remote_mask])
-    # exchange the request lists: counts first, then the ids
-    counts = torch.from_numpy(recv_counts.copy())
+    return b, e, halo, recv_counts, local
+
+
+def build_halo_plans_local(indptr: np.ndarray, indices: np.ndarray,
+                           offsets: np.ndarray) -> list:
+    """Every rank's HaloPlan computed in one process (no communication):
+    the same result build_halo_plan agrees on collectively.  Used by
+    single-device tests of the shard kernels and by planning tools."""
+    world = offsets.size - 1
+    views = []
+    for r in range(world):
+        p0, p1 = int(indptr[offsets[r]]), int(indptr[offsets[r + 1]])
+        views.append(_local_view(indices[p0:p1], offsets, r, world))
+    plans = []
+    for r in range(world):
+        b, e, halo, recv_counts, local = views[r]
+        send_rows = []
+        for q in range(world):
+            if q == r:
+                send_rows.append(np.zeros(0, dtype=np.int64))
+                continue
+            hq = views[q][2]
+            oq = np.searchsorted(offsets, hq, side="right") - 1
+            send_rows.append(hq[oq == r] - b)
+        plans.append(HaloPlan(r, world, offsets, e - b, halo, recv_counts, send_rows, local))
+    return plans
+
+
+def _comm_device(group=None) -> torch.device:
+    """Tensors for collectives must live where the backend expects them."""
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def build_halo_plan(indices_global: np.ndarray, offsets: np.ndarray, rank: int, world: int,
+                    group=None) -> HaloPlan:
+    """Remap a rank's CSR columns into [own | halo] and agree on the send
+    lists with every peer (collective over ``group``)."""
+    b, e, halo, recv_counts, local = _local_view(indices_global, offsets, rank, world)
+    # exchange the request lists: counts first, then the ids (on the device
+    # for NCCL groups, on the host for gloo)
+    cdev = _comm_device(group)
+    counts = torch.from_numpy(recv_counts.copy()).to(cdev)
     all_counts = [torch.zeros_like(counts) for _ in range(world)]
     dist.all_gather(all_counts, counts, group=group)
     send_counts = np.array([int(all_counts[q][rank]) for q in range(world)], dtype=np.int64)
@@ -92,10 +131,10 @@ def build_halo_plan(indices_global: np.ndarray, offsets: np.ndarray, rank: int, 
         if q == rank:
             continue
         if recv_counts[q]:
-            req = torch.from_numpy(halo[starts[q]:starts[q + 1]].copy())
+            req = torch.from_numpy(halo[starts[q]:starts[q + 1]].copy()).to(cdev)
             ops.append(dist.P2POp(dist.isend, req, q, group=group))
         if send_counts[q]:
-            buf = torch.empty(int(send_counts[q]), dtype=torch.int64)
+            buf = torch.empty(int(send_counts[q]), dtype=torch.int64, device=cdev)
             recv_bufs[q] = buf
             ops.append(dist.P2POp(dist.irecv, buf, q, group=group))
     if ops:
@@ -104,7 +143,7 @@ def build_halo_plan(indices_global: np.ndarray, offsets: np.ndarray, rank: int, 
     send_rows = []
     for q in range(world):
         if q in recv_bufs:
-            send_rows.append(recv_bufs[q].numpy() - b)
+            send_rows.append(recv_bufs[q].cpu().numpy() - b)
         else:
             send_rows.append(np.zeros(0, dtype=np.int64))
     return HaloPlan(rank, world, offsets, e - b, halo, recv_counts, send_rows, local)
@@ -157,7 +196,7 @@ class ShardedLaplacian:
     """This rank's rows of L on its GPU, plus the halo plan."""
 
     def __init__(self, full_laplacian, rank: int, world: int, group=None,
-                 offsets: np.ndarray | None = None):
+                 offsets: np.ndarray | None = None, plan: HaloPlan | None = None):
         lap = full_laplacian
         self.full = lap
         self.device = lap.device
@@ -165,8 +204,10 @@ class ShardedLaplacian:
         self.offsets = partition_rows(indptr_h, world) if offsets is None else offsets
         b, e = int(self.offsets[rank]), int(self.offsets[rank + 1])
         p0, p1 = int(indptr_h[b]), int(indptr_h[e])
-        cols = lap.indices[p0:p1].cpu().numpy()
-        self.plan = build_halo_plan(cols, self.offsets, rank, world, group)
+        if plan is None:
+            cols = lap.indices[p0:p1].cpu().numpy()
+            plan = build_halo_plan(cols, self.offsets, rank, world, group)
+        self.plan = plan
         self.group = group
         self.rank, self.world = rank, world
         self.n_own = e - b
@@ -179,6 +220,9 @@ class ShardedLaplacian:
         self.values = None if lap.values is None else lap.values[p0:p1].contiguous()
         self.implicit = lap.values is None
         self.long_threshold, self.chunk_len = lap.long_threshold, lap.chunk_len
+        self.rowlen = np.diff(indptr_h[b:e + 1])
+        self.sorted_rows = lap.reordered
+        self._segments = {}
         self._plan_chunks()
 
     def _plan_chunks(self):
@@ -196,14 +240,23 @@ class ShardedLaplacian:
         self.chunk_desc = desc[: max(4 * self.n_chunks, 4)].clone() if self.n_chunks else None
         self.tickets = torch.zeros(max(self.n_chunks, 1), dtype=torch.int32, device=self.device)
 
+    def segments(self, k):
+        from .graph import segment_table
+        key = min(k, 128)
+        if key not in self._segments:
+            self._segments[key] = segment_table(self.rowlen, key, self.sorted_rows,
+                                                self.long_threshold if self.n_chunks else None)
+        return self._segments[key]
+
     def local_term(self, E, x_own, out, alpha, beta, gamma, w0, lam_f, s_final, k):
         lib = _lib.load()
+        nseg, seg = self.segments(k)
         partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=self.device)
                     if self.n_chunks else None)
         rc = lib.sped_csr_poly_apply(
             self.n_own, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
             self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
-            _lib.ptr(partials), _lib.ptr(self.tickets if self.n_chunks else None), None, 0,
+            _lib.ptr(partials), _lib.ptr(self.tickets if self.n_chunks else None), seg, nseg,
             self.n_own + self.plan.n_halo, _lib.ptr(x_own), _lib.ptr(E),
             None, None, _lib.ptr(out), 1, _lib.dbl_array([alpha]), _lib.dbl_array([beta]),
             _lib.dbl_array([gamma]), float(w0), float(lam_f), float(s_final),

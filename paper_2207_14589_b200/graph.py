@@ -203,6 +203,45 @@ HOT_FRACTION = 0.7          # share of L2 reserved for the hot (evict_last) rows
 SKEW_REORDER = 16.0         # max degree / mean degree above which rows are degree-ordered
 
 
+def segment_table(rowlen: np.ndarray, k: int, sorted_desc: bool, long_threshold):
+    """Row ranges of similar length sharing a lanes-per-row choice for the
+    SpMM (``sped_csr_poly_apply`` ``segments``).  Rows sorted by descending
+    length (degree-ordered graphs) get: long rows (> 64 nonzeros) one warp per
+    row, the rest (k/4) lanes per row; chunked rows (> long_threshold) are
+    skipped (their own kernel).  Unsorted graphs get one range sized from the
+    mean row length.  Returns ``(n_segments, int64 ctypes array)``."""
+    n = int(rowlen.size)
+    lpr = max(1, min(32, k // 4))
+    smax = max(1, 32 // lpr)
+    use_short = os.environ.get("SPED_SHORT", "0") == "1"
+    if n == 0:
+        seg = []
+    elif sorted_desc:
+        L = rowlen
+        cap = 2 * lpr      # rows the pipelined short-row kernel covers from registers
+        thr = long_threshold if long_threshold is not None else np.iinfo(np.int64).max
+        r_long = int(np.searchsorted(-L, -thr, side="left"))    # rows with len > thr
+        r_64 = max(int(np.searchsorted(-L, -64, side="left")), r_long)
+        r_cap = max(int(np.searchsorted(-L, -cap, side="left")), r_64)
+        if not use_short:
+            r_cap = n
+        seg = []
+        if r_64 > r_long:
+            seg.append((r_long, r_64, smax))      # long rows: warp per row
+        if r_cap > r_64:
+            seg.append((r_64, r_cap, 1))          # medium/short rows: LPR lanes per row
+        if n > r_cap:
+            seg.append((r_cap, n, 0))             # short rows: pipelined kernel (opt-in)
+    else:
+        mean = float(rowlen.sum()) / n
+        if use_short and mean <= 2 * lpr:
+            seg = [(0, n, 0)]
+        else:
+            seg = [(0, n, smax if mean >= 64 else 1)]
+    flat = [x for t in seg for x in t]
+    return len(seg), _lib.i64_array(flat)
+
+
 class LaplacianOperator:
     """Device CSR Laplacian; ``mode`` in {"unnormalized", "normalized"}.
 
@@ -325,42 +364,11 @@ class LaplacianOperator:
         return self.perm is not None
 
     def segments(self, k: int):
-        """Row-range table ``[(begin, end, sub), ...]`` for width k: rows in
-        ranges of similar length share a lanes-per-row choice (degree-ordered
-        graphs); otherwise one range sized from the mean degree."""
+        """Row-range table ``[(begin, end, sub), ...]`` for width k (cached)."""
         key = min(k, 128)
-        if key in self._segments:
-            return self._segments[key]
-        n = self.n
-        lpr = max(1, min(32, key // 4))
-        smax = max(1, 32 // lpr)
-        use_short = os.environ.get("SPED_SHORT", "0") == "1"
-        if n == 0:
-            seg = []
-        elif self.reordered:
-            L = self.rowlen
-            cap = 2 * lpr      # rows the pipelined short-row kernel covers from registers
-            thr = self.long_threshold if self.n_chunks else np.iinfo(np.int64).max
-            r_long = int(np.searchsorted(-L, -thr, side="left"))    # rows with len > thr
-            r_64 = max(int(np.searchsorted(-L, -64, side="left")), r_long)
-            r_cap = max(int(np.searchsorted(-L, -cap, side="left")), r_64)
-            seg = []
-            if r_64 > r_long:
-                seg.append((r_long, r_64, smax))      # long rows: warp per row
-            if not use_short:
-                r_cap = n
-            if r_cap > r_64:
-                seg.append((r_64, r_cap, 1))          # medium rows: LPR lanes per row
-            if n > r_cap:
-                seg.append((r_cap, n, 0))             # short rows: pipelined kernel
-        else:
-            mean = self.nnz / n
-            if use_short and mean <= 2 * lpr:
-                seg = [(0, n, 0)]
-            else:
-                seg = [(0, n, smax if mean >= 64 else 1)]
-        flat = [x for t in seg for x in t]
-        self._segments[key] = (len(seg), _lib.i64_array(flat))
+        if key not in self._segments:
+            self._segments[key] = segment_table(self.rowlen, key, self.reordered,
+                                                self.long_threshold if self.n_chunks else None)
         return self._segments[key]
 
     def hot_rows(self, k: int) -> int:
