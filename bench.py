@@ -130,6 +130,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_traffic(workload):
+    """DRAM bytes per term of the SpMM launches from the committed ncu
+    capture (profiles/r01_traffic.json), or None."""
+    p = ROOT / "profiles" / "r01_traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text()).get(workload)
+    if not d:
+        return None, None
+    return float(d["dram_bytes_per_term"]), d["source"]
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -353,6 +365,7 @@ def run_sped(args):
                          stored, any(a != 0 for a in al), lf != 0.0)
     peak, peak_src = measured_peak()
     achieved = bpt / t_term_s / 1e9
+    traffic, traffic_src = measured_traffic(spec["name"]) if not sharded else (None, None)
     launches_per_step = n_terms + 5
     if sharded:
         launches_per_step = n_terms * 2 + 5
@@ -422,9 +435,11 @@ def run_sped(args):
                                       "gram+coeffs+update": solve_ms / args.steps,
                                       "per_term": 1e3 * t_term_s},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "spmm_term_kernel (one fused polynomial term)",
-                         "algorithmic_bytes_per_launch": bpt, "peak_source": peak_src},
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "spmm_term_kernel + spmm_chunk_kernel (one fused polynomial term)",
+                         "algorithmic_bytes_per_launch": bpt, "peak_source": peak_src,
+                         "traffic_source": traffic_src,
+                         "dram_frac_actual": (traffic / t_term_s / 1e9 / peak) if traffic else None},
             "cpu_baseline": cpu,
             "time_to_angle": conv,
             "e2e": e2e,
