@@ -18,6 +18,9 @@
  *                              (+ restated per-term composition)
  *   sped_gram / sped_mueg_coeffs / sped_block_update
  *                              mu_eg_step                        solvers.py:121-144
+ *   sped_small_mueg / sped_persistent_mueg
+ *                              run_solver's step loop (mu-eg)    solvers.py:227-292
+ *                              (whole steps per launch)          solvers.py:121-144
  *   sped_oja_coeffs (+ gram/update)  oja_step + _orthonormalize  solvers.py:84-118
  *   sped_pcg64_integers        Generator(PCG64).integers(0,m,B)  solvers.py:171
  *   sped_kmeans_*              kmeans_cluster                    metrics.py:143-176
@@ -153,6 +156,18 @@ int sped_small_mueg(int32_t n, int32_t k, const int32_t* indptr, const int32_t* 
                     const double* beta, const double* gamma, double w0_scale, double lam_f,
                     double s_final, double eta, int32_t steps, float* V, int32_t* flag,
                     sped_stream_t stream);
+/* Grid-resident fast path (k <= 32): `steps` whole mu-EG steps in ONE
+ * cooperative launch (one CTA per SM, grid barriers between phases; state in
+ * HBM/L2).  Same contract as sped_small_mueg; `workspace` of at least
+ * sped_persistent_workspace_bytes(n, k) bytes (two n x k blocks + Gram
+ * partials). */
+int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* bytes);
+int sped_persistent_mueg(int32_t n, int32_t k, const int32_t* indptr, const int32_t* indices,
+                         const float* values, int32_t n_terms, const double* alpha,
+                         const double* beta, const double* gamma, double w0_scale,
+                         double lam_f, double s_final, double eta, int32_t steps, float* V,
+                         int32_t* flag, void* workspace, int64_t workspace_bytes,
+                         sped_stream_t stream);
 /* out = (P*A + M*B) * diag(scale).  A k x k fp32; M may be NULL; B may be
  * NULL meaning B = eta*I; scale may be NULL (ones).  upper != 0 promises A is
  * upper triangular (mu-EG), letting the kernel skip the zero half. */

@@ -289,6 +289,7 @@ class LaplacianOperator:
         self.epos = epos
         self.edge_w = None if graph.is_unit_weight() else w.to(torch.float32)
         self.rowlen = np.diff(self.indptr.cpu().numpy().astype(np.int64))
+        self.max_row_nnz = int(self.rowlen.max()) if n else 0
         self.long_threshold = int(long_threshold)
         self.chunk_len = int(chunk_len)
         self._plan()

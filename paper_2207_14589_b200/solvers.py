@@ -14,6 +14,7 @@ Public step functions accept numpy or CUDA states; numpy in -> numpy out.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import time
 import warnings
@@ -443,17 +444,82 @@ class _SmallStepper:
     cur = 0
 
 
+PERSISTENT_MAX_NK = 1 << 22
+
+
+def persistent_solver_eligible(op, k: int, solver: str) -> bool:
+    """Graphs small enough that a mu-EG step is launch bound run whole steps
+    inside one grid-resident launch (sped_persistent_mueg, K7): polynomial
+    transforms, k <= 32, n*k <= 4M, no row longer than 512 nonzeros (one
+    thread per output entry walks its row, so a hub row would serialise the
+    term)."""
+    if not (solver == "mu-eg" and isinstance(op, TransformedOperator)
+            and op.transform.is_polynomial and k <= 32 and op.n * k <= PERSISTENT_MAX_NK
+            and op.n_terms <= 64):
+        return False
+    return op.laplacian.max_row_nnz <= 512
+
+
+class _PersistentStepper:
+    """Many whole mu-EG steps per cooperative launch (K7)."""
+
+    def __init__(self, op: TransformedOperator, eta: float, V0: torch.Tensor):
+        self.op, self.eta = op, eta
+        self.V_ = V0.clone().contiguous()
+        k = int(V0.shape[1])
+        self.ws = StepWorkspace(op.n, k, V0.device)
+        lib = _lib.load()
+        nbytes = ctypes.c_int64(0)
+        _lib.check(lib.sped_persistent_workspace_bytes(op.n, k, ctypes.byref(nbytes)),
+                   "sped_persistent_workspace_bytes")
+        self.scratch = torch.empty(int(nbytes.value), dtype=torch.uint8, device=V0.device)
+        al, be, ga, w0, lf, s = op.schedule
+        self._coef = (len(al), _lib.dbl_array(al), _lib.dbl_array(be), _lib.dbl_array(ga),
+                      float(w0), float(lf), float(s))
+
+    def advance(self, m: int):
+        if m <= 0:
+            return
+        lib = _lib.load()
+        lap = self.op.laplacian
+        nt, al, be, ga, w0, lf, s = self._coef
+        rc = lib.sped_persistent_mueg(lap.n, int(self.V_.shape[1]), _lib.ptr(lap.indptr),
+                                      _lib.ptr(lap.indices), _lib.ptr(lap.values), nt, al, be,
+                                      ga, w0, lf, s, float(self.eta), int(m),
+                                      _lib.ptr(self.V_), _lib.ptr(self.ws.flag),
+                                      _lib.ptr(self.scratch), self.scratch.numel(),
+                                      _lib.stream_ptr(self.V_.device))
+        _lib.check(rc, "sped_persistent_mueg")
+
+    def step(self):
+        self.advance(1)
+
+    @property
+    def V(self):
+        return self.V_
+
+    @property
+    def bufs(self):
+        return [self.V_]
+
+    cur = 0
+
+
 def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
                mode: str = "unnormalized", ground_truth: GroundTruth | None = None,
                operator: TransformedOperator | None = None,
                streak_target: int | None = None, subspace_target: float | None = None,
                stop_on_targets: bool = False, record_timing: bool = True,
                device=None, use_cuda_graphs: bool = True,
-               index_source: str = "device", use_small_kernel: bool = False) -> SolverRun:
+               index_source: str = "device", use_small_kernel: bool = False,
+               use_persistent_kernel: bool | None = None) -> SolverRun:
     """Run a solver on the reversed transformed Laplacian (solvers.py:227-292),
     entirely on the device.  Metrics are evaluated on the host every
     ``eval_every`` steps against the original Laplacian's bottom-k truth
-    (dense, n <= 5000, as in the reference)."""
+    (dense, n <= 5000, as in the reference).  Deterministic polynomial
+    mu-EG runs on small graphs use the grid-resident kernel K7
+    (``use_persistent_kernel=None`` = when eligible), other graphable runs
+    replay whole steps as CUDA graphs."""
     if config.k > g.n:
         raise ValueError("k exceeds the node count")
     dev = _lib.require_cuda(device)
@@ -505,8 +571,12 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
     out_order = (lambda X: lap.from_internal(X)) if internal else (lambda X: X)
     steps_done = 0
     if graphable:
+        persistent = (persistent_solver_eligible(op, config.k, config.solver)
+                      if use_persistent_kernel is None else use_persistent_kernel)
         if use_small_kernel and small_solver_eligible(op, config.k, config.solver):
             stepper = _SmallStepper(op, config.eta, V)
+        elif persistent:
+            stepper = _PersistentStepper(op, config.eta, V)
         else:
             stepper = _GraphStepper(op, config.solver, config.eta, V)
         t = 0

@@ -234,12 +234,19 @@ def test_run_solver_cuda_graph_equals_eager(cuda, golden):
     g = _graph(golden, "cfg1")
     t = sp.SpectralTransform("negexp-limit", 13)
     cfg = sp.SolverConfig(solver="mu-eg", k=10, eta=0.1, steps=40, eval_every=20, seed=1)
-    a = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=True)
+    a = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=True,
+                      use_persistent_kernel=False)
     b = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=False)
     assert torch.equal(a.V, b.V)
     # the single-block kernel (K2, opt-in): same result to fp32 rounding
     c = sp.run_solver(g, t, cfg, record_timing=False, use_small_kernel=True)
     assert rel_fro(c.V.cpu().numpy(), b.V.cpu().numpy()) <= 1e-5
+    # the grid-resident kernel (K7, the default here): same to fp32 rounding,
+    # and bit-reproducible run to run
+    d = sp.run_solver(g, t, cfg, record_timing=False)
+    e = sp.run_solver(g, t, cfg, record_timing=False, use_persistent_kernel=True)
+    assert rel_fro(d.V.cpu().numpy(), b.V.cpu().numpy()) <= 1e-5
+    assert torch.equal(d.V, e.V)
     cfg = sp.SolverConfig(solver="oja", k=10, eta=0.1, steps=40, eval_every=20, seed=1)
     a = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=True)
     b = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=False)
@@ -337,3 +344,63 @@ def test_small_single_block_solver_vs_reference(cuda, golden, name, mode, kind, 
         st.advance(1)
         V1 = op.laplacian.from_internal(st.V).cpu().numpy()
         assert rel_fro(V1, golden[f"{base}/mueg/{eta}"]) <= 1e-5, eta
+
+
+@pytest.mark.parametrize("name,mode,kind,ell,k", [("cfg1", "unnormalized", "negexp-limit", 13, 10),
+                                                  ("er0", "unnormalized", "negexp-limit", 9, 3),
+                                                  ("er1", "normalized", "negexp-taylor", 8, 4)])
+def test_persistent_solver_vs_reference(cuda, golden, name, mode, kind, ell, k):
+    """sped_persistent_mueg (K7): one whole mu-EG step in one cooperative
+    launch == the reference's mu_eg_step (goldens) to 1e-5."""
+    sp = _sp()
+    from paper_2207_14589_b200.solvers import _PersistentStepper, persistent_solver_eligible
+    op = sp.make_reversed_operator(_graph(golden, name), sp.SpectralTransform(kind, ell), mode)
+    base = f"step/{name}/{mode}/{kind}/{ell}/{k}"
+    V0 = torch.as_tensor(golden[base + "/V0"], dtype=torch.float32, device="cuda")
+    assert persistent_solver_eligible(op, k, "mu-eg")
+    for eta in (0.05, 0.5):
+        st = _PersistentStepper(op, eta, op.laplacian.to_internal(V0))
+        st.advance(1)
+        V1 = op.laplacian.from_internal(st.V).cpu().numpy()
+        assert rel_fro(V1, golden[f"{base}/mueg/{eta}"]) <= 1e-5, eta
+        assert not st.ws.take_flag()
+
+
+@pytest.mark.parametrize("graph,mode,kind,ell,eta,k", [
+    ("cfg2", "normalized", "negexp-limit", 17, 1.0, 16),
+    ("sbm20k", "normalized", "negexp-taylor", 12, 0.1, 32),
+    ("sbm20k", "unnormalized", "negexp-limit", 9, 0.3, 7)])
+def test_persistent_solver_multi_cta(cuda, graph, mode, kind, ell, eta, k):
+    """K7 on graphs spread over every SM (config 2's 10^4-node grid; a 2x10^4
+    node SBM with stored normalized values / implicit unit weights, odd k):
+    25 steps equal the CUDA-graph multi-kernel path to fp32 rounding, and the
+    oracle's fp64 steps to 1e-4."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    from paper_2207_14589_b200.solvers import (_GraphStepper, _PersistentStepper,
+                                               persistent_solver_eligible)
+    if graph == "cfg2":
+        n, u, v, w = G.config_graph(2)
+    else:
+        n, u, v, w = G.sbm_sparse(20000, 100, 20.0, 0.9)
+    g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
+    op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell), mode)
+    assert persistent_solver_eligible(op, k, "mu-eg")
+    V0 = sp.init_state(n, k, 11).V
+    Vi = op.laplacian.to_internal(V0)
+    p = _PersistentStepper(op, eta, Vi)
+    q = _GraphStepper(op, "mu-eg", eta, Vi)
+    p.advance(25)
+    q.advance(25)
+    Vp = op.laplacian.from_internal(p.V).cpu().numpy()
+    Vq = op.laplacian.from_internal(q.V).cpu().numpy()
+    assert rel_fro(Vp, Vq) <= 1e-5
+    csr = O.laplacian_csr(n, g.u, g.v, g.w, mode)
+    lam = O.choose_lambda_star(kind, O.lambda_upper(n, g.u, g.v, g.w, mode))
+    Vo = V0.cpu().numpy().astype(np.float64)
+    for _ in range(25):
+        Vo = O.mu_eg_step(Vo, O.apply_transform(csr, kind, ell, 1e-6, lam, Vo), eta)
+    assert rel_fro(Vp, Vo) <= 1e-4
+    p2 = _PersistentStepper(op, eta, Vi)
+    p2.advance(25)
+    assert torch.equal(p.V, p2.V)
