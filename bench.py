@@ -209,7 +209,8 @@ def time_to_angle(cfg=1, target=1e-3, eval_every=50, max_steps=20000, cpu=True,
     import oracle as O
     import paper_2207_14589_b200 as sp
     from paper_2207_14589_b200 import generators as G
-    from paper_2207_14589_b200.solvers import _GraphStepper, _SmallStepper, small_solver_eligible
+    from paper_2207_14589_b200.solvers import (_GraphStepper, _PersistentStepper,
+                                               persistent_solver_eligible)
     spec = G.CONFIGS[cfg]
     k = spec["k"]
     n, u, v, w = G.config_graph(cfg)
@@ -224,23 +225,32 @@ def time_to_angle(cfg=1, target=1e-3, eval_every=50, max_steps=20000, cpu=True,
     init_seed, _, _ = O.solver_seeds(0)
     op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell), spec["mode"])
     V0 = sp.init_state(n, k, init_seed).V
-    small = False  # the multi-SM CUDA-graph path is faster than the single-block K2 kernel
     Vi = op.laplacian.to_internal(V0)
-    stepper = _SmallStepper(op, eta, Vi) if small else _GraphStepper(op, "mu-eg", eta, Vi)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    gpu_steps = None
-    for t in range(eval_every, max_steps + 1, eval_every):
-        stepper.advance(eval_every)
-        Vh = op.laplacian.from_internal(stepper.V).cpu().numpy().astype(np.float64)
-        if sp.principal_angles(Vh, U) <= target:
-            gpu_steps = t
-            break
-    gpu_s = time.perf_counter() - t0
+
+    def run_gpu(stepper):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for t in range(eval_every, max_steps + 1, eval_every):
+            stepper.advance(eval_every)
+            Vh = op.laplacian.from_internal(stepper.V).cpu().numpy().astype(np.float64)
+            if sp.principal_angles(Vh, U) <= target:
+                return t, time.perf_counter() - t0
+        return None, time.perf_counter() - t0
+
+    # the multi-kernel CUDA-graph path, and the grid-resident K7 kernel (the
+    # default for graphs this small) -- same steps, same result to fp32 rounding
+    graph_steps, graph_s = run_gpu(_GraphStepper(op, "mu-eg", eta, Vi))
+    gpu_path, gpu_steps, gpu_s = "CUDA-graph steps", graph_steps, graph_s
     out = {"config": spec["name"], "transform": f"{kind}({ell})", "eta": eta, "k": k,
-           "gpu_path": "single-block K2 kernel (sped_small_mueg)" if small else "CUDA-graph steps",
            "target_angle": target, "eval_every": eval_every,
-           "gpu_steps": gpu_steps, "gpu_s": gpu_s}
+           "gpu_steps_cuda_graph": graph_steps, "gpu_s_cuda_graph": graph_s}
+    if persistent_solver_eligible(op, k, "mu-eg"):
+        p_steps, p_s = run_gpu(_PersistentStepper(op, eta, Vi))
+        out.update(gpu_steps_persistent=p_steps, gpu_s_persistent=p_s)
+        if p_steps is not None:
+            gpu_path, gpu_steps, gpu_s = ("grid-resident K7 kernel (sped_persistent_mueg)",
+                                          p_steps, p_s)
+    out.update(gpu_path=gpu_path, gpu_steps=gpu_steps, gpu_s=gpu_s)
     if cpu:
         csr = O.laplacian_csr(n, g.u, g.v, g.w, spec["mode"])
         lam = O.choose_lambda_star(kind, O.lambda_upper(n, g.u, g.v, g.w, spec["mode"]))

@@ -158,12 +158,12 @@ int sped_small_mueg(int32_t n, int32_t k, const int32_t* indptr, const int32_t* 
                     sped_stream_t stream);
 /* Grid-resident fast path (k <= 32): `steps` whole mu-EG steps in ONE
  * cooperative launch (one CTA per SM, grid barriers between phases; state in
- * HBM/L2).  Same contract as sped_small_mueg; `workspace` of at least
- * sped_persistent_workspace_bytes(n, k) bytes (two n x k blocks + Gram
- * partials). */
+ * HBM/L2).  Same contract as sped_small_mueg; `nnz` = indptr[n] (host copy,
+ * sizes the launch); `workspace` of at least sped_persistent_workspace_bytes(n, k)
+ * bytes (two n x k blocks + Gram partials). */
 int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* bytes);
-int sped_persistent_mueg(int32_t n, int32_t k, const int32_t* indptr, const int32_t* indices,
-                         const float* values, int32_t n_terms, const double* alpha,
+int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
+                         const int32_t* indices, const float* values, int32_t n_terms, const double* alpha,
                          const double* beta, const double* gamma, double w0_scale,
                          double lam_f, double s_final, double eta, int32_t steps, float* V,
                          int32_t* flag, void* workspace, int64_t workspace_bytes,

@@ -49,7 +49,7 @@ SIGNATURES = {
     "sped_small_mueg": (C.c_int, [_i32, _i32, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64, _f64,
                                   _f64, _i32, _p, _p, _p]),
     "sped_persistent_workspace_bytes": (C.c_int, [_i32, _i32, _p]),
-    "sped_persistent_mueg": (C.c_int, [_i32, _i32, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64,
+    "sped_persistent_mueg": (C.c_int, [_i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64,
                                        _f64, _f64, _i32, _p, _p, _p, _i64, _p]),
     "sped_axpby": (C.c_int, [_i64, _f64, _p, _f64, _p, _p, _p]),
     "sped_pcg64_workspace_bytes": (_sz, [_i64]),

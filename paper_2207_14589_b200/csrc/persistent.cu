@@ -30,17 +30,33 @@
 
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cmath>
+
 #include "sped_common.cuh"
 
 namespace cg = cooperative_groups;
 
+#ifdef PT_PROFILE  // probe build: CTA 0 records per-phase times of step 1
+#define PT_MARK(name)                                                          \
+  do {                                                                         \
+    if (step == 1 && b == 0 && tid == 0 && pt_n < 64) {                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt_t[pt_n]));           \
+      pt_name[pt_n++] = name;                                                  \
+    }                                                                          \
+  } while (0)
+#else
+#define PT_MARK(name) \
+  do {                \
+  } while (0)
+#endif
+
 namespace sped {
 namespace {
 
-constexpr int PT_THREADS = 1024;
 constexpr int PT_MAX_K = 32;
 constexpr int PT_MAX_TERMS = 64;
-constexpr int PT_STAGE_BYTES = 96 * 1024;  // dynamic smem for staged own rows
+constexpr int PT_DYN_BYTES = 180 * 1024;  // dynamic smem: own rows + CSR slice
 
 struct PArgs {
   int32_t n, k, nterms;
@@ -51,6 +67,7 @@ struct PArgs {
   float w0, lamf, sfin;
   double eta;
   int32_t steps;
+  int32_t slots;  // nonzero slots per row (lanes per row = slots * k)
   float* V;  // in/out
   float* B0;
   float* B1;
@@ -78,6 +95,20 @@ __device__ __forceinline__ void entry_cols(int e, int k, int nS, int nC, int& ca
   }
 }
 
+// Scatter reduced Gram entry e into the dense S (symmetric), C and diag Q.
+__device__ __forceinline__ void put_gram(double* Gs, int e, int k, int nS, int nC, double g) {
+  int ca, cb;
+  entry_cols(e, k, nS, nC, ca, cb);
+  if (e < nS) {
+    Gs[ca * k + cb] = g;
+    Gs[cb * k + ca] = g;
+  } else if (e < nS + nC) {
+    Gs[k * k + ca * k + cb] = g;
+  } else {
+    Gs[2 * k * k + ca] = g;
+  }
+}
+
 __device__ __forceinline__ int row_lower_bound(const int32_t* indptr, int n, int64_t target) {
   int lo = 0, hi = n;  // first row r with indptr[r] >= target
   while (lo < hi) {
@@ -90,33 +121,95 @@ __device__ __forceinline__ int row_lower_bound(const int32_t* indptr, int n, int
   return lo;
 }
 
+template <int PT_THREADS>
 __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PArgs a) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ float stage[];  // own rows of X and M for the Gram partials
+  extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ double Gs[2 * PT_MAX_K * PT_MAX_K + PT_MAX_K];  // S, C, diag Q
+  __shared__ double Ad[PT_MAX_K * PT_MAX_K];                 // A (fp64)
+  __shared__ double Tn[PT_MAX_K * PT_MAX_K];                 // column-norm terms
+  __shared__ double red[PT_THREADS];
   __shared__ float Acoef[PT_MAX_K * PT_MAX_K];
   __shared__ float scale[PT_MAX_K];
 
   const int n = a.n, k = a.k, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int nb = gridDim.x, b = blockIdx.x;
   const int64_t nnz = __ldg(a.indptr + n);
   // nnz-balanced contiguous row range, identical for every phase
   const int r0 = (b == 0) ? 0 : row_lower_bound(a.indptr, n, nnz * b / nb);
   const int r1 = (b == nb - 1) ? n : row_lower_bound(a.indptr, n, nnz * (b + 1) / nb);
+  const int nr = r1 - r0;
   const int64_t i0 = (int64_t)r0 * k, i1 = (int64_t)r1 * k;
   const int nS = k * (k + 1) / 2, nC = k * k, nE = nS + nC + k;
-  const int stage_rows = max(1, PT_STAGE_BYTES / (int)(2 * sizeof(float) * k));
   const bool has_vals = (a.values != nullptr);
   const float eta_f = (float)a.eta;
 
+  // ---- shared-memory residency of this CTA's slice --------------------------
+  // Layout of the dynamic buffer: [CSR slice of own rows][state].  The state
+  // is either resident (own rows of X in two generations + M, kept across
+  // phases) or a staging area the Gram streams own rows through.
+  const size_t blk = (size_t)nr * k * sizeof(float);
+  const bool resident = 3 * blk <= (size_t)PT_DYN_BYTES;
+  const int e0 = __ldg(a.indptr + r0), e1 = __ldg(a.indptr + r1);
+  const size_t csr_bytes =
+      (sizeof(int32_t) * ((size_t)nr + 1 + (size_t)(e1 - e0) * (has_vals ? 2 : 1)) + 15) & ~size_t(15);
+  const size_t min_state = resident ? 3 * blk : 2 * sizeof(float) * k * 64;
+  const bool csr_smem = csr_bytes + min_state <= (size_t)PT_DYN_BYTES;
+  const size_t state_off = csr_smem ? csr_bytes : 0;
+  int32_t* cptr = reinterpret_cast<int32_t*>(dyn);
+  int32_t* cidx = cptr + nr + 1;
+  float* cval = reinterpret_cast<float*>(cidx + (e1 - e0));
+  float* sXa = reinterpret_cast<float*>(dyn + state_off);
+  float* sXb = sXa + (size_t)nr * k;  // resident mode only
+  float* sM = sXb + (size_t)nr * k;   // resident mode only
+  if (csr_smem) {
+    for (int i = tid; i <= nr; i += PT_THREADS) cptr[i] = __ldg(a.indptr + r0 + i) - e0;
+    for (int i = tid; i < e1 - e0; i += PT_THREADS) {
+      cidx[i] = __ldg(a.indices + e0 + i);
+      if (has_vals) cval[i] = __ldg(a.values + e0 + i);
+    }
+  }
+  if (resident)
+    for (int i = tid; i < nr * k; i += PT_THREADS) sXa[i] = a.V[i0 + i];
+  // non-resident CTAs stage own rows in chunks through the state area
+  const int stage_rows =
+      max(1, (int)(((size_t)PT_DYN_BYTES - state_off) / (2 * sizeof(float) * k)));
+  const int* rp = csr_smem ? cptr : a.indptr + r0;  // row pointers of own rows
+  const int rbase = csr_smem ? 0 : e0;               // rp[] - rbase indexes ix/vx
+  const int32_t* ix = csr_smem ? cidx : a.indices + e0;
+  const float* vx = csr_smem ? cval : (has_vals ? a.values + e0 : nullptr);
+  __syncthreads();
+
+  // Gram work split: `parts` threads per entry, `per_pass` entries per pass
+  const int parts = max(1, PT_THREADS / nE), per_pass = PT_THREADS / parts;
+  const int passes = (nE + per_pass - 1) / per_pass;  // <= 2 for k <= 32
+  // small partial tables are reduced redundantly by every CTA (one grid
+  // barrier less per step); large ones by one warp per entry
+  const bool redundant_reduce = (int64_t)nb * nE <= 8192;
+  // term lanes: a row is S nonzero slots x k columns; a warp takes RW rows
+  const int S = a.slots, LR = S * k, RW = 32 / LR;
+  const int lg = lane / LR, lrem = lane - lg * LR, lc = lrem % k, ls = lrem / k;
+  const bool active = lg < RW;
+  const int rows_per_pass = (PT_THREADS / 32) * RW;
+
   float* X = a.V;
+  float* sX = sXa;   // own rows of X (resident mode)
+  float* sXn = sXb;  // next generation
   float* bufs[3] = {a.V, a.B0, a.B1};
   int xi = 0;  // which of bufs holds X
 
+#ifdef PT_PROFILE
+  uint64_t pt_t[64];
+  const char* pt_name[64];
+  int pt_n = 0;
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt_t[pt_n]));
+  pt_name[pt_n++] = "start";
+#endif
   for (int step = 0; step < a.steps; ++step) {
     float* P0 = bufs[(xi + 1) % 3];
     float* P1 = bufs[(xi + 2) % 3];
-    // ---- M = p(L) X ---------------------------------------------------------
+    // ---- M = p(L) X: RW rows per warp, S slots x k columns per row ---------
     const float* win = X;
     float* M = P0;
     for (int t = 0; t < a.nterms; ++t) {
@@ -124,117 +217,182 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
       float* wout = (t & 1) ? P1 : P0;
       const float sc = (t == 0) ? a.w0 : 1.f;
       const float al = a.alpha[t], be = a.beta[t] * sc, ga = a.gamma[t] * sc;
-      for (int64_t i = i0 + tid; i < i1; i += PT_THREADS) {
-        const int r = (int)(i / k), c = (int)(i - (int64_t)r * k);
-        const int rb = __ldg(a.indptr + r), re = __ldg(a.indptr + r + 1);
-        float acc0 = 0.f, acc1 = 0.f;
-        int p = rb;
-        for (; p + 1 < re; p += 2) {  // two independent gather chains
-          const int c0 = __ldg(a.indices + p), c1 = __ldg(a.indices + p + 1);
-          const float v0 = has_vals ? __ldg(a.values + p) : (c0 == r ? (float)(re - rb - 1) : -1.f);
-          const float v1 = has_vals ? __ldg(a.values + p + 1) : (c1 == r ? (float)(re - rb - 1) : -1.f);
-          acc0 = fmaf(v0, __ldcg(win + (int64_t)c0 * k + c), acc0);
-          acc1 = fmaf(v1, __ldcg(win + (int64_t)c1 * k + c), acc1);
+      for (int lr0 = warp * RW; lr0 < nr; lr0 += rows_per_pass) {
+        const int lr = min(lr0 + lg, nr - 1);  // idle groups re-read the last row
+        const bool own = active && (lr0 + lg < nr);
+        const int r = r0 + lr;
+        const int rb = rp[lr] - rbase, re = rp[lr + 1] - rbase;
+        const float dg = (float)(re - rb - 1);
+        const int64_t i = (int64_t)r * k + lc;
+        const bool lead = (ls == 0 && own);
+        // own-row operands issued before the gathers (independent loads)
+        const float wself = (lead && ga != 0.f) ? __ldcg(win + i) : 0.f;
+        const float xv = (lead && (al != 0.f || final))
+                             ? (resident ? sX[lr * k + lc] : __ldcg(X + i)) : 0.f;
+        float acc = 0.f;
+        if (active) {
+          // all of a lane's gathers (up to 8) in flight at once, predicated
+          for (int base = rb + ls; base < re; base += 8 * S) {
+            int c[8];
+            float v[8], x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int p = base + j * S;
+              c[j] = (p < re) ? ix[p] : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int p = base + j * S;
+              v[j] = (c[j] < 0) ? 0.f : (has_vals ? vx[p] : (c[j] == r ? dg : -1.f));
+              x[j] = (c[j] < 0) ? 0.f : __ldcg(win + (int64_t)c[j] * k + lc);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc = fmaf(v[j], x[j], acc);
+          }
         }
-        if (p < re) {
-          const int c0 = __ldg(a.indices + p);
-          const float v0 = has_vals ? __ldg(a.values + p) : (c0 == r ? (float)(re - rb - 1) : -1.f);
-          acc0 = fmaf(v0, __ldcg(win + (int64_t)c0 * k + c), acc0);
+        float tot = acc;  // slots folded in fixed order
+        for (int s2 = 1; s2 < S; ++s2) {
+          const float o = __shfl_sync(0xffffffffu, acc, lg * LR + s2 * k + lc);
+          if (ls == 0) tot += o;
         }
-        float o = be * (acc0 + acc1);
-        if (al != 0.f) o = fmaf(al, __ldcg(X + i), o);
-        if (ga != 0.f) o = fmaf(ga, __ldcg(win + i), o);
-        if (final) o = fmaf(a.lamf, __ldcg(X + i), a.sfin * o);
-        wout[i] = o;
+        if (lead) {
+          float o = be * tot;
+          if (al != 0.f) o = fmaf(al, xv, o);
+          if (ga != 0.f) o = fmaf(ga, wself, o);
+          if (final) {
+            o = fmaf(a.lamf, xv, a.sfin * o);
+            if (resident) sM[lr * k + lc] = o;  // M is only read back by this CTA
+          }
+          if (!(final && resident)) wout[i] = o;
+        }
       }
       win = wout;
       M = wout;
+      PT_MARK("term");
+#ifdef PT_PROFILE
+      __syncthreads();
+      PT_MARK("term-cta");
+#endif
       if (!final) grid.sync();
+      PT_MARK("term-sync");
     }
     if (a.nterms == 0) {
       M = P0;
-      for (int64_t i = i0 + tid; i < i1; i += PT_THREADS) M[i] = (a.lamf + a.sfin * a.w0) * __ldcg(X + i);
+      for (int64_t i = i0 + tid; i < i1; i += PT_THREADS) {
+        const float o = (a.lamf + a.sfin * a.w0) * (resident ? sX[i - i0] : __ldcg(X + i));
+        if (resident)
+          sM[i - i0] = o;
+        else
+          M[i] = o;
+      }
     }
     float* Xn = (M == P0) ? P1 : P0;  // free buffer for X'
     __syncthreads();                  // own rows of M complete
 
     // ---- Gram partials over own rows (fp64 accumulation, fixed order) ------
     {
-      float* sX = stage;
-      float* sM = stage + (size_t)stage_rows * k;
-      double acc0 = 0.0, acc1 = 0.0;  // entries tid and tid + PT_THREADS
-      for (int rr = r0; rr < r1; rr += stage_rows) {
-        const int nr = min(stage_rows, r1 - rr);
-        for (int i = tid; i < nr * k; i += PT_THREADS) {
-          sX[i] = __ldcg(X + (int64_t)rr * k + i);
-          sM[i] = __ldcg(M + (int64_t)rr * k + i);
+      double acc[2] = {0.0, 0.0};
+      const int chunk = resident ? max(nr, 1) : stage_rows;
+      float* qX = resident ? sX : sXa;
+      float* qM = resident ? sM : sXa + (size_t)stage_rows * k;
+      for (int rr = 0; rr < nr; rr += chunk) {
+        const int nrr = min(chunk, nr - rr);
+        if (!resident) {
+          for (int i = tid; i < nrr * k; i += PT_THREADS) {
+            qX[i] = __ldcg(X + i0 + (int64_t)rr * k + i);
+            qM[i] = __ldcg(M + i0 + (int64_t)rr * k + i);
+          }
+          __syncthreads();
         }
-        __syncthreads();
-        for (int e = tid, slot = 0; e < nE; e += PT_THREADS, ++slot) {
-          int ca, cb;
-          entry_cols(e, k, nS, nC, ca, cb);
-          const float* P = (e < nS + nC) ? sX : sM;
-          const float* R = (e < nS) ? sX : sM;
+        for (int pass = 0; pass < passes; ++pass) {
+          const int e = pass * per_pass + tid / parts, q = tid % parts;
           double s = 0.0;
-          for (int r = 0; r < nr; ++r) s += (double)P[r * k + ca] * (double)R[r * k + cb];
-          if (slot == 0)
-            acc0 += s;
-          else
-            acc1 += s;
+          if (tid < per_pass * parts && e < nE) {
+            int ca, cb;
+            entry_cols(e, k, nS, nC, ca, cb);
+            const float* P = (e < nS + nC) ? qX : qM;
+            const float* R = (e < nS) ? qX : qM;
+            for (int r = q; r < nrr; r += parts) s += (double)P[r * k + ca] * (double)R[r * k + cb];
+          }
+          red[tid] = s;
+          __syncthreads();
+          if (tid < per_pass) {
+            double t2 = 0.0;
+            for (int qq = 0; qq < parts; ++qq) t2 += red[tid * parts + qq];
+            acc[pass] += t2;
+          }
+          __syncthreads();
         }
-        __syncthreads();
       }
-      if (tid < nE) a.partials[(size_t)b * nE + tid] = acc0;
-      if (tid + PT_THREADS < nE) a.partials[(size_t)b * nE + tid + PT_THREADS] = acc1;
+      for (int pass = 0; pass < passes; ++pass) {
+        const int e = pass * per_pass + tid;
+        if (tid < per_pass && e < nE) a.partials[(size_t)b * nE + e] = acc[pass];
+      }
     }
+    PT_MARK("gram");
     grid.sync();
+    PT_MARK("gram-sync");
 
-    // ---- reduce: one warp per entry, fixed lane order + shuffle tree ------
-    {
-      const int warp = (b * PT_THREADS + tid) >> 5, lane = tid & 31;
+    // ---- reduce the per-CTA partials (fixed order) --------------------------
+    if (redundant_reduce) {  // 8 lanes per entry, all of a lane's loads in flight
+      const int sub = lane & 7;
+      for (int e0 = warp * 4; e0 < nE; e0 += (PT_THREADS / 32) * 4) {
+        const int e = e0 + (lane >> 3);
+        double s = 0.0;
+        if (e < nE) {
+#pragma unroll 4
+          for (int q = sub; q < nb; q += 8) s += __ldcg(a.partials + (size_t)q * nE + e);
+        }
+        s += __shfl_down_sync(0xffffffffu, s, 4, 8);
+        s += __shfl_down_sync(0xffffffffu, s, 2, 8);
+        s += __shfl_down_sync(0xffffffffu, s, 1, 8);
+        if (sub == 0 && e < nE) put_gram(Gs, e, k, nS, nC, s);
+      }
+    } else {
+      const int gw = b * (PT_THREADS / 32) + warp;
       const int nwarps = nb * (PT_THREADS / 32);
-      for (int e = warp; e < nE; e += nwarps) {
+      for (int e = gw; e < nE; e += nwarps) {
         double s = 0.0;
         for (int q = lane; q < nb; q += 32) s += __ldcg(a.partials + (size_t)q * nE + e);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
         if (lane == 0) a.G[e] = s;
       }
+      grid.sync();
+      for (int e = tid; e < nE; e += PT_THREADS) put_gram(Gs, e, k, nS, nC, __ldcg(a.G + e));
     }
-    grid.sync();
+    __syncthreads();
+    PT_MARK("reduce");
 
-    // ---- coefficients (every CTA, fp64) ------------------------------------
-    for (int e = tid; e < nE; e += PT_THREADS) {
-      int ca, cb;
-      entry_cols(e, k, nS, nC, ca, cb);
-      const double g = __ldcg(a.G + e);
-      if (e < nS) {
-        Gs[ca * k + cb] = g;
-        Gs[cb * k + ca] = g;
-      } else if (e < nS + nC) {
-        Gs[k * k + ca * k + cb] = g;
-      } else {
-        Gs[2 * k * k + ca] = g;
+    // ---- coefficients (every CTA, fp64; solvers.py:121-144 in Gram form) ---
+    const double* Sg = Gs;
+    const double* Cg = Gs + k * k;
+    const double eta = a.eta;
+    if (tid < k) {  // column i of A: -eta C[r,i] above, 1 - eta d_i on the diagonal
+      const int i = tid;
+      double d = Cg[i * k + i];
+      for (int j = 0; j < i; ++j) d -= Sg[i * k + j] * Cg[j * k + i];
+      for (int r = 0; r < k; ++r)
+        Ad[r * k + i] = (r < i) ? -eta * Cg[r * k + i] : (r == i ? 1.0 - eta * d : 0.0);
+    }
+    __syncthreads();
+    // norm terms T[bb,i] = A[bb,i] (sum_{r<=i} S[bb,r] A[r,i] + 2 eta C[bb,i]), bb <= i
+    for (int q = tid; q < PT_MAX_K * PT_MAX_K; q += PT_THREADS) {
+      const int tb = q / PT_MAX_K, ti = q % PT_MAX_K;
+      double tval = 0.0;
+      if (tb < k && ti < k && tb <= ti) {
+        double sa = 0.0;
+        for (int r = 0; r <= ti; ++r) sa += Sg[tb * k + r] * Ad[r * k + ti];
+        tval = Ad[tb * k + ti] * (sa + 2.0 * eta * Cg[tb * k + ti]);
       }
+      Tn[q] = tval;
     }
     __syncthreads();
     if (tid < k) {
       const int i = tid;
-      const double* S = Gs;
-      const double* C = Gs + k * k;
-      const double eta = a.eta;
-      double d = C[i * k + i];
-      for (int j = 0; j < i; ++j) d -= S[i * k + j] * C[j * k + i];
-      double acol[PT_MAX_K];
-      for (int r = 0; r < k; ++r)
-        acol[r] = (r < i) ? -eta * C[r * k + i] : (r == i ? 1.0 - eta * d : 0.0);
       double nrm2 = eta * eta * Gs[2 * k * k + i];
-      for (int bb = 0; bb <= i; ++bb) {
-        double sa = 0.0;
-        for (int r = 0; r <= i; ++r) sa += S[bb * k + r] * acol[r];
-        nrm2 += acol[bb] * sa + 2.0 * eta * acol[bb] * C[bb * k + i];
-      }
-      for (int r = 0; r < k; ++r) Acoef[r * k + i] = (float)acol[r];
+      for (int bb = 0; bb <= i; ++bb) nrm2 += Tn[bb * PT_MAX_K + i];
+      for (int r = 0; r < k; ++r) Acoef[r * k + i] = (float)Ad[r * k + i];
       const double nrm = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
       if (!(nrm >= 1e-12)) {
         if (b == 0) atomicExch(a.flag, 1);
@@ -248,17 +406,39 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
     // ---- update own rows: X' = (X A + eta M) diag(scale) ------------------
     for (int64_t i = i0 + tid; i < i1; i += PT_THREADS) {
       const int r = (int)(i / k), c = (int)(i - (int64_t)r * k);
-      const float* xr = X + (int64_t)r * k;
-      float acc = 0.f;
-      for (int q = 0; q <= c; ++q) acc = fmaf(__ldcg(xr + q), Acoef[q * k + c], acc);
-      Xn[i] = fmaf(eta_f, __ldcg(M + i), acc) * scale[c];
+      float acc = 0.f, m;
+      if (resident) {
+        const float* xr = sX + (r - r0) * k;
+        for (int q = 0; q <= c; ++q) acc = fmaf(xr[q], Acoef[q * k + c], acc);
+        m = sM[i - i0];
+      } else {
+        const float* xr = X + (int64_t)r * k;
+        for (int q = 0; q <= c; ++q) acc = fmaf(__ldcg(xr + q), Acoef[q * k + c], acc);
+        m = __ldcg(M + i);
+      }
+      const float o = fmaf(eta_f, m, acc) * scale[c];
+      Xn[i] = o;
+      if (resident) sXn[i - i0] = o;
     }
     X = Xn;
+    {
+      float* tmp = sX;
+      sX = sXn;
+      sXn = tmp;
+    }
     xi = (Xn == bufs[(xi + 1) % 3]) ? (xi + 1) % 3 : (xi + 2) % 3;
+    PT_MARK("coef+upd");
     grid.sync();
+    PT_MARK("upd-sync");
   }
   if (X != a.V)
-    for (int64_t i = i0 + tid; i < i1; i += PT_THREADS) a.V[i] = __ldcg(X + i);
+    for (int64_t i = i0 + tid; i < i1; i += PT_THREADS)
+      a.V[i] = resident ? sX[i - i0] : __ldcg(X + i);
+#ifdef PT_PROFILE
+  if (b == 0 && tid == 0)
+    for (int q = 2; q < pt_n; ++q)
+      printf("pt %-10s %7.3f us\n", pt_name[q], (pt_t[q] - pt_t[q - 1]) * 1e-3);
+#endif
 }
 
 }  // namespace
@@ -274,13 +454,14 @@ extern "C" int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* by
   return SPED_OK;
 }
 
-extern "C" int sped_persistent_mueg(int32_t n, int32_t k, const int32_t* indptr,
+extern "C" int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
                                     const int32_t* indices, const float* values, int32_t n_terms,
                                     const double* alpha, const double* beta, const double* gamma,
                                     double w0_scale, double lam_f, double s_final, double eta,
                                     int32_t steps, float* V, int32_t* flag, void* workspace,
                                     int64_t workspace_bytes, sped_stream_t stream) {
-  SPED_CHECK_ARG(n >= 1 && k >= 1 && V && flag && indptr && indices && workspace && steps >= 0,
+  SPED_CHECK_ARG(n >= 1 && k >= 1 && nnz >= 0 && V && flag && indptr && indices && workspace &&
+                     steps >= 0,
                  "bad persistent_mueg arguments");
   if (k > PT_MAX_K || n_terms > PT_MAX_TERMS) {
     set_error("persistent solver supports k <= %d and <= %d terms", PT_MAX_K, PT_MAX_TERMS);
@@ -291,21 +472,34 @@ extern "C" int sped_persistent_mueg(int32_t n, int32_t k, const int32_t* indptr,
   SPED_CHECK_ARG(workspace_bytes >= need, "persistent workspace too small (%lld < %lld)",
                  (long long)workspace_bytes, (long long)need);
   if (steps == 0) return SPED_OK;
+  // block size: 512 threads when every warp of a 512-thread grid already
+  // holds at most one row group (cheaper barriers), else 1024
+  const double avg = (double)nnz / n;
+  int slots = (int)std::ceil(avg / 8.0);  // ~8 gathers in flight per lane
+  slots = std::max(1, std::min(slots, 32 / k));
+  const int rw = 32 / (slots * k);
+  const int sms = num_sms();
+  const bool small_block = (int64_t)n <= (int64_t)sms * 16 * rw;
+  const int nt = small_block ? 512 : 1024;
+  const void* fn = small_block ? (const void*)persistent_mueg_kernel<512>
+                               : (const void*)persistent_mueg_kernel<1024>;
   static bool attr = false;
   if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PT_STAGE_BYTES));
+    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<512>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
+    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<1024>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
     attr = true;
   }
   int per_sm = 0;
-  SPED_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persistent_mueg_kernel,
-                                                          PT_THREADS, PT_STAGE_BYTES));
+  SPED_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, PT_DYN_BYTES));
   if (per_sm < 1) {
     set_error("persistent solver kernel cannot be resident");
     return SPED_ERR_CUDA;
   }
-  // one CTA per SM, but never more CTAs than there are rows
-  const int grid = (int)std::min<int64_t>(num_sms(), n);
+  // one CTA per SM, but no more CTAs than it takes to give each warp a row group
+  const int64_t rows_per_cta = (int64_t)(nt / 32) * rw;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (n + rows_per_cta - 1) / rows_per_cta));
   const int64_t nE = (int64_t)k * (k + 1) / 2 + (int64_t)k * k + k;
   PArgs a;
   a.n = n;
@@ -324,6 +518,7 @@ extern "C" int sped_persistent_mueg(int32_t n, int32_t k, const int32_t* indptr,
   a.sfin = (float)s_final;
   a.eta = eta;
   a.steps = steps;
+  a.slots = slots;
   a.V = V;
   char* ws = static_cast<char*>(workspace);
   a.B0 = reinterpret_cast<float*>(ws);
@@ -334,8 +529,7 @@ extern "C" int sped_persistent_mueg(int32_t n, int32_t k, const int32_t* indptr,
   a.G = a.partials + (size_t)grid * nE;
   a.flag = flag;
   void* args[] = {&a};
-  SPED_CUDA(cudaLaunchCooperativeKernel((const void*)persistent_mueg_kernel, dim3(grid),
-                                        dim3(PT_THREADS), args, PT_STAGE_BYTES,
+  SPED_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(nt), args, PT_DYN_BYTES,
                                         as_stream(stream)));
   return SPED_OK;
 }

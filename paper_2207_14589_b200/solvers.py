@@ -483,7 +483,8 @@ class _PersistentStepper:
         lib = _lib.load()
         lap = self.op.laplacian
         nt, al, be, ga, w0, lf, s = self._coef
-        rc = lib.sped_persistent_mueg(lap.n, int(self.V_.shape[1]), _lib.ptr(lap.indptr),
+        rc = lib.sped_persistent_mueg(lap.n, int(self.V_.shape[1]), int(lap.nnz),
+                                      _lib.ptr(lap.indptr),
                                       _lib.ptr(lap.indices), _lib.ptr(lap.values), nt, al, be,
                                       ga, w0, lf, s, float(self.eta), int(m),
                                       _lib.ptr(self.V_), _lib.ptr(self.ws.flag),
