@@ -16,6 +16,9 @@
 // All k x k algebra runs on the device in fp64 so the whole step can be
 // captured in one CUDA graph (no host round trip).
 
+#include <cstdlib>
+
+#include "async_copy.cuh"
 #include "sped_common.cuh"
 
 namespace sped {
@@ -289,6 +292,182 @@ __global__ void __launch_bounds__(256) block_update_rows(
   }
 }
 
+// v2 update for k in {32, 64, 128}: out = (P A [+ M B | + eta M]) diag(s).
+// Memory bound (reads P and M once, writes out once), so the kernel is built
+// around the copy: warp 8 streams tiles of TR rows of P (and M) through a
+// cp.async.bulk ring of NSTAGE shared-memory stages; warps 0-7 each take a
+// row at a time, lane c owning output columns c, c+32, ... (KPL = K/32 per
+// lane) with the matching columns of A (and B) held in REGISTERS.  The P row
+// is read as float4 broadcasts (one shared-memory wavefront per 4 inputs),
+// M and the output are coalesced 128-B rows.
+template <int K>
+struct UpdCfg {
+  static constexpr int KPL = K / 32;
+  static constexpr int NSTAGE = 4;
+  static constexpr int STAGE_BYTES = 16384;  // P + M rows of one stage
+};
+
+template <int K, int MODE>  // MODE 0: P A; 1: P A + eta M; 2: P A + M B
+__global__ void __launch_bounds__(288) block_update_v2(int64_t n, const float* __restrict__ P,
+                                                      const float* __restrict__ A,
+                                                      const float* __restrict__ M,
+                                                      const float* __restrict__ B, float eta,
+                                                      const float* __restrict__ scale,
+                                                      float* __restrict__ out, int tr) {
+  using namespace ::sped::async;
+  constexpr int KPL = UpdCfg<K>::KPL, NS = UpdCfg<K>::NSTAGE;
+  extern __shared__ __align__(128) float stage[];
+  __shared__ uint64_t full[NS], empty[NS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int stage_floats = tr * K * (MODE == 0 ? 1 : 2);
+  const int64_t ntiles = (n + tr - 1) / tr;
+  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int64_t j = 0; j < my_tiles; ++j) {
+        const int st = (int)(j % NS);
+        if (j >= NS) mbar_wait(&empty[st], (uint32_t)(((j / NS) - 1) & 1));
+        const int64_t r0 = (blockIdx.x + j * gridDim.x) * (int64_t)tr;
+        const int rows = (int)min((int64_t)tr, n - r0);
+        const uint32_t bytes = (uint32_t)rows * K * 4u;
+        float* dst = stage + (size_t)st * stage_floats;
+        mbar_expect_tx(&full[st], (MODE == 0 ? 1u : 2u) * bytes);
+        bulk_g2s(dst, P + r0 * K, bytes, &full[st]);
+        if (MODE != 0) bulk_g2s(dst + tr * K, M + r0 * K, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  // A (and B) columns of this lane in registers
+  float a[K][KPL];
+  float bm[MODE == 2 ? K : 1][KPL];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      a[i][j] = __ldg(A + i * K + lane + 32 * j);
+      if (MODE == 2) bm[i][j] = __ldg(B + i * K + lane + 32 * j);
+    }
+  float sc[KPL];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) sc[j] = scale ? __ldg(scale + lane + 32 * j) : 1.f;
+  for (int64_t j = 0; j < my_tiles; ++j) {
+    const int st = (int)(j % NS);
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * (int64_t)tr;
+    const int rows = (int)min((int64_t)tr, n - r0);
+    mbar_wait(&full[st], (uint32_t)((j / NS) & 1));
+    const float* ps = stage + (size_t)st * stage_floats;
+    const float* ms = ps + tr * K;
+    // k = 32: two rows per pass (r, r + 8) reuse the A registers and
+    // interleave two FMA chains; k = 64 keeps one row (register budget)
+    constexpr int RB = (K == 32) ? 2 : 1;
+    for (int r = warp; r < rows; r += 8 * RB) {
+      const bool two = RB == 2 && (r + 8 < rows);
+      const int r2 = two ? r + 8 : r;
+      float acc[2][KPL];
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) acc[0][q] = acc[1][q] = 0.f;
+      const float4* prow0 = reinterpret_cast<const float4*>(ps + r * K);
+      const float4* prow1 = reinterpret_cast<const float4*>(ps + r2 * K);
+#pragma unroll
+      for (int i4 = 0; i4 < K / 4; ++i4) {
+        const float4 p0 = prow0[i4];  // broadcasts
+        const float4 p1 = (RB == 2) ? prow1[i4] : p0;
+#pragma unroll
+        for (int q = 0; q < KPL; ++q) {
+          acc[0][q] = fmaf(p0.x, a[4 * i4 + 0][q], acc[0][q]);
+          acc[0][q] = fmaf(p0.y, a[4 * i4 + 1][q], acc[0][q]);
+          acc[0][q] = fmaf(p0.z, a[4 * i4 + 2][q], acc[0][q]);
+          acc[0][q] = fmaf(p0.w, a[4 * i4 + 3][q], acc[0][q]);
+          if (RB == 2) {
+            acc[1][q] = fmaf(p1.x, a[4 * i4 + 0][q], acc[1][q]);
+            acc[1][q] = fmaf(p1.y, a[4 * i4 + 1][q], acc[1][q]);
+            acc[1][q] = fmaf(p1.z, a[4 * i4 + 2][q], acc[1][q]);
+            acc[1][q] = fmaf(p1.w, a[4 * i4 + 3][q], acc[1][q]);
+          }
+        }
+      }
+      if (MODE == 2) {
+        const float4* mrow0 = reinterpret_cast<const float4*>(ms + r * K);
+        const float4* mrow1 = reinterpret_cast<const float4*>(ms + r2 * K);
+#pragma unroll
+        for (int i4 = 0; i4 < K / 4; ++i4) {
+          const float4 m0 = mrow0[i4];
+          const float4 m1 = (RB == 2) ? mrow1[i4] : m0;
+#pragma unroll
+          for (int q = 0; q < KPL; ++q) {
+            acc[0][q] = fmaf(m0.x, bm[4 * i4 + 0][q], acc[0][q]);
+            acc[0][q] = fmaf(m0.y, bm[4 * i4 + 1][q], acc[0][q]);
+            acc[0][q] = fmaf(m0.z, bm[4 * i4 + 2][q], acc[0][q]);
+            acc[0][q] = fmaf(m0.w, bm[4 * i4 + 3][q], acc[0][q]);
+            if (RB == 2) {
+              acc[1][q] = fmaf(m1.x, bm[4 * i4 + 0][q], acc[1][q]);
+              acc[1][q] = fmaf(m1.y, bm[4 * i4 + 1][q], acc[1][q]);
+              acc[1][q] = fmaf(m1.z, bm[4 * i4 + 2][q], acc[1][q]);
+              acc[1][q] = fmaf(m1.w, bm[4 * i4 + 3][q], acc[1][q]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        const int rr = h ? r2 : r;
+        float* orow = out + (r0 + rr) * K;
+#pragma unroll
+        for (int q = 0; q < KPL; ++q) {
+          float o = acc[h][q];
+          if (MODE == 1) o = fmaf(eta, ms[rr * K + lane + 32 * q], o);
+          __stcs(orow + lane + 32 * q, o * sc[q]);
+        }
+      }
+    }
+    mbar_arrive(&empty[st]);
+  }
+}
+
+template <int K>
+int launch_v2(int64_t n, const float* P, const float* A, const float* M, const float* B, float eta,
+              const float* scale, float* out, cudaStream_t s) {
+  using C = UpdCfg<K>;
+  const int mode = M ? (B ? 2 : 1) : 0;
+  const int tr = C::STAGE_BYTES / (K * 4 * (mode == 0 ? 1 : 2));
+  const size_t smem = (size_t)C::NSTAGE * C::STAGE_BYTES;
+  // register budget: A (and B) columns live in registers, so k = 64 with
+  // M*B (Oja) takes the v1 kernel
+  static bool attr = false;
+  if (!attr) {
+    SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if constexpr (K == 32)
+      SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t ntiles = (n + tr - 1) / tr;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * 2));
+  switch (mode) {
+    case 0: block_update_v2<K, 0><<<grid, 288, smem, s>>>(n, P, A, M, B, eta, scale, out, tr); break;
+    case 1: block_update_v2<K, 1><<<grid, 288, smem, s>>>(n, P, A, M, B, eta, scale, out, tr); break;
+    default:
+      if constexpr (K == 32) {
+        block_update_v2<K, 2><<<grid, 288, smem, s>>>(n, P, A, M, B, eta, scale, out, tr);
+        break;
+      }
+      set_error("update v2: M*B needs k = 32");
+      return SPED_ERR_UNSUPPORTED;
+  }
+  SPED_LAUNCH_CHECK();
+  return SPED_OK;
+}
+
 template <int K>
 int launch_rows(int64_t n, const float* P, const float* A, const float* M, const float* B,
                 float eta, const float* scale, float* out, bool upper, cudaStream_t s) {
@@ -402,10 +581,16 @@ extern "C" int sped_block_update(int64_t n, int32_t k, const float* P, const flo
                         16) == 0;
   if (aligned) {
     const bool upper = (upper_flag != 0);
+    static const bool v1 = [] {
+      const char* e = getenv("SPED_UPDATE_V1");
+      return e && e[0] == '1';
+    }();
     switch (k) {
       case 16: return launch_update<16>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 32: return launch_rows<32>(n, P, A, M, B, (float)eta, scale, out, upper, s);
-      case 64: return launch_rows<64>(n, P, A, M, B, (float)eta, scale, out, upper, s);
+      case 32: return v1 ? launch_rows<32>(n, P, A, M, B, (float)eta, scale, out, upper, s)
+                         : launch_v2<32>(n, P, A, M, B, (float)eta, scale, out, s);
+      case 64: return (v1 || (M && B)) ? launch_rows<64>(n, P, A, M, B, (float)eta, scale, out, upper, s)
+                                       : launch_v2<64>(n, P, A, M, B, (float)eta, scale, out, s);
       case 128: return launch_rows<128>(n, P, A, M, B, (float)eta, scale, out, upper, s);
       default: break;
     }
