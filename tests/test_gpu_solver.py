@@ -325,6 +325,9 @@ def test_block_update_vs_fp64(cuda, k):
         ws.update(P, A.contiguous(), M, Bm, eta, sc, out, upper=upper)
         ref = (Pd @ Ad + (Md @ Bd if Bm is not None else eta * Md)) * sd
         assert rel_fro(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-6, (upper, Bm is not None)
+    # no M, no scale (the CholQR2 / orthonormalisation form)
+    ws.update(P, A.contiguous(), None, None, 0.0, None, out)
+    assert rel_fro(out.cpu().numpy(), (Pd @ Ad).cpu().numpy()) <= 1e-6
 
 
 @pytest.mark.parametrize("name,mode,kind,ell,k", [("cfg1", "unnormalized", "negexp-limit", 13, 10),
