@@ -105,13 +105,19 @@ int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_threshold,
  * lane groups per row); n_segments == 0 means one warp per row.  Gathered rows
  * with index < hot_rows are cached with L2 evict_last, others evict_first.
  * w_init (optional) lets a row shard start from its halo-extended block
- * while x stays its own rows.  x / w_init must not alias out, w_a or w_b. */
+ * while x stays its own rows.  x / w_init must not alias out, w_a or w_b.
+ * row_scale (optional, fp32[n] = d_i^-1/2): the caller asserts L is the
+ * normalized Laplacian of a unit-weight graph without self loops; terms after
+ * the first then run on u = D^-1/2 w and skip the values stream (values must
+ * still be given: the first term reads them).  Ignored for k not in
+ * {4,...,128}, unaligned buffers, w_init, or opt-in short-row segments. */
 int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                         const int32_t* indices, const float* values,
                         int32_t long_threshold, int32_t chunk_len,
                         const int32_t* chunk_desc, int64_t n_chunks,
                         float* partials, int32_t* tickets,
                         const int64_t* segments, int32_t n_segments, int64_t hot_rows,
+                        const float* row_scale,
                         const float* x, const float* w_init, float* w_a, float* w_b, float* out,
                         int32_t n_terms, const double* alpha, const double* beta,
                         const double* gamma, double w0_scale, double lam_f,

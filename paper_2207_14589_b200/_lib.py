@@ -37,7 +37,7 @@ SIGNATURES = {
     "sped_spmm_plan": (C.c_int, [_i64, _p, _i32, _i32, _p, _i64, C.POINTER(_i64),
                                  C.POINTER(_i64), _p]),
     "sped_csr_poly_apply": (C.c_int, [_i64, _i32, _p, _p, _p, _i32, _i32, _p, _i64, _p, _p, _p,
-                                      _i32, _i64, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _f64,
+                                      _i32, _i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _f64,
                                       _f64, _f64, _p]),
     "sped_edge_batch_poly_apply": (C.c_int, [_i64, _i32, _i64, _p, _p, _p, _p, _p, _i64, _p, _p,
                                              _p, _p, _p, _i32, _p, _p, _p, _f64, _f64, _f64, _p]),

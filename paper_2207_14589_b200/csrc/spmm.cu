@@ -19,7 +19,10 @@
 //  * index/value/x streams use L2::evict_first, gathered w rows
 //    L2::evict_last so the block being multiplied stays in the 126 MB L2;
 //  * unweighted combinatorial Laplacians use implicit values (-1 off the
-//    diagonal, row_len-1 on it): 4 B per nonzero instead of 8.
+//    diagonal, row_len-1 on it): 4 B per nonzero instead of 8;
+//  * unweighted NORMALIZED Laplacians (no self loops) run every term after
+//    the first on the scaled block u = D^-1/2 w: (L w)_i = w_i -
+//    d_i^-1/2 sum_{j~i} u_j needs no values either (VM 2, row_scale = d^-1/2).
 //  * column slabs of <= 128 floats (row stride `ld`) cover any k.
 
 #include <cstdlib>
@@ -49,6 +52,8 @@ enum TermFlags : int {
   TF_GAMMA = 2,   // gamma != 0: read w row
   TF_FINAL = 4,   // last term: out = lam_f*x + s*w'
   TF_LAMF = 8,    // lam_f != 0
+  TF_NORM_IN = 16,    // win holds u = D^-1/2 w; gathers are unweighted (VM 2)
+  TF_SCALE_OUT = 32,  // write u' = D^-1/2 w' (the next term gathers it)
 };
 
 struct TermArgs {
@@ -72,12 +77,17 @@ struct TermArgs {
   int32_t* tickets;
   int64_t row_begin, row_end;  // this launch's row segment
   int64_t hot_rows;        // gathered rows < hot_rows are kept in L2 (evict_last)
+  const float* rscale;     // d^-1/2 per row (TF_NORM_IN / TF_SCALE_OUT)
 };
 
-template <bool IMPLICIT>
+// VM 0: stored values; 1: implicit combinatorial (-1, row_len-1 on the
+// diagonal); 2: implicit normalized on the scaled block (1 off the diagonal,
+// the diagonal handled in the epilogue)
+template <int VM>
 __device__ __forceinline__ float entry_value(const float* values, int64_t p, int32_t col, int64_t row,
                                              int32_t rowlen) {
-  if (IMPLICIT) return col == row ? (float)(rowlen - 1) : -1.0f;
+  if (VM == 1) return col == row ? (float)(rowlen - 1) : -1.0f;
+  if (VM == 2) return col == row ? 0.0f : 1.0f;
   return ld_stream_f32(values + p);
 }
 
@@ -195,7 +205,7 @@ __device__ __forceinline__ void st_stream_vec(float* p, const Vf<W>& x) {
 // per round.  Loop bounds are warp-uniform (max over the warp's rows) so the
 // shuffles stay convergent; rows are predicated.  Returns the folded row sum
 // in the sub==0 lanes of each group.
-template <int W, int LPR, int SUB, int U, bool IMPLICIT>
+template <int W, int LPR, int SUB, int U, int VM>
 __device__ __forceinline__ Vf<W> group_row_accumulate(const TermArgs& a, int32_t row, bool valid,
                                                       int32_t b, int32_t e, int32_t rowlen,
                                                       int lane) {
@@ -228,8 +238,10 @@ __device__ __forceinline__ Vf<W> group_row_accumulate(const TermArgs& a, int32_t
 #else
       col = ld_idx(a.indices + p);
 #endif
-      if (IMPLICIT)
+      if (VM == 1)
         val = col == row ? (float)(rowlen - 1) : -1.0f;
+      else if (VM == 2)
+        val = col == row ? 0.0f : 1.0f;
       else
 #if SPED_HINTS
         val = ld_val_pol(a.values + p, pol_cold);
@@ -271,22 +283,35 @@ __device__ __forceinline__ Vf<W> group_row_accumulate(const TermArgs& a, int32_t
   return acc;
 }
 
+// ds = d_i^-1/2 (only read with TF_NORM_IN / TF_SCALE_OUT).  With TF_NORM_IN
+// the own row wr is u_i = ds*w_i and y the unweighted neighbour sum of u:
+// (L w)_i = u_i/ds - ds*y_i.
 template <int W>
 __device__ __forceinline__ Vf<W> term_epilogue(const TermArgs& a, const Vf<W>& y, const Vf<W>& xr,
-                                               const Vf<W>& wr) {
+                                               const Vf<W>& wr, float ds = 1.f) {
   Vf<W> r;
+  const float inv = (a.flags & TF_NORM_IN) ? 1.0f / ds : 1.f;
 #pragma unroll
   for (int i = 0; i < W; ++i) {
-    float t = a.beta * y.v[i];
+    float lw = y.v[i], wv = wr.v[i];
+    if (a.flags & TF_NORM_IN) {
+      wv = wr.v[i] * inv;
+      lw = fmaf(-ds, y.v[i], wv);
+    }
+    float t = a.beta * lw;
     if (a.flags & TF_ALPHA) t = fmaf(a.alpha, xr.v[i], t);
-    if (a.flags & TF_GAMMA) t = fmaf(a.gamma, wr.v[i], t);
+    if (a.flags & TF_GAMMA) t = fmaf(a.gamma, wv, t);
     if (a.flags & TF_FINAL) {
       t *= a.sfin;
       if (a.flags & TF_LAMF) t = fmaf(a.lamf, xr.v[i], t);
     }
+    if (a.flags & TF_SCALE_OUT) t *= ds;
     r.v[i] = t;
   }
   return r;
+}
+__device__ __forceinline__ float row_ds(const TermArgs& a, int64_t row) {
+  return (a.flags & (TF_NORM_IN | TF_SCALE_OUT)) ? __ldg(a.rscale + row) : 1.f;
 }
 
 __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, float4 xr, float4 wr) {
@@ -302,7 +327,7 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
 // chunk's nonzeros).  The last chunk of a row to finish (ticket) folds the
 // partial rows in chunk order and applies the epilogue: deterministic, no
 // float atomics.
-template <int W, int LPR, int U, bool IMPLICIT>
+template <int W, int LPR, int U, int VM>
 __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   const int lane = threadIdx.x & 31;
   const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
@@ -313,7 +338,7 @@ __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
   const int32_t pe = a.chunk_desc[4 * c + 2];
   const int32_t c0 = a.chunk_desc[4 * c + 3];
   const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
-  const Vf<W> acc = group_row_accumulate<W, LPR, 32 / LPR, U, IMPLICIT>(
+  const Vf<W> acc = group_row_accumulate<W, LPR, 32 / LPR, U, VM>(
       a, row, true, pb, pe, re - rb, lane);
   const int lsub = lane / LPR, lcl = lane % LPR;
   if (lsub == 0) {
@@ -345,13 +370,13 @@ __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
     xr.zero();
     wr.zero();
     if (need_x) xr = ld_stream_vec<W>(a.x + off);
-    if (a.flags & TF_GAMMA) wr = ldg_vec<W>(a.win + off);
-    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, y, xr, wr));
+    if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
+    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, y, xr, wr, row_ds(a, row)));
   }
   if (lane == 0) a.tickets[c0] = 0;
 }
 
-template <int W, int LPR, int SUB, int U, bool IMPLICIT>
+template <int W, int LPR, int SUB, int U, int VM>
 __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : TERM_MIN_BLOCKS)) spmm_term_kernel(const TermArgs a) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
@@ -369,7 +394,7 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : TERM_MIN_BLO
     if (e - b > a.long_thresh) valid = false;
   }
   if (__all_sync(0xffffffffu, !valid)) return;
-  const Vf<W> acc = group_row_accumulate<W, LPR, SUB, U, IMPLICIT>(a, row, valid, b, e, e - b, lane);
+  const Vf<W> acc = group_row_accumulate<W, LPR, SUB, U, VM>(a, row, valid, b, e, e - b, lane);
   if (valid && sub == 0) {
     const int64_t off = (int64_t)row * a.ld + cl * W;
     const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
@@ -377,15 +402,15 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : TERM_MIN_BLO
     xr.zero();
     wr.zero();
     if (need_x) xr = ld_stream_vec<W>(a.x + off);
-    if (a.flags & TF_GAMMA) wr = ldg_vec<W>(a.win + off);
-    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, acc, xr, wr));
+    if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
+    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
   }
 }
 
 #ifndef SHORT_U
 #define SHORT_U 4
 #endif
-template <int LPR, bool IMPLICIT>
+template <int LPR, int VM>
 __global__ void __launch_bounds__(256, 4) spmm_short_kernel(const TermArgs a) {
   constexpr int G = LPR;
   constexpr int RPW = 32 / G;
@@ -421,7 +446,7 @@ __global__ void __launch_bounds__(256, 4) spmm_short_kernel(const TermArgs a) {
       val[q] = 0.f;
       if (p < e) {
         col[q] = ld_stream_i32(a.indices + p);
-        val[q] = entry_value<IMPLICIT>(a.values, p, col[q], row, e - b);
+        val[q] = entry_value<VM>(a.values, p, col[q], row, e - b);
       }
     }
   };
@@ -484,7 +509,7 @@ __global__ void __launch_bounds__(256, 4) spmm_short_kernel(const TermArgs a) {
       float v = 0.f;
       if (o + g < len) {
         c = ld_stream_i32(a.indices + p);
-        v = entry_value<IMPLICIT>(a.values, p, c, row, len);
+        v = entry_value<VM>(a.values, p, c, row, len);
       }
       const int cnt = max(0, min(G, len - o));
 #pragma unroll
@@ -519,32 +544,32 @@ __global__ void __launch_bounds__(256, 4) spmm_short_kernel(const TermArgs a) {
 }
 
 template <int LPR>
-static void launch_short(const TermArgs& a, bool implicit, cudaStream_t s) {
+static void launch_short(const TermArgs& a, int vm, cudaStream_t s) {  // vm 0 / 1
   const int64_t rows = a.row_end - a.row_begin;
   const int64_t batches = (rows + (32 / LPR) - 1) / (32 / LPR);
   // persistent grid = exactly the resident capacity (no second wave)
   static int per_sm[2] = {0, 0};
-  int& ps = per_sm[implicit ? 1 : 0];
+  int& ps = per_sm[vm == 1 ? 1 : 0];
   if (ps == 0) {
-    if (implicit)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, true>, 256, 0);
+    if (vm == 1)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, 1>, 256, 0);
     else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, false>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, 0>, 256, 0);
     if (ps < 1) ps = 1;
   }
   const int64_t blocks = std::min<int64_t>((batches + 7) / 8, (int64_t)num_sms() * ps);
   const unsigned grid = (unsigned)blocks;
   if (grid == 0) return;
-  if (implicit)
-    spmm_short_kernel<LPR, true><<<grid, 256, 0, s>>>(a);
+  if (vm == 1)
+    spmm_short_kernel<LPR, 1><<<grid, 256, 0, s>>>(a);
   else
-    spmm_short_kernel<LPR, false><<<grid, 256, 0, s>>>(a);
+    spmm_short_kernel<LPR, 0><<<grid, 256, 0, s>>>(a);
 }
 
 // Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
 // lanes over columns (CPL columns each), SUB groups over nonzeros.  Handles
 // every row itself (no long-row plan).
-template <int LPR, int CPL, bool IMPLICIT>
+template <int LPR, int CPL, int VM>
 __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
   constexpr int SUB = 32 / LPR;
   const int lane = threadIdx.x & 31;
@@ -562,7 +587,7 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
     float val = 0.f;
     if (p < e) {
       col = ld_stream_i32(a.indices + p);
-      val = entry_value<IMPLICIT>(a.values, p, col, row, e - b);
+      val = entry_value<VM>(a.values, p, col, row, e - b);
     }
     const int cnt = min(32, e - p0);
     const int T = (cnt + SUB - 1) / SUB;
@@ -617,7 +642,7 @@ constexpr int UNROLL = 4;
 
 template <int W, int LPR, int SUB,
           int U = (SUB > 1 ? (W == 8 ? 4 : LONG_U) : (W == 8 ? W8_U : SUB1_U))>
-static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
+static void launch_fast(const TermArgs& a, int vm, cudaStream_t s) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
   const int threads = 256;
@@ -626,66 +651,70 @@ static void launch_fast(const TermArgs& a, bool implicit, cudaStream_t s) {
   const int64_t warps = (rows + RPW - 1) / RPW;
   const unsigned grid = (unsigned)((warps + wpb - 1) / wpb);
   if (grid == 0) return;
-  if (implicit)
-    spmm_term_kernel<W, LPR, SUB, U, true><<<grid, threads, 0, s>>>(a);
+  if (vm == 1)
+    spmm_term_kernel<W, LPR, SUB, U, 1><<<grid, threads, 0, s>>>(a);
+  else if (vm == 2)
+    spmm_term_kernel<W, LPR, SUB, U, 2><<<grid, threads, 0, s>>>(a);
   else
-    spmm_term_kernel<W, LPR, SUB, U, false><<<grid, threads, 0, s>>>(a);
+    spmm_term_kernel<W, LPR, SUB, U, 0><<<grid, threads, 0, s>>>(a);
 }
 
 template <int W, int LPR>
-static void launch_chunks(const TermArgs& a, bool implicit, cudaStream_t s) {
+static void launch_chunks(const TermArgs& a, int vm, cudaStream_t s) {
   const unsigned grid = (unsigned)((a.n_chunks + 7) / 8);
   if (grid == 0) return;
-  if (implicit)
-    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), true><<<grid, 256, 0, s>>>(a);
+  if (vm == 1)
+    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), 1><<<grid, 256, 0, s>>>(a);
+  else if (vm == 2)
+    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), 2><<<grid, 256, 0, s>>>(a);
   else
-    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), false><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), 0><<<grid, 256, 0, s>>>(a);
 }
 
 template <int W, int LPR>
-static void launch_fast_sub(const TermArgs& a, int sub, bool implicit, cudaStream_t s) {
+static void launch_fast_sub(const TermArgs& a, int sub, int vm, cudaStream_t s) {
   switch (sub) {
-    case 1: launch_fast<W, LPR, 1>(a, implicit, s); break;
-    case 2: if constexpr (LPR * 2 <= 32) { launch_fast<W, LPR, 2>(a, implicit, s); break; } [[fallthrough]];
-    case 4: if constexpr (LPR * 4 <= 32) { launch_fast<W, LPR, 4>(a, implicit, s); break; } [[fallthrough]];
-    case 8: if constexpr (LPR * 8 <= 32) { launch_fast<W, LPR, 8>(a, implicit, s); break; } [[fallthrough]];
-    default: launch_fast<W, LPR, 32 / LPR>(a, implicit, s); break;
+    case 1: launch_fast<W, LPR, 1>(a, vm, s); break;
+    case 2: if constexpr (LPR * 2 <= 32) { launch_fast<W, LPR, 2>(a, vm, s); break; } [[fallthrough]];
+    case 4: if constexpr (LPR * 4 <= 32) { launch_fast<W, LPR, 4>(a, vm, s); break; } [[fallthrough]];
+    case 8: if constexpr (LPR * 8 <= 32) { launch_fast<W, LPR, 8>(a, vm, s); break; } [[fallthrough]];
+    default: launch_fast<W, LPR, 32 / LPR>(a, vm, s); break;
   }
 }
 
 // width dispatch: W = 8 (256-bit gathers) when k % 8 == 0 and rows are 32 B
 // aligned, else W = 4.  lpr = k / W.
 template <int W>
-static void launch_chunks_w(int lpr, const TermArgs& a, bool implicit, cudaStream_t s) {
+static void launch_chunks_w(int lpr, const TermArgs& a, int vm, cudaStream_t s) {
   switch (lpr) {
-    case 1: launch_chunks<W, 1>(a, implicit, s); break;
-    case 2: launch_chunks<W, 2>(a, implicit, s); break;
-    case 4: launch_chunks<W, 4>(a, implicit, s); break;
-    case 8: launch_chunks<W, 8>(a, implicit, s); break;
-    case 16: launch_chunks<W, 16>(a, implicit, s); break;
-    default: if constexpr (W == 4) launch_chunks<W, 32>(a, implicit, s); break;
+    case 1: launch_chunks<W, 1>(a, vm, s); break;
+    case 2: launch_chunks<W, 2>(a, vm, s); break;
+    case 4: launch_chunks<W, 4>(a, vm, s); break;
+    case 8: launch_chunks<W, 8>(a, vm, s); break;
+    case 16: launch_chunks<W, 16>(a, vm, s); break;
+    default: if constexpr (W == 4) launch_chunks<W, 32>(a, vm, s); break;
   }
 }
 template <int W>
-static void launch_rows_w(int lpr, int sub, const TermArgs& a, bool implicit, cudaStream_t s) {
+static void launch_rows_w(int lpr, int sub, const TermArgs& a, int vm, cudaStream_t s) {
   switch (lpr) {
-    case 1: launch_fast_sub<W, 1>(a, sub, implicit, s); break;
-    case 2: launch_fast_sub<W, 2>(a, sub, implicit, s); break;
-    case 4: launch_fast_sub<W, 4>(a, sub, implicit, s); break;
-    case 8: launch_fast_sub<W, 8>(a, sub, implicit, s); break;
-    case 16: launch_fast_sub<W, 16>(a, sub, implicit, s); break;
-    default: if constexpr (W == 4) launch_fast_sub<W, 32>(a, sub, implicit, s); break;
+    case 1: launch_fast_sub<W, 1>(a, sub, vm, s); break;
+    case 2: launch_fast_sub<W, 2>(a, sub, vm, s); break;
+    case 4: launch_fast_sub<W, 4>(a, sub, vm, s); break;
+    case 8: launch_fast_sub<W, 8>(a, sub, vm, s); break;
+    case 16: launch_fast_sub<W, 16>(a, sub, vm, s); break;
+    default: if constexpr (W == 4) launch_fast_sub<W, 32>(a, sub, vm, s); break;
   }
 }
 
 template <int LPR, int CPL>
-static void launch_generic(const TermArgs& a, bool implicit, cudaStream_t s) {
+static void launch_generic(const TermArgs& a, int vm, cudaStream_t s) {  // vm 0 / 1
   const int threads = 256;
   const unsigned grid = grid_for(a.n, threads / 32);
-  if (implicit)
-    spmm_term_generic<LPR, CPL, true><<<grid, threads, 0, s>>>(a);
+  if (vm == 1)
+    spmm_term_generic<LPR, CPL, 1><<<grid, threads, 0, s>>>(a);
   else
-    spmm_term_generic<LPR, CPL, false><<<grid, threads, 0, s>>>(a);
+    spmm_term_generic<LPR, CPL, 0><<<grid, threads, 0, s>>>(a);
 }
 
 struct Segment {
@@ -695,7 +724,7 @@ struct Segment {
 
 // Launch one term over one column slab: one launch per row segment, the
 // long-row chunks riding in the leading blocks of the first launch.
-static int launch_term_slab(TermArgs a, bool implicit, bool aligned, bool aligned32,
+static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
                             const Segment* segs, int nseg, cudaStream_t s) {
   const int k = a.k;
   const bool fast = aligned && (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128);
@@ -708,8 +737,8 @@ static int launch_term_slab(TermArgs a, bool implicit, bool aligned, bool aligne
     const bool w8 = wide && (k % 8 == 0) && aligned32 && k >= 64;
     const int lpr = k / (w8 ? 8 : 4);
     if (a.n_chunks > 0) {
-      if (w8) launch_chunks_w<8>(lpr, a, implicit, s);
-      else launch_chunks_w<4>(lpr, a, implicit, s);
+      if (w8) launch_chunks_w<8>(lpr, a, vm, s);
+      else launch_chunks_w<4>(lpr, a, vm, s);
       SPED_LAUNCH_CHECK();
     }
     for (int i = 0; i < nseg; ++i) {
@@ -718,34 +747,34 @@ static int launch_term_slab(TermArgs a, bool implicit, bool aligned, bool aligne
       int sub = segs[i].sub;
       if (sub == 0 && !w8) {  // software-pipelined short rows (128-bit path only)
         switch (lpr) {
-          case 1: launch_short<1>(a, implicit, s); break;
-          case 2: launch_short<2>(a, implicit, s); break;
-          case 4: launch_short<4>(a, implicit, s); break;
-          case 8: launch_short<8>(a, implicit, s); break;
-          case 16: launch_short<16>(a, implicit, s); break;
-          default: launch_short<32>(a, implicit, s); break;
+          case 1: launch_short<1>(a, vm, s); break;
+          case 2: launch_short<2>(a, vm, s); break;
+          case 4: launch_short<4>(a, vm, s); break;
+          case 8: launch_short<8>(a, vm, s); break;
+          case 16: launch_short<16>(a, vm, s); break;
+          default: launch_short<32>(a, vm, s); break;
         }
         SPED_LAUNCH_CHECK();
         continue;
       }
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
-      if (w8) launch_rows_w<8>(lpr, sub, a, implicit, s);
-      else launch_rows_w<4>(lpr, sub, a, implicit, s);
+      if (w8) launch_rows_w<8>(lpr, sub, a, vm, s);
+      else launch_rows_w<4>(lpr, sub, a, vm, s);
       SPED_LAUNCH_CHECK();
     }
   } else {
     a.chunk_blocks = 0;
     a.long_thresh = INT32_MAX;
-    if (k <= 1) launch_generic<1, 1>(a, implicit, s);
-    else if (k <= 2) launch_generic<2, 1>(a, implicit, s);
-    else if (k <= 4) launch_generic<4, 1>(a, implicit, s);
-    else if (k <= 8) launch_generic<8, 1>(a, implicit, s);
-    else if (k <= 16) launch_generic<16, 1>(a, implicit, s);
-    else if (k <= 32) launch_generic<32, 1>(a, implicit, s);
-    else if (k <= 64) launch_generic<32, 2>(a, implicit, s);
-    else if (k <= 96) launch_generic<32, 3>(a, implicit, s);
-    else launch_generic<32, 4>(a, implicit, s);
+    if (k <= 1) launch_generic<1, 1>(a, vm, s);
+    else if (k <= 2) launch_generic<2, 1>(a, vm, s);
+    else if (k <= 4) launch_generic<4, 1>(a, vm, s);
+    else if (k <= 8) launch_generic<8, 1>(a, vm, s);
+    else if (k <= 16) launch_generic<16, 1>(a, vm, s);
+    else if (k <= 32) launch_generic<32, 1>(a, vm, s);
+    else if (k <= 64) launch_generic<32, 2>(a, vm, s);
+    else if (k <= 96) launch_generic<32, 3>(a, vm, s);
+    else launch_generic<32, 4>(a, vm, s);
     SPED_LAUNCH_CHECK();
   }
   return SPED_OK;
@@ -820,7 +849,8 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                                    int32_t long_threshold, int32_t chunk_len,
                                    const int32_t* chunk_desc, int64_t n_chunks, float* partials,
                                    int32_t* tickets, const int64_t* segments, int32_t n_segments,
-                                   int64_t hot_rows, const float* x, const float* w_init,
+                                   int64_t hot_rows, const float* row_scale, const float* x,
+                                   const float* w_init,
                                    float* w_a, float* w_b,
                                    float* out, int32_t n_terms, const double* alpha,
                                    const double* beta, const double* gamma, double w0_scale,
@@ -842,6 +872,16 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
   cudaStream_t s = as_stream(stream);
   const bool implicit = (values == nullptr);
   const int32_t slabs = (k + 127) / 128;
+  // scaled-block mode (VM 2) for unit-weight normalized Laplacians: the
+  // first term reads the stored values and writes u = D^-1/2 w, later terms
+  // gather u unweighted.  Only on the fast path with every buffer 16-B
+  // aligned and no opt-in short-row segments; otherwise stored values.
+  bool norm = row_scale && values && !w_init && n_terms >= 2 && slabs == 1 &&
+              (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128) &&
+              ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w_a) |
+                reinterpret_cast<uintptr_t>(w_b) | reinterpret_cast<uintptr_t>(out)) % 16 == 0);
+  for (int i = 0; i < n_segments; ++i)
+    if (segments[3 * i + 2] == 0) norm = false;
   Segment segs[8];
   int nseg = n_segments;
   for (int i = 0; i < nseg; ++i) {
@@ -853,7 +893,14 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
   }
   auto term = [&](int32_t t, const float* win, float* wout, float al, float be, float ga,
                   float lf, float sf, int flags) -> int {
-    (void)t;
+    int vm = implicit ? 1 : 0;
+    if (norm) {
+      if (t > 0) {
+        vm = 2;
+        flags |= TF_NORM_IN;
+      }
+      if (!(flags & TF_FINAL)) flags |= TF_SCALE_OUT;
+    }
     for (int32_t sl = 0; sl < slabs; ++sl) {
       const int32_t c0 = sl * 128;
       const int32_t kw = min(128, k - c0);
@@ -883,6 +930,7 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
       a.row_begin = 0;
       a.row_end = n;
       a.hot_rows = hot_rows;
+      a.rscale = row_scale;
       Segment fixed[8];
       int ns = nseg;
       for (int i = 0; i < ns; ++i) fixed[i] = segs[i];
@@ -896,7 +944,7 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                               reinterpret_cast<uintptr_t>(wout);
       const bool aligned = (k % 4 == 0) && (pbits % 16 == 0);
       const bool aligned32 = (k % 8 == 0) && (pbits % 32 == 0);
-      int rc = launch_term_slab(a, implicit, aligned, aligned32, fixed, ns, s);
+      int rc = launch_term_slab(a, vm, aligned, aligned32, fixed, ns, s);
       if (rc != SPED_OK) return rc;
     }
     return SPED_OK;

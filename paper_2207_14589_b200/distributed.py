@@ -257,7 +257,7 @@ class ShardedLaplacian:
             self.n_own, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
             self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
             _lib.ptr(partials), _lib.ptr(self.tickets if self.n_chunks else None), seg, nseg,
-            self.n_own + self.plan.n_halo, _lib.ptr(x_own), _lib.ptr(E),
+            self.n_own + self.plan.n_halo, None, _lib.ptr(x_own), _lib.ptr(E),
             None, None, _lib.ptr(out), 1, _lib.dbl_array([alpha]), _lib.dbl_array([beta]),
             _lib.dbl_array([gamma]), float(w0), float(lam_f), float(s_final),
             _lib.stream_ptr(self.device))

@@ -286,6 +286,15 @@ class LaplacianOperator:
         self.indptr, self.nnz = indptr, nnz
         self.indices = indices[: max(nnz, 1)]
         self.values = None if vals is None else vals[: max(nnz, 1)]
+        # unit-weight normalized Laplacian without self loops: the SpMM runs
+        # terms after the first on u = D^-1/2 w without reading values
+        # (row_scale = d^-1/2 in internal order; SPED_SCALED_NORM=0 disables)
+        self.row_scale = None
+        if (mode == "normalized" and self.values is not None and n > 0
+                and os.environ.get("SPED_SCALED_NORM", "1") != "0" and graph.is_unit_weight()
+                and not bool((u == v).any())):
+            rs = torch.rsqrt(deg[:n].double()).float()
+            self.row_scale = rs[self.perm_rows.long()] if self.perm is not None else rs
         self.epos = epos
         self.edge_w = None if graph.is_unit_weight() else w.to(torch.float32)
         self.rowlen = np.diff(self.indptr.cpu().numpy().astype(np.int64))
@@ -451,7 +460,8 @@ class LaplacianOperator:
                 n, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
                 self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
                 _lib.ptr(partials), _lib.ptr(self._tickets), seg, nseg, self.hot_rows(k),
-                _lib.ptr(xd), None, _lib.ptr(wa), _lib.ptr(wb), _lib.ptr(out), nt,
+                _lib.ptr(self.row_scale), _lib.ptr(xd), None, _lib.ptr(wa), _lib.ptr(wb),
+                _lib.ptr(out), nt,
                 _lib.dbl_array(alpha), _lib.dbl_array(beta), _lib.dbl_array(gamma), float(w0),
                 float(lam_f), float(s_final), _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_csr_poly_apply")

@@ -272,3 +272,34 @@ def test_relabelled_stochastic_oracle_matches_unrelabelled(cuda):
         oracle = sp.make_stochastic_oracle(op, 20000, seed=9)
         outs.append(oracle(x).cpu().numpy())
     assert rel_fro(outs[1], outs[0]) <= PV_TOL
+
+
+@pytest.mark.parametrize("k", [4, 32, 64, 128, 10])
+def test_scaled_normalized_path(cuda, k, monkeypatch):
+    """Unit-weight normalized Laplacians run terms after the first on
+    u = D^-1/2 w without the values stream (row_scale set): every kind
+    matches the oracle, and the stored-values path (SPED_SCALED_NORM=0) to
+    fp32 rounding.  k = 10 (generic kernel) silently keeps stored values."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.chung_lu(30000, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    L = sp.LaplacianOperator(g, "normalized", long_threshold=256, chunk_len=128)
+    assert L.row_scale is not None and L.reordered and L.n_chunks > 0
+    monkeypatch.setenv("SPED_SCALED_NORM", "0")
+    L0 = sp.LaplacianOperator(g, "normalized", long_threshold=256, chunk_len=128)
+    assert L0.row_scale is None
+    csr = O.laplacian_csr(n, g.u, g.v, g.w, "normalized")
+    x = np.random.default_rng(k).standard_normal((n, k)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    for kind, ell in (("negexp-taylor", 12), ("negexp-limit", 9), ("log-taylor", 7),
+                      ("identity", None)):
+        t = sp.SpectralTransform(kind, ell, 0.5 if kind == "log-taylor" else 1e-6)
+        ref = O.apply_transform(csr, kind, ell, t.epsilon, 0.0, x.astype(np.float64))
+        y = sp.TransformedOperator(L, t, 0.0, 2.0).apply(xd)
+        y0 = sp.TransformedOperator(L0, t, 0.0, 2.0).apply(xd)
+        assert rel_fro(y.cpu().numpy(), ref) <= PV_TOL, kind
+        assert rel_fro(y.cpu().numpy(), y0.cpu().numpy()) <= 2e-6, kind
+    # weighted graphs keep the stored values
+    wg = sp.Graph(n, g.u, g.v, np.full(g.m, 2.0))
+    assert sp.LaplacianOperator(wg, "normalized").row_scale is None
