@@ -51,7 +51,6 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
-    ap.add_argument("--stochastic", action="store_true", help="edge-minibatch mode (configs 3/5)")
     return ap.parse_args()
 
 
