@@ -33,8 +33,10 @@ __global__ void batch_hist_kernel(int64_t B, const int32_t* __restrict__ batch,
   for (; i < B; i += stride) {
     const int64_t e = batch[i];
     const float we = edge_w ? edge_w[e] : 1.0f;
-    atomicAdd(hitw + epos[2 * e], we);
-    atomicAdd(hitw + epos[2 * e + 1], we);
+    const int32_t p0 = epos[2 * e], p1 = epos[2 * e + 1];
+    // a row shard's epos marks endpoints it does not own with -1
+    if (p0 >= 0) atomicAdd(hitw + p0, we);
+    if (p1 >= 0) atomicAdd(hitw + p1, we);
   }
 }
 
@@ -307,7 +309,8 @@ using namespace sped;
 extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indptr,
                                           const int32_t* indices, const float* edge_w,
                                           const int32_t* epos, const int32_t* batch, int64_t B,
-                                          float* hitw, const float* x, float* w_a, float* w_b,
+                                          float* hitw, const float* x, const float* w_init,
+                                          float* w_a, float* w_b,
                                           float* out, int32_t n_terms, const double* alpha,
                                           const double* beta, const double* gamma,
                                           double w0_scale, double lam_f, double s_final,
@@ -315,6 +318,8 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
   SPED_CHECK_ARG(n >= 0 && k >= 1 && m >= 0 && B >= 1, "bad sizes");
   SPED_CHECK_ARG(n_terms >= 0 && (n_terms == 0 || (alpha && beta && gamma)), "bad schedule");
   SPED_CHECK_ARG(x != out && x != w_a && x != w_b, "x must not alias outputs");
+  SPED_CHECK_ARG(w_init == nullptr || (w_init != out && w_init != w_a && w_init != w_b),
+                 "w_init must not alias outputs");
   SPED_CHECK_ARG(n < INT32_MAX, "problem too large");
   if (n == 0) return SPED_OK;
   cudaStream_t s = as_stream(stream);
@@ -322,7 +327,7 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
   SPED_CHECK_ARG(m > 0 && indptr && indices && epos && batch && hitw, "null graph/batch array");
   const double scale = (double)m / (double)B;
   const int32_t slabs = (k + 127) / 128;
-  const float* cur = x;
+  const float* cur = w_init ? w_init : x;
   for (int32_t t = 0; t < n_terms; ++t) {
     const bool final = (t == n_terms - 1);
     float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);

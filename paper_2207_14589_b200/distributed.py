@@ -11,8 +11,13 @@ grouped by owner rank.  Per polynomial term the owners send exactly those
 rows (grouped NCCL send/recv over NVLink, ``batch_isend_irecv``) straight
 into the halo region of E, then the fused SpMM term kernel runs on the local
 rows reading E (C1).  Per solver step the 3 k x k Gram blocks are summed with
-one all-reduce (C2) and every rank applies the same k x k coefficients to its
-rows.  No other data crosses ranks.
+one all-reduce (C2; Oja's CholQR2 needs a second one) and every rank applies
+the same k x k coefficients to its rows.  No other data crosses ranks.
+
+Stochastic mode: every rank draws the SAME global edge batch (same PCG64
+seed), the histogram kernel drops the endpoints it does not own (local epos =
+-1) and the row sweep writes only owned rows, gathering the other endpoint's
+row from the halo-extended block -- the single-GPU arithmetic row for row.
 
 The exchange/partition logic is device-agnostic (it also runs on CPU tensors
 under gloo, which is how it is tested without GPUs); the local term on a GPU
@@ -30,7 +35,7 @@ import torch.distributed as dist
 from . import _lib
 
 __all__ = ["partition_rows", "HaloPlan", "ShardedLaplacian", "ShardedOperator",
-           "sharded_mu_eg_step"]
+           "ShardedStochasticOperator", "sharded_mu_eg_step", "sharded_oja_step"]
 
 
 def partition_rows(indptr: np.ndarray, parts: int) -> np.ndarray:
@@ -222,7 +227,10 @@ class ShardedLaplacian:
         self.long_threshold, self.chunk_len = lap.long_threshold, lap.chunk_len
         self.rowlen = np.diff(indptr_h[b:e + 1])
         self.sorted_rows = lap.reordered
+        self.pos0, self.pos1 = p0, p1
         self._segments = {}
+        self._epos = None
+        self._hitw = None
         self._plan_chunks()
 
     def _plan_chunks(self):
@@ -262,6 +270,34 @@ class ShardedLaplacian:
             _lib.dbl_array([gamma]), float(w0), float(lam_f), float(s_final),
             _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_csr_poly_apply (shard)")
+
+
+    # -- stochastic (edge-minibatch) term on the shard -------------------------
+    @property
+    def epos_local(self) -> torch.Tensor:
+        """Per edge, the local CSR positions of its two entries (-1 where the
+        entry's row belongs to another shard)."""
+        if self._epos is None:
+            ep = self.full.epos.long()
+            own = (ep >= self.pos0) & (ep < self.pos1)
+            self._epos = torch.where(own, ep - self.pos0, torch.full_like(ep, -1)).to(torch.int32)
+        return self._epos
+
+    def local_batch_term(self, E, x_own, out, batch_t, B, alpha, beta, gamma, w0, lam_f,
+                         s_final, k):
+        """One edge-minibatch term (sped_edge_batch_poly_apply) on the own
+        rows, neighbour rows read from E = [own | halo]."""
+        lib = _lib.load()
+        if self._hitw is None:
+            self._hitw = torch.zeros(max(self.nnz_local, 1), dtype=torch.float32,
+                                     device=self.device)
+        rc = lib.sped_edge_batch_poly_apply(
+            self.n_own, k, self.full.graph.m, _lib.ptr(self.indptr), _lib.ptr(self.indices),
+            _lib.ptr(self.full.edge_w), _lib.ptr(self.epos_local), _lib.ptr(batch_t), int(B),
+            _lib.ptr(self._hitw), _lib.ptr(x_own), _lib.ptr(E), None, None, _lib.ptr(out), 1,
+            _lib.dbl_array([alpha]), _lib.dbl_array([beta]), _lib.dbl_array([gamma]), float(w0),
+            float(lam_f), float(s_final), _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_edge_batch_poly_apply (shard)")
 
 
 class ShardedOperator:
@@ -304,10 +340,61 @@ class ShardedOperator:
             ex.exchange(cur)
             final = t == len(al) - 1
             dst = out if final else nxt[: sh.n_own]
-            self.term_fn(cur, x_own, dst, al[t], be[t], ga[t], w0 if t == 0 else 1.0,
-                         lf if final else 0.0, s if final else 1.0, k)
+            self._term(t, cur, x_own, dst, al[t], be[t], ga[t], w0 if t == 0 else 1.0,
+                       lf if final else 0.0, s if final else 1.0, k)
             cur, nxt = nxt, cur
         return out
+
+    def _term(self, t, E, x_own, dst, al, be, ga, w0, lf, s, k):
+        self.term_fn(E, x_own, dst, al, be, ga, w0, lf, s, k)
+
+
+class ShardedStochasticOperator(ShardedOperator):
+    """make_stochastic_oracle (solvers.py:150-180, per-term batches) over a
+    ShardedLaplacian.  Every rank holds the same PCG64 stream (same seed), so
+    the ranks draw identical global batches without communicating."""
+
+    def __init__(self, shard: ShardedLaplacian, transform, lambda_star: float,
+                 batch_size: int, seed: int, index_source: str = "device", term_fn=None):
+        super().__init__(shard, transform, lambda_star)
+        if index_source not in ("device", "host"):
+            raise ValueError("index_source must be 'device' or 'host'")
+        self.batch_size = int(batch_size)
+        self.rng = np.random.default_rng(seed)
+        self.index_source = index_source
+        self.batch_fn = term_fn or shard.local_batch_term
+        self._batch = None
+
+    def draw(self, count: int) -> torch.Tensor:
+        from .sampling import host_draw, pcg64_draw
+        m = self.shard.full.graph.m
+        if self.index_source == "device":
+            return pcg64_draw(self.rng, m, count, self.shard.device)
+        return host_draw(self.rng, m, count, self.shard.device)
+
+    def apply_local(self, x_own: torch.Tensor, out: torch.Tensor | None = None,
+                    batch: torch.Tensor | None = None) -> torch.Tensor:
+        nt = len(self.schedule[0])
+        self._batch = batch if batch is not None else (self.draw(nt * self.batch_size)
+                                                       if nt > 0 else None)
+        return super().apply_local(x_own, out)
+
+    def _term(self, t, E, x_own, dst, al, be, ga, w0, lf, s, k):
+        B = self.batch_size
+        self.batch_fn(E, x_own, dst, self._batch[t * B:(t + 1) * B], B, al, be, ga, w0, lf, s, k)
+
+
+class _Reducing:
+    """Within the block every Gram the workspace forms is all-reduced."""
+
+    def __init__(self, ws, group):
+        self.ws, self.group = ws, group
+
+    def __enter__(self):
+        self.ws.reduce = lambda G: dist.all_reduce(G, op=dist.ReduceOp.SUM, group=self.group)
+
+    def __exit__(self, *exc):
+        self.ws.reduce = None
 
 
 def sharded_mu_eg_step(op: ShardedOperator, V_own: torch.Tensor, eta: float, ws,
@@ -315,12 +402,18 @@ def sharded_mu_eg_step(op: ShardedOperator, V_own: torch.Tensor, eta: float, ws,
     """mu_eg_step (solvers.py:121-144) on row shards: local Gram, one
     all-reduce of the 3 k x k blocks, identical k x k algebra on every rank,
     local update."""
-    lib = _lib.load()
     MV = op.apply_local(V_own, out=MV)
-    ws.gram(V_own, MV)
-    dist.all_reduce(ws.G, op=dist.ReduceOp.SUM, group=group)
-    rc = lib.sped_mueg_coeffs(ws.k, _lib.ptr(ws.G), float(eta), _lib.ptr(ws.A),
-                              _lib.ptr(ws.scale), _lib.ptr(ws.flag), _lib.stream_ptr(ws.device))
-    _lib.check(rc, "sped_mueg_coeffs")
-    ws.update(V_own, ws.A, MV, None, eta, ws.scale, out, upper=True)
+    with _Reducing(ws, group):
+        ws.mu_eg(V_own, MV, eta, out)
+    return out
+
+
+def sharded_oja_step(op: ShardedOperator, V_own: torch.Tensor, eta: float, ws,
+                     out: torch.Tensor, MV: torch.Tensor | None = None, group=None):
+    """oja_step (solvers.py:114-118, MGS as CholQR2) on row shards: the Gram
+    of W = V + eta*MV and the Gram of the first CholQR pass are each one
+    all-reduce; the triangular solves are identical on every rank."""
+    MV = op.apply_local(V_own, out=MV)
+    with _Reducing(ws, group):
+        ws.oja(V_own, MV, eta, out)
     return out

@@ -165,7 +165,7 @@ class EdgeBatchOracle:
         wb = torch.empty_like(xd) if nt >= 3 else None
         rc = lib.sped_edge_batch_poly_apply(
             self.n, k, self.m, _lib.ptr(lap.indptr), _lib.ptr(lap.indices), _lib.ptr(lap.edge_w),
-            _lib.ptr(lap.epos), _lib.ptr(batch), B, _lib.ptr(self.hitw), _lib.ptr(xd),
+            _lib.ptr(lap.epos), _lib.ptr(batch), B, _lib.ptr(self.hitw), _lib.ptr(xd), None,
             _lib.ptr(wa), _lib.ptr(wb), _lib.ptr(out), nt, _lib.dbl_array(al),
             _lib.dbl_array(be), _lib.dbl_array(ga), float(w0), float(lf), float(s),
             _lib.stream_ptr(self.device))

@@ -108,12 +108,16 @@ class StepWorkspace:
         self.scale = torch.empty(k, dtype=torch.float32, device=device)
         self.flag = torch.zeros(1, dtype=torch.int32, device=device)
         self.tmp = torch.empty((n, k), dtype=torch.float32, device=device)
+        # row shards: called on G after every Gram (the all-reduce, C2)
+        self.reduce = None
 
     def gram(self, V, M=None):
         lib = _lib.load()
         rc = lib.sped_gram(self.n, self.k, _lib.ptr(V), _lib.ptr(M), _lib.ptr(self.G),
                            _lib.ptr(self.gram_ws), self.gram_bytes, _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_gram")
+        if self.reduce is not None:
+            self.reduce(self.G)
 
     def update(self, P, A, M, B, eta, scale, out, upper=False):
         lib = _lib.load()
