@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--no-extra", action="store_true", help="skip the stochastic (config 3s) line")
     return ap.parse_args()
 
 
@@ -275,6 +276,54 @@ def time_to_angle(cfg=1, target=1e-3, eval_every=50, max_steps=20000, cpu=True,
     return out
 
 
+def stochastic_line(cfg=3, reps=5):
+    """Edge-minibatch apply on a BASELINE stochastic config (3s: B = 1e6 per
+    term): device PCG64 draw + per-term histogram/row-sweep kernels, CUDA
+    events.  Throughput as sampled-edges*k/s and the compulsory
+    bytes B*(4 idx + 8 endpoints + 4 [weighted]) + 8nk (+4nk with an x term)
+    per term against the HBM peak."""
+    import torch
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200 import generators as G
+    spec = G.CONFIGS[cfg]
+    dev = torch.device("cuda")
+    n, u, v, w = G.config_graph(cfg, device=dev)
+    g = sp.Graph.from_canonical(n, u, v, w, validate=False)
+    k, B = spec["k"], spec["batch"]
+    t = sp.SpectralTransform("negexp-limit", spec["ell"] + 1)  # SURVEY 8d note (i)
+    op = sp.make_reversed_operator(g, t, spec["mode"], device=dev)
+    orc = sp.make_stochastic_oracle(op, B, seed=7)
+    X = torch.randn((n, k), device=dev)
+    nt = op.n_terms
+    for _ in range(2):
+        orc.apply_internal(X)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    draw_ms = apply_ms = 0.0
+    for _ in range(reps):
+        ev[0].record()
+        batch = orc.draw(nt * B)
+        ev[1].record()
+        orc.apply_internal(X, batch=batch)
+        ev[2].record()
+        torch.cuda.synchronize()
+        draw_ms += ev[0].elapsed_time(ev[1]) / reps
+        apply_ms += ev[1].elapsed_time(ev[2]) / reps
+    al = op.schedule[0]
+    weighted = not g.is_unit_weight()
+    bpt = B * (4 + 8 + (4 if weighted else 0)) + 8 * n * k + (4 * n * k if any(a != 0 for a in al)
+                                                              else 0)
+    t_term = apply_ms / nt / 1e3
+    peak, _ = measured_peak()
+    return {"config": f"{spec['name']}s (B={B} per term)", "transform": f"negexp-limit({spec['ell'] + 1})",
+            "n": n, "nnz": op.laplacian.nnz, "k": k, "terms": nt,
+            "ms_per_term": apply_ms / nt, "draw_ms_per_apply": draw_ms,
+            "sampled_edges_k_per_s": nt * B * k / (apply_ms / 1e3),
+            "equiv_4Bk_per_s": 4 * nt * B * k / (apply_ms / 1e3),
+            "compulsory_bytes_per_term": bpt, "achieved_GBps": bpt / t_term / 1e9,
+            "frac_of_peak": bpt / t_term / 1e9 / peak}
+
+
 # ------------------------------------------------------------------------------ sped arm
 
 def run_sped(args):
@@ -449,6 +498,9 @@ def run_sped(args):
                 # the CPU leg is a 300-step sample scaled to the GPU's step count
                 time_to_angle(2, kind="negexp-limit", ell=17, eta=1.0, eval_every=100,
                               cpu_sample_steps=300)]
+    sto = None
+    if rank == 0 and not sharded and not args.no_extra:
+        sto = stochastic_line(3)
 
     if rank == 0:
         line = {
@@ -479,6 +531,7 @@ def run_sped(args):
                          "dram_frac_actual": (traffic / t_term_s / 1e9 / peak) if traffic else None},
             "cpu_baseline": cpu,
             "time_to_angle": conv,
+            "stochastic": sto,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
