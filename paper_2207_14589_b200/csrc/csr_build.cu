@@ -17,10 +17,14 @@
 //                   (graph.py:193-198, (D L) D evaluated left to right)
 // degrees reproduce np.bincount(u,w) + np.bincount(v,w) bit for bit.
 //
-// Layout choices (B200): one thread per row for the fill (each row's
-// diagonal must be a sequential fold to be bit-exact); the transposed
-// (lower-triangle) order comes from a stable radix sort of the edges by v,
-// which keeps edges with equal v in increasing u (= edge) order.
+// Layout choices (B200): entry-parallel, no atomics.  The upper-triangle
+// entries of row i are the edges u_e == i (a contiguous run of the lexsorted
+// edge list), the lower-triangle entries the edges v_e == i in a stable radix
+// sort by v (equal v keep increasing u = edge order), so every entry's CSR
+// position is known in closed form and one thread per entry writes it
+// (coalesced).  Only the weighted diagonal (and weighted degree) is a
+// sequential per-row fold, which bit-exactness requires; unit weights make it
+// the integer count.
 
 #include <cub/cub.cuh>
 
@@ -29,45 +33,65 @@
 namespace sped {
 namespace {
 
-__global__ void count_kernel(int64_t m, const int64_t* __restrict__ u,
-                             const int64_t* __restrict__ v, int32_t* cnt_up,
-                             int32_t* cnt_lo, int32_t* vkey, int32_t* eval) {
+__global__ void unit_check_kernel(int64_t m, const double* __restrict__ w, int32_t* nonunit) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (; e < m; e += stride) bad |= (w[e] != 1.0);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonunit, 1);
+}
+
+__global__ void keys_kernel(int64_t m, const int64_t* __restrict__ v, int32_t* vkey, int32_t* eval) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m) return;
-  int64_t a = u[e], b = v[e];
-  atomicAdd(&cnt_up[a], 1);
-  atomicAdd(&cnt_lo[b], 1);
-  vkey[e] = (int32_t)b;
+  vkey[e] = (int32_t)v[e];
   eval[e] = (int32_t)e;
 }
 
-__global__ void rowlen_kernel(int64_t n, const int32_t* __restrict__ cnt_up,
-                              const int32_t* __restrict__ cnt_lo, int32_t* rowlen) {
+// start[i] = first index whose key >= i, for a key array sorted ascending
+// (start[n] = m).  Thread t covers the rows in (key[t-1], key[t]].
+template <typename K>
+__global__ void run_starts_kernel(int64_t m, int64_t n, const K* __restrict__ key,
+                                  int32_t* __restrict__ start) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > m) return;
+  const int64_t lo = (t == 0) ? -1 : (int64_t)key[t - 1];
+  const int64_t hi = (t == m) ? n : (int64_t)key[t];
+  for (int64_t i = lo + 1; i <= hi; ++i) start[i] = (int32_t)t;
+}
+
+__global__ void rowlen_kernel(int64_t n, const int32_t* __restrict__ up_start,
+                              const int32_t* __restrict__ lo_start, int32_t* rowlen) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
   if (i == n) {
     rowlen[n] = 0;
     return;
   }
-  int32_t d = cnt_up[i] + cnt_lo[i];
+  int32_t d = (up_start[i + 1] - up_start[i]) + (lo_start[i + 1] - lo_start[i]);
   rowlen[i] = d + (d > 0 ? 1 : 0);
 }
 
+// np.bincount(u, w) + np.bincount(v, w): per bin a sequential fold in edge
+// order; with unit weights that is the exact integer count
 __global__ void degree_kernel(int64_t n, const int32_t* __restrict__ up_start,
                               const int32_t* __restrict__ lo_start,
                               const int32_t* __restrict__ sorted_e,
-                              const double* __restrict__ w, int normalized,
-                              double* __restrict__ degrees, double* __restrict__ dinv,
-                              int32_t* zero_flag) {
+                              const double* __restrict__ w, const int32_t* __restrict__ nonunit,
+                              int normalized, double* __restrict__ degrees,
+                              double* __restrict__ dinv, int32_t* zero_flag) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  // np.bincount(u, weights=w): sequential over edges with u == i in edge order
-  double su = 0.0;
-  for (int32_t e = up_start[i]; e < up_start[i + 1]; ++e) su += w[e];
-  // np.bincount(v, weights=w): edges with v == i, edge order == sorted order
-  double sv = 0.0;
-  for (int32_t j = lo_start[i]; j < lo_start[i + 1]; ++j) sv += w[sorted_e[j]];
-  double d = su + sv;
+  double d;
+  if (*nonunit) {
+    double su = 0.0;
+    for (int32_t e = up_start[i]; e < up_start[i + 1]; ++e) su += w[e];
+    double sv = 0.0;
+    for (int32_t j = lo_start[i]; j < lo_start[i + 1]; ++j) sv += w[sorted_e[j]];
+    d = su + sv;
+  } else {
+    d = (double)((up_start[i + 1] - up_start[i]) + (lo_start[i + 1] - lo_start[i]));
+  }
   degrees[i] = d;
   if (normalized) {
     if (d == 0.0) {
@@ -79,66 +103,92 @@ __global__ void degree_kernel(int64_t n, const int32_t* __restrict__ up_start,
   }
 }
 
-__global__ void fill_kernel(int64_t n, const int64_t* __restrict__ u,
-                            const int64_t* __restrict__ v, const double* __restrict__ w,
-                            const int32_t* __restrict__ up_start,
-                            const int32_t* __restrict__ lo_start,
-                            const int32_t* __restrict__ sorted_e,
-                            const int32_t* __restrict__ indptr,
-                            const double* __restrict__ dinv, int normalized,
-                            int32_t* __restrict__ indices, float* __restrict__ values,
-                            int32_t* __restrict__ epos) {
+// lower-triangle entries: sorted position j -> edge e with v_e = i, column u_e
+__global__ void fill_lower_kernel(int64_t m, const int64_t* __restrict__ u,
+                                  const int32_t* __restrict__ sorted_v,
+                                  const int32_t* __restrict__ sorted_e,
+                                  const double* __restrict__ w,
+                                  const int32_t* __restrict__ lo_start,
+                                  const int32_t* __restrict__ indptr,
+                                  const double* __restrict__ dinv, int normalized,
+                                  int32_t* __restrict__ indices, float* __restrict__ values,
+                                  int32_t* __restrict__ epos) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int32_t i = sorted_v[j];
+  const int32_t e = sorted_e[j];
+  const int32_t c = (int32_t)u[e];
+  const int32_t p = indptr[i] + ((int32_t)j - lo_start[i]);
+  indices[p] = c;
+  if (values) {
+    double val = -w[e];
+    if (normalized) val = (dinv[i] * val) * dinv[c];
+    values[p] = (float)val;
+  }
+  epos[2 * (int64_t)e + 1] = p;
+}
+
+// upper-triangle entries: edge e (lexsorted, u_e = i), column v_e, placed
+// after row i's lower entries and its diagonal
+__global__ void fill_upper_kernel(int64_t m, const int64_t* __restrict__ u,
+                                  const int64_t* __restrict__ v, const double* __restrict__ w,
+                                  const int32_t* __restrict__ up_start,
+                                  const int32_t* __restrict__ lo_start,
+                                  const int32_t* __restrict__ indptr,
+                                  const double* __restrict__ dinv, int normalized,
+                                  int32_t* __restrict__ indices, float* __restrict__ values,
+                                  int32_t* __restrict__ epos) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const int32_t i = (int32_t)u[e];
+  const int32_t c = (int32_t)v[e];
+  const int32_t p =
+      indptr[i] + (lo_start[i + 1] - lo_start[i]) + 1 + ((int32_t)e - up_start[i]);
+  indices[p] = c;
+  if (values) {
+    double val = -w[e];
+    if (normalized) val = (dinv[i] * val) * dinv[c];
+    values[p] = (float)val;
+  }
+  epos[2 * (int64_t)e] = p;
+}
+
+// diagonal: scipy's duplicate fold in coo input order -- the (u,u) block in
+// edge order, then the (v,v) block in edge order (graph.py:189-192)
+__global__ void fill_diag_kernel(int64_t n, const double* __restrict__ w,
+                                 const int32_t* __restrict__ up_start,
+                                 const int32_t* __restrict__ lo_start,
+                                 const int32_t* __restrict__ sorted_e,
+                                 const int32_t* __restrict__ indptr,
+                                 const double* __restrict__ dinv,
+                                 const int32_t* __restrict__ nonunit, int normalized,
+                                 int32_t* __restrict__ indices, float* __restrict__ values) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int32_t p = indptr[i];
-  const double di = normalized ? dinv[i] : 1.0;
-  const int32_t lo0 = lo_start[i], lo1 = lo_start[i + 1];
   const int32_t up0 = up_start[i], up1 = up_start[i + 1];
-  // lower triangle: columns u_e < i, increasing
-  for (int32_t j = lo0; j < lo1; ++j) {
-    int32_t e = sorted_e[j];
-    int32_t c = (int32_t)u[e];
-    indices[p] = c;
-    if (values) {
-      double val = -w[e];
-      if (normalized) val = (di * val) * dinv[c];
-      values[p] = (float)val;
+  const int32_t lo0 = lo_start[i], lo1 = lo_start[i + 1];
+  if (up1 == up0 && lo1 == lo0) return;  // isolated row: empty
+  const int32_t p = indptr[i] + (lo1 - lo0);
+  indices[p] = (int32_t)i;
+  if (!values) return;
+  double acc;
+  if (*nonunit) {
+    acc = 0.0;
+    bool first = true;
+    for (int32_t e = up0; e < up1; ++e) {
+      acc = first ? w[e] : acc + w[e];
+      first = false;
     }
-    epos[2 * (int64_t)e + 1] = p;
-    ++p;
-  }
-  if (lo1 > lo0 || up1 > up0) {
-    indices[p] = (int32_t)i;
-    if (values) {
-      // scipy duplicate fold: (u,u) block in edge order, then (v,v) block
-      double acc = 0.0;
-      bool first = true;
-      for (int32_t e = up0; e < up1; ++e) {
-        acc = first ? w[e] : acc + w[e];
-        first = false;
-      }
-      for (int32_t j = lo0; j < lo1; ++j) {
-        double x = w[sorted_e[j]];
-        acc = first ? x : acc + x;
-        first = false;
-      }
-      if (normalized) acc = (di * acc) * di;
-      values[p] = (float)acc;
+    for (int32_t j = lo0; j < lo1; ++j) {
+      const double x = w[sorted_e[j]];
+      acc = first ? x : acc + x;
+      first = false;
     }
-    ++p;
+  } else {
+    acc = (double)((up1 - up0) + (lo1 - lo0));
   }
-  // upper triangle: columns v_e > i, increasing (edges are lexsorted)
-  for (int32_t e = up0; e < up1; ++e) {
-    int32_t c = (int32_t)v[e];
-    indices[p] = c;
-    if (values) {
-      double val = -w[e];
-      if (normalized) val = (di * val) * dinv[c];
-      values[p] = (float)val;
-    }
-    epos[2 * (int64_t)e] = p;
-    ++p;
-  }
+  if (normalized) acc = (dinv[i] * acc) * dinv[i];
+  values[p] = (float)acc;
 }
 
 struct AsyncBuf {
@@ -175,11 +225,8 @@ extern "C" int sped_laplacian_build(int64_t n, int64_t m, const int64_t* u, cons
   SPED_CHECK_ARG(m == 0 || (u && v && w && indices && epos && degrees), "null edge/output array");
   SPED_CHECK_ARG(!store_values || values, "values requested but NULL");
 
-  AsyncBuf b_cnt(s), b_len(s), b_up(s), b_lo(s), b_keys(s), b_vals(s), b_keys2(s), b_vals2(s),
-      b_dinv(s), b_flag(s), b_tmp(s);
-  SPED_CUDA(b_cnt.alloc(sizeof(int32_t) * 2 * n));
-  int32_t* cnt_up = (int32_t*)b_cnt.p;
-  int32_t* cnt_lo = cnt_up + n;
+  AsyncBuf b_len(s), b_up(s), b_lo(s), b_keys(s), b_vals(s), b_keys2(s), b_vals2(s), b_dinv(s),
+      b_flag(s), b_tmp(s);
   SPED_CUDA(b_len.alloc(sizeof(int32_t) * (n + 1)));
   SPED_CUDA(b_up.alloc(sizeof(int32_t) * (n + 1)));
   SPED_CUDA(b_lo.alloc(sizeof(int32_t) * (n + 1)));
@@ -188,63 +235,66 @@ extern "C" int sped_laplacian_build(int64_t n, int64_t m, const int64_t* u, cons
   SPED_CUDA(b_keys2.alloc(sizeof(int32_t) * m));
   SPED_CUDA(b_vals2.alloc(sizeof(int32_t) * m));
   SPED_CUDA(b_dinv.alloc(sizeof(double) * n));
-  SPED_CUDA(b_flag.alloc(sizeof(int32_t)));
-  SPED_CUDA(cudaMemsetAsync(cnt_up, 0, sizeof(int32_t) * 2 * n, s));
-  SPED_CUDA(cudaMemsetAsync(b_flag.p, 0, sizeof(int32_t), s));
+  SPED_CUDA(b_flag.alloc(sizeof(int32_t) * 2));  // [zero degree, non-unit weights]
+  SPED_CUDA(cudaMemsetAsync(b_flag.p, 0, sizeof(int32_t) * 2, s));
+  int32_t* zero_flag_d = (int32_t*)b_flag.p;
+  int32_t* nonunit_d = zero_flag_d + 1;
 
   int32_t* rowlen = (int32_t*)b_len.p;
   int32_t* up_start = (int32_t*)b_up.p;
   int32_t* lo_start = (int32_t*)b_lo.p;
   int32_t* keys = (int32_t*)b_keys.p;
   int32_t* vals = (int32_t*)b_vals.p;
+  int32_t* sorted_v = (int32_t*)b_keys2.p;
+  int32_t* sorted_e = (int32_t*)b_vals2.p;
 
-  if (m > 0) {
-    count_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, u, v, cnt_up, cnt_lo, keys, vals);
-    SPED_LAUNCH_CHECK();
-  }
-  rowlen_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(n, cnt_up, cnt_lo, rowlen);
-  SPED_LAUNCH_CHECK();
-
-  // scans (n+1 elements; the trailing zero makes element n the total)
-  size_t tmp_scan = 0;
+  size_t tmp_scan = 0, tmp_sort = 0;
   SPED_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, rowlen, indptr, (int)(n + 1), s));
-  size_t tmp_sort = 0;
   int end_bit = 1;
   while (end_bit < 31 && ((int64_t)1 << end_bit) < n) ++end_bit;
   if (m > 0) {
-    SPED_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, keys, (int32_t*)b_keys2.p, vals,
-                                              (int32_t*)b_vals2.p, (int)m, 0, end_bit, s));
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, keys, sorted_v, vals, sorted_e,
+                                              (int)m, 0, end_bit, s));
   }
   SPED_CUDA(b_tmp.alloc(tmp_scan > tmp_sort ? tmp_scan : tmp_sort));
+  if (m > 0) {
+    unit_check_kernel<<<grid_for(m, 256, num_sms() * 8), 256, 0, s>>>(m, w, nonunit_d);
+    keys_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, v, keys, vals);
+    SPED_LAUNCH_CHECK();
+    // stable: equal v keep increasing edge (= u) order, scipy's transpose order
+    size_t sb = tmp_sort;
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(b_tmp.p, sb, keys, sorted_v, vals, sorted_e, (int)m,
+                                              0, end_bit, s));
+  }
+  run_starts_kernel<int64_t><<<grid_for(m + 1, 256), 256, 0, s>>>(m, n, u, up_start);
+  run_starts_kernel<int32_t><<<grid_for(m + 1, 256), 256, 0, s>>>(m, n, sorted_v, lo_start);
+  rowlen_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(n, up_start, lo_start, rowlen);
+  SPED_LAUNCH_CHECK();
   size_t tmp_bytes = tmp_scan;
   SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp_bytes, rowlen, indptr, (int)(n + 1), s));
-  // up/lo starts: reuse rowlen as the (n+1) input with a trailing zero
-  SPED_CUDA(cudaMemcpyAsync(rowlen, cnt_up, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-  SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp_bytes, rowlen, up_start, (int)(n + 1), s));
-  SPED_CUDA(cudaMemcpyAsync(rowlen, cnt_lo, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-  SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp_bytes, rowlen, lo_start, (int)(n + 1), s));
 
-  const int32_t* sorted_e = vals;
-  if (m > 0) {
-    size_t sb = tmp_sort;
-    SPED_CUDA(cub::DeviceRadixSort::SortPairs(b_tmp.p, sb, keys, (int32_t*)b_keys2.p, vals,
-                                              (int32_t*)b_vals2.p, (int)m, 0, end_bit, s));
-    sorted_e = (const int32_t*)b_vals2.p;
-  }
-
-  degree_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, up_start, lo_start, sorted_e, w, normalized,
-                                                   degrees, (double*)b_dinv.p, (int32_t*)b_flag.p);
+  degree_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, up_start, lo_start, sorted_e, w, nonunit_d,
+                                                   normalized, degrees, (double*)b_dinv.p,
+                                                   zero_flag_d);
   SPED_LAUNCH_CHECK();
   int32_t zero_flag = 0;
-  SPED_CUDA(cudaMemcpyAsync(&zero_flag, b_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaMemcpyAsync(&zero_flag, zero_flag_d, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SPED_CUDA(cudaStreamSynchronize(s));
   if (normalized && zero_flag) {
     set_error("normalized Laplacian requires all degrees > 0");
     return SPED_ERR_ZERO_DEGREE;
   }
-  fill_kernel<<<grid_for(n, 128), 128, 0, s>>>(n, u, v, w, up_start, lo_start, sorted_e, indptr,
-                                                 (const double*)b_dinv.p, normalized, indices,
-                                                 store_values ? values : nullptr, epos);
+  const double* dinv = (const double*)b_dinv.p;
+  float* vout = store_values ? values : nullptr;
+  if (m > 0) {
+    fill_lower_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, u, sorted_v, sorted_e, w, lo_start,
+                                                         indptr, dinv, normalized, indices, vout,
+                                                         epos);
+    fill_upper_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, u, v, w, up_start, lo_start, indptr,
+                                                         dinv, normalized, indices, vout, epos);
+  }
+  fill_diag_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, w, up_start, lo_start, sorted_e, indptr,
+                                                      dinv, nonunit_d, normalized, indices, vout);
   SPED_LAUNCH_CHECK();
   int32_t nnz = 0;
   SPED_CUDA(cudaMemcpyAsync(&nnz, indptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
