@@ -32,11 +32,17 @@
 #ifndef TERM_MIN_BLOCKS
 #define TERM_MIN_BLOCKS 6
 #endif
+#ifndef TERM_MIN_BLOCKS_W8
+#define TERM_MIN_BLOCKS_W8 8  // full occupancy for the 256-bit one-group-per-row kernels (r01 sweep)
+#endif
 #ifndef SUB1_U
 #define SUB1_U 4
 #endif
 #ifndef W8_U
-#define W8_U 2
+#define W8_U 1  // one 256-bit gather in flight per lane, more rows resident instead
+#endif
+#ifndef W8_LONG_U
+#define W8_LONG_U 4
 #endif
 #ifndef LONG_MIN_BLOCKS
 #define LONG_MIN_BLOCKS 4
@@ -377,7 +383,7 @@ __global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
 }
 
 template <int W, int LPR, int SUB, int U, int VM>
-__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : TERM_MIN_BLOCKS)) spmm_term_kernel(const TermArgs a) {
+__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? TERM_MIN_BLOCKS_W8 : TERM_MIN_BLOCKS))) spmm_term_kernel(const TermArgs a) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -641,7 +647,7 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
 constexpr int UNROLL = 4;
 
 template <int W, int LPR, int SUB,
-          int U = (SUB > 1 ? (W == 8 ? 4 : LONG_U) : (W == 8 ? W8_U : SUB1_U))>
+          int U = (SUB > 1 ? (W == 8 ? W8_LONG_U : LONG_U) : (W == 8 ? W8_U : SUB1_U))>
 static void launch_fast(const TermArgs& a, int vm, cudaStream_t s) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
@@ -664,11 +670,11 @@ static void launch_chunks(const TermArgs& a, int vm, cudaStream_t s) {
   const unsigned grid = (unsigned)((a.n_chunks + 7) / 8);
   if (grid == 0) return;
   if (vm == 1)
-    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), 1><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 1><<<grid, 256, 0, s>>>(a);
   else if (vm == 2)
-    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), 2><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 2><<<grid, 256, 0, s>>>(a);
   else
-    spmm_chunk_kernel<W, LPR, (W == 8 ? 4 : LONG_U), 0><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 0><<<grid, 256, 0, s>>>(a);
 }
 
 template <int W, int LPR>
@@ -734,7 +740,10 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       const char* e = getenv("SPED_VEC");
       wide = (e && e[0] == '4') ? 0 : 1;
     }
-    const bool w8 = wide && (k % 8 == 0) && aligned32 && k >= 64;
+#ifndef W8_MIN_K
+#define W8_MIN_K 32  // k = 32: 4 lanes x 256-bit per row (config 4: 3.53 -> 3.22 ms/term)
+#endif
+    const bool w8 = wide && (k % 8 == 0) && aligned32 && k >= W8_MIN_K;
     const int lpr = k / (w8 ? 8 : 4);
     if (a.n_chunks > 0) {
       if (w8) launch_chunks_w<8>(lpr, a, vm, s);
