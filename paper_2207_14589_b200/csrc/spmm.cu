@@ -746,8 +746,9 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
     const bool w8 = wide && (k % 8 == 0) && aligned32 && k >= W8_MIN_K;
     const int lpr = k / (w8 ? 8 : 4);
     if (a.n_chunks > 0) {
-      if (w8) launch_chunks_w<8>(lpr, a, vm, s);
-      else launch_chunks_w<4>(lpr, a, vm, s);
+      // hub chunks keep 128-bit gathers at k = 32 (0.78 vs 0.87 ms at config 4)
+      if (w8 && k >= 64) launch_chunks_w<8>(lpr, a, vm, s);
+      else launch_chunks_w<4>(k / 4, a, vm, s);
       SPED_LAUNCH_CHECK();
     }
     for (int i = 0; i < nseg; ++i) {
