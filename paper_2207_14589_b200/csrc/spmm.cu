@@ -41,6 +41,9 @@
 #ifndef W8_U
 #define W8_U 1  // one 256-bit gather in flight per lane, more rows resident instead
 #endif
+#ifndef CHUNK_MIN_BLOCKS
+#define CHUNK_MIN_BLOCKS 4
+#endif
 #ifndef W8_LONG_U
 #define W8_LONG_U 4
 #endif
@@ -334,7 +337,7 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
 // partial rows in chunk order and applies the epilogue: deterministic, no
 // float atomics.
 template <int W, int LPR, int U, int VM>
-__global__ void __launch_bounds__(256, 4) spmm_chunk_kernel(const TermArgs a) {
+__global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const TermArgs a) {
   const int lane = threadIdx.x & 31;
   const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
