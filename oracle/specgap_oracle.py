@@ -20,6 +20,11 @@ import numpy as np
 import scipy.sparse as sp
 
 __all__ = [
+    "walk_chunk_key",
+    "incidence_lists",
+    "walk_sample_chunk",
+    "walk_estimate",
+    "walk_oracle_apply",
     "versions",
     "canonical_edges",
     "degrees",
@@ -529,3 +534,133 @@ def threaded_csr_matmul(csr, x, threads):
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(work, range(threads)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# walk-based polynomial estimator (walks.py), restated.  numpy's Philox is the
+# reference's own RNG (walks.py:196-198); the incidence lists are built
+# directly from the canonical (lexsorted) edge list.
+
+_WALK_CHUNK = 8192  # walks.py:45
+
+
+def walk_chunk_key(seed: int, chunk: int) -> np.ndarray:
+    """Philox key of chunk ``chunk`` (walks.py:196-198: Philox(SeedSequence((seed, chunk))),
+    counter 0): the two uint64 words SeedSequence hands the bit generator."""
+    return np.random.SeedSequence((seed, chunk)).generate_state(2, np.uint64)
+
+
+def incidence_lists(n, u, v):
+    """Edge incidence graph (graph.py:326-342): for edge e the sorted union of
+    the edge ids at its two endpoints (e itself included once).  Returns
+    (indptr, indices, deg_inc)."""
+    m = u.size
+    at = [[] for _ in range(n)]
+    for e in range(m):
+        at[int(u[e])].append(e)
+        at[int(v[e])].append(e)
+    indptr = [0]
+    indices = []
+    for e in range(m):
+        inc = np.unique(np.asarray(at[int(u[e])] + at[int(v[e])], dtype=np.int64))
+        indices.extend(inc.tolist())
+        indptr.append(len(indices))
+    indptr = np.asarray(indptr, dtype=np.int64)
+    return indptr, np.asarray(indices, dtype=np.int64), np.diff(indptr)
+
+
+def walk_sample_chunk(inc, m, ell, count, rng):
+    """walks.py:175-193: uniform first edge, uniform incident successor."""
+    indptr, indices, deg_inc = inc
+    E = np.empty((count, ell), dtype=np.int64)
+    E[:, 0] = (rng.random(count) * m).astype(np.int64)
+    log_p = np.full(count, -math.log(m))
+    for j in range(ell - 1):
+        cur = E[:, j]
+        deg = deg_inc[cur]
+        pick = (rng.random(count) * deg).astype(np.int64)
+        E[:, j + 1] = indices[indptr[cur] + pick]
+        log_p -= np.log(deg)
+    return E, log_p
+
+
+def _alpha(u, v, e1, e2):
+    """Incidence inner product (walks.py:83-103)."""
+    return ((u[e1] == u[e2]).astype(np.int64) + (v[e1] == v[e2])
+            - (u[e1] == v[e2]) - (v[e1] == u[e2]))
+
+
+def walk_estimate(n, u, v, w, coeffs, x, walks, seed, mode="importance", inc=None):
+    """estimate_polynomial_matvec / estimate_power_matvec (walks.py:225-341):
+    sum over chunks (reduced in chunk order) of each walk's prefix
+    contributions coeffs[i] * chain / p, accumulated at the first edge's
+    endpoints; importance mode returns coeffs[0] x + total / N, rejection
+    mode (single power coeffs = e_ell) total / (N p_min)."""
+    coeffs = np.asarray(coeffs, dtype=np.float64)
+    x = np.asarray(x, dtype=np.float64)
+    m = u.size
+    ell = coeffs.size - 1
+    if inc is None:
+        inc = incidence_lists(n, u, v)
+    deg_star = int(np.max(np.bincount(u, minlength=n) + np.bincount(v, minlength=n)))
+    lpmin = -ell * math.log(2 * deg_star - 1) - math.log(m)
+    n_chunks = -(-walks // _WALK_CHUNK)
+    total = np.zeros(n)
+    n_acc = 0
+    for c in range(n_chunks):
+        size = min(_WALK_CHUNK, walks - c * _WALK_CHUNK)
+        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence((seed, c))))
+        E, log_p_full = walk_sample_chunk(inc, m, ell, size, rng)
+        logmag = np.cumsum(np.log(w[E]), axis=1)
+        sign = np.ones((size, ell))
+        if ell > 1:
+            a = _alpha(u, v, E[:, :-1].ravel(), E[:, 1:].ravel()).reshape(size, ell - 1)
+            sign[:, 1:] = np.cumprod(np.sign(a), axis=1)
+            logmag[:, 1:] += np.cumsum(np.log(np.abs(a)), axis=1)
+        acc = np.zeros(n)
+
+        def accumulate(Es, coefs, which):
+            e_last = Es[:, which - 1]
+            contrib = coefs * (x[u[e_last]] - x[v[e_last]])
+            acc[:] += np.bincount(u[Es[:, 0]], weights=contrib, minlength=n)
+            acc[:] -= np.bincount(v[Es[:, 0]], weights=contrib, minlength=n)
+
+        if mode == "importance":
+            deg_logs = np.zeros((size, ell))
+            if ell > 1:
+                deg_logs[:, 1:] = np.cumsum(np.log(inc[2][E[:, :-1]]), axis=1)
+            for i in range(1, ell + 1):
+                if coeffs[i] == 0.0:
+                    continue
+                lp = -math.log(m) - deg_logs[:, i - 1]
+                accumulate(E, coeffs[i] * sign[:, i - 1] * np.exp(logmag[:, i - 1] - lp), i)
+        else:
+            keep = rng.random(size) < np.exp(lpmin - log_p_full)
+            n_acc += int(keep.sum())
+            if keep.any():
+                accumulate(E[keep], coeffs[ell] * sign[keep, ell - 1]
+                           * np.exp(logmag[keep, ell - 1]), ell)
+        total += acc
+    if mode == "importance":
+        return coeffs[0] * x + total / walks
+    if n_acc == 0:
+        raise RuntimeError("no walk survived rejection")
+    return total / (walks * math.exp(lpmin))
+
+
+def walk_oracle_apply(n, u, v, w, coeffs, lam_star, x, walks, seed, call0):
+    """make_stochastic_oracle's walk oracle (solvers.py:183-200): one estimate
+    per column, column j of call c seeded with
+    SeedSequence((seed, counter)).generate_state(1)[0]; returns
+    (lam_star x - f(L) x, next counter)."""
+    x = np.asarray(x, dtype=np.float64)
+    cols = x[:, None] if x.ndim == 1 else x
+    out = np.empty_like(cols)
+    inc = incidence_lists(n, u, v)
+    counter = call0
+    for j in range(cols.shape[1]):
+        call_seed = int(np.random.SeedSequence((seed, counter)).generate_state(1)[0])
+        counter += 1
+        fx = walk_estimate(n, u, v, w, coeffs, cols[:, j], walks, call_seed, inc=inc)
+        out[:, j] = lam_star * cols[:, j] - fx
+    return (out[:, 0] if x.ndim == 1 else out), counter

@@ -190,6 +190,40 @@ def main():
         if name == "cfg1":
             data[key + "/labels"] = sg.kmeans_cluster(run.V, 10, seed=5)
             data[key + "/gt_labels"] = sg.kmeans_cluster(gt.bottom(10), 10, seed=5)
+    # ---- walk-based polynomial estimator (walks.py) --------------------------
+    from specgap import walks as wk
+    for name, coeffs, W, seed in [("path3", [0.5, -1.0, 0.25], 3000, 1),
+                                  ("k3", [0.0, 0.0, 1.0], 5000, 2),
+                                  ("two_triangles_bridge", [1.0, -0.5, 0.1, -0.02], 20000, 3),
+                                  ("er0", [0.2, -0.3, 0.05, 0.0, 0.01], 30000, 4),
+                                  ("er1", [1.0, -0.7, 0.2], 20000, 5)]:
+        g = G[name]
+        ell = len(coeffs) - 1
+        x = np.random.default_rng(seed).standard_normal(g.n)
+        key = f"walk/{name}/{seed}"
+        data[key + "/coeffs"] = np.asarray(coeffs)
+        data[key + "/walks"] = np.array(W)
+        data[key + "/x"] = x
+        data[key + "/y"] = wk.estimate_polynomial_matvec(
+            g, coeffs, x, wk.SamplerConfig(ell, W, 1, "importance", seed))
+        E, lp = wk._sample_chunk(wk.edge_incidence_graph(g), ell, min(8192, W),
+                                 wk._chunk_generator(seed, 0))
+        data[key + "/E0"] = E[:256]
+        data[key + "/logp0"] = lp[:256]
+        if ell >= 1:
+            data[key + "/rejection"] = wk.estimate_power_matvec(
+                g, ell, x, wk.SamplerConfig(ell, W, 1, "rejection", seed))
+    for name, kind, ell, B, seed in [("two_triangles_bridge", "negexp-limit", 3, 4000, 7),
+                                     ("er2", "negexp-taylor", 4, 3000, 8)]:
+        g = G[name]
+        op = sg.make_reversed_operator(g, sg.SpectralTransform(kind, ell))
+        orc = sg.make_stochastic_oracle(op, B, seed=seed)
+        X = np.random.default_rng(seed).standard_normal((g.n, 2))
+        key = f"walkorc/{name}/{kind}/{ell}/{B}/{seed}"
+        data[key + "/x"] = X
+        data[key + "/lambda_star"] = np.array(op.lambda_star)
+        data[key + "/y0"] = orc(X)
+        data[key + "/y1"] = orc(X)
     # ---- k-means -------------------------------------------------------------
     rng = np.random.default_rng(0)
     X = np.concatenate([rng.normal(0, 0.1, (40, 3)), rng.normal(3, 0.1, (50, 3)),

@@ -209,3 +209,51 @@ def test_row_sample_csr_equals_full_rows(golden, mode):
             np.testing.assert_array_equal(part.indptr, ref.indptr)
             np.testing.assert_array_equal(part.indices, ref.indices)
             np.testing.assert_array_equal(part.data.astype(np.float32), ref.data.astype(np.float32))
+
+
+# --- walk-based estimator (walks.py) --------------------------------------------------
+
+def test_walk_estimator_oracle_vs_reference(golden):
+    """The restated walk sampler reproduces the reference's walks (chunk-0
+    edge sequences and log-probabilities bit for bit) and its importance /
+    rejection estimates."""
+    for key in golden.keys("walk/"):
+        if not key.endswith("/y"):
+            continue
+        base = key[:-2]
+        name, seed = base.split("/")[1], int(base.split("/")[2])
+        n, u, v, w = golden.graph(name)
+        coeffs = golden[base + "/coeffs"]
+        W = int(golden[base + "/walks"])
+        x = golden[base + "/x"]
+        inc = O.incidence_lists(n, u, v)
+        ell = coeffs.size - 1
+        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence((seed, 0))))
+        E, lp = O.walk_sample_chunk(inc, u.size, ell, min(8192, W), rng)
+        assert np.array_equal(E[:256], golden[base + "/E0"]), base
+        assert np.array_equal(lp[:256], golden[base + "/logp0"]), base
+        y = O.walk_estimate(n, u, v, w, coeffs, x, W, seed, inc=inc)
+        np.testing.assert_allclose(y, golden[key], rtol=1e-12, atol=1e-12)
+        e = np.zeros_like(coeffs)
+        e[-1] = 1.0
+        yr = O.walk_estimate(n, u, v, w, e, x, W, seed, mode="rejection", inc=inc)
+        np.testing.assert_allclose(yr, golden[base + "/rejection"], rtol=1e-12, atol=1e-12)
+
+
+def test_walk_oracle_composition_vs_reference(golden):
+    """make_stochastic_oracle's walk oracle (solvers.py:183-200): per-column
+    call seeds from SeedSequence((seed, counter)), counter carried across
+    calls."""
+    for key in golden.keys("walkorc/"):
+        if not key.endswith("/y0"):
+            continue
+        base = key[:-3]
+        _, name, kind, ell, B, seed = base.split("/")
+        n, u, v, w = golden.graph(name)
+        coeffs = O.polynomial_coefficients(kind, int(ell))
+        lam = float(golden[base + "/lambda_star"])
+        X = golden[base + "/x"]
+        y0, c = O.walk_oracle_apply(n, u, v, w, coeffs, lam, X, int(B), int(seed), 0)
+        y1, _ = O.walk_oracle_apply(n, u, v, w, coeffs, lam, X, int(B), int(seed), c)
+        np.testing.assert_allclose(y0, golden[base + "/y0"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(y1, golden[base + "/y1"], rtol=1e-12, atol=1e-12)
