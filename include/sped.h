@@ -24,6 +24,9 @@
  *   sped_oja_coeffs (+ gram/update)  oja_step + _orthonormalize  solvers.py:84-118
  *   sped_pcg64_integers        Generator(PCG64).integers(0,m,B)  solvers.py:171
  *   sped_kmeans_*              kmeans_cluster                    metrics.py:143-176
+ *   sped_walk_index_build / sped_walk_poly_estimate
+ *                              estimate_polynomial_matvec        walks.py:276-341
+ *                              (edge incidence walks, Philox)    walks.py:175-273
  *   sped_gather_rows/scatter   (new) halo exchange staging for row-sharded L
  */
 #ifndef SPED_H_
@@ -179,6 +182,31 @@ int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int32_t* indpt
                          double lam_f, double s_final, double eta, int32_t steps, float* V,
                          int32_t* flag, void* workspace, int64_t workspace_bytes,
                          sped_stream_t stream);
+/* ---- walk-based polynomial estimator (walks.py) ---------------------------
+ * sped_walk_index_build: from the canonical lexsorted edge list (u < v,
+ * int64, device) the incidence index: up_start[n+1] (edges with u == x are
+ * ids [up_start[x], up_start[x+1])), lo_start[n+1] and sorted_e[m] (the ids
+ * stably sorted by v; node x's v-run is sorted_e[lo_start[x] .. lo_start[x+1])).
+ * sped_walk_poly_estimate: for each of the k columns of x (fp64 n x k,
+ * row-major) one estimate of sum_i coeffs[i] L^i x_j (mode 0, importance,
+ * walks.py:311-341) or of L^ell x_j / (N p_min) with coeffs = e_ell (mode 1,
+ * rejection, walks.py:276-308) from `walks` walks of length ell on the edge
+ * incidence graph; keys = uint64[k][ceil(walks/8192)][2], the Philox keys of
+ * SeedSequence((seed_j, chunk)) (walks.py:196-198).  coeffs is a HOST array of
+ * ell+1 doubles; deg_star_inc = 2 * max unweighted degree - 1 (rejection).
+ * The walks reproduce numpy's Philox draws bit for bit; out is fp64. */
+int64_t sped_walk_index_workspace_bytes(int64_t n, int64_t m);
+int sped_walk_index_build(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                          int32_t* up_start, int32_t* lo_start, int32_t* sorted_e,
+                          void* workspace, int64_t workspace_bytes, sped_stream_t stream);
+int64_t sped_walk_workspace_bytes(int64_t n, int32_t k, int64_t walks);
+int sped_walk_poly_estimate(int64_t n, int64_t m, int32_t k, const int64_t* u, const int64_t* v,
+                            const double* w, const int32_t* up_start, const int32_t* lo_start,
+                            const int32_t* sorted_e, int32_t ell, const double* coeffs,
+                            int32_t mode, int64_t deg_star_inc, int64_t walks,
+                            const uint64_t* keys, const double* x, double* out, void* workspace,
+                            int64_t workspace_bytes, sped_stream_t stream);
+
 /* out = (P*A + M*B) * diag(scale).  A k x k fp32; M may be NULL; B may be
  * NULL meaning B = eta*I; scale may be NULL (ones).  upper != 0 promises A is
  * upper triangular (mu-EG), letting the kernel skip the zero half. */

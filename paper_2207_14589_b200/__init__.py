@@ -15,6 +15,12 @@ from .graph import (
     dense_laplacian,
     degree_bounds,
 )
+from .walks import (
+    SamplerConfig,
+    estimate_power_matvec,
+    estimate_polynomial_matvec,
+    WalkOracle,
+)
 from .transforms import (
     SpectralTransform,
     TransformedOperator,

@@ -314,22 +314,31 @@ _STEP_RULES = {"oja": oja_step, "mu-eg": mu_eg_step}
 
 
 def make_stochastic_oracle(op: TransformedOperator, batch_size: int, seed: int,
-                           sampler=None, index_source: str = "device"):
+                           sampler=None, index_source: str = "device",
+                           estimator: str = "edge-batch"):
     """Unbiased stochastic estimate of the reversed transformed matvec
-    (solvers.py:150-202).  Batch size 0 returns ``op.apply``.  Every
-    polynomial kind uses per-term seeded edge minibatches drawn from ONE
-    numpy PCG64 stream seeded with ``seed`` (identity: exactly the
-    reference's identity oracle; other kinds: the restated composition of
-    SURVEY 8c(1) — the reference's walk sampler is not on this path)."""
+    (solvers.py:150-202).  Batch size 0 returns ``op.apply``.
+
+    * Default (the north-star device path): per-term seeded edge minibatches
+      drawn from ONE numpy PCG64 stream seeded with ``seed`` (identity kind:
+      exactly the reference's identity oracle; other kinds: the restated
+      per-term composition of SURVEY 8c(1)).
+    * ``sampler=SamplerConfig(...)`` or ``estimator="walk"``: the reference's
+      walk oracle for non-identity polynomials (solvers.py:183-200), one
+      importance estimate per column with the reference's per-call seeds and
+      bit-identical walks (``walks.WalkOracle``)."""
     if batch_size == 0:
         return op.apply
     if batch_size < 0:
         raise ValueError("batch size must be nonnegative")
     if not op.transform.is_polynomial:
         raise ValueError("stochastic sampling needs a polynomial transform")
-    if sampler is not None:
-        raise NotImplementedError("the walk sampler (walks.py) is not part of the device path; "
-                                  "per-term edge minibatches are used instead")
+    if (sampler is not None or estimator == "walk") and op.transform.kind != "identity":
+        from .walks import WalkOracle
+        walks = sampler.walks_per_estimate if sampler is not None else batch_size
+        return WalkOracle(op, walks, seed)
+    if estimator not in ("edge-batch", "walk"):
+        raise ValueError(f"unknown estimator {estimator!r}")
     return EdgeBatchOracle(op, batch_size, seed, index_source=index_source)
 
 
