@@ -131,18 +131,21 @@ int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
  * edge ids batch[t*B .. t*B+B) (int32, the numpy rng.integers stream).
  * edge_w fp32[m] (NULL = unit weights) are the RAW graph weights, exactly as
  * the reference's identity oracle uses g.w (also in normalized mode).
- * hitw fp32[nnz] must be zero on entry and is left zero.  epos int32[2m] =
- * the CSR positions of each edge's two entries; -1 marks an entry this call
- * does not own (a row shard's view: only owned rows are written).  w_init
- * (optional) is the term-0 input with halo rows appended (row shards), x
- * stays the own rows; neither may alias out / w_a / w_b. */
-int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indptr,
-                               const int32_t* indices, const float* edge_w,
-                               const int32_t* epos, const int32_t* batch, int64_t B,
-                               float* hitw, const float* x, const float* w_init,
-                               float* w_a, float* w_b,
-                               float* out, int32_t n_terms, const double* alpha,
-                               const double* beta, const double* gamma,
+ * epos int32[2m] = the CSR positions of each edge's two entries (the entry's
+ * CSR column is the neighbour); -1 marks an entry this call does not own.
+ * erow int32[2m] (optional) = the row of each entry; NULL derives it from the
+ * partner entry's column (whole graph; a row shard must pass it).  workspace
+ * >= sped_edge_batch_workspace_bytes(n, B).  w_init (optional) is the term-0
+ * input with halo rows appended (row shards), x stays the own rows; neither
+ * may alias out / w_a / w_b.  Deterministic (sorted records, no float
+ * atomics). */
+int64_t sped_edge_batch_workspace_bytes(int64_t n, int64_t B);
+int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
+                               const float* edge_w, const int32_t* epos, const int32_t* erow,
+                               const int32_t* batch, int64_t B, void* workspace,
+                               int64_t workspace_bytes, const float* x, const float* w_init,
+                               float* w_a, float* w_b, float* out, int32_t n_terms,
+                               const double* alpha, const double* beta, const double* gamma,
                                double w0_scale, double lam_f, double s_final,
                                sped_stream_t stream);
 

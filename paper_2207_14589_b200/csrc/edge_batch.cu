@@ -8,15 +8,19 @@
 // and, per term, the restated composition of SURVEY 8c(1) (term t uses the
 // t-th minibatch of the same PCG64 stream).
 //
-// Deterministic formulation (no float atomics on the block): the sampled
-// estimate is the weighted Laplacian of the sampled multiset,
-//     est_r = sum_{p in row r, p off-diag} h_p (w_r - w_{col_p}),
-//     h_p   = (multiplicity of edge(p) in the batch) * w_edge(p),
-// so each term is (1) a histogram of the batch into the CSR positions of the
-// sampled edges (`epos`, built with the CSR) and (2) a warp-per-row sweep
-// that skips positions with h_p == 0, gathers only the sampled neighbours,
-// applies the recurrence epilogue and clears h.  Every atomicAdd into h_p adds
-// the SAME value w_e, so h_p is independent of the atomic order.
+// Deterministic formulation (no float atomics): the sampled estimate of row r
+//     est_r = sum_{b : r endpoint of e_b} w_b (w_r - w_{other end of e_b})
+// is formed from SORTED RECORDS.  Per term, one thread per sampled edge writes
+// a (row, neighbour, weight) record for each endpoint the call owns (its CSR
+// positions `epos` say where the entries live; a row shard marks the others
+// -1), a stable radix sort groups the records by row keeping sample order,
+// and a warp-per-row sweep folds each row's records in that order, gathers
+// the sampled neighbours' rows and applies the recurrence epilogue.  Rows
+// without records only run the epilogue.  (The first version histogrammed
+// the batch into an nnz-sized array and scanned all nnz positions per term;
+// config 3s: 0.41 ms/term.)
+
+#include <cub/cub.cuh>
 
 #include <algorithm>
 
@@ -25,33 +29,56 @@
 namespace sped {
 namespace {
 
-__global__ void batch_hist_kernel(int64_t B, const int32_t* __restrict__ batch,
-                                  const int32_t* __restrict__ epos,
-                                  const float* __restrict__ edge_w, float* __restrict__ hitw) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; i < B; i += stride) {
-    const int64_t e = batch[i];
-    const float we = edge_w ? edge_w[e] : 1.0f;
-    const int32_t p0 = epos[2 * e], p1 = epos[2 * e + 1];
-    // a row shard's epos marks endpoints it does not own with -1
-    if (p0 >= 0) atomicAdd(hitw + p0, we);
-    if (p1 >= 0) atomicAdd(hitw + p1, we);
+// one record per owned endpoint of each sampled edge: key = row, value =
+// (float weight bits << 32) | neighbour column (the entry's CSR column: the
+// node id, or the [own | halo] index of a row shard); unowned -> key n
+__global__ void records_kernel(int64_t B, int64_t n, const int32_t* __restrict__ batch,
+                               const int32_t* __restrict__ epos, const int32_t* __restrict__ erow,
+                               const int32_t* __restrict__ indices,
+                               const float* __restrict__ edge_w, int32_t* __restrict__ keys,
+                               uint64_t* __restrict__ vals) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t e = batch[b];
+  const float we = edge_w ? edge_w[e] : 1.0f;
+  const int32_t p0 = epos[2 * e], p1 = epos[2 * e + 1];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int32_t p = s ? p1 : p0;
+    int32_t row = (int32_t)n;
+    uint64_t val = 0;
+    if (p >= 0) {
+      // the entry's row is the column of its partner entry (whole graph), or
+      // the shard's row table
+      row = erow ? erow[2 * e + s] : indices[s ? p0 : p1];
+      val = ((uint64_t)__float_as_uint(we) << 32) | (uint32_t)indices[p];
+    }
+    keys[2 * b + s] = row;
+    vals[2 * b + s] = val;
   }
+}
+
+// start[i] = first sorted record with row >= i (i in [0, n])
+__global__ void row_starts_kernel(int64_t R, int64_t n, const int32_t* __restrict__ key,
+                                  int32_t* __restrict__ start) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > R) return;
+  const int64_t lo = (t == 0) ? -1 : (int64_t)key[t - 1];
+  const int64_t hi = (t == R) ? n : min((int64_t)key[t], n);
+  for (int64_t i = lo + 1; i <= hi; ++i) start[i] = (int32_t)t;
 }
 
 struct BatchArgs {
   int64_t n;
   int32_t k;   // slab width
   int64_t ld;
-  const int32_t* indptr;
-  const int32_t* indices;
-  float* hitw;
+  const int32_t* start;  // n+1 record runs
+  const uint64_t* rec;   // sorted records
   const float* x;
   const float* win;
   float* wout;
   float alpha, beta, gamma, lamf, sfin;  // beta already includes m/B
-  int flags;   // bit0 alpha, bit1 gamma, bit2 final, bit3 lamf, bit4 reset hits
+  int flags;   // bit0 alpha, bit1 gamma, bit2 final, bit3 lamf
 };
 
 template <int LPR, int CPL, bool VEC>
@@ -91,9 +118,9 @@ struct Slab {
   }
 };
 
-// One warp per row, grid-stride over rows with a resident grid: the next
-// row's bounds are loaded before this row's work (config 3: 0.52 -> 0.41
-// ms/term).
+// One warp per row (grid-stride, resident grid, the next row's record run
+// prefetched).  The row's records are read 32 at a time in sorted (= sample)
+// order; SUB lane groups gather the sampled neighbours' rows.
 template <int LPR, int CPL, bool VEC>
 __global__ void __launch_bounds__(256) batch_row_kernel(const BatchArgs a) {
   constexpr int SUB = 32 / LPR;
@@ -105,37 +132,34 @@ __global__ void __launch_bounds__(256) batch_row_kernel(const BatchArgs a) {
   int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= a.n) return;
   const bool need_x = (a.flags & 1) || ((a.flags & 4) && (a.flags & 8));
-  int32_t b = __ldg(a.indptr + row), e = __ldg(a.indptr + row + 1);
+  int32_t hb = __ldg(a.start + row), he = __ldg(a.start + row + 1);
   for (; row < a.n; row += nwarps) {
     const int64_t nrow = row + nwarps;
     int32_t nb = 0, ne = 0;
-    if (nrow < a.n) {  // prefetch the next row's bounds
-      nb = __ldg(a.indptr + nrow);
-      ne = __ldg(a.indptr + nrow + 1);
+    if (nrow < a.n) {
+      nb = __ldg(a.start + nrow);
+      ne = __ldg(a.start + nrow + 1);
     }
     S wr, xr, acc;
     wr.load(a.win + row * a.ld, cl, a.k, true);
     if (need_x) xr.load(a.x + row * a.ld, cl, a.k, false); else xr.zero();
     acc.zero();
-    float hsum = 0.f;  // sum of h over the row (for the h*w_r part)
-    for (int32_t p0 = b; p0 < e; p0 += 32) {
+    float hsum = 0.f;  // sum of the row's record weights (the h*w_r part)
+    for (int32_t p0 = hb; p0 < he; p0 += 32) {
       const int32_t p = p0 + lane;
       float h = 0.f;
       int32_t col = 0;
-      if (p < e) h = __ldcg(a.hitw + p);
-      if (h != 0.f) {
-        col = ld_stream_i32(a.indices + p);
-        if (col == row) h = 0.f;  // the diagonal position is never a sampled edge
-        else if (a.flags & 16) a.hitw[p] = 0.f;
+      if (p < he) {
+        const uint64_t r = __ldg(reinterpret_cast<const unsigned long long*>(a.rec) + p);
+        col = (int32_t)(uint32_t)r;
+        h = __uint_as_float((uint32_t)(r >> 32));
       }
-      const unsigned mask = __ballot_sync(0xffffffffu, h != 0.f);
       hsum += h;
-      const int cnt = __popc(mask);
+      const int cnt = min(32, he - p0);
       for (int j0 = 0; j0 < cnt; j0 += SUB) {
         const int j = j0 + sub;
-        const int src = (j < cnt) ? (int)__fns(mask, 0, j + 1) : 0;
-        const int32_t c = __shfl_sync(0xffffffffu, col, src);
-        const float hh = __shfl_sync(0xffffffffu, h, src);
+        const int32_t c = __shfl_sync(0xffffffffu, col, j & 31);
+        const float hh = __shfl_sync(0xffffffffu, h, j & 31);
         if (j < cnt) {
           S g;
           g.load(a.win + (int64_t)c * a.ld, cl, a.k, true);
@@ -172,92 +196,13 @@ __global__ void __launch_bounds__(256) batch_row_kernel(const BatchArgs a) {
         }
       }
     }
-    b = nb;
-    e = ne;
-  }
-}
-
-// One warp per row, one row per warp (full grid).  Kept for k = 128, where
-// it holds 32 registers (full occupancy) and beats the strided version.
-template <int LPR, int CPL, bool VEC>
-__global__ void __launch_bounds__(256) batch_row_single(const BatchArgs a) {
-  constexpr int SUB = 32 / LPR;
-  using S = Slab<LPR, CPL, VEC>;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane / LPR;
-  const int cl = lane % LPR;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= a.n) return;
-  const int32_t b = a.indptr[row], e = a.indptr[row + 1];
-  S wr, xr, acc;
-  wr.load(a.win + row * a.ld, cl, a.k, true);
-  const bool need_x = (a.flags & 1) || ((a.flags & 4) && (a.flags & 8));
-  if (need_x) xr.load(a.x + row * a.ld, cl, a.k, false); else xr.zero();
-  acc.zero();
-  float hsum = 0.f;  // sum of h over the row (for the h*w_r part)
-  for (int32_t p0 = b; p0 < e; p0 += 32) {
-    const int32_t p = p0 + lane;
-    float h = 0.f;
-    int32_t col = 0;
-    if (p < e) {
-      h = __ldcg(a.hitw + p);
-      if (h != 0.f) {
-        col = ld_stream_i32(a.indices + p);
-        if (col == row) h = 0.f;  // the diagonal position is never a sampled edge
-        else if (a.flags & 16) a.hitw[p] = 0.f;
-      }
-    }
-    const unsigned mask = __ballot_sync(0xffffffffu, h != 0.f);
-    hsum += h;
-    const int cnt = __popc(mask);
-    for (int j0 = 0; j0 < cnt; j0 += SUB) {
-      const int j = j0 + sub;
-      const int src = (j < cnt) ? (int)__fns(mask, 0, j + 1) : 0;
-      const int32_t c = __shfl_sync(0xffffffffu, col, src);
-      float hh = __shfl_sync(0xffffffffu, h, src);
-      if (j < cnt) {
-        S g;
-        g.load(a.win + (int64_t)c * a.ld, cl, a.k, true);
-        acc.fma(-hh, g);
-      }
-    }
-  }
-  // fold: nonzero-parallel groups, and the row-sum of h across all lanes
-#pragma unroll
-  for (int off = LPR; off < 32; off <<= 1) acc.fold_xor(off);
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
-  if (sub != 0) return;
-#pragma unroll
-  for (int q = 0; q < CPL; ++q) {
-#pragma unroll
-    for (int i = 0; i < S::W; ++i) {
-      const float est = fmaf(hsum, wr.v[q][i], acc.v[q][i]);
-      float r = a.beta * est;
-      if (a.flags & 1) r = fmaf(a.alpha, xr.v[q][i], r);
-      if (a.flags & 2) r = fmaf(a.gamma, wr.v[q][i], r);
-      if (a.flags & 4) {
-        r *= a.sfin;
-        if (a.flags & 8) r = fmaf(a.lamf, xr.v[q][i], r);
-      }
-      acc.v[q][i] = r;
-    }
-    const int c = S::col0(q, cl);
-    float* dst = a.wout + row * a.ld + c;
-    if (VEC) {
-      st_stream_f4(dst, make_float4(acc.v[q][0], acc.v[q][1], acc.v[q][2], acc.v[q][3]));
-    } else if (c < a.k) {
-      dst[0] = acc.v[q][0];
-    }
+    hb = nb;
+    he = ne;
   }
 }
 
 template <int LPR, int CPL, bool VEC>
 void launch_rows(const BatchArgs& a, cudaStream_t s) {
-  if (LPR == 32 && CPL == 1 && VEC) {
-    batch_row_single<LPR, CPL, VEC><<<grid_for(a.n, 8), 256, 0, s>>>(a);
-    return;
-  }
   static int per_sm = 0;  // grid = resident capacity; warps stride over rows
   if (per_sm == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_row_kernel<LPR, CPL, VEC>, 256, 0);
@@ -297,6 +242,38 @@ int launch_batch_slab(const BatchArgs& a, bool aligned, cudaStream_t s) {
   return SPED_OK;
 }
 
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+struct BatchWs {
+  int32_t *kin, *kout, *start;
+  uint64_t *vin, *vout;
+  void* tmp;
+  size_t tmp_bytes, bytes;
+};
+
+BatchWs batch_ws_layout(char* base, int64_t n, int64_t B) {
+  BatchWs w{};
+  const int64_t R = 2 * B;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* p = base ? base + off : nullptr;
+    off += align256(b);
+    return p;
+  };
+  w.kin = (int32_t*)take(sizeof(int32_t) * R);
+  w.kout = (int32_t*)take(sizeof(int32_t) * R);
+  w.vin = (uint64_t*)take(sizeof(uint64_t) * R);
+  w.vout = (uint64_t*)take(sizeof(uint64_t) * R);
+  w.start = (int32_t*)take(sizeof(int32_t) * (n + 2));
+  size_t t = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t, (int32_t*)nullptr, (int32_t*)nullptr,
+                                  (uint64_t*)nullptr, (uint64_t*)nullptr, (int)R);
+  w.tmp_bytes = t;
+  w.tmp = take(t);
+  w.bytes = off + 256;
+  return w;
+}
+
 }  // namespace
 
 int launch_axpby(int64_t count, double a, const float* x, double b, const float* y, float* out,
@@ -306,34 +283,50 @@ int launch_axpby(int64_t count, double a, const float* x, double b, const float*
 
 using namespace sped;
 
-extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indptr,
-                                          const int32_t* indices, const float* edge_w,
-                                          const int32_t* epos, const int32_t* batch, int64_t B,
-                                          float* hitw, const float* x, const float* w_init,
-                                          float* w_a, float* w_b,
-                                          float* out, int32_t n_terms, const double* alpha,
-                                          const double* beta, const double* gamma,
-                                          double w0_scale, double lam_f, double s_final,
-                                          sped_stream_t stream) {
+extern "C" int64_t sped_edge_batch_workspace_bytes(int64_t n, int64_t B) {
+  return (int64_t)batch_ws_layout(nullptr, n, std::max<int64_t>(B, 1)).bytes;
+}
+
+extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
+                                          const float* edge_w, const int32_t* epos,
+                                          const int32_t* erow, const int32_t* batch, int64_t B,
+                                          void* workspace, int64_t workspace_bytes,
+                                          const float* x, const float* w_init, float* w_a,
+                                          float* w_b, float* out, int32_t n_terms,
+                                          const double* alpha, const double* beta,
+                                          const double* gamma, double w0_scale, double lam_f,
+                                          double s_final, sped_stream_t stream) {
   SPED_CHECK_ARG(n >= 0 && k >= 1 && m >= 0 && B >= 1, "bad sizes");
   SPED_CHECK_ARG(n_terms >= 0 && (n_terms == 0 || (alpha && beta && gamma)), "bad schedule");
   SPED_CHECK_ARG(x != out && x != w_a && x != w_b, "x must not alias outputs");
   SPED_CHECK_ARG(w_init == nullptr || (w_init != out && w_init != w_a && w_init != w_b),
                  "w_init must not alias outputs");
-  SPED_CHECK_ARG(n < INT32_MAX, "problem too large");
+  SPED_CHECK_ARG(n < INT32_MAX && 2 * B < INT32_MAX, "problem too large");
   if (n == 0) return SPED_OK;
   cudaStream_t s = as_stream(stream);
   if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0_scale, x, 0.0, nullptr, out, s);
-  SPED_CHECK_ARG(m > 0 && indptr && indices && epos && batch && hitw, "null graph/batch array");
+  SPED_CHECK_ARG(m > 0 && indices && epos && batch && workspace, "null graph/batch array");
+  char* base = (char*)(((uintptr_t)workspace + 255) & ~uintptr_t(255));
+  BatchWs ws = batch_ws_layout(base, n, B);
+  SPED_CHECK_ARG(workspace_bytes >= (int64_t)ws.bytes, "edge batch workspace too small");
   const double scale = (double)m / (double)B;
   const int32_t slabs = (k + 127) / 128;
+  const int64_t R = 2 * B;
+  int end_bit = 1;
+  while (end_bit < 31 && ((int64_t)1 << end_bit) <= n) ++end_bit;  // keys in [0, n]
   const float* cur = w_init ? w_init : x;
   for (int32_t t = 0; t < n_terms; ++t) {
     const bool final = (t == n_terms - 1);
     float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);
     SPED_CHECK_ARG(dst != nullptr, "scratch buffer for term %d is NULL", t);
-    batch_hist_kernel<<<grid_for(B, 256, num_sms() * 8), 256, 0, s>>>(B, batch + (int64_t)t * B,
-                                                                        epos, edge_w, hitw);
+    records_kernel<<<grid_for(B, 256), 256, 0, s>>>(B, n, batch + (int64_t)t * B, epos, erow,
+                                                    indices, edge_w, ws.kin, ws.vin);
+    SPED_LAUNCH_CHECK();
+    size_t tb = ws.tmp_bytes;
+    // stable: a row's records keep sample order -> fixed summation order
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(ws.tmp, tb, ws.kin, ws.kout, ws.vin, ws.vout,
+                                              (int)R, 0, end_bit, s));
+    row_starts_kernel<<<grid_for(R + 1, 256), 256, 0, s>>>(R, n, ws.kout, ws.start);
     SPED_LAUNCH_CHECK();
     const double sc = (t == 0) ? w0_scale : 1.0;
     for (int32_t sl = 0; sl < slabs; ++sl) {
@@ -342,9 +335,8 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
       a.n = n;
       a.k = min(128, k - c0);
       a.ld = k;
-      a.indptr = indptr;
-      a.indices = indices;
-      a.hitw = hitw;
+      a.start = ws.start;
+      a.rec = ws.vout;
       a.x = x + c0;
       a.win = cur + c0;
       a.wout = dst + c0;
@@ -355,7 +347,7 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
       a.lamf = (float)lam_f;
       a.sfin = (float)s_final;
       a.flags = (alpha[t] != 0.0 ? 1 : 0) | (gamma[t] != 0.0 ? 2 : 0) | (final ? 4 : 0) |
-                (lam_f != 0.0 ? 8 : 0) | (sl == slabs - 1 ? 16 : 0);
+                (lam_f != 0.0 ? 8 : 0);
       const bool aligned = (k % 4 == 0) &&
                            ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(cur) |
                              reinterpret_cast<uintptr_t>(dst)) % 16 == 0);

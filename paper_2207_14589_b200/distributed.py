@@ -230,7 +230,8 @@ class ShardedLaplacian:
         self.pos0, self.pos1 = p0, p1
         self._segments = {}
         self._epos = None
-        self._hitw = None
+        self._erow = None
+        self._bws = None
         self._plan_chunks()
 
     def _plan_chunks(self):
@@ -283,18 +284,28 @@ class ShardedLaplacian:
             self._epos = torch.where(own, ep - self.pos0, torch.full_like(ep, -1)).to(torch.int32)
         return self._epos
 
+    @property
+    def erow_local(self) -> torch.Tensor:
+        """Per edge entry, its local row (-1 where not owned)."""
+        if self._erow is None:
+            ep = self.epos_local.long()
+            rows = torch.searchsorted(self.indptr.long(), ep.clamp_min(0), right=True) - 1
+            self._erow = torch.where(ep >= 0, rows, torch.full_like(rows, -1)).to(torch.int32)
+        return self._erow
+
     def local_batch_term(self, E, x_own, out, batch_t, B, alpha, beta, gamma, w0, lam_f,
                          s_final, k):
         """One edge-minibatch term (sped_edge_batch_poly_apply) on the own
         rows, neighbour rows read from E = [own | halo]."""
         lib = _lib.load()
-        if self._hitw is None:
-            self._hitw = torch.zeros(max(self.nnz_local, 1), dtype=torch.float32,
-                                     device=self.device)
+        nbytes = int(lib.sped_edge_batch_workspace_bytes(self.n_own, int(B)))
+        if self._bws is None or self._bws.numel() < nbytes:
+            self._bws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         rc = lib.sped_edge_batch_poly_apply(
-            self.n_own, k, self.full.graph.m, _lib.ptr(self.indptr), _lib.ptr(self.indices),
-            _lib.ptr(self.full.edge_w), _lib.ptr(self.epos_local), _lib.ptr(batch_t), int(B),
-            _lib.ptr(self._hitw), _lib.ptr(x_own), _lib.ptr(E), None, None, _lib.ptr(out), 1,
+            self.n_own, k, self.full.graph.m, _lib.ptr(self.indices), _lib.ptr(self.full.edge_w),
+            _lib.ptr(self.epos_local), _lib.ptr(self.erow_local), _lib.ptr(batch_t), int(B),
+            _lib.ptr(self._bws), self._bws.numel(), _lib.ptr(x_own), _lib.ptr(E), None, None,
+            _lib.ptr(out), 1,
             _lib.dbl_array([alpha]), _lib.dbl_array([beta]), _lib.dbl_array([gamma]), float(w0),
             float(lam_f), float(s_final), _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_edge_batch_poly_apply (shard)")

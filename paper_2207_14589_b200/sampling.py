@@ -123,7 +123,9 @@ class EdgeBatchOracle:
         lap = op.laplacian
         self.device = lap.device
         self.m = lap.graph.m
-        self.hitw = torch.zeros(max(lap.nnz, 1), dtype=torch.float32, device=self.device)
+        lib = _lib.load()
+        self.ws_bytes = int(lib.sped_edge_batch_workspace_bytes(lap.n, self.batch_size))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.last_batch = None
 
     @property
@@ -164,8 +166,8 @@ class EdgeBatchOracle:
         wa = torch.empty_like(xd) if nt >= 2 else None
         wb = torch.empty_like(xd) if nt >= 3 else None
         rc = lib.sped_edge_batch_poly_apply(
-            self.n, k, self.m, _lib.ptr(lap.indptr), _lib.ptr(lap.indices), _lib.ptr(lap.edge_w),
-            _lib.ptr(lap.epos), _lib.ptr(batch), B, _lib.ptr(self.hitw), _lib.ptr(xd), None,
+            self.n, k, self.m, _lib.ptr(lap.indices), _lib.ptr(lap.edge_w), _lib.ptr(lap.epos),
+            None, _lib.ptr(batch), B, _lib.ptr(self.ws), self.ws_bytes, _lib.ptr(xd), None,
             _lib.ptr(wa), _lib.ptr(wb), _lib.ptr(out), nt, _lib.dbl_array(al),
             _lib.dbl_array(be), _lib.dbl_array(ga), float(w0), float(lf), float(s),
             _lib.stream_ptr(self.device))

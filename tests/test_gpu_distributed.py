@@ -123,8 +123,6 @@ def test_sharded_stochastic_terms_match_single_gpu(cuda, world, cfg):
         cur = 1 - cur
     got = torch.cat(outs)
     assert rel_fro(got.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
-    # hit buffers are left zero for the next call
-    assert all(float(sh._hitw.abs().sum()) == 0.0 for sh in shards)
 
 
 def test_sharded_solver_steps_single_rank(cuda):
