@@ -18,7 +18,7 @@
  *                              (+ restated per-term composition)
  *   sped_gram / sped_mueg_coeffs / sped_block_update
  *                              mu_eg_step                        solvers.py:121-144
- *   sped_small_mueg / sped_persistent_mueg
+ *   sped_persistent_mueg
  *                              run_solver's step loop (mu-eg)    solvers.py:227-292
  *                              (whole steps per launch)          solvers.py:121-144
  *   sped_oja_coeffs (+ gram/update)  oja_step + _orthonormalize  solvers.py:84-118
@@ -113,7 +113,7 @@ int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_threshold,
  * normalized Laplacian of a unit-weight graph without self loops; terms after
  * the first then run on u = D^-1/2 w and skip the values stream (values must
  * still be given: the first term reads them).  Ignored for k not in
- * {4,...,128}, unaligned buffers, w_init, or opt-in short-row segments. */
+ * {4,...,128}, unaligned buffers or w_init. */
 int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                         const int32_t* indices, const float* values,
                         int32_t long_threshold, int32_t chunk_len,
@@ -164,18 +164,11 @@ int sped_mueg_coeffs(int32_t k, const double* G, double eta, float* A, float* sc
  * with_m=0: Gram = S.  T = R^{-1} for R = chol(Gram)^T (upper), fp32. */
 int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, float* T,
                     int32_t* flag, sped_stream_t stream);
-/* Desk-scale fast path (n*k <= 12288, k <= 32): `steps` whole mu-EG steps
- * (polynomial apply, Gram, k x k algebra, update) in one thread block with
- * the state in shared memory.  V (n x k) is updated in place; flag as above;
- * returns SPED_ERR_UNSUPPORTED when the graph is too large. */
-int sped_small_mueg(int32_t n, int32_t k, const int32_t* indptr, const int32_t* indices,
-                    const float* values, int32_t n_terms, const double* alpha,
-                    const double* beta, const double* gamma, double w0_scale, double lam_f,
-                    double s_final, double eta, int32_t steps, float* V, int32_t* flag,
-                    sped_stream_t stream);
 /* Grid-resident fast path (k <= 32): `steps` whole mu-EG steps in ONE
  * cooperative launch (one CTA per SM, grid barriers between phases; state in
- * HBM/L2).  Same contract as sped_small_mueg; `nnz` = indptr[n] (host copy,
+ * HBM/L2).  V (n x k) is updated in place; flag is set when a column's norm
+ * vanishes (rank collapse, solvers.py:136-143); SPED_ERR_UNSUPPORTED for
+ * k > 32 or > 64 terms.  `nnz` = indptr[n] (host copy,
  * sizes the launch); `workspace` of at least sped_persistent_workspace_bytes(n, k)
  * bytes (two n x k blocks + Gram partials). */
 int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* bytes);

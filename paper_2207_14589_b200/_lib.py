@@ -48,8 +48,6 @@ SIGNATURES = {
     "sped_mueg_coeffs": (C.c_int, [_i32, _p, _f64, _p, _p, _p, _p]),
     "sped_oja_coeffs": (C.c_int, [_i32, _p, _f64, _i32, _p, _p, _p]),
     "sped_block_update": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _f64, _p, _i32, _p, _p]),
-    "sped_small_mueg": (C.c_int, [_i32, _i32, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64, _f64,
-                                  _f64, _i32, _p, _p, _p]),
     "sped_persistent_workspace_bytes": (C.c_int, [_i32, _i32, _p]),
     "sped_persistent_mueg": (C.c_int, [_i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64,
                                        _f64, _f64, _i32, _p, _p, _p, _i64, _p]),

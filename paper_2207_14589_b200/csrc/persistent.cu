@@ -77,7 +77,7 @@ struct PArgs {
 };
 
 // Gram entry e -> (column a, column b): S upper triangle (row-major), then
-// C (k x k), then diag Q (the small_solver.cu order).
+// C (k x k), then diag Q.
 __device__ __forceinline__ void entry_cols(int e, int k, int nS, int nC, int& ca, int& cb) {
   if (e < nS) {
     int rem = e, ia = 0;

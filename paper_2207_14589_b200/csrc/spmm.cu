@@ -100,14 +100,6 @@ __device__ __forceinline__ float entry_value(const float* values, int64_t p, int
   return ld_stream_f32(values + p);
 }
 
-__device__ __forceinline__ float4 ld_gather_hot_cold(const float* p, bool hot, uint64_t pol_hot,
-                                                     uint64_t pol_cold) {
-  float4 r;
-  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-      : "l"(p), "l"(hot ? pol_hot : pol_cold));
-  return r;
-}
 __device__ __forceinline__ float4 ldg_f4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
@@ -120,10 +112,6 @@ __device__ __forceinline__ float ld_val(const float* p) {
   float r;
   asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
-}
-__device__ __forceinline__ void st_evict_first_f4(float* p, float4 v, uint64_t pol) {
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
-               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
 }
 
 // W-float lane vectors: W = 4 (128-bit loads) or W = 8 (256-bit loads,
@@ -416,164 +404,6 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? TE
   }
 }
 
-#ifndef SHORT_U
-#define SHORT_U 4
-#endif
-template <int LPR, int VM>
-__global__ void __launch_bounds__(256, 4) spmm_short_kernel(const TermArgs a) {
-  constexpr int G = LPR;
-  constexpr int RPW = 32 / G;
-  constexpr int CAP = 2 * G;
-  constexpr int U = SHORT_U;
-  const int lane = threadIdx.x & 31;
-  const int grp = lane / G;
-  const int g = lane % G;
-  const int gbase = grp * G;
-  const uint64_t pol_hot = policy_evict_last();
-  const uint64_t pol_cold = policy_evict_first();
-  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
-  const int64_t rows = a.row_end - a.row_begin;
-  const int64_t nbatch = (rows + RPW - 1) / RPW;
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
-  int64_t bi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (bi >= nbatch) return;
-
-  auto load_bounds = [&](int64_t batch, int32_t& b, int32_t& e) {
-    const int64_t row = a.row_begin + batch * RPW + grp;
-    b = 0;
-    e = 0;
-    if (batch < nbatch && row < a.row_end) {
-      b = __ldg(a.indptr + row);
-      e = __ldg(a.indptr + row + 1);
-    }
-  };
-  auto load_cols = [&](int32_t b, int32_t e, int64_t row, int32_t (&col)[2], float (&val)[2]) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int32_t p = b + g + q * G;
-      col[q] = 0;
-      val[q] = 0.f;
-      if (p < e) {
-        col[q] = ld_stream_i32(a.indices + p);
-        val[q] = entry_value<VM>(a.values, p, col[q], row, e - b);
-      }
-    }
-  };
-
-  int32_t b0, e0, b1, e1;
-  load_bounds(bi, b0, e0);
-  load_bounds(bi + wstride, b1, e1);
-  int32_t col0[2], col1[2];
-  float val0[2], val1[2];
-  load_cols(b0, e0, a.row_begin + bi * RPW + grp, col0, val0);
-
-  for (; bi < nbatch; bi += wstride) {
-    const int64_t row = a.row_begin + bi * RPW + grp;
-    const bool valid = row < a.row_end;
-    // ---- prefetch: bounds of batch +2, columns of batch +1, x of this batch
-    int32_t b2, e2;
-    load_bounds(bi + 2 * wstride, b2, e2);
-    load_cols(b1, e1, row + wstride * RPW, col1, val1);
-    const int64_t off = row * a.ld + g * 4;
-    float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), wr = xr;
-    if (valid) {
-      if (need_x) xr = ld_stream_f4(a.x + off);
-      if (a.flags & TF_GAMMA) wr = ld_gather_f4(a.win + off);
-    }
-    // ---- gathers of this batch from the prefetched columns
-    const int32_t len = valid ? e0 - b0 : 0;
-    int32_t mlen = min(len, CAP);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mlen = max(mlen, __shfl_xor_sync(0xffffffffu, mlen, o));
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int j0 = 0; j0 < CAP; j0 += U) {
-      if (j0 >= mlen) break;
-      float4 gv[U];
-      float w[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = j0 + u;
-        const int src = gbase + (j % G);
-        const int32_t c = __shfl_sync(0xffffffffu, (j < G) ? col0[0] : col0[1], src);
-        w[u] = __shfl_sync(0xffffffffu, (j < G) ? val0[0] : val0[1], src);
-        if (j < len) {
-          gv[u] = ld_gather_hot_cold(a.win + (int64_t)c * a.ld + g * 4, c < a.hot_rows, pol_hot,
-                                     pol_cold);
-        } else {
-          gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          w[u] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = f4_fma(w[u], gv[u], acc);
-    }
-    // rows longer than CAP: finish in a plain loop (rare here)
-    int32_t mall = len;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mall = max(mall, __shfl_xor_sync(0xffffffffu, mall, o));
-    for (int32_t o = CAP; o < mall; o += G) {
-      const int32_t p = b0 + o + g;
-      int32_t c = 0;
-      float v = 0.f;
-      if (o + g < len) {
-        c = ld_stream_i32(a.indices + p);
-        v = entry_value<VM>(a.values, p, c, row, len);
-      }
-      const int cnt = max(0, min(G, len - o));
-#pragma unroll
-      for (int j0 = 0; j0 < G; j0 += 4) {
-        float4 gv[4];
-        float wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u;
-          const int32_t cj = __shfl_sync(0xffffffffu, c, gbase + (j % G));
-          wv[u] = __shfl_sync(0xffffffffu, v, gbase + (j % G));
-          gv[u] = (j < cnt) ? ld_gather_f4(a.win + (int64_t)cj * a.ld + g * 4)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (j >= cnt) wv[u] = 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc = f4_fma(wv[u], gv[u], acc);
-      }
-    }
-    if (valid && len <= a.long_thresh)
-      st_evict_first_f4(a.wout + off, term_epilogue(a, acc, xr, wr), pol_cold);
-    // ---- rotate the pipeline
-    b0 = b1;
-    e0 = e1;
-    b1 = b2;
-    e1 = e2;
-    col0[0] = col1[0];
-    col0[1] = col1[1];
-    val0[0] = val1[0];
-    val0[1] = val1[1];
-  }
-}
-
-template <int LPR>
-static void launch_short(const TermArgs& a, int vm, cudaStream_t s) {  // vm 0 / 1
-  const int64_t rows = a.row_end - a.row_begin;
-  const int64_t batches = (rows + (32 / LPR) - 1) / (32 / LPR);
-  // persistent grid = exactly the resident capacity (no second wave)
-  static int per_sm[2] = {0, 0};
-  int& ps = per_sm[vm == 1 ? 1 : 0];
-  if (ps == 0) {
-    if (vm == 1)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, 1>, 256, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmm_short_kernel<LPR, 0>, 256, 0);
-    if (ps < 1) ps = 1;
-  }
-  const int64_t blocks = std::min<int64_t>((batches + 7) / 8, (int64_t)num_sms() * ps);
-  const unsigned grid = (unsigned)blocks;
-  if (grid == 0) return;
-  if (vm == 1)
-    spmm_short_kernel<LPR, 1><<<grid, 256, 0, s>>>(a);
-  else
-    spmm_short_kernel<LPR, 0><<<grid, 256, 0, s>>>(a);
-}
 
 // Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
 // lanes over columns (CPL columns each), SUB groups over nonzeros.  Handles
@@ -758,18 +588,6 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       a.row_begin = segs[i].begin;
       a.row_end = segs[i].end;
       int sub = segs[i].sub;
-      if (sub == 0 && !w8) {  // software-pipelined short rows (128-bit path only)
-        switch (lpr) {
-          case 1: launch_short<1>(a, vm, s); break;
-          case 2: launch_short<2>(a, vm, s); break;
-          case 4: launch_short<4>(a, vm, s); break;
-          case 8: launch_short<8>(a, vm, s); break;
-          case 16: launch_short<16>(a, vm, s); break;
-          default: launch_short<32>(a, vm, s); break;
-        }
-        SPED_LAUNCH_CHECK();
-        continue;
-      }
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
       if (w8) launch_rows_w<8>(lpr, sub, a, vm, s);
@@ -888,13 +706,11 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
   // scaled-block mode (VM 2) for unit-weight normalized Laplacians: the
   // first term reads the stored values and writes u = D^-1/2 w, later terms
   // gather u unweighted.  Only on the fast path with every buffer 16-B
-  // aligned and no opt-in short-row segments; otherwise stored values.
+  // aligned; otherwise stored values.
   bool norm = row_scale && values && !w_init && n_terms >= 2 && slabs == 1 &&
               (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128) &&
               ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w_a) |
                 reinterpret_cast<uintptr_t>(w_b) | reinterpret_cast<uintptr_t>(out)) % 16 == 0);
-  for (int i = 0; i < n_segments; ++i)
-    if (segments[3 * i + 2] == 0) norm = false;
   Segment segs[8];
   int nseg = n_segments;
   for (int i = 0; i < nseg; ++i) {

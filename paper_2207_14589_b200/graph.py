@@ -213,31 +213,21 @@ def segment_table(rowlen: np.ndarray, k: int, sorted_desc: bool, long_threshold)
     n = int(rowlen.size)
     lpr = max(1, min(32, k // 4))
     smax = max(1, 32 // lpr)
-    use_short = os.environ.get("SPED_SHORT", "0") == "1"
     if n == 0:
         seg = []
     elif sorted_desc:
         L = rowlen
-        cap = 2 * lpr      # rows the pipelined short-row kernel covers from registers
         thr = long_threshold if long_threshold is not None else np.iinfo(np.int64).max
         r_long = int(np.searchsorted(-L, -thr, side="left"))    # rows with len > thr
         r_64 = max(int(np.searchsorted(-L, -64, side="left")), r_long)
-        r_cap = max(int(np.searchsorted(-L, -cap, side="left")), r_64)
-        if not use_short:
-            r_cap = n
         seg = []
         if r_64 > r_long:
             seg.append((r_long, r_64, smax))      # long rows: warp per row
-        if r_cap > r_64:
-            seg.append((r_64, r_cap, 1))          # medium/short rows: LPR lanes per row
-        if n > r_cap:
-            seg.append((r_cap, n, 0))             # short rows: pipelined kernel (opt-in)
+        if n > r_64:
+            seg.append((r_64, n, 1))              # medium/short rows: LPR lanes per row
     else:
         mean = float(rowlen.sum()) / n
-        if use_short and mean <= 2 * lpr:
-            seg = [(0, n, 0)]
-        else:
-            seg = [(0, n, smax if mean >= 64 else 1)]
+        seg = [(0, n, smax if mean >= 64 else 1)]
     flat = [x for t in seg for x in t]
     return len(seg), _lib.i64_array(flat)
 

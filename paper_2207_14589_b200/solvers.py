@@ -410,53 +410,6 @@ class _GraphStepper:
         return self.bufs[self.cur]
 
 
-SMALL_MAX_NK = 12288
-
-
-def small_solver_eligible(op, k: int, solver: str) -> bool:
-    """Desk-scale graphs whose whole mu-EG state fits one thread block's
-    shared memory run on the single-block kernel (sped_small_mueg)."""
-    return (solver == "mu-eg" and isinstance(op, TransformedOperator)
-            and op.transform.is_polynomial and op.n * k <= SMALL_MAX_NK and k <= 32
-            and op.n_terms <= 64)
-
-
-class _SmallStepper:
-    """Many whole mu-EG steps per launch in one thread block (K2)."""
-
-    def __init__(self, op: TransformedOperator, eta: float, V0: torch.Tensor):
-        self.op, self.eta = op, eta
-        self.V_ = V0.clone().contiguous()
-        self.ws = StepWorkspace(op.n, int(V0.shape[1]), V0.device)
-
-    def advance(self, m: int):
-        if m <= 0:
-            return
-        lib = _lib.load()
-        lap = self.op.laplacian
-        al, be, ga, w0, lf, s = self.op.schedule
-        rc = lib.sped_small_mueg(lap.n, int(self.V_.shape[1]), _lib.ptr(lap.indptr),
-                                 _lib.ptr(lap.indices), _lib.ptr(lap.values), len(al),
-                                 _lib.dbl_array(al), _lib.dbl_array(be), _lib.dbl_array(ga),
-                                 float(w0), float(lf), float(s), float(self.eta), int(m),
-                                 _lib.ptr(self.V_), _lib.ptr(self.ws.flag),
-                                 _lib.stream_ptr(self.V_.device))
-        _lib.check(rc, "sped_small_mueg")
-
-    def step(self):
-        self.advance(1)
-
-    @property
-    def V(self):
-        return self.V_
-
-    @property
-    def bufs(self):
-        return [self.V_]
-
-    cur = 0
-
-
 PERSISTENT_MAX_NK = 1 << 22
 
 
@@ -525,7 +478,7 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
                streak_target: int | None = None, subspace_target: float | None = None,
                stop_on_targets: bool = False, record_timing: bool = True,
                device=None, use_cuda_graphs: bool = True,
-               index_source: str = "device", use_small_kernel: bool = False,
+               index_source: str = "device",
                use_persistent_kernel: bool | None = None) -> SolverRun:
     """Run a solver on the reversed transformed Laplacian (solvers.py:227-292),
     entirely on the device.  Metrics are evaluated on the host every
@@ -587,9 +540,7 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
     if graphable:
         persistent = (persistent_solver_eligible(op, config.k, config.solver)
                       if use_persistent_kernel is None else use_persistent_kernel)
-        if use_small_kernel and small_solver_eligible(op, config.k, config.solver):
-            stepper = _SmallStepper(op, config.eta, V)
-        elif persistent:
+        if persistent:
             stepper = _PersistentStepper(op, config.eta, V)
         else:
             stepper = _GraphStepper(op, config.solver, config.eta, V)

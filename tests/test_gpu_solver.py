@@ -240,9 +240,6 @@ def test_run_solver_cuda_graph_equals_eager(cuda, golden):
                       use_persistent_kernel=False)
     b = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=False)
     assert torch.equal(a.V, b.V)
-    # the single-block kernel (K2, opt-in): same result to fp32 rounding
-    c = sp.run_solver(g, t, cfg, record_timing=False, use_small_kernel=True)
-    assert rel_fro(c.V.cpu().numpy(), b.V.cpu().numpy()) <= 1e-5
     # the grid-resident kernel (K7, the default here): same to fp32 rounding,
     # and bit-reproducible run to run
     d = sp.run_solver(g, t, cfg, record_timing=False)
@@ -330,25 +327,6 @@ def test_block_update_vs_fp64(cuda, k):
     # no M, no scale (the CholQR2 / orthonormalisation form)
     ws.update(P, A.contiguous(), None, None, 0.0, None, out)
     assert rel_fro(out.cpu().numpy(), (Pd @ Ad).cpu().numpy()) <= 1e-6
-
-
-@pytest.mark.parametrize("name,mode,kind,ell,k", [("cfg1", "unnormalized", "negexp-limit", 13, 10),
-                                                  ("er0", "unnormalized", "negexp-limit", 9, 3),
-                                                  ("er1", "normalized", "negexp-taylor", 8, 4)])
-def test_small_single_block_solver_vs_reference(cuda, golden, name, mode, kind, ell, k):
-    """sped_small_mueg: one whole mu-EG step in one thread block == the
-    reference's mu_eg_step (goldens) to 1e-5."""
-    sp = _sp()
-    from paper_2207_14589_b200.solvers import _SmallStepper, small_solver_eligible
-    op = sp.make_reversed_operator(_graph(golden, name), sp.SpectralTransform(kind, ell), mode)
-    base = f"step/{name}/{mode}/{kind}/{ell}/{k}"
-    V0 = torch.as_tensor(golden[base + "/V0"], dtype=torch.float32, device="cuda")
-    assert small_solver_eligible(op, k, "mu-eg")
-    for eta in (0.05, 0.5):
-        st = _SmallStepper(op, eta, op.laplacian.to_internal(V0))
-        st.advance(1)
-        V1 = op.laplacian.from_internal(st.V).cpu().numpy()
-        assert rel_fro(V1, golden[f"{base}/mueg/{eta}"]) <= 1e-5, eta
 
 
 @pytest.mark.parametrize("name,mode,kind,ell,k", [("cfg1", "unnormalized", "negexp-limit", 13, 10),

@@ -1,5 +1,5 @@
 """Per-step time of the small-graph solver paths (configs 1-2): CUDA-graph
-multi-kernel steps vs the grid-resident K7 kernel (and K2 where eligible).
+multi-kernel steps vs the grid-resident K7 kernel.
 
     python tools/bench_small.py [--steps 2000]
 """
@@ -15,8 +15,7 @@ import torch  # noqa: E402
 
 import paper_2207_14589_b200 as sp  # noqa: E402
 from paper_2207_14589_b200 import generators as G  # noqa: E402
-from paper_2207_14589_b200.solvers import (_GraphStepper, _PersistentStepper,  # noqa: E402
-                                           _SmallStepper, small_solver_eligible)
+from paper_2207_14589_b200.solvers import _GraphStepper, _PersistentStepper  # noqa: E402
 
 CASES = [(1, "negexp-limit", 13, 0.1), (2, "negexp-limit", 17, 1.0)]
 
@@ -48,8 +47,6 @@ def main():
         row["cuda_graph_us_per_step"] = per_step_us(_GraphStepper(op, "mu-eg", eta, Vi), args.steps)
         t0 = time.perf_counter()
         row["persistent_us_per_step"] = per_step_us(_PersistentStepper(op, eta, Vi), args.steps)
-        if small_solver_eligible(op, k, "mu-eg"):
-            row["single_block_us_per_step"] = per_step_us(_SmallStepper(op, eta, Vi), args.steps)
         print(json.dumps(row), flush=True)
 
 
