@@ -351,13 +351,20 @@ struct Cfg2 {
   // all four 3xTF32 products (plus lo*lo) at the M=128 rate, where three
   // M=64 MMAs run at well under half of it (SS-mode M=64).  Otherwise (K2 =
   // 128) separate hi / lo tiles and three M=128 x N=128 MMAs.
+  // BIG mode (K2 = 256): two MMA groups per K step -- rows 0..127 x cols
+  // 0..255 (M=128, N=256: S and C) and rows 128..255 x cols 128..255 (N=128:
+  // Q) -- 384 TMEM columns, so one accumulator bank, and the fp64 row sums
+  // (128 x 384) live in the CTA's global partial (read-modify-write by the
+  // owning drain thread) instead of shared memory.
   static constexpr bool YM = (K2 == 64);
-  static constexpr int NACC = 2;                      // accumulators per bank
-  static constexpr int ACC_COLS = YM ? 2 * K2 : K2;   // TMEM columns per accumulator
+  static constexpr bool BIG = (K2 == 256);
+  static constexpr int NACC = BIG ? 1 : 2;            // accumulators per bank
+  static constexpr int NBANK = BIG ? 1 : 2;
+  static constexpr int ACC_COLS = YM ? 2 * K2 : (BIG ? 384 : K2);  // TMEM columns per accumulator
   static constexpr int SPLIT = (K2 == 64) ? 1024 : 512;  // rows per slice (drain)
-  static constexpr int KC = (K2 == 64) ? 64 : 32;     // rows per chunk
-  static constexpr int NR = (K2 == 64) ? 4 : 3;       // raw (bulk copy) stages
-  static constexpr int NTB = (K2 == 64) ? 3 : 2;      // converted tile buffers
+  static constexpr int KC = (K2 == 64) ? 64 : (BIG ? 16 : 32);  // rows per chunk
+  static constexpr int NR = (K2 == 64) ? 4 : (BIG ? 4 : 3);     // raw (bulk copy) stages
+  static constexpr int NTB = (K2 == 64) ? 3 : (BIG ? 3 : 2);    // converted tile buffers
   static constexpr int RAW_FLOATS = KC * K2;
   static constexpr int TCOLS = YM ? 2 * K2 : K2;      // columns of one K-major tile
   static constexpr int KSTEP_FLOATS = (TCOLS / 8) * (SBO_B / 4);
@@ -368,7 +375,7 @@ struct Cfg2 {
   static constexpr int SUM_LD = K2 + 1;               // padded fp64 row stride (rows < k)
   static constexpr int QLD = HALF + 1;                // padded stride of the Q block
   static constexpr int SUM_BLOCK = HALF * SUM_LD + HALF * QLD;
-  static constexpr int SUM_DOUBLES = (YM ? 2 : 1) * SUM_BLOCK;  // Y: H rows + L rows
+  static constexpr int SUM_DOUBLES = BIG ? 0 : (YM ? 2 : 1) * SUM_BLOCK;  // Y: H rows + L rows
   static constexpr int SMEM = NR * RAW_FLOATS * 4 + NTB * TBUF_FLOATS * 4 + SUM_DOUBLES * 8 + 1024;
   static constexpr int NTHREADS = 14 * 32;
 };
@@ -412,6 +419,10 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int e = tid; e < C::SUM_DOUBLES; e += C::NTHREADS) sums[e] = 0.0;
+  // fp64 partial of this CTA: rows 0..k-1 (K2 columns), then Q (k x k)
+  double* out = partial + (int64_t)blockIdx.x * (C::HALF * K2 + C::HALF * C::HALF);
+  if constexpr (C::BIG)
+    for (int e = tid; e < C::HALF * K2 + C::HALF * C::HALF; e += C::NTHREADS) out[e] = 0.0;
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -498,14 +509,17 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t KSTEP_B = C::KSTEP_FLOATS * 4;
-      constexpr uint32_t idesc = instr_desc_tf32(C::YM ? 128 : K2, C::ACC_COLS);
+      constexpr uint32_t idesc = C::BIG ? instr_desc_tf32(128, 256)
+                                        : instr_desc_tf32(C::YM ? 128 : K2, C::ACC_COLS);
+      constexpr uint32_t idesc_q = instr_desc_tf32(128, 128);  // BIG: the Q block
       for (int64_t q = 0; q < nq; ++q) {
         const int ts = (int)(q % C::NTB);
         const int64_t s = q / C::CPS;
         const int ch = (int)(q % C::CPS);
-        const int bank = (int)(s & 1);
+        const int bank = (int)(s % C::NBANK);
         const bool slice_end = (ch == C::CPS - 1) || (q == nq - 1);
-        if (ch == 0 && s >= 2) mbar_wait_sleep(&bank_free[bank], (uint32_t)(((s >> 1) - 1) & 1));
+        if (ch == 0 && s >= C::NBANK)
+          mbar_wait_sleep(&bank_free[bank], (uint32_t)(((s / C::NBANK) - 1) & 1));
         mbar_wait(&tile_full[ts], (uint32_t)((q / C::NTB) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const float* hi = tiles + ts * C::TBUF_FLOATS;
@@ -518,6 +532,18 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
           const uint64_t dh = smem_desc(hi_a + kb * KSTEP_B, SBO_B, LBO_B);
           if constexpr (C::YM) {
             mma_tf32(tacc, dh, dh, idesc, acc0);  // [H|L]^T [H|L]
+          } else if constexpr (C::BIG) {
+            // rows 0..127 x cols 0..255, then rows/cols 128..255 (16 column groups on)
+            const uint64_t dl = smem_desc(lo_a + kb * KSTEP_B, SBO_B, LBO_B);
+            mma_tf32(tacc, dh, dh, idesc, acc0);
+            mma_tf32(tacc, dh, dl, idesc, 1u);
+            mma_tf32(tacc, dl, dh, idesc, 1u);
+            const uint32_t goff = 16u * SBO_B;
+            const uint64_t qh = smem_desc(hi_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
+            const uint64_t ql = smem_desc(lo_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
+            mma_tf32(tacc + 256, qh, qh, idesc_q, acc0);
+            mma_tf32(tacc + 256, qh, ql, idesc_q, 1u);
+            mma_tf32(tacc + 256, ql, qh, idesc_q, 1u);
           } else {
             const uint64_t dl = smem_desc(lo_a + kb * KSTEP_B, SBO_B, LBO_B);
             mma_tf32(tacc, dh, dh, idesc, acc0);
@@ -540,11 +566,27 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
     const int row = C::YM ? (quarter * 32 + lane) & (K2 - 1) : quarter * 32 + lane;
     double* sblk = sums + ((C::YM && quarter >= 2) ? C::SUM_BLOCK : 0);
     for (int64_t s = 0; s < my_slices; ++s) {
-      const int bank = (int)(s & 1);
-      mbar_wait_sleep(&bank_full[bank], (uint32_t)((s >> 1) & 1));
+      const int bank = (int)(s % C::NBANK);
+      mbar_wait_sleep(&bank_full[bank], (uint32_t)((s / C::NBANK) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int chunks = (s == my_slices - 1) ? last_chunks : C::CPS;
       const int nk = min(C::NACC, chunks * (C::KC / 8));
+      if constexpr (C::BIG) {
+        // TMEM lane m: row m of [S | C] (cols 0..255) and row m of Q (cols
+        // 256..383); fp64 sums accumulate in the global partial
+#pragma unroll 1
+        for (int c0 = 0; c0 < 384; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem + (uint32_t)c0 + lane_base, v);
+          double* dst = (c0 < 256) ? out + row * K2 + c0
+                                   : out + C::HALF * K2 + row * C::HALF + (c0 - 256);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) dst[i] += (double)v[i];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&bank_free[bank]);
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < K2; c0 += 16) {
         double acc[16];
@@ -578,12 +620,12 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // fp64 partial of this CTA: rows 0..k-1 (K2 columns), then Q (k x k)
-  double* out = partial + (int64_t)blockIdx.x * (C::HALF * K2 + C::HALF * C::HALF);
+  if constexpr (!C::BIG)
   for (int e = tid; e < C::HALF * K2; e += C::NTHREADS) {
     const int i = (e / K2) * C::SUM_LD + (e % K2);
     out[e] = C::YM ? sums[i] + sums[C::SUM_BLOCK + i] : sums[i];
   }
+  if constexpr (!C::BIG)
   for (int e = tid; e < C::HALF * C::HALF; e += C::NTHREADS) {
     const int i = C::HALF * C::SUM_LD + (e / C::HALF) * C::QLD + (e % C::HALF);
     out[C::HALF * K2 + e] = C::YM ? sums[i] + sums[C::SUM_BLOCK + i] : sums[i];
@@ -694,7 +736,8 @@ int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, voi
                        : tc::launch2<64>(n, k, V, M, G, partial, s);
     case 64: return v1 ? tc::launch<128>(n, k, V, M, G, partial, s)
                        : tc::launch2<128>(n, k, V, M, G, partial, s);
-    case 128: return tc::launch<256>(n, k, V, M, G, partial, s);
+    case 128: return v1 ? tc::launch<256>(n, k, V, M, G, partial, s)
+                        : tc::launch2<256>(n, k, V, M, G, partial, s);
     default: set_error("gram_tc: unsupported k=%d", k); return SPED_ERR_UNSUPPORTED;
   }
 }
