@@ -199,7 +199,7 @@ def degree_bounds(g: Graph) -> DegreeBounds:
 
 
 L2_BYTES = 126 * 1024 * 1024
-HOT_FRACTION = 0.7          # share of L2 reserved for the hot (evict_last) rows
+HOT_FRACTION = 0.3          # share of L2 held by the hub-prefix persisting window
 SKEW_REORDER = 16.0         # max degree / mean degree above which rows are degree-ordered
 
 
