@@ -126,6 +126,24 @@ int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                         const double* gamma, double w0_scale, double lam_f,
                         double s_final, sped_stream_t stream);
 
+/* ---- split shard term (row-sharded L) ------------------------
+ * One term of sped_csr_poly_apply's schedule on a row shard whose CSR is
+ * split into the entries that read the shard's own rows (L_own) and those
+ * that read halo rows (L_halo), so the halo exchange overlaps pass 0:
+ *   raw_out = 1 (pass 0): out = L_own w                      (no epilogue)
+ *   raw_out = 0 (pass 1): out = lam_f x + s_final (alpha x + beta w0 (L_halo w
+ *                          + partial_in) + gamma w0 w)
+ * w is the [own | halo] block (own rows first), x / out / partial_in the own
+ * rows (n x k); values are required (stored fp32).  Replaces, per term, the
+ * ell x LaplacianOperator.matvec of transforms.py:241-262 on one shard. */
+int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr, const int32_t* indices,
+                        const float* values, int32_t long_threshold, int32_t chunk_len,
+                        const int32_t* chunk_desc, int64_t n_chunks, float* partials,
+                        int32_t* tickets, const int64_t* segments, int32_t n_segments,
+                        const float* x, const float* w, const float* partial_in,
+                        int32_t raw_out, float* out, double alpha, double beta, double gamma,
+                        double w0_scale, double lam_f, double s_final, sped_stream_t stream);
+
 /* ---- edge-minibatch apply (solvers.py:166-178, per term) ----------------
  * Term t replaces L w by (m/B) * sum_{b<B} w_e x_e x_e^T w over the sampled
  * edge ids batch[t*B .. t*B+B) (int32, the numpy rng.integers stream).

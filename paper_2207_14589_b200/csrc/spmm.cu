@@ -63,6 +63,7 @@ enum TermFlags : int {
   TF_LAMF = 8,    // lam_f != 0
   TF_NORM_IN = 16,    // win holds u = D^-1/2 w; gathers are unweighted (VM 2)
   TF_SCALE_OUT = 32,  // write u' = D^-1/2 w' (the next term gathers it)
+  TF_RAW_OUT = 64,    // split shard pass 0: write the raw neighbour sum, no epilogue
 };
 
 struct TermArgs {
@@ -87,11 +88,13 @@ struct TermArgs {
   int64_t row_begin, row_end;  // this launch's row segment
   int64_t hot_rows;        // hub prefix kept in L2 (persisting window; evict_last with SPED_HINTS)
   const float* rscale;     // d^-1/2 per row (TF_NORM_IN / TF_SCALE_OUT)
+  const float* acc_in;     // VM 3: partial neighbour sum added before the epilogue (or NULL)
 };
 
 // VM 0: stored values; 1: implicit combinatorial (-1, row_len-1 on the
 // diagonal); 2: implicit normalized on the scaled block (1 off the diagonal,
-// the diagonal handled in the epilogue)
+// the diagonal handled in the epilogue); 3: stored values, split-shard term
+// (pass 0 writes the raw sum, pass 1 adds acc_in before the epilogue)
 template <int VM>
 __device__ __forceinline__ float entry_value(const float* values, int64_t p, int32_t col, int64_t row,
                                              int32_t rowlen) {
@@ -126,6 +129,10 @@ struct Vf {
   __device__ __forceinline__ void fma(float s, const Vf& x) {
 #pragma unroll
     for (int i = 0; i < W; ++i) v[i] = fmaf(s, x.v[i], v[i]);
+  }
+  __device__ __forceinline__ void add(const Vf& x) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) v[i] += x.v[i];
   }
   __device__ __forceinline__ void add_xor(int off) {
 #pragma unroll
@@ -363,12 +370,21 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
       }
     }
     const int64_t off = (int64_t)row * a.ld + lcl * W;
-    Vf<W> xr, wr;
-    xr.zero();
-    wr.zero();
-    if (need_x) xr = ld_stream_vec<W>(a.x + off);
-    if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
-    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, y, xr, wr, row_ds(a, row)));
+    if (VM == 3) {
+      if (a.acc_in) y.add(ldg_vec<W>(a.acc_in + off));
+      if (a.flags & TF_RAW_OUT) {
+        st_stream_vec<W>(a.wout + off, y);
+        y.zero();
+      }
+    }
+    if (VM != 3 || !(a.flags & TF_RAW_OUT)) {
+      Vf<W> xr, wr;
+      xr.zero();
+      wr.zero();
+      if (need_x) xr = ld_stream_vec<W>(a.x + off);
+      if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
+      st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, y, xr, wr, row_ds(a, row)));
+    }
   }
   if (lane == 0) a.tickets[c0] = 0;
 }
@@ -391,9 +407,16 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? TE
     if (e - b > a.long_thresh) valid = false;
   }
   if (__all_sync(0xffffffffu, !valid)) return;
-  const Vf<W> acc = group_row_accumulate<W, LPR, SUB, U, VM>(a, row, valid, b, e, e - b, lane);
+  Vf<W> acc = group_row_accumulate<W, LPR, SUB, U, VM>(a, row, valid, b, e, e - b, lane);
   if (valid && sub == 0) {
     const int64_t off = (int64_t)row * a.ld + cl * W;
+    if (VM == 3) {
+      if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + off));
+      if (a.flags & TF_RAW_OUT) {
+        st_stream_vec<W>(a.wout + off, acc);
+        return;
+      }
+    }
     const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
     Vf<W> xr, wr;
     xr.zero();
@@ -464,6 +487,13 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
     const int cc = q * LPR + cl;
     if (cc >= a.k) continue;
     const int64_t off = row * a.ld + cc;
+    if (VM == 3) {
+      if (a.acc_in) acc[q] += a.acc_in[off];
+      if (a.flags & TF_RAW_OUT) {
+        a.wout[off] = acc[q];
+        continue;
+      }
+    }
     float r = a.beta * acc[q];
     const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
     const float xv = need_x ? a.x[off] : 0.f;
@@ -494,6 +524,8 @@ static void launch_fast(const TermArgs& a, int vm, cudaStream_t s) {
     spmm_term_kernel<W, LPR, SUB, U, 1><<<grid, threads, 0, s>>>(a);
   else if (vm == 2)
     spmm_term_kernel<W, LPR, SUB, U, 2><<<grid, threads, 0, s>>>(a);
+  else if (vm == 3)
+    spmm_term_kernel<W, LPR, SUB, U, 3><<<grid, threads, 0, s>>>(a);
   else
     spmm_term_kernel<W, LPR, SUB, U, 0><<<grid, threads, 0, s>>>(a);
 }
@@ -506,6 +538,8 @@ static void launch_chunks(const TermArgs& a, int vm, cudaStream_t s) {
     spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 1><<<grid, 256, 0, s>>>(a);
   else if (vm == 2)
     spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 2><<<grid, 256, 0, s>>>(a);
+  else if (vm == 3)
+    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 3><<<grid, 256, 0, s>>>(a);
   else
     spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 0><<<grid, 256, 0, s>>>(a);
 }
@@ -547,11 +581,13 @@ static void launch_rows_w(int lpr, int sub, const TermArgs& a, int vm, cudaStrea
 }
 
 template <int LPR, int CPL>
-static void launch_generic(const TermArgs& a, int vm, cudaStream_t s) {  // vm 0 / 1
+static void launch_generic(const TermArgs& a, int vm, cudaStream_t s) {  // vm 0 / 1 / 3
   const int threads = 256;
   const unsigned grid = grid_for(a.n, threads / 32);
   if (vm == 1)
     spmm_term_generic<LPR, CPL, 1><<<grid, threads, 0, s>>>(a);
+  else if (vm == 3)
+    spmm_term_generic<LPR, CPL, 3><<<grid, threads, 0, s>>>(a);
   else
     spmm_term_generic<LPR, CPL, 0><<<grid, threads, 0, s>>>(a);
 }
@@ -813,6 +849,7 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
       a.row_end = n;
       a.hot_rows = hot_rows;
       a.rscale = row_scale;
+      a.acc_in = nullptr;
       Segment fixed[8];
       int ns = nseg;
       for (int i = 0; i < ns; ++i) fixed[i] = segs[i];
@@ -836,4 +873,95 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
                               w0_scale, lam_f, s_final, s, term);
   if (hot_rows > 0 && hot_rows < n) l2_window(s, nullptr, 0);
   return rc;
+}
+
+// One term of a row shard whose CSR is split into own-column entries and
+// halo-column entries: pass 0 (raw_out) runs while the halo rows
+// are in flight and writes the raw own-column sum; pass 1 adds it to the
+// halo-column sum and applies the term epilogue.  Single term, stored values.
+extern "C" int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr,
+                                   const int32_t* indices, const float* values,
+                                   int32_t long_threshold, int32_t chunk_len,
+                                   const int32_t* chunk_desc, int64_t n_chunks, float* partials,
+                                   int32_t* tickets, const int64_t* segments, int32_t n_segments,
+                                   const float* x, const float* w, const float* partial_in,
+                                   int32_t raw_out, float* out, double alpha, double beta,
+                                   double gamma, double w0_scale, double lam_f, double s_final,
+                                   sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && k >= 1, "bad shape n=%lld k=%d", (long long)n, k);
+  SPED_CHECK_ARG(n == 0 || (indptr && values && w && out), "null array");
+  SPED_CHECK_ARG(raw_out || x, "the epilogue pass needs x");
+  SPED_CHECK_ARG(!raw_out || partial_in == nullptr, "the raw pass takes no partial input");
+  SPED_CHECK_ARG(out != w && out != x, "out must not alias w or x");  // may alias partial_in
+  SPED_CHECK_ARG(n_chunks == 0 || (chunk_desc && partials && tickets && chunk_len > 0 &&
+                                   long_threshold > 0),
+                 "null or inconsistent long-row plan");
+  SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX, "problem too large");
+  SPED_CHECK_ARG(n_segments >= 0 && n_segments <= 8 && (n_segments == 0 || segments),
+                 "bad segment table");
+  if (n == 0) return SPED_OK;
+  cudaStream_t s = as_stream(stream);
+  Segment fixed[8];
+  int ns = n_segments;
+  for (int i = 0; i < ns; ++i) {
+    fixed[i].begin = segments[3 * i];
+    fixed[i].end = segments[3 * i + 1];
+    fixed[i].sub = (int)segments[3 * i + 2];
+    SPED_CHECK_ARG(fixed[i].begin >= 0 && fixed[i].end <= n && fixed[i].begin <= fixed[i].end,
+                   "segment %d out of range", i);
+  }
+  if (ns == 0) {
+    fixed[0].begin = 0;
+    fixed[0].end = n;
+    fixed[0].sub = 32;
+    ns = 1;
+  }
+  int flags = TF_FINAL;
+  if (raw_out) {
+    flags |= TF_RAW_OUT;
+  } else {
+    if (alpha != 0.0) flags |= TF_ALPHA;
+    if (gamma != 0.0) flags |= TF_GAMMA;
+    if (lam_f != 0.0) flags |= TF_LAMF;
+  }
+  const int32_t slabs = (k + 127) / 128;
+  for (int32_t sl = 0; sl < slabs; ++sl) {
+    const int32_t c0 = sl * 128;
+    TermArgs a;
+    a.n = n;
+    a.k = min(128, k - c0);
+    a.ld = k;
+    a.indptr = indptr;
+    a.indices = indices;
+    a.values = values;
+    a.x = x ? x + c0 : nullptr;
+    a.win = w + c0;
+    a.wout = out + c0;
+    a.alpha = (float)alpha;
+    a.beta = (float)(beta * w0_scale);
+    a.gamma = (float)(gamma * w0_scale);
+    a.lamf = (float)lam_f;
+    a.sfin = (float)s_final;
+    a.flags = flags;
+    a.long_thresh = n_chunks > 0 ? long_threshold : INT32_MAX;
+    a.chunk_desc = chunk_desc;
+    a.n_chunks = (int32_t)n_chunks;
+    a.chunk_blocks = 0;
+    a.chunk_len = chunk_len > 0 ? chunk_len : 1;
+    a.partials = partials;
+    a.tickets = tickets;
+    a.row_begin = 0;
+    a.row_end = n;
+    a.hot_rows = 0;
+    a.rscale = nullptr;
+    a.acc_in = partial_in ? partial_in + c0 : nullptr;
+    const uintptr_t pbits = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) |
+                            reinterpret_cast<uintptr_t>(out) |
+                            reinterpret_cast<uintptr_t>(partial_in);
+    const bool aligned = (k % 4 == 0) && (pbits % 16 == 0);
+    const bool aligned32 = (k % 8 == 0) && (pbits % 32 == 0);
+    int rc = launch_term_slab(a, 3, aligned, aligned32, fixed, ns, s);
+    if (rc != SPED_OK) return rc;
+  }
+  return SPED_OK;
 }

@@ -10,7 +10,14 @@ where the halo is the sorted set of off-shard columns its rows reference,
 grouped by owner rank.  Per polynomial term the owners send exactly those
 rows (grouped NCCL send/recv over NVLink, ``batch_isend_irecv``) straight
 into the halo region of E, then the fused SpMM term kernel runs on the local
-rows reading E (C1).  Per solver step the 3 k x k Gram blocks are summed with
+rows reading E (C1).  With halos, the shard's CSR is split into own-column
+and halo-column entries: the own-column pass runs while the halo rows are in
+flight (NCCL's stream only waits for the pack kernel), the halo-column pass
+adds its partial sums and applies the term epilogue
+(``sped_csr_term_split``).  The exchange is deduplicated on purpose: direct
+NVLink peer loads inside the term kernel would move every remote nonzero's
+row (config 4 at 8 GPUs: ~2.2 GB per GPU per term) instead of each distinct
+halo row once (~0.56 GB).  Per solver step the 3 k x k Gram blocks are summed with
 one all-reduce (C2; Oja's CholQR2 needs a second one) and every rank applies
 the same k x k coefficients to its rows.  No other data crosses ranks.
 
@@ -180,6 +187,18 @@ class HaloExchanger:
 
     def exchange(self, E: torch.Tensor):
         """E[:n_own] holds this rank's rows; fill E[n_own:] from the owners."""
+        self.finish(self.start(E))
+
+    @staticmethod
+    def finish(works):
+        """Wait for a started exchange (stream-ordered for NCCL)."""
+        for r in works:
+            r.wait()
+
+    def start(self, E: torch.Tensor) -> list:
+        """Pack this rank's send rows and post the grouped send/recv; returns
+        the works to ``finish``.  E's own rows may be read meanwhile, its halo
+        rows only after ``finish``."""
         p = self.plan
         self.gather(E)
         ops = []
@@ -192,9 +211,87 @@ class HaloExchanger:
             r0, r1 = self.recv_off[q], self.recv_off[q + 1]
             if r1 > r0:
                 ops.append(dist.P2POp(dist.irecv, E[p.n_own + r0:p.n_own + r1], q, group=self.group))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+
+class SplitCSR:
+    """One half of a shard's CSR (own-column or halo-column entries): device
+    arrays, long-row plan and segment table for ``sped_csr_term_split``."""
+
+    def __init__(self, indptr: np.ndarray, indices: np.ndarray, values: np.ndarray, device,
+                 long_threshold: int, chunk_len: int):
+        self.n = int(indptr.size - 1)
+        self.nnz = int(indptr[-1])
+        self.rowlen = np.diff(indptr)
+        self.indptr = torch.from_numpy(indptr.astype(np.int32)).to(device)
+        self.indices = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int32)).to(device)
+        self.values = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(device)
+        self.long_threshold, self.chunk_len = long_threshold, chunk_len
+        self.n_chunks, self.chunk_desc, self.tickets = _plan_chunks(
+            self.n, self.nnz, self.indptr, long_threshold, chunk_len, device)
+        self._segments = {}
+
+    def segments(self, k):
+        from .graph import segment_table
+        key = min(k, 128)
+        if key not in self._segments:
+            self._segments[key] = segment_table(self.rowlen, key, False,
+                                                self.long_threshold if self.n_chunks else None)
+        return self._segments[key]
+
+    def term(self, E, x_own, partial_in, raw_out, out, alpha, beta, gamma, w0, lam_f, s_final, k):
+        lib = _lib.load()
+        nseg, seg = self.segments(k)
+        partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=E.device)
+                    if self.n_chunks else None)
+        rc = lib.sped_csr_term_split(
+            self.n, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
+            self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
+            _lib.ptr(partials), _lib.ptr(self.tickets if self.n_chunks else None), seg, nseg,
+            _lib.ptr(x_own), _lib.ptr(E), _lib.ptr(partial_in), int(raw_out), _lib.ptr(out),
+            float(alpha), float(beta), float(gamma), float(w0), float(lam_f), float(s_final),
+            _lib.stream_ptr(E.device))
+        _lib.check(rc, "sped_csr_term_split")
+
+
+def _plan_chunks(n, nnz, indptr_dev, long_threshold, chunk_len, device):
+    """Long-row chunk plan (sped_spmm_plan) of a CSR: (n_chunks, desc, tickets)."""
+    import ctypes as C
+    lib = _lib.load()
+    maxc = int(lib.sped_spmm_plan_max_chunks(n, nnz, long_threshold, chunk_len))
+    desc = torch.empty(max(4 * maxc, 4), dtype=torch.int32, device=device)
+    nch, nlong = C.c_int64(0), C.c_int64(0)
+    rc = lib.sped_spmm_plan(n, _lib.ptr(indptr_dev), long_threshold, chunk_len, _lib.ptr(desc),
+                            maxc, C.byref(nch), C.byref(nlong), _lib.stream_ptr(device))
+    _lib.check(rc, "sped_spmm_plan")
+    n_chunks = int(nch.value)
+    chunk_desc = desc[: max(4 * n_chunks, 4)].clone() if n_chunks else None
+    tickets = torch.zeros(max(n_chunks, 1), dtype=torch.int32, device=device)
+    return n_chunks, chunk_desc, tickets
+
+
+def split_local_csr(indptr: np.ndarray, local_indices: np.ndarray, values, n_own: int):
+    """Split a shard's CSR (columns in E numbering) into own-column entries
+    (col < n_own, diagonal included) and halo-column entries, keeping each
+    row's entry order.  ``values`` None = implicit unit-weight combinatorial
+    Laplacian (materialised: -1 off the diagonal, row length - 1 on it, the
+    values the implicit kernel synthesises).  Returns two (indptr, indices,
+    values) triples."""
+    rowlen = np.diff(indptr)
+    rows = np.repeat(np.arange(n_own, dtype=np.int64), rowlen)
+    cols = np.asarray(local_indices, dtype=np.int64)
+    if values is None:
+        vals = np.full(cols.size, -1.0, dtype=np.float32)
+        diag = cols == rows
+        vals[diag] = (rowlen[rows[diag]] - 1).astype(np.float32)
+    else:
+        vals = np.asarray(values, dtype=np.float32)
+    out = []
+    for mask in (cols < n_own, cols >= n_own):
+        ip = np.zeros(n_own + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows[mask], minlength=n_own), out=ip[1:])
+        out.append((ip, cols[mask], vals[mask]))
+    return out
 
 
 class ShardedLaplacian:
@@ -232,22 +329,38 @@ class ShardedLaplacian:
         self._epos = None
         self._erow = None
         self._bws = None
+        self._split = None
         self._plan_chunks()
 
     def _plan_chunks(self):
-        import ctypes as C
-        lib = _lib.load()
-        n = self.n_own
-        maxc = int(lib.sped_spmm_plan_max_chunks(n, self.nnz_local, self.long_threshold, self.chunk_len))
-        desc = torch.empty(max(4 * maxc, 4), dtype=torch.int32, device=self.device)
-        nch, nlong = C.c_int64(0), C.c_int64(0)
-        rc = lib.sped_spmm_plan(n, _lib.ptr(self.indptr), self.long_threshold, self.chunk_len,
-                                _lib.ptr(desc), maxc, C.byref(nch), C.byref(nlong),
-                                _lib.stream_ptr(self.device))
-        _lib.check(rc, "sped_spmm_plan")
-        self.n_chunks = int(nch.value)
-        self.chunk_desc = desc[: max(4 * self.n_chunks, 4)].clone() if self.n_chunks else None
-        self.tickets = torch.zeros(max(self.n_chunks, 1), dtype=torch.int32, device=self.device)
+        self.n_chunks, self.chunk_desc, self.tickets = _plan_chunks(
+            self.n_own, self.nnz_local, self.indptr, self.long_threshold, self.chunk_len,
+            self.device)
+
+    # -- split CSR: own-column pass overlapping the halo exchange --------------
+    @property
+    def split_terms(self) -> bool:
+        """Terms run as own-column pass + halo-column pass (halos exist)."""
+        return self.plan.n_halo > 0
+
+    @property
+    def split(self):
+        if self._split is None:
+            ip = (self.rowlen.cumsum() if self.n_own else np.zeros(0, np.int64))
+            indptr = np.concatenate([[0], ip]).astype(np.int64)
+            vals = None if self.values is None else self.values.cpu().numpy()
+            parts = split_local_csr(indptr, self.plan.local_indices, vals, self.n_own)
+            self._split = [SplitCSR(ipp, idx, v, self.device, self.long_threshold,
+                                    self.chunk_len) for ipp, idx, v in parts]
+        return self._split
+
+    def partial_term(self, E, P, k):
+        """Pass 0: P = L_own E[:n_own] (own-column entries, no epilogue)."""
+        self.split[0].term(E, None, None, True, P, 0.0, 1.0, 0.0, 1.0, 0.0, 1.0, k)
+
+    def remote_term(self, E, x_own, out, P, alpha, beta, gamma, w0, lam_f, s_final, k):
+        """Pass 1: the term epilogue on L_halo E + P (= L E for the own rows)."""
+        self.split[1].term(E, x_own, P, False, out, alpha, beta, gamma, w0, lam_f, s_final, k)
 
     def segments(self, k):
         from .graph import segment_table
@@ -322,8 +435,11 @@ class ShardedOperator:
         self.lambda_star = lambda_star
         self.schedule = term_schedule(transform, lambda_star)
         self.term_fn = term_fn or shard.local_term
+        # own-column pass overlapping the exchange (product term kernels only)
+        self.overlap = term_fn is None and bool(getattr(shard, "split_terms", False))
         self._ex = {}
         self._bufs = {}
+        self._pbuf = {}
 
     def _buffers(self, k):
         if k not in self._bufs:
@@ -347,12 +463,24 @@ class ShardedOperator:
             return out
         Ea[: sh.n_own].copy_(x_own)
         cur, nxt = Ea, Eb
+        P = None
+        if self.overlap:
+            if k not in self._pbuf:
+                self._pbuf[k] = torch.empty((sh.n_own, k), dtype=torch.float32, device=sh.device)
+            P = self._pbuf[k]
         for t in range(len(al)):
-            ex.exchange(cur)
             final = t == len(al) - 1
             dst = out if final else nxt[: sh.n_own]
-            self._term(t, cur, x_own, dst, al[t], be[t], ga[t], w0 if t == 0 else 1.0,
-                       lf if final else 0.0, s if final else 1.0, k)
+            coeffs = (al[t], be[t], ga[t], w0 if t == 0 else 1.0, lf if final else 0.0,
+                      s if final else 1.0)
+            if P is not None:
+                works = ex.start(cur)
+                sh.partial_term(cur, P, k)       # overlaps the halo transfer
+                ex.finish(works)
+                sh.remote_term(cur, x_own, dst, P, *coeffs, k)
+            else:
+                ex.exchange(cur)
+                self._term(t, cur, x_own, dst, *coeffs, k)
             cur, nxt = nxt, cur
         return out
 
@@ -375,6 +503,7 @@ class ShardedStochasticOperator(ShardedOperator):
         self.index_source = index_source
         self.batch_fn = term_fn or shard.local_batch_term
         self._batch = None
+        self.overlap = False  # edge-minibatch terms: one pass after the exchange
 
     def draw(self, count: int) -> torch.Tensor:
         from .sampling import host_draw, pcg64_draw

@@ -50,8 +50,40 @@ class CpuShard:
         wnew = al * x + be * w0 * Lw + ga * w0 * Ew[: self.n_own]
         out.copy_(torch.from_numpy(lf * x + s * wnew))
 
+    local_term = term
 
-def _worker(rank, world, port, n, u, v, w, mode, kind, ell, k, result_q):
+    # split-term protocol of ShardedLaplacian (overlapped exchange): the
+    # product's split_local_csr, scipy passes standing in for the kernels
+    @property
+    def split_terms(self):
+        return self.plan.n_halo > 0
+
+    def _split(self):
+        import scipy.sparse as sps
+        from paper_2207_14589_b200.distributed import split_local_csr
+        if not hasattr(self, "_parts"):
+            ncols = self.n_own + self.plan.n_halo
+            self._parts = [sps.csr_matrix((v, c, ip), shape=(self.n_own, ncols))
+                           for ip, c, v in split_local_csr(self.local.indptr.astype(np.int64),
+                                                           self.local.indices, self.local.data,
+                                                           self.n_own)]
+        return self._parts
+
+    def partial_term(self, E, P, k):
+        own = E[: self.n_own].double().numpy()  # the halo rows are still in flight
+        A = self._split()[0]
+        P.copy_(torch.from_numpy(A[:, : self.n_own] @ own))
+        self.partial_calls = getattr(self, "partial_calls", 0) + 1
+
+    def remote_term(self, E, x_own, out, P, al, be, ga, w0, lf, s, k):
+        Ew = E.double().numpy()
+        x = x_own.double().numpy()
+        Lw = self._split()[1] @ Ew + P.double().numpy()
+        wnew = al * x + be * w0 * Lw + ga * w0 * Ew[: self.n_own]
+        out.copy_(torch.from_numpy(lf * x + s * wnew))
+
+
+def _worker(rank, world, port, n, u, v, w, mode, kind, ell, k, result_q, split=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -62,7 +94,8 @@ def _worker(rank, world, port, n, u, v, w, mode, kind, ell, k, result_q):
         shard = CpuShard(csr, rank, world)
         lam = O.choose_lambda_star(kind, O.lambda_upper(n, u, v, w, mode))
         t = sp.SpectralTransform(kind, ell)
-        op = ShardedOperator(shard, t, lam, term_fn=shard.term)
+        op = ShardedOperator(shard, t, lam, term_fn=None if split else shard.term)
+        assert op.overlap == split
         X = np.random.default_rng(0).standard_normal((n, k)).astype(np.float32)
         b, e = shard.row0, shard.row0 + shard.n_own
         y_own = op.apply_local(torch.from_numpy(X[b:e].copy()))
@@ -70,6 +103,8 @@ def _worker(rank, world, port, n, u, v, w, mode, kind, ell, k, result_q):
         G = torch.from_numpy(X[b:e].astype(np.float64).T @ X[b:e].astype(np.float64))
         dist.all_reduce(G)
         parts = [None] * world
+        if split:
+            assert shard.partial_calls == len(op.schedule[0])
         dist.all_gather_object(parts, (b, y_own.numpy(), G.numpy(), shard.plan.n_halo))
         if rank == 0:
             result_q.put(parts)
@@ -77,20 +112,25 @@ def _worker(rank, world, port, n, u, v, w, mode, kind, ell, k, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,graph,mode,kind,ell", [
-    (2, "cfg4s", "normalized", "negexp-taylor", 6),
-    (3, "cfg4s", "normalized", "negexp-taylor", 6),
-    (2, "cfg5s", "unnormalized", "negexp-limit", 5),
-    (3, "cfg3s", "unnormalized", "identity", None),
+@pytest.mark.parametrize("world,graph,mode,kind,ell,split", [
+    (2, "cfg4s", "normalized", "negexp-taylor", 6, False),
+    (3, "cfg4s", "normalized", "negexp-taylor", 6, False),
+    (2, "cfg5s", "unnormalized", "negexp-limit", 5, False),
+    (3, "cfg3s", "unnormalized", "identity", None, False),
+    (2, "cfg4s", "normalized", "negexp-taylor", 6, True),
+    (3, "cfg5s", "unnormalized", "negexp-limit", 5, True),
 ])
-def test_sharded_apply_matches_oracle(golden, world, graph, mode, kind, ell):
+def test_sharded_apply_matches_oracle(golden, world, graph, mode, kind, ell, split):
+    """split=True: the overlapped schedule (exchange started, own-column
+    pass, exchange finished, halo-column pass) of ShardedOperator."""
     n, u, v, w = golden.graph(graph)
     u, v, w = O.canonical_edges(n, u, v, w)
     k = 4
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, u, v, w, mode, kind, ell, k, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, u, v, w, mode, kind, ell, k, q,
+                                               split))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -121,3 +161,21 @@ def test_partition_rows_balances_nnz():
         assert off[0] == 0 and off[-1] == 1000 and np.all(np.diff(off) > 0)
         loads = np.diff(indptr[off])
         assert loads.max() <= indptr[-1] / parts + 5000
+
+
+def test_split_local_csr_partitions_entries():
+    """Own-column + halo-column parts re-assemble the shard CSR; implicit
+    unit-weight values are materialised as the kernel synthesises them."""
+    from paper_2207_14589_b200.distributed import split_local_csr
+    import scipy.sparse as sps
+    indptr = np.array([0, 3, 5, 9], dtype=np.int64)
+    cols = np.array([0, 2, 4, 1, 3, 0, 2, 5, 6], dtype=np.int64)   # n_own = 3, halo cols 3..6
+    vals = np.arange(9, dtype=np.float32) + 1
+    (ip0, c0, v0), (ip1, c1, v1) = split_local_csr(indptr, cols, vals, 3)
+    A = sps.csr_matrix((vals, cols, indptr), shape=(3, 7)).toarray()
+    B = (sps.csr_matrix((v0, c0, ip0), shape=(3, 7)) + sps.csr_matrix((v1, c1, ip1), shape=(3, 7)))
+    np.testing.assert_array_equal(B.toarray(), A)
+    assert np.all(c0 < 3) and np.all(c1 >= 3)
+    (_, c0, v0), (_, c1, v1) = split_local_csr(indptr, cols, None, 3)
+    np.testing.assert_array_equal(v0, [2, -1, 1, -1, 3])  # diag = row length - 1
+    np.testing.assert_array_equal(v1, [-1, -1, -1, -1])

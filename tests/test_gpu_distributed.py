@@ -13,16 +13,20 @@ from conftest import rel_fro
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("cfg,kind,ell", [(4, "negexp-taylor", 12), (5, "negexp-limit", 9),
-                                          (3, "identity", None)])
-def test_sharded_terms_match_single_gpu(cuda, world, cfg, kind, ell):
+                                          (3, "identity", None), (1, "negexp-limit", 9)])
+def test_sharded_terms_match_single_gpu(cuda, world, cfg, kind, ell, split):
+    """split=True: the own-column pass runs BEFORE the halo rows arrive (the
+    halo region holds NaN then), the halo-column pass after, as in the
+    overlapped NCCL path (sped_csr_term_split)."""
     import paper_2207_14589_b200 as sp
     from paper_2207_14589_b200 import generators as G
     from paper_2207_14589_b200.distributed import (ShardedLaplacian, build_halo_plans_local,
                                                    partition_rows)
     spec = G.CONFIGS[cfg]
-    n, u, v, w = G.config_graph(cfg, device="cuda", scale=0.02)
+    n, u, v, w = G.config_graph(cfg, device="cuda", scale=0.02 if cfg > 2 else 1.0)
     g = sp.Graph.from_canonical(n, u, v, w)
     L = sp.LaplacianOperator(g, spec["mode"])
     t = sp.SpectralTransform(kind, ell)
@@ -44,8 +48,14 @@ def test_sharded_terms_match_single_gpu(cuda, world, cfg, kind, ell):
     outs = [torch.empty_like(xs[r]) for r in range(world)]
     for r in range(world):
         E[r][0][: shards[r].n_own].copy_(xs[r])
+    P = [torch.empty_like(xs[r]) for r in range(world)]
     cur = 0
     for tt in range(len(al)):
+        final = tt == len(al) - 1
+        if split:
+            for r in range(world):
+                E[r][cur][shards[r].n_own:].fill_(float("nan"))
+                shards[r].partial_term(E[r][cur], P[r], k)
         # halo fill: rank r receives from owner q the rows q's send list names
         for r in range(world):
             roff = np.concatenate([[0], np.cumsum(plans[r].recv_counts)])
@@ -55,14 +65,18 @@ def test_sharded_terms_match_single_gpu(cuda, world, cfg, kind, ell):
                 rows = torch.from_numpy(plans[q].send_rows[r]).cuda()
                 dst = E[r][cur][shards[r].n_own + roff[q]: shards[r].n_own + roff[q + 1]]
                 dst.copy_(E[q][cur][rows])
-        final = tt == len(al) - 1
         for r in range(world):
             sh = shards[r]
             dst = outs[r] if final else E[r][1 - cur][: sh.n_own]
-            sh.local_term(E[r][cur], xs[r], dst, al[tt], be[tt], ga[tt], w0 if tt == 0 else 1.0,
-                          lf if final else 0.0, s if final else 1.0, k)
+            coeffs = (al[tt], be[tt], ga[tt], w0 if tt == 0 else 1.0, lf if final else 0.0,
+                      s if final else 1.0)
+            if split:
+                sh.remote_term(E[r][cur], xs[r], dst, P[r], *coeffs, k)
+            else:
+                sh.local_term(E[r][cur], xs[r], dst, *coeffs, k)
         cur = 1 - cur
     got = torch.cat(outs)
+    assert torch.isfinite(got).all()
     assert rel_fro(got.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
 
 
