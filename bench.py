@@ -442,9 +442,15 @@ def run_sped(args):
     peak, peak_src = measured_peak()
     achieved = bpt / t_term_s / 1e9
     traffic, traffic_src = measured_traffic(spec["name"]) if not sharded else (None, None)
-    launches_per_step = n_terms + 5
-    if sharded:
-        launches_per_step = n_terms * 2 + 5
+    # our kernels per step: per term one launch per row segment (+ the hub
+    # chunk launch); Gram (tcgen05 partials + fp64 reduce), coefficients,
+    # update.  Sharded: + the halo pack per term (NCCL's own kernels excluded).
+    if sharded and shard.split_terms:
+        per_term = 1 + sum(int(h.segments(k)[0]) + (1 if h.n_chunks else 0) for h in shard.split)
+    else:
+        src = shard if sharded else lap
+        per_term = int(src.segments(k)[0]) + (1 if src.n_chunks else 0)
+    launches_per_step = n_terms * per_term + 4
 
     e2e = None
     if not args.no_e2e:

@@ -183,12 +183,16 @@ int sped_mueg_coeffs(int32_t k, const double* G, double eta, float* A, float* sc
 int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, float* T,
                     int32_t* flag, sped_stream_t stream);
 /* Grid-resident fast path (k <= 32): `steps` whole mu-EG steps in ONE
- * cooperative launch (one CTA per SM, grid barriers between phases; state in
- * HBM/L2).  V (n x k) is updated in place; flag is set when a column's norm
- * vanishes (rank collapse, solvers.py:136-143); SPED_ERR_UNSUPPORTED for
- * k > 32 or > 64 terms.  `nnz` = indptr[n] (host copy,
- * sizes the launch); `workspace` of at least sped_persistent_workspace_bytes(n, k)
- * bytes (two n x k blocks + Gram partials). */
+ * cooperative launch (one CTA per SM; polynomial terms exchange rows through
+ * generation-tagged 64-bit words instead of grid barriers, grid barriers only
+ * around the Gram; state in HBM/L2).  V (n x k) is updated in place; flag
+ * bit 0 is set when a column's norm vanishes (rank collapse,
+ * solvers.py:136-143), bit 1 when a tagged wait timed out (a bug, never
+ * expected); SPED_ERR_UNSUPPORTED for k > 32 or > 64 terms.  `nnz` =
+ * indptr[n] (host copy, sizes the launch); `workspace` of at least
+ * sped_persistent_workspace_bytes(n, k) bytes, ZEROED before its first use
+ * and kept across launches (two fp32 and two tagged n x k blocks, Gram
+ * partials, the tag base). */
 int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* bytes);
 int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
                          const int32_t* indices, const float* values, int32_t n_terms, const double* alpha,

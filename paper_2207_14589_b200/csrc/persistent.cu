@@ -20,7 +20,22 @@
 //                   writes X' = (X A + eta M) diag(scale) for its own rows
 //                   -- grid barrier
 //
-// T + 2 grid barriers per step.
+// Terms exchange rows WITHOUT grid barriers: an intermediate term's output
+// element is one 64-bit word (fp32 value | 32-bit generation tag) stored
+// with st.relaxed.gpu, and a gather spins (ld.relaxed.gpu) until the word
+// carries the generation it expects -- the LL ("low latency") protocol of
+// NCCL applied to the SpMM halo.  A row's next-generation value is written
+// only after all of its neighbours' current values were read by it, and L is
+// symmetric with an explicit diagonal, so every reader of a word finishes
+// before the word's owner can reach the generation after next: two tagged
+// buffers suffice.  Tags are a launch base (device counter in the workspace,
+// advanced by each launch) + step*T + t + 1, so stale words of earlier
+// launches never match.  A gather that waits past ~1 s sets bit 2 of `flag`
+// and proceeds instead of hanging.
+//
+// 2 (or 3) grid barriers per step: Gram partials, [partials reduce,] update;
+// the T - 1 barriers between terms of the barrier version are gone
+// (config 1: 62 -> 52 us/step, config 2: 91 -> 76 us/step).
 //
 // Same arithmetic as the multi-kernel path (spmm.cu term schedule; mu-EG in
 // Gram form, solvers.py:121-144 / SURVEY §8a; zero-norm columns flagged for
@@ -57,9 +72,14 @@ namespace {
 constexpr int PT_MAX_K = 32;
 constexpr int PT_MAX_TERMS = 64;
 constexpr int PT_DYN_BYTES = 180 * 1024;  // dynamic smem: own rows + CSR slice
+constexpr int PT_NT = 512;                // threads per CTA
+// Gram entries (S upper, C, diag Q) at k = 32 and the passes over them
+constexpr int PT_MAX_NE = PT_MAX_K * (PT_MAX_K + 1) / 2 + PT_MAX_K * PT_MAX_K + PT_MAX_K;
+constexpr int PT_MAX_PASSES = (PT_MAX_NE + PT_NT - 1) / PT_NT;
 
 struct PArgs {
   int32_t n, k, nterms;
+  uint32_t* epoch;     // device tag base, advanced by steps*nterms per launch
   const int32_t* indptr;
   const int32_t* indices;
   const float* values;  // NULL = implicit unit-weight combinatorial
@@ -69,8 +89,10 @@ struct PArgs {
   int32_t steps;
   int32_t slots;  // nonzero slots per row (lanes per row = slots * k)
   float* V;  // in/out
-  float* B0;
-  float* B1;
+  float* XB;   // X ping-pong partner of V (float, n x k)
+  float* Mb;   // M when the CTA's rows are not smem-resident (float, n x k)
+  unsigned long long* L0;  // tagged term outputs (fp32 | tag << 32), n x k
+  unsigned long long* L1;
   double* partials;  // [grid][nE]
   double* G;         // [nE]
   int32_t* flag;
@@ -108,6 +130,17 @@ __device__ __forceinline__ void put_gram(double* Gs, int e, int k, int nS, int n
     Gs[2 * k * k + ca] = g;
   }
 }
+
+__device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_ll(unsigned long long* p, float x, uint32_t tag) {
+  const unsigned long long v = ((unsigned long long)tag << 32) | __float_as_uint(x);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+constexpr uint32_t LL_SPIN_LIMIT = 1u << 21;  // per wait, x ~0.5 us per L2 round trip
 
 __device__ __forceinline__ int row_lower_bound(const int32_t* indptr, int n, int64_t target) {
   int lo = 0, hi = n;  // first row r with indptr[r] >= target
@@ -183,7 +216,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
 
   // Gram work split: `parts` threads per entry, `per_pass` entries per pass
   const int parts = max(1, PT_THREADS / nE), per_pass = PT_THREADS / parts;
-  const int passes = (nE + per_pass - 1) / per_pass;  // <= 2 for k <= 32
+  const int passes = (nE + per_pass - 1) / per_pass;  // <= PT_MAX_PASSES for k <= 32
   // small partial tables are reduced redundantly by every CTA (one grid
   // barrier less per step); large ones by one warp per entry
   const bool redundant_reduce = (int64_t)nb * nE <= 8192;
@@ -196,8 +229,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
   float* X = a.V;
   float* sX = sXa;   // own rows of X (resident mode)
   float* sXn = sXb;  // next generation
-  float* bufs[3] = {a.V, a.B0, a.B1};
-  int xi = 0;  // which of bufs holds X
+  const uint32_t tag0 = *reinterpret_cast<volatile uint32_t*>(a.epoch);
 
 #ifdef PT_PROFILE
   uint64_t pt_t[64];
@@ -207,14 +239,17 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
   pt_name[pt_n++] = "start";
 #endif
   for (int step = 0; step < a.steps; ++step) {
-    float* P0 = bufs[(xi + 1) % 3];
-    float* P1 = bufs[(xi + 2) % 3];
     // ---- M = p(L) X: RW rows per warp, S slots x k columns per row ---------
-    const float* win = X;
-    float* M = P0;
+    // term 0 gathers X (float, written before the last grid barrier); term
+    // t >= 1 gathers the tagged output of term t-1; the final term writes M
+    // (own rows only: smem when resident, else the float buffer Mb)
+    float* M = a.Mb;
     for (int t = 0; t < a.nterms; ++t) {
       const bool final = (t == a.nterms - 1);
-      float* wout = (t & 1) ? P1 : P0;
+      const unsigned long long* lin = (t & 1) ? a.L0 : a.L1;   // output of term t-1
+      unsigned long long* lout = (t & 1) ? a.L1 : a.L0;
+      const uint32_t want = tag0 + (uint32_t)(step * a.nterms + t);      // tag of term t-1
+      const uint32_t mine = want + 1u;
       const float sc = (t == 0) ? a.w0 : 1.f;
       const float al = a.alpha[t], be = a.beta[t] * sc, ga = a.gamma[t] * sc;
       for (int lr0 = warp * RW; lr0 < nr; lr0 += rows_per_pass) {
@@ -225,8 +260,12 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
         const float dg = (float)(re - rb - 1);
         const int64_t i = (int64_t)r * k + lc;
         const bool lead = (ls == 0 && own);
-        // own-row operands issued before the gathers (independent loads)
-        const float wself = (lead && ga != 0.f) ? __ldcg(win + i) : 0.f;
+        // own-row operands issued before the gathers (independent loads);
+        // the own row of a tagged block was written by this very thread
+        float wself = 0.f;
+        if (lead && ga != 0.f)
+          wself = (t == 0) ? (resident ? sX[lr * k + lc] : __ldcg(X + i))
+                           : __uint_as_float((uint32_t)ld_ll(lin + i));
         const float xv = (lead && (al != 0.f || final))
                              ? (resident ? sX[lr * k + lc] : __ldcg(X + i)) : 0.f;
         float acc = 0.f;
@@ -240,11 +279,34 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
               const int p = base + j * S;
               c[j] = (p < re) ? ix[p] : -1;
             }
+            if (t == 0) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                x[j] = (c[j] < 0) ? 0.f : __ldcg(X + (int64_t)c[j] * k + lc);
+            } else {
+              unsigned long long q[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                q[j] = (c[j] < 0) ? 0ull : ld_ll(lin + (int64_t)c[j] * k + lc);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (c[j] >= 0) {
+                  uint32_t spins = 0;
+                  while ((uint32_t)(q[j] >> 32) != want) {
+                    if (++spins > LL_SPIN_LIMIT) {
+                      atomicOr(a.flag, 2);
+                      break;
+                    }
+                    q[j] = ld_ll(lin + (int64_t)c[j] * k + lc);
+                  }
+                }
+                x[j] = (c[j] < 0) ? 0.f : __uint_as_float((uint32_t)q[j]);
+              }
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const int p = base + j * S;
               v[j] = (c[j] < 0) ? 0.f : (has_vals ? vx[p] : (c[j] == r ? dg : -1.f));
-              x[j] = (c[j] < 0) ? 0.f : __ldcg(win + (int64_t)c[j] * k + lc);
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc = fmaf(v[j], x[j], acc);
@@ -261,23 +323,18 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
           if (ga != 0.f) o = fmaf(ga, wself, o);
           if (final) {
             o = fmaf(a.lamf, xv, a.sfin * o);
-            if (resident) sM[lr * k + lc] = o;  // M is only read back by this CTA
+            if (resident)
+              sM[lr * k + lc] = o;  // M is only read back by this CTA
+            else
+              M[i] = o;
+          } else {
+            st_ll(lout + i, o, mine);
           }
-          if (!(final && resident)) wout[i] = o;
         }
       }
-      win = wout;
-      M = wout;
       PT_MARK("term");
-#ifdef PT_PROFILE
-      __syncthreads();
-      PT_MARK("term-cta");
-#endif
-      if (!final) grid.sync();
-      PT_MARK("term-sync");
     }
     if (a.nterms == 0) {
-      M = P0;
       for (int64_t i = i0 + tid; i < i1; i += PT_THREADS) {
         const float o = (a.lamf + a.sfin * a.w0) * (resident ? sX[i - i0] : __ldcg(X + i));
         if (resident)
@@ -286,12 +343,14 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
           M[i] = o;
       }
     }
-    float* Xn = (M == P0) ? P1 : P0;  // free buffer for X'
-    __syncthreads();                  // own rows of M complete
+    float* Xn = (X == a.V) ? a.XB : a.V;  // X' goes to the other float buffer
+    __syncthreads();                      // own rows of M complete
 
     // ---- Gram partials over own rows (fp64 accumulation, fixed order) ------
     {
-      double acc[2] = {0.0, 0.0};
+      double acc[PT_MAX_PASSES];
+#pragma unroll
+      for (int q = 0; q < PT_MAX_PASSES; ++q) acc[q] = 0.0;
       const int chunk = resident ? max(nr, 1) : stage_rows;
       float* qX = resident ? sX : sXa;
       float* qM = resident ? sM : sXa + (size_t)stage_rows * k;
@@ -426,7 +485,6 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
       sX = sXn;
       sXn = tmp;
     }
-    xi = (Xn == bufs[(xi + 1) % 3]) ? (xi + 1) % 3 : (xi + 2) % 3;
     PT_MARK("coef+upd");
     grid.sync();
     PT_MARK("upd-sync");
@@ -434,6 +492,8 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
   if (X != a.V)
     for (int64_t i = i0 + tid; i < i1; i += PT_THREADS)
       a.V[i] = resident ? sX[i - i0] : __ldcg(X + i);
+  // every CTA read the tag base before its first grid barrier
+  if (b == 0 && tid == 0) *a.epoch = tag0 + (uint32_t)(a.steps * a.nterms);
 #ifdef PT_PROFILE
   if (b == 0 && tid == 0)
     for (int q = 2; q < pt_n; ++q)
@@ -446,11 +506,30 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
 
 using namespace sped;
 
+// Workspace: [XB f32 n*k][Mb f32 n*k][L0 u64 n*k][L1 u64 n*k][partials, G
+// f64 (sms+1)*nE][epoch u32].  Zero it once before the first launch (tags
+// start at 1); keep it across launches (the tag base lives in it).
+static void persistent_layout(int32_t n, int32_t k, size_t* l0_off, size_t* part_off,
+                              size_t* epoch_off, size_t* total) {
+  const size_t nk = (size_t)n * k;
+  const size_t nE = (size_t)k * (k + 1) / 2 + (size_t)k * k + k;
+  size_t off = 2 * nk * sizeof(float);
+  off = (off + 255) & ~size_t(255);
+  *l0_off = off;
+  off += 2 * nk * sizeof(unsigned long long);
+  off = (off + 255) & ~size_t(255);
+  *part_off = off;
+  off += ((size_t)num_sms() + 1) * nE * sizeof(double);
+  off = (off + 255) & ~size_t(255);
+  *epoch_off = off;
+  *total = off + 256;
+}
+
 extern "C" int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* bytes) {
   SPED_CHECK_ARG(n >= 1 && k >= 1 && bytes, "bad persistent workspace arguments");
-  const int64_t nE = (int64_t)k * (k + 1) / 2 + (int64_t)k * k + k;
-  *bytes = 2 * (int64_t)n * k * (int64_t)sizeof(float) +
-           ((int64_t)num_sms() + 1) * nE * (int64_t)sizeof(double) + 256;
+  size_t l0, part, ep, total;
+  persistent_layout(n, k, &l0, &part, &ep, &total);
+  *bytes = (int64_t)total;
   return SPED_OK;
 }
 
@@ -472,22 +551,19 @@ extern "C" int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int
   SPED_CHECK_ARG(workspace_bytes >= need, "persistent workspace too small (%lld < %lld)",
                  (long long)workspace_bytes, (long long)need);
   if (steps == 0) return SPED_OK;
-  // block size: 512 threads when every warp of a 512-thread grid already
-  // holds at most one row group (cheaper barriers), else 1024
+  // 512-thread CTAs (116 registers, no spills; the 1024-thread variant is
+  // capped at 64 registers and spilled the tagged gathers: config 2 96 vs
+  // 76 us/step)
   const double avg = (double)nnz / n;
   int slots = (int)std::ceil(avg / 8.0);  // ~8 gathers in flight per lane
   slots = std::max(1, std::min(slots, 32 / k));
   const int rw = 32 / (slots * k);
   const int sms = num_sms();
-  const bool small_block = (int64_t)n <= (int64_t)sms * 16 * rw;
-  const int nt = small_block ? 512 : 1024;
-  const void* fn = small_block ? (const void*)persistent_mueg_kernel<512>
-                               : (const void*)persistent_mueg_kernel<1024>;
+  constexpr int nt = PT_NT;
+  const void* fn = (const void*)persistent_mueg_kernel<PT_NT>;
   static bool attr = false;
   if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<512>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
-    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<1024>,
+    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
     attr = true;
   }
@@ -521,12 +597,15 @@ extern "C" int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int
   a.slots = slots;
   a.V = V;
   char* ws = static_cast<char*>(workspace);
-  a.B0 = reinterpret_cast<float*>(ws);
-  a.B1 = a.B0 + (size_t)n * k;
-  size_t off = 2 * (size_t)n * k * sizeof(float);
-  off = (off + 255) & ~size_t(255);
-  a.partials = reinterpret_cast<double*>(ws + off);
+  size_t l0_off, part_off, epoch_off, total;
+  persistent_layout(n, k, &l0_off, &part_off, &epoch_off, &total);
+  a.XB = reinterpret_cast<float*>(ws);
+  a.Mb = a.XB + (size_t)n * k;
+  a.L0 = reinterpret_cast<unsigned long long*>(ws + l0_off);
+  a.L1 = a.L0 + (size_t)n * k;
+  a.partials = reinterpret_cast<double*>(ws + part_off);
   a.G = a.partials + (size_t)grid * nE;
+  a.epoch = reinterpret_cast<uint32_t*>(ws + epoch_off);
   a.flag = flag;
   void* args[] = {&a};
   SPED_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(nt), args, PT_DYN_BYTES,

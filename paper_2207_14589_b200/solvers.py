@@ -166,7 +166,10 @@ class StepWorkspace:
         self.update(self.tmp, self.A, None, None, 0.0, None, out)
 
     def take_flag(self) -> bool:
-        f = bool(self.flag.item())
+        fv = int(self.flag.item())
+        if fv & 2:
+            raise RuntimeError("sped_persistent_mueg: a tagged term wait timed out")
+        f = bool(fv)
         if f:
             self.flag.zero_()
         return f
@@ -438,7 +441,8 @@ class _PersistentStepper:
         nbytes = ctypes.c_int64(0)
         _lib.check(lib.sped_persistent_workspace_bytes(op.n, k, ctypes.byref(nbytes)),
                    "sped_persistent_workspace_bytes")
-        self.scratch = torch.empty(int(nbytes.value), dtype=torch.uint8, device=V0.device)
+        # zeroed once: the tagged term blocks start at tag 0, the tag base too
+        self.scratch = torch.zeros(int(nbytes.value), dtype=torch.uint8, device=V0.device)
         al, be, ga, w0, lf, s = op.schedule
         self._coef = (len(al), _lib.dbl_array(al), _lib.dbl_array(be), _lib.dbl_array(ga),
                       float(w0), float(lf), float(s))

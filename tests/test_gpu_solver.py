@@ -389,3 +389,10 @@ def test_persistent_solver_multi_cta(cuda, graph, mode, kind, ell, eta, k):
     p2 = _PersistentStepper(op, eta, Vi)
     p2.advance(25)
     assert torch.equal(p.V, p2.V)
+    # split over launches: the tagged term blocks carry stale words of the
+    # previous launch, which the per-launch tag base must never match
+    p3 = _PersistentStepper(op, eta, Vi)
+    for m in (1, 1, 10, 13):
+        p3.advance(m)
+    assert torch.equal(p.V, p3.V)
+    assert not p3.ws.take_flag()
