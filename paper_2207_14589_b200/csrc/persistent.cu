@@ -35,7 +35,7 @@
 //
 // 2 (or 3) grid barriers per step: Gram partials, [partials reduce,] update;
 // the T - 1 barriers between terms of the barrier version are gone
-// (config 1: 62 -> 52 us/step, config 2: 91 -> 76 us/step).
+// (config 1: 62 -> 50 us/step, config 2: 91 -> 72 us/step).
 //
 // Same arithmetic as the multi-kernel path (spmm.cu term schedule; mu-EG in
 // Gram form, solvers.py:121-144 / SURVEY §8a; zero-norm columns flagged for
@@ -73,6 +73,9 @@ constexpr int PT_MAX_K = 32;
 constexpr int PT_MAX_TERMS = 64;
 constexpr int PT_DYN_BYTES = 180 * 1024;  // dynamic smem: own rows + CSR slice
 constexpr int PT_NT = 512;                // threads per CTA
+#ifndef PT_REDUNDANT_MAX
+#define PT_REDUNDANT_MAX 8192  // partial-table entries every CTA reduces itself
+#endif
 // Gram entries (S upper, C, diag Q) at k = 32 and the passes over them
 constexpr int PT_MAX_NE = PT_MAX_K * (PT_MAX_K + 1) / 2 + PT_MAX_K * PT_MAX_K + PT_MAX_K;
 constexpr int PT_MAX_PASSES = (PT_MAX_NE + PT_NT - 1) / PT_NT;
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
   const int passes = (nE + per_pass - 1) / per_pass;  // <= PT_MAX_PASSES for k <= 32
   // small partial tables are reduced redundantly by every CTA (one grid
   // barrier less per step); large ones by one warp per entry
-  const bool redundant_reduce = (int64_t)nb * nE <= 8192;
+  const bool redundant_reduce = (int64_t)nb * nE <= PT_REDUNDANT_MAX;
   // term lanes: a row is S nonzero slots x k columns; a warp takes RW rows
   const int S = a.slots, LR = S * k, RW = 32 / LR;
   const int lg = lane / LR, lrem = lane - lg * LR, lc = lrem % k, ls = lrem / k;
@@ -288,20 +291,25 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 q[j] = (c[j] < 0) ? 0ull : ld_ll(lin + (int64_t)c[j] * k + lc);
+              // re-poll every stale word of the batch in the same round (one
+              // L2 round trip per round, not one per stale word)
+              for (uint32_t spins = 0;; ++spins) {
+                bool ready = true;
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                if (c[j] >= 0) {
-                  uint32_t spins = 0;
-                  while ((uint32_t)(q[j] >> 32) != want) {
-                    if (++spins > LL_SPIN_LIMIT) {
-                      atomicOr(a.flag, 2);
-                      break;
-                    }
-                    q[j] = ld_ll(lin + (int64_t)c[j] * k + lc);
-                  }
+                for (int j = 0; j < 8; ++j)
+                  ready &= (c[j] < 0) || ((uint32_t)(q[j] >> 32) == want);
+                if (ready) break;
+                if (spins > LL_SPIN_LIMIT) {
+                  atomicOr(a.flag, 2);
+                  break;
                 }
-                x[j] = (c[j] < 0) ? 0.f : __uint_as_float((uint32_t)q[j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if (c[j] >= 0 && (uint32_t)(q[j] >> 32) != want)
+                    q[j] = ld_ll(lin + (int64_t)c[j] * k + lc);
               }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) x[j] = (c[j] < 0) ? 0.f : __uint_as_float((uint32_t)q[j]);
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
