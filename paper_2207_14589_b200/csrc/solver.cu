@@ -673,6 +673,11 @@ int launch_update(int64_t n, const float* P, const float* A, const float* M, con
 }  // namespace
 }  // namespace sped
 
+namespace sped {
+int launch_update_tc128(int64_t n, const float* P, const float* A, const float* M, float eta,
+                        const float* scale, float* out, cudaStream_t s);  // update_tc.cu
+}  // namespace sped
+
 using namespace sped;
 
 extern "C" int sped_mueg_coeffs(int32_t k, const double* G, double eta, float* A, float* scale,
@@ -722,8 +727,16 @@ extern "C" int sped_block_update(int64_t n, int32_t k, const float* P, const flo
                          : launch_v2<32>(n, P, A, M, B, (float)eta, scale, out, s);
       case 64: return (v1 || (M && B)) ? launch_rows<64>(n, P, A, M, B, (float)eta, scale, out, upper, s)
                                        : launch_v2<64>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 128: return (v1 || (M && B)) ? launch_rows<128>(n, P, A, M, B, (float)eta, scale, out, upper, s)
-                                        : launch_k128(n, P, A, M, B, (float)eta, scale, out, s);
+      case 128: {
+        // tcgen05 3xTF32 GEMM (update_tc.cu); SPED_UPDATE_TC=0 keeps the SIMT kernel
+        static const bool tc = [] {
+          const char* e = getenv("SPED_UPDATE_TC");
+          return !(e && e[0] == '0');
+        }();
+        if (v1 || (M && B)) return launch_rows<128>(n, P, A, M, B, (float)eta, scale, out, upper, s);
+        if (tc) return launch_update_tc128(n, P, A, M, (float)eta, scale, out, s);
+        return launch_k128(n, P, A, M, B, (float)eta, scale, out, s);
+      }
       default: break;
     }
   }

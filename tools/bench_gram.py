@@ -56,9 +56,12 @@ def main():
         sc = torch.rand(k, device="cuda", generator=g) + 0.5
         out = torch.empty_like(V)
         upd_ms = timed(lambda: ws.update(V, A, M, None, 0.1, sc, out, upper=True), args.reps)
+        ref_u = ((V.double() @ A.double() + 0.1 * M.double()) * sc.double())
+        upd_err = ((out.double() - ref_u).norm() / ref_u.norm()).item()
+        del ref_u
         gb = 8 * n * k / 1e9
         print(json.dumps({"n": n, "k": k, "gram_ms": gram_ms, "gram_GBps": gb / gram_ms * 1e3,
-                          "gram_rel_err": err, "update_ms": upd_ms,
+                          "gram_rel_err": err, "update_ms": upd_ms, "update_rel_err": upd_err,
                           "update_GBps": 1.5 * gb / upd_ms * 1e3}), flush=True)
         del V, M, out, ws
         torch.cuda.empty_cache()
