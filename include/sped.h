@@ -227,7 +227,9 @@ int sped_walk_poly_estimate(int64_t n, int64_t m, int32_t k, const int64_t* u, c
 
 /* out = (P*A + M*B) * diag(scale).  A k x k fp32; M may be NULL; B may be
  * NULL meaning B = eta*I; scale may be NULL (ones).  upper != 0 promises A is
- * upper triangular (mu-EG), letting the kernel skip the zero half. */
+ * upper triangular (mu-EG), letting the SIMT kernels skip the zero half.
+ * k = 128 without B runs on the tensor cores (tcgen05 3xTF32, ~1e-6
+ * relative; SPED_UPDATE_TC=0 selects the SIMT kernel). */
 int sped_block_update(int64_t n, int32_t k, const float* P, const float* A,
                       const float* M, const float* B, double eta, const float* scale,
                       int32_t upper, float* out, sped_stream_t stream);

@@ -320,13 +320,16 @@ def test_block_update_vs_fp64(cuda, k):
     ws = StepWorkspace(n, k, torch.device("cuda"))
     out = torch.empty_like(P)
     Pd, Md, Ad, Bd, sd = (t.double() for t in (P, M, A, B, sc))
+    # k = 128 runs on tcgen05 in 3xTF32 (no lo*lo term, fp32 accumulation in
+    # TMEM): ~7e-7 relative on random data; the SIMT kernels are ~1e-7
+    tol = 3e-6 if k == 128 else 1e-6
     for upper, Bm, eta in ((True, None, 0.3), (False, None, 0.7), (False, B, 0.0)):
         ws.update(P, A.contiguous(), M, Bm, eta, sc, out, upper=upper)
         ref = (Pd @ Ad + (Md @ Bd if Bm is not None else eta * Md)) * sd
-        assert rel_fro(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-6, (upper, Bm is not None)
+        assert rel_fro(out.cpu().numpy(), ref.cpu().numpy()) <= tol, (upper, Bm is not None)
     # no M, no scale (the CholQR2 / orthonormalisation form)
     ws.update(P, A.contiguous(), None, None, 0.0, None, out)
-    assert rel_fro(out.cpu().numpy(), (Pd @ Ad).cpu().numpy()) <= 1e-6
+    assert rel_fro(out.cpu().numpy(), (Pd @ Ad).cpu().numpy()) <= tol
 
 
 @pytest.mark.parametrize("name,mode,kind,ell,k", [("cfg1", "unnormalized", "negexp-limit", 13, 10),
