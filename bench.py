@@ -418,7 +418,7 @@ def run_sped(args):
         if ev is not None:
             ev[1].record(stream)
         if sharded:
-            ws.gram(Vin, MV)
+            ws.gram(Vin, MV, diag_q=True)
             dist.all_reduce(ws.G)
             lib = sp._lib.load()
             lib.sped_mueg_coeffs(k, ws.G.data_ptr(), eta, ws.A.data_ptr(), ws.scale.data_ptr(),

@@ -173,6 +173,13 @@ int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* i
 size_t sped_gram_workspace_bytes(int64_t n, int32_t k);
 int sped_gram(int64_t n, int32_t k, const float* V, const float* M, double* G,
               void* workspace, size_t workspace_bytes, sped_stream_t stream);
+/* As sped_gram with M required, for mu-EG, which reads S, C and diag(Q)
+ * only: at k = 128 the Q block's MMAs are skipped (diag(Q) is summed in fp64
+ * from the converted M values; Q's off-diagonal entries come back 0).  Other
+ * k: identical to sped_gram.  Replaces the V^T MV / column-norm work of
+ * mu_eg_step, solvers.py:121-144. */
+int sped_gram_mueg(int64_t n, int32_t k, const float* V, const float* M, double* G,
+                   void* workspace, size_t workspace_bytes, sped_stream_t stream);
 /* mu-EG k x k algebra: A = I - eta*(triu(C,1) + diag d),
  * scale_i = 1/||W_i||.  flag int32[1]: set to 1 if a column norm < 1e-12
  * (rank collapse, solvers.py:136-143); left unchanged otherwise. */

@@ -48,6 +48,7 @@ SIGNATURES = {
                                              _p]),
     "sped_gram_workspace_bytes": (_sz, [_i64, _i32]),
     "sped_gram": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _sz, _p]),
+    "sped_gram_mueg": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _sz, _p]),
     "sped_mueg_coeffs": (C.c_int, [_i32, _p, _f64, _p, _p, _p, _p]),
     "sped_oja_coeffs": (C.c_int, [_i32, _p, _f64, _i32, _p, _p, _p]),
     "sped_block_update": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _f64, _p, _i32, _p, _p]),

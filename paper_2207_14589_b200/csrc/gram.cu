@@ -137,7 +137,7 @@ void gram_geometry(int64_t n, int32_t k, bool with_m, int* ntiles, int* splits,
 bool gram_tc_supported(int32_t k, bool with_m);
 size_t gram_tc_workspace(int64_t n, int32_t k);
 int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, void* ws,
-            cudaStream_t s);
+            cudaStream_t s, bool diag_q);
 
 static bool use_tc(int32_t k, bool with_m) {
   static int force_simt = -1;
@@ -164,14 +164,14 @@ extern "C" size_t sped_gram_workspace_bytes(int64_t n, int32_t k) {
   return best;
 }
 
-extern "C" int sped_gram(int64_t n, int32_t k, const float* V, const float* M, double* G,
-                         void* workspace, size_t workspace_bytes, sped_stream_t stream) {
+static int gram_impl(int64_t n, int32_t k, const float* V, const float* M, double* G,
+                     void* workspace, size_t workspace_bytes, sped_stream_t stream, bool diag_q) {
   SPED_CHECK_ARG(n >= 1 && k >= 1 && V && G && workspace, "bad gram arguments");
   cudaStream_t s = as_stream(stream);
   const bool with_m = (M != nullptr);
   if (use_tc(k, with_m)) {
     SPED_CHECK_ARG(workspace_bytes >= gram_tc_workspace(n, k), "gram workspace too small");
-    return gram_tc(n, k, V, M, G, workspace, s);
+    return gram_tc(n, k, V, M, G, workspace, s, diag_q);
   }
   const int K2 = with_m ? 2 * k : k;
   int ntiles, splits;
@@ -193,4 +193,18 @@ extern "C" int sped_gram(int64_t n, int32_t k, const float* V, const float* M, d
   gram_reduce_kernel<<<ntiles, 256, 0, s>>>(k, K2, tiles, ntiles, splits, partial, G);
   SPED_LAUNCH_CHECK();
   return SPED_OK;
+}
+
+extern "C" int sped_gram(int64_t n, int32_t k, const float* V, const float* M, double* G,
+                         void* workspace, size_t workspace_bytes, sped_stream_t stream) {
+  return gram_impl(n, k, V, M, G, workspace, workspace_bytes, stream, false);
+}
+
+// mu-EG needs S, C and only diag(Q): at k = 128 the tensor-core kernel then
+// skips the Q MMA group (off-diagonal Q entries are returned as 0); other k
+// compute the full Q as sped_gram.
+extern "C" int sped_gram_mueg(int64_t n, int32_t k, const float* V, const float* M, double* G,
+                              void* workspace, size_t workspace_bytes, sped_stream_t stream) {
+  SPED_CHECK_ARG(M != nullptr, "sped_gram_mueg needs M");
+  return gram_impl(n, k, V, M, G, workspace, workspace_bytes, stream, true);
 }

@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(256, 1) gram_tc_kernel(int64_t n, int32_t k,
 // Only the blocks the solvers read are kept: rows 0..k-1 of G (S and C) and
 // the Q = M^T M block (rows and columns k..2k-1).  The CTA writes its fp64
 // partial once at the end (rows 0..k-1, then Q).
-template <int K2>
+template <int K2, bool DQ = false>
 struct Cfg2 {
   // Y mode (K2 = 64): the tile is Y = [hi | lo] (128 columns) and ONE
   // M=128 x N=128 MMA per 8-row K step forms Y^T Y = [[HH, HL], [LH, LL]]:
@@ -302,11 +302,16 @@ struct Cfg2 {
   // Q) -- 384 TMEM columns, so one accumulator bank, and the fp64 row sums
   // (128 x 384) live in the CTA's global partial (read-modify-write by the
   // owning drain thread) instead of shared memory.
+  // DQ (diag-Q mode, mu-EG): only diag(Q) is needed, so the Q MMA group is
+  // dropped and the converters sum the squares of the M values they convert
+  // (fp64, fixed per-thread columns); 256 TMEM columns per bank then leave
+  // room for two banks, so the drain of slice s overlaps the MMAs of s+1.
   static constexpr bool YM = (K2 == 64);
   static constexpr bool BIG = (K2 == 256);
+  static constexpr bool BIGQ = BIG && !DQ;            // BIG with the Q MMA group
   static constexpr int NACC = BIG ? 1 : 2;            // accumulators per bank
-  static constexpr int NBANK = BIG ? 1 : 2;
-  static constexpr int ACC_COLS = YM ? 2 * K2 : (BIG ? 384 : K2);  // TMEM columns per accumulator
+  static constexpr int NBANK = BIGQ ? 1 : 2;
+  static constexpr int ACC_COLS = YM ? 2 * K2 : (BIG ? (DQ ? 256 : 384) : K2);  // TMEM columns per accumulator
   static constexpr int SPLIT = (K2 == 64) ? 1024 : 512;  // rows per slice (drain)
   static constexpr int KC = (K2 == 64) ? 64 : (BIG ? 16 : 32);  // rows per chunk
   static constexpr int NR = (K2 == 64) ? 4 : (BIG ? 4 : 3);     // raw (bulk copy) stages
@@ -327,11 +332,12 @@ struct Cfg2 {
 };
 
 
-template <int K2>
-__global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
+template <int K2, bool DQ>
+__global__ void __launch_bounds__(Cfg2<K2, DQ>::NTHREADS, 1)
     gram_tc2_kernel(int64_t n, int32_t k, const float* __restrict__ V, const float* __restrict__ M,
                     double* __restrict__ partial, int64_t nslices) {
-  using C = Cfg2<K2>;
+  using C = Cfg2<K2, DQ>;
+  static_assert(!DQ || K2 == 256, "diag-Q mode is the k = 128 kernel");
   extern __shared__ __align__(1024) uint8_t smem[];
   float* raw = reinterpret_cast<float*>(smem);
   float* tiles = raw + C::NR * C::RAW_FLOATS;
@@ -392,6 +398,10 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
     return (int)(v > C::KC ? C::KC : v);
   };
 
+  // DQ: sum of squares of this thread's M columns (fixed per thread: one
+  // 4-row x 4-column block per chunk, (KC/4)*(K2/4) == 256 converter threads)
+  double dq[4] = {0.0, 0.0, 0.0, 0.0};
+  __shared__ double dq_s[DQ ? 4 * 128 : 1];
   if (warp < 8) {
     // ---------------- converters ----------------
     for (int64_t q = 0; q < nq; ++q) {
@@ -420,6 +430,18 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
                              : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         const int off = kmaj_offset2<C::TCOLS>(rq * 4, c);
+        if constexpr (DQ) {
+          static_assert(!DQ || (C::KC / 4) * (K2 / 4) == 256, "one block per converter thread");
+          if (c >= C::HALF) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              dq[0] += (double)z[i].x * (double)z[i].x;
+              dq[1] += (double)z[i].y * (double)z[i].y;
+              dq[2] += (double)z[i].z * (double)z[i].z;
+              dq[3] += (double)z[i].w * (double)z[i].w;
+            }
+          }
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float x0 = (&z[0].x)[j], x1 = (&z[1].x)[j], x2 = (&z[2].x)[j], x3 = (&z[3].x)[j];
@@ -484,6 +506,7 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
             mma_tf32(tacc, dh, dh, idesc, acc0);
             mma_tf32(tacc, dh, dl, idesc, 1u);
             mma_tf32(tacc, dl, dh, idesc, 1u);
+            if constexpr (DQ) continue;  // diag(Q) comes from the converters
             const uint32_t goff = 16u * SBO_B;
             const uint64_t qh = smem_desc(hi_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
             const uint64_t ql = smem_desc(lo_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
@@ -519,11 +542,11 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
       const int nk = min(C::NACC, chunks * (C::KC / 8));
       if constexpr (C::BIG) {
         // TMEM lane m: row m of [S | C] (cols 0..255) and row m of Q (cols
-        // 256..383); fp64 sums accumulate in the global partial
+        // 256..383; not in DQ mode); fp64 sums accumulate in the global partial
 #pragma unroll 1
-        for (int c0 = 0; c0 < 384; c0 += 16) {
+        for (int c0 = 0; c0 < C::ACC_COLS; c0 += 16) {
           float v[16];
-          tmem_ld16(tmem + (uint32_t)c0 + lane_base, v);
+          tmem_ld16(tmem + (uint32_t)(bank * C::ACC_COLS + c0) + lane_base, v);
           double* dst = (c0 < 256) ? out + row * K2 + c0
                                    : out + C::HALF * K2 + row * C::HALF + (c0 - 256);
 #pragma unroll
@@ -563,9 +586,21 @@ __global__ void __launch_bounds__(Cfg2<K2>::NTHREADS, 1)
       mbar_arrive(&bank_free[bank]);
     }
   }
+  if constexpr (DQ) {
+    if (tid < 256 && (tid % (K2 / 4)) * 4 >= C::HALF) {
+      const int rq = tid / (K2 / 4), c = (tid % (K2 / 4)) * 4 - C::HALF;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dq_s[rq * 128 + c + j] = dq[j];
+    }
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if constexpr (DQ) {  // diag(Q) of this CTA's rows, fixed summation order
+    for (int e = tid; e < C::HALF; e += C::NTHREADS)
+      out[C::HALF * K2 + e * C::HALF + e] =
+          ((dq_s[e] + dq_s[128 + e]) + dq_s[256 + e]) + dq_s[384 + e];
+  }
   if constexpr (!C::BIG)
   for (int e = tid; e < C::HALF * K2; e += C::NTHREADS) {
     const int i = (e / K2) * C::SUM_LD + (e % K2);
@@ -600,19 +635,19 @@ __global__ void gram_tc2_reduce(int32_t k, int32_t nparts, const double* __restr
   }
 }
 
-template <int K2>
+template <int K2, bool DQ = false>
 int launch2(int64_t n, int32_t k, const float* V, const float* M, double* G, double* partial,
             cudaStream_t s) {
-  using C = Cfg2<K2>;
+  using C = Cfg2<K2, DQ>;
   static bool attr = false;
   if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(gram_tc2_kernel<K2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   C::SMEM));
+    SPED_CUDA(cudaFuncSetAttribute(gram_tc2_kernel<K2, DQ>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   const int64_t nslices = (n + C::SPLIT - 1) / C::SPLIT;
   const unsigned grid = (unsigned)std::min<int64_t>(nslices, (int64_t)num_sms());
-  gram_tc2_kernel<K2><<<grid, C::NTHREADS, C::SMEM, s>>>(n, k, V, M, partial, nslices);
+  gram_tc2_kernel<K2, DQ><<<grid, C::NTHREADS, C::SMEM, s>>>(n, k, V, M, partial, nslices);
   SPED_LAUNCH_CHECK();
   const int per = k * K2 + k * k;
   gram_tc2_reduce<<<(per + 255) / 256, 256, 0, s>>>(k, (int)grid, partial, G);
@@ -671,7 +706,7 @@ size_t gram_tc_workspace(int64_t n, int32_t k) {
 }
 
 int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, void* ws,
-            cudaStream_t s) {
+            cudaStream_t s, bool diag_q) {
   double* partial = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   static const bool v1 = [] {
     const char* e = getenv("SPED_GRAM_V1");
@@ -682,8 +717,10 @@ int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, voi
                        : tc::launch2<64>(n, k, V, M, G, partial, s);
     case 64: return v1 ? tc::launch<128>(n, k, V, M, G, partial, s)
                        : tc::launch2<128>(n, k, V, M, G, partial, s);
-    case 128: return v1 ? tc::launch<256>(n, k, V, M, G, partial, s)
-                        : tc::launch2<256>(n, k, V, M, G, partial, s);
+    case 128:
+      if (v1) return tc::launch<256>(n, k, V, M, G, partial, s);
+      return diag_q ? tc::launch2<256, true>(n, k, V, M, G, partial, s)
+                    : tc::launch2<256>(n, k, V, M, G, partial, s);
     default: set_error("gram_tc: unsupported k=%d", k); return SPED_ERR_UNSUPPORTED;
   }
 }

@@ -111,10 +111,12 @@ class StepWorkspace:
         # row shards: called on G after every Gram (the all-reduce, C2)
         self.reduce = None
 
-    def gram(self, V, M=None):
+    def gram(self, V, M=None, diag_q=False):
+        """G = {S, C, Q}; diag_q: Q's diagonal only (mu-EG, sped_gram_mueg)."""
         lib = _lib.load()
-        rc = lib.sped_gram(self.n, self.k, _lib.ptr(V), _lib.ptr(M), _lib.ptr(self.G),
-                           _lib.ptr(self.gram_ws), self.gram_bytes, _lib.stream_ptr(self.device))
+        fn = lib.sped_gram_mueg if (diag_q and M is not None) else lib.sped_gram
+        rc = fn(self.n, self.k, _lib.ptr(V), _lib.ptr(M), _lib.ptr(self.G),
+                _lib.ptr(self.gram_ws), self.gram_bytes, _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_gram")
         if self.reduce is not None:
             self.reduce(self.G)
@@ -136,7 +138,7 @@ class StepWorkspace:
     def mu_eg(self, V, MV, eta, out):
         """solvers.py:121-144 in Gram form."""
         lib = _lib.load()
-        self.gram(V, MV)
+        self.gram(V, MV, diag_q=True)
         rc = lib.sped_mueg_coeffs(self.k, _lib.ptr(self.G), float(eta), _lib.ptr(self.A),
                                   _lib.ptr(self.scale), _lib.ptr(self.flag),
                                   _lib.stream_ptr(self.device))

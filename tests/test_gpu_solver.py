@@ -305,6 +305,19 @@ def test_gram_kernels_vs_fp64(cuda, k, n):
     ws.gram(V)
     S = ws.G.cpu().numpy()[: k * k].reshape(k, k)
     assert np.abs(S - Vh.T @ Vh).max() <= 1e-5 * np.abs(Vh.T @ Vh).max()
+    # sped_gram_mueg (the mu-EG Gram): S, C and diag(Q); at k = 128 the Q
+    # block's MMAs are skipped and its off-diagonal comes back 0
+    ws.gram(V, M, diag_q=True)
+    G = ws.G.cpu().numpy()
+    for blk, ref in ((0, Vh.T @ Vh), (1, Vh.T @ Mh)):
+        got = G[blk * k * k:(blk + 1) * k * k].reshape(k, k)
+        assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max(), blk
+    Q = G[2 * k * k:].reshape(k, k)
+    qref = (Mh * Mh).sum(0)
+    assert np.abs(np.diag(Q) - qref).max() <= 1e-5 * qref.max()
+    if k == 128:
+        assert not np.any(Q - np.diag(np.diag(Q)))
+        assert np.abs(np.diag(Q) - qref).max() <= 1e-12 * qref.max()  # fp64 sums of squares
 
 
 @pytest.mark.parametrize("k", [10, 16, 32, 64, 128])
