@@ -468,8 +468,15 @@ __global__ void __launch_bounds__(Cfg2<K2, DQ>::NTHREADS, 1)
         float* dst = raw + rs * C::RAW_FLOATS;
         const uint32_t bytes = (uint32_t)valid * (uint32_t)C::HALF * 4u;
         mbar_expect_tx(&full_bar[rs], 2 * bytes);
-        bulk_g2s(dst, V + r0 * C::HALF, bytes, &full_bar[rs]);
-        bulk_g2s(dst + C::KC * C::HALF, M + r0 * C::HALF, bytes, &full_bar[rs]);
+        // BIG: read-once stream evict_first, so the fp64 partial rows the
+        // drain read-modify-writes stay in L2 (they went to DRAM: +1.5 GB)
+        if constexpr (C::BIG) {
+          bulk_g2s_stream(dst, V + r0 * C::HALF, bytes, &full_bar[rs]);
+          bulk_g2s_stream(dst + C::KC * C::HALF, M + r0 * C::HALF, bytes, &full_bar[rs]);
+        } else {
+          bulk_g2s(dst, V + r0 * C::HALF, bytes, &full_bar[rs]);
+          bulk_g2s(dst + C::KC * C::HALF, M + r0 * C::HALF, bytes, &full_bar[rs]);
+        }
       }
     }
     __syncwarp();

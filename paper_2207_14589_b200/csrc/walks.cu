@@ -19,7 +19,7 @@
 //   * the walk's prefix contributions coeffs[i] * chain_i / p_i (signs and
 //     log magnitudes accumulated as in walks.py:207-222) are summed per walk
 //     and emitted as two (node, value) records at the first edge's endpoints;
-//     the records are reduced by a stable sort + reduce-by-key, so the result
+//     the records are reduced by a stable sort + per-run sequential sums, so the result
 //     is deterministic.
 // Values are fp64 like the reference; agreement is to fp64 rounding (the
 // walks themselves are identical).
@@ -205,14 +205,22 @@ __global__ void walk_kernel(const WalkArgs a) {
   a.rec_val[r0 + 1] = -total;
 }
 
-__global__ void scatter_sums_kernel(int64_t count, const int32_t* __restrict__ keys,
-                                    const double* __restrict__ sums, const int32_t* num,
-                                    int64_t n, int32_t k, double* __restrict__ total) {
+// Sum each run of equal sorted keys in sorted (= walk) order, one thread per
+// run, and scatter it to total[node][col].  (cub::DeviceReduce::ReduceByKey
+// combined the partial sums of runs spanning tiles in a timing-dependent
+// grouping -- decoupled look-back -- so fp64 results differed in the last
+// bit between calls.)
+__global__ void run_sums_kernel(int64_t count, const int32_t* __restrict__ keys,
+                                const double* __restrict__ vals, int64_t n, int32_t k,
+                                double* __restrict__ total) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= *num) return;
+  if (i >= count) return;
   const int32_t key = keys[i];
+  if (i > 0 && keys[i - 1] == key) return;
+  double s = 0.0;
+  for (int64_t j = i; j < count && keys[j] == key; ++j) s += vals[j];
   const int64_t col = key / n, node = key - col * n;
-  total[node * k + col] = sums[i];
+  total[node * k + col] = s;
 }
 
 __global__ void finish_kernel(int64_t nk, double c0, double scale, const double* __restrict__ x,
@@ -287,8 +295,8 @@ extern "C" int sped_walk_index_build(int64_t n, int64_t m, const int64_t* u, con
 namespace sped {
 namespace {
 struct WalkWs {
-  int32_t *key_in, *key_out, *uniq, *num;
-  double *val_in, *val_out, *sums, *total;
+  int32_t *key_in, *key_out;
+  double *val_in, *val_out, *total;
   void* tmp;
   size_t tmp_bytes;
   size_t bytes;
@@ -305,19 +313,13 @@ WalkWs walk_ws_layout(char* base, int64_t n, int32_t k, int64_t walks) {
   };
   w.key_in = (int32_t*)take(sizeof(int32_t) * R);
   w.key_out = (int32_t*)take(sizeof(int32_t) * R);
-  w.uniq = (int32_t*)take(sizeof(int32_t) * R);
-  w.num = (int32_t*)take(sizeof(int32_t) * 2);
   w.val_in = (double*)take(sizeof(double) * R);
   w.val_out = (double*)take(sizeof(double) * R);
-  w.sums = (double*)take(sizeof(double) * R);
   w.total = (double*)take(sizeof(double) * n * k);
-  size_t t1 = 0, t2 = 0;
+  size_t t1 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t1, (int32_t*)nullptr, (int32_t*)nullptr,
                                   (double*)nullptr, (double*)nullptr, (int)R);
-  cub::DeviceReduce::ReduceByKey(nullptr, t2, (int32_t*)nullptr, (int32_t*)nullptr,
-                                 (double*)nullptr, (double*)nullptr, (int32_t*)nullptr,
-                                 cuda::std::plus<double>{}, (int)R);
-  w.tmp_bytes = std::max(t1, t2);
+  w.tmp_bytes = t1;
   w.tmp = take(w.tmp_bytes);
   w.bytes = off + 256;
   return w;
@@ -374,11 +376,8 @@ extern "C" int sped_walk_poly_estimate(int64_t n, int64_t m, int32_t k, const in
   // stable sort by (column, node): records of one node stay in walk order
   SPED_CUDA(cub::DeviceRadixSort::SortPairs(ws.tmp, tb, ws.key_in, ws.key_out, ws.val_in,
                                             ws.val_out, R, 0, end_bit, s));
-  tb = ws.tmp_bytes;
-  SPED_CUDA(cub::DeviceReduce::ReduceByKey(ws.tmp, tb, ws.key_out, ws.uniq, ws.val_out, ws.sums,
-                                           ws.num, cuda::std::plus<double>{}, R, s));
   SPED_CUDA(cudaMemsetAsync(ws.total, 0, sizeof(double) * n * k, s));
-  scatter_sums_kernel<<<grid_for(R, 256), 256, 0, s>>>(R, ws.uniq, ws.sums, ws.num, n, k, ws.total);
+  run_sums_kernel<<<grid_for(R, 256), 256, 0, s>>>(R, ws.key_out, ws.val_out, n, k, ws.total);
   SPED_LAUNCH_CHECK();
   // importance: coeffs[0] x + total / N; rejection: total / (N p_min)
   const double scale = (mode == 0) ? 1.0 / (double)walks
