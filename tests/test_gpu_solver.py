@@ -412,3 +412,23 @@ def test_persistent_solver_multi_cta(cuda, graph, mode, kind, ell, eta, k):
         p3.advance(m)
     assert torch.equal(p.V, p3.V)
     assert not p3.ws.take_flag()
+
+
+@pytest.mark.parametrize("n,d,c,spread", [(3000, 8, 6, 0.3), (20000, 16, 12, 1.0)])
+def test_kmeans_labels_vs_oracle_and_deterministic(cuda, n, d, c, spread):
+    """kmeans_cluster (device assignment, fixed-point centroid sums) gives the
+    oracle's labels (metrics.py:143-176 restated; index work, bit-exact) on
+    blobs of increasing overlap, and identical labels run to run at a size
+    where fp64 atomics would reorder their sums."""
+    sp = _sp()
+    rng = np.random.default_rng(n + c)
+    centers = rng.standard_normal((c, d)) * 3.0
+    X = (centers[rng.integers(0, c, n)] + spread * rng.standard_normal((n, d))).astype(np.float32)
+    got = sp.kmeans_cluster(X, c, seed=3)
+    ref = O.kmeans_cluster(X.astype(np.float64), c, seed=3)
+    assert np.array_equal(got, ref)
+    Xd = torch.as_tensor(X, device="cuda")
+    big = torch.cat([Xd] * 10)  # 2e5 rows
+    a = sp.kmeans_cluster(big, c, seed=1)
+    b = sp.kmeans_cluster(big, c, seed=1)
+    assert np.array_equal(a, b)
