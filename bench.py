@@ -282,6 +282,18 @@ def time_to_angle(cfg=1, target=1e-3, eval_every=50, max_steps=20000, cpu=True,
             gpu_path, gpu_steps, gpu_s = ("grid-resident K7 kernel (sped_persistent_mueg)",
                                           p_steps, p_s)
     out.update(gpu_path=gpu_path, gpu_steps=gpu_steps, gpu_s=gpu_s)
+    # per-step latency of the same stepper without evaluations (SURVEY 8d:
+    # configs 1-2 report latency, not a roofline fraction)
+    stp = (_PersistentStepper(op, eta, Vi) if gpu_path.startswith("grid")
+           else _GraphStepper(op, "mu-eg", eta, Vi))
+    stp.advance(20)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    stp.advance(500)
+    e1.record()
+    torch.cuda.synchronize()
+    out["gpu_us_per_step"] = e0.elapsed_time(e1) * 1e3 / 500
     if cpu:
         csr = O.laplacian_csr(n, g.u, g.v, g.w, spec["mode"])
         lam = O.choose_lambda_star(kind, O.lambda_upper(n, g.u, g.v, g.w, spec["mode"]))
@@ -305,6 +317,51 @@ def time_to_angle(cfg=1, target=1e-3, eval_every=50, max_steps=20000, cpu=True,
         if gpu_steps and cpu_steps:
             out["speedup"] = out["cpu_s"] / gpu_s
     return out
+
+
+def exact_step_line(cfg, steps=5, warmup=2):
+    """One exact mu-EG step on another BASELINE config (SBM configs 3 / 5:
+    natural order, L2-resident gathers; config 5's k = 128 Gram and update
+    run on the tensor cores): per-term, apply, Gram+coefficients+update and
+    whole-step times (CUDA events), throughput in the headline unit."""
+    import torch
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200 import generators as G
+    from paper_2207_14589_b200.solvers import StepWorkspace
+    spec = G.CONFIGS[cfg]
+    dev = torch.device("cuda")
+    n, u, v, w = G.config_graph(cfg, device=dev)
+    g = sp.Graph.from_canonical(n, u, v, w, validate=False)
+    k, ell = spec["k"], spec["ell"]
+    t = sp.SpectralTransform("negexp-taylor", ell)
+    op = sp.make_reversed_operator(g, t, spec["mode"], device=dev)
+    V = torch.randn((n, k), device=dev, generator=torch.Generator(device=dev).manual_seed(cfg))
+    V /= torch.linalg.norm(V, dim=0)
+    Vn, MV = torch.empty_like(V), torch.empty_like(V)
+    ws = StepWorkspace(n, k, dev)
+    eta = 0.1
+    for _ in range(warmup):
+        op.apply_internal(V, out=MV)
+        ws.mu_eg(V, MV, eta, Vn)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for i in range(steps):
+        ev[i][0].record()
+        op.apply_internal(V, out=MV)
+        ev[i][1].record()
+        ws.mu_eg(V, MV, eta, Vn)
+        ev[i][2].record()
+        V, Vn = Vn, V
+    torch.cuda.synchronize()
+    apply_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+    solve_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
+    nt, nnz = op.n_terms, op.laplacian.nnz
+    return {"config": spec["name"], "n": n, "nnz": nnz, "k": k,
+            "transform": f"negexp-taylor({ell})", "terms": nt,
+            "ms_per_step": apply_ms + solve_ms, "ms_per_term": apply_ms / nt,
+            "gram_coeffs_update_ms": solve_ms,
+            "nnz_k_per_s": nt * nnz * k / ((apply_ms + solve_ms) / 1e3),
+            "pLV_nnz_k_per_s": nt * nnz * k / (apply_ms / 1e3)}
 
 
 def stochastic_line(cfg=3, reps=5):
@@ -536,8 +593,10 @@ def run_sped(args):
                 time_to_angle(2, kind="negexp-limit", ell=17, eta=1.0, eval_every=100,
                               cpu_sample_steps=300)]
     sto = None
+    extra = None
     if rank == 0 and not sharded and not args.no_extra:
         sto = stochastic_line(3)
+        extra = [exact_step_line(3), exact_step_line(5)]
 
     if rank == 0:
         line = {
@@ -552,6 +611,7 @@ def run_sped(args):
                        "parallelism": f"row-shard x{world}" if sharded else "single GPU",
                        "l2": "inputs (V 4nk B, CSR) larger than the 126 MB L2; no flush",
                        "setup_s": setup_s},
+            "pLV_nnz_k_per_s": work * args.steps / (apply_ms / 1e3),
             "breakdown_ms_per_step": {"p(L)V": apply_ms / args.steps,
                                       "gram+coeffs+update": solve_ms / args.steps,
                                       "per_term": 1e3 * t_term_s},
@@ -569,6 +629,7 @@ def run_sped(args):
             "cpu_baseline": cpu,
             "time_to_angle": conv,
             "stochastic": sto,
+            "other_configs_exact": extra,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
