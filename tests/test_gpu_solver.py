@@ -432,3 +432,35 @@ def test_kmeans_labels_vs_oracle_and_deterministic(cuda, n, d, c, spread):
     a = sp.kmeans_cluster(big, c, seed=1)
     b = sp.kmeans_cluster(big, c, seed=1)
     assert np.array_equal(a, b)
+
+
+def test_power_law_graph_capture_with_l2_window(cuda):
+    """A degree-relabelled power-law graph whose SpMM sets the persisting-L2
+    window over the hub prefix: whole steps captured as CUDA graphs equal
+    the eager steps bit for bit, and the apply equals the oracle."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    from paper_2207_14589_b200.solvers import _GraphStepper
+    n, u, v, w = G.chung_lu(600_000, cap=20000.0, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-taylor", 6), "normalized")
+    lap = op.laplacian
+    assert lap.reordered and 0 < lap.hot_rows(32) < n  # the window is in play
+    V = torch.randn((n, 32), device="cuda", generator=torch.Generator(device="cuda").manual_seed(2))
+    V /= torch.linalg.norm(V, dim=0)
+    a = _GraphStepper(op, "mu-eg", 0.1, V)
+    a.advance(3)
+    from paper_2207_14589_b200.solvers import StepWorkspace
+    ws = StepWorkspace(n, 32, "cuda")
+    X = V.clone()
+    Y, MV = torch.empty_like(X), torch.empty_like(X)
+    for _ in range(3):
+        op.apply_internal(X, out=MV)
+        ws.mu_eg(X, MV, 0.1, Y)
+        X, Y = Y, X
+    assert torch.equal(a.V, X)
+    csr = O.laplacian_csr(n, g.u, g.v, g.w, "normalized")
+    x = np.random.default_rng(1).standard_normal((n, 8)).astype(np.float32)
+    got = op.apply(torch.as_tensor(x, device="cuda")).cpu().numpy()
+    ref = O.apply_transform(csr, "negexp-taylor", 6, 1e-6, op.lambda_star, x.astype(np.float64))
+    assert rel_fro(got, ref) <= 1e-5
