@@ -10,6 +10,7 @@
  *
  * Reference interfaces replaced (paths relative to
  * /root/reference/pkg/src/specgap/):
+ *   sped_canonicalize_edges    Graph.__post_init__               graph.py:64-88
  *   sped_laplacian_build       LaplacianOperator.__post_init__   graph.py:182-199
  *                              (+ Graph.degrees graph.py:118-122)
  *   sped_csr_poly_apply        TransformedOperator.apply         transforms.py:229-262
@@ -70,6 +71,17 @@ int sped_laplacian_build(int64_t n, int64_t m, const int64_t* u, const int64_t* 
                          int32_t* indptr, int32_t* indices, float* values,
                          double* degrees, int32_t* epos, int64_t* nnz_out,
                          sped_stream_t stream);
+
+/* ---- graph canonicalisation (Graph.__post_init__, graph.py:64-88) -------
+ * Drops w == 0 edges, orients u < v and sorts by (u, v) on the device (the
+ * reference's lexsort, bit for bit: a radix sort of the unique keys u*n+v).
+ * Outputs (device, capacity m) receive the *m_out (host) kept edges.
+ * *status_out (host) is a bit set of the reference's ValueErrors: 1 negative
+ * weight, 2 self loop, 4 endpoint out of range, 8 duplicate unordered pair;
+ * outputs are only written when it is 0.  Synchronises `stream`. */
+int sped_canonicalize_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                            const double* w, int64_t* u_out, int64_t* v_out, double* w_out,
+                            int64_t* m_out, int32_t* status_out, sped_stream_t stream);
 
 /* ---- locality ordering for power-law graphs -----------------------------
  * perm (new -> old) lists nodes by descending row length (stable), iperm is

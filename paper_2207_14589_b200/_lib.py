@@ -31,6 +31,8 @@ SIGNATURES = {
     "sped_abi_version": (C.c_int, []),
     "sped_laplacian_build": (C.c_int, [_i64, _i64, _p, _p, _p, C.c_int, C.c_int, _p, _p, _p, _p,
                                        _p, C.POINTER(_i64), _p]),
+    "sped_canonicalize_edges": (C.c_int, [_i64, _i64, _p, _p, _p, _p, _p, _p, C.POINTER(_i64),
+                                          C.POINTER(_i32), _p]),
     "sped_degree_order": (C.c_int, [_i64, _p, _p, _p, _p]),
     "sped_relabel_edges": (C.c_int, [_i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sped_spmm_plan_max_chunks": (_i64, [_i64, _i64, _i32, _i32]),

@@ -493,3 +493,117 @@ extern "C" int sped_relabel_edges(int64_t n, int64_t m, const int64_t* u, const 
   SPED_LAUNCH_CHECK();
   return SPED_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Graph canonicalisation on the device (Graph.__post_init__, graph.py:64-88):
+// drop zero-weight edges, validate (negative weights, self loops, endpoint
+// range, duplicate unordered pairs -- the reference's checks and order of
+// precedence), orient u < v and sort lexicographically by (u, v).  The key
+// lo*n + hi is unique per unordered pair, so an integer radix sort gives the
+// reference's lexsort order bit for bit.  Dropped / invalid edges get a
+// sentinel key that sorts after every valid one.
+
+namespace sped {
+namespace {
+enum CanonStatus : int { CS_NEG = 1, CS_SELF = 2, CS_RANGE = 4, CS_DUP = 8 };
+
+__global__ void canon_key_kernel(int64_t m, int64_t n, const int64_t* __restrict__ u,
+                                 const int64_t* __restrict__ v, const double* __restrict__ w,
+                                 unsigned long long sentinel, unsigned long long* __restrict__ key,
+                                 int32_t* __restrict__ ids, int32_t* __restrict__ keep,
+                                 int* __restrict__ status) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const double we = w[e];
+  const int64_t a = u[e], b = v[e];
+  int st = 0;
+  bool kept = false;
+  if (we < 0.0) {
+    st |= CS_NEG;
+  } else if (we > 0.0) {
+    if (a == b) st |= CS_SELF;
+    if (a < 0 || a >= n || b < 0 || b >= n) st |= CS_RANGE;
+    kept = (st == 0);
+  }
+  if (st) atomicOr(status, st);
+  const int64_t lo = a < b ? a : b, hi = a < b ? b : a;
+  key[e] = kept ? (unsigned long long)(lo * n + hi) : sentinel;
+  ids[e] = (int32_t)e;
+  keep[e] = (we > 0.0) ? 1 : 0;  // the reference drops w == 0 before its checks
+}
+
+__global__ void canon_gather_kernel(int64_t mk, int64_t n, const unsigned long long* __restrict__ key,
+                                    const int32_t* __restrict__ ids, const double* __restrict__ w,
+                                    int64_t* __restrict__ u2, int64_t* __restrict__ v2,
+                                    double* __restrict__ w2, int* __restrict__ status) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= mk) return;
+  const unsigned long long kk = key[e];
+  if (e > 0 && key[e - 1] == kk) atomicOr(status, CS_DUP);
+  u2[e] = (int64_t)(kk / (unsigned long long)n);
+  v2[e] = (int64_t)(kk % (unsigned long long)n);
+  w2[e] = w[ids[e]];
+}
+}  // namespace
+}  // namespace sped
+
+extern "C" int sped_canonicalize_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                                       const double* w, int64_t* u2, int64_t* v2, double* w2,
+                                       int64_t* m_out, int32_t* status_out,
+                                       sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && m >= 0 && m < INT32_MAX, "bad sizes");
+  SPED_CHECK_ARG(m_out && status_out, "null output");
+  SPED_CHECK_ARG((double)n * (double)n < 9.2e18, "node count too large for 64-bit pair keys");
+  *m_out = 0;
+  *status_out = 0;
+  if (m == 0) return SPED_OK;
+  SPED_CHECK_ARG(u && v && w && u2 && v2 && w2, "null array");
+  cudaStream_t s = as_stream(stream);
+  AsyncBuf b_key(s), b_key2(s), b_ids(s), b_ids2(s), b_keep(s), b_cnt(s), b_tmp(s), b_tmp2(s);
+  SPED_CUDA(b_key.alloc(sizeof(unsigned long long) * m));
+  SPED_CUDA(b_key2.alloc(sizeof(unsigned long long) * m));
+  SPED_CUDA(b_ids.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_ids2.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_keep.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_cnt.alloc(sizeof(int64_t) + sizeof(int)));
+  int64_t* d_cnt = (int64_t*)b_cnt.p;
+  int* d_status = (int*)(d_cnt + 1);
+  SPED_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), s));
+  // 2^end_bit > n*n: every valid key < n*n - n, the sentinel 2^end_bit - 1
+  int end_bit = 1;
+  const unsigned long long nn = (unsigned long long)n * (unsigned long long)n;
+  while (end_bit < 64 && (1ULL << end_bit) <= nn) ++end_bit;
+  const unsigned long long sentinel = (end_bit >= 64) ? ~0ULL : ((1ULL << end_bit) - 1ULL);
+  canon_key_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, n, u, v, w, sentinel,
+                                                      (unsigned long long*)b_key.p,
+                                                      (int32_t*)b_ids.p, (int32_t*)b_keep.p,
+                                                      d_status);
+  SPED_LAUNCH_CHECK();
+  size_t t1 = 0, t2 = 0;
+  SPED_CUDA(cub::DeviceReduce::Sum(nullptr, t2, (int32_t*)b_keep.p, d_cnt, (int)m, s));
+  SPED_CUDA(b_tmp2.alloc(t2));
+  SPED_CUDA(cub::DeviceReduce::Sum(b_tmp2.p, t2, (int32_t*)b_keep.p, d_cnt, (int)m, s));
+  SPED_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, (unsigned long long*)b_key.p,
+                                            (unsigned long long*)b_key2.p, (int32_t*)b_ids.p,
+                                            (int32_t*)b_ids2.p, (int)m, 0, end_bit, s));
+  SPED_CUDA(b_tmp.alloc(t1));
+  SPED_CUDA(cub::DeviceRadixSort::SortPairs(b_tmp.p, t1, (unsigned long long*)b_key.p,
+                                            (unsigned long long*)b_key2.p, (int32_t*)b_ids.p,
+                                            (int32_t*)b_ids2.p, (int)m, 0, end_bit, s));
+  int64_t mk = 0;
+  int st = 0;
+  SPED_CUDA(cudaMemcpyAsync(&mk, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaMemcpyAsync(&st, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaStreamSynchronize(s));
+  if (st == 0 && mk > 0) {
+    canon_gather_kernel<<<grid_for(mk, 256), 256, 0, s>>>(mk, n, (unsigned long long*)b_key2.p,
+                                                            (int32_t*)b_ids2.p, w, u2, v2, w2,
+                                                            d_status);
+    SPED_LAUNCH_CHECK();
+    SPED_CUDA(cudaMemcpyAsync(&st, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPED_CUDA(cudaStreamSynchronize(s));
+  }
+  *m_out = mk;
+  *status_out = st;
+  return SPED_OK;
+}

@@ -45,13 +45,21 @@ class Graph:
     """Undirected weighted graph stored as a canonical edge list (u < v,
     lexsorted, unique, w > 0).  Same contract as ``specgap.Graph``."""
 
-    def __init__(self, n: int, u, v, w, *, _canonical: bool = False):
+    def __init__(self, n: int, u, v, w, *, device=None, _canonical: bool = False):
+        """``device`` (or CUDA tensor inputs): canonicalise on that GPU
+        (``sped_canonicalize_edges``: same result bit for bit and the same
+        ValueErrors as the host path, which follows graph.py:64-88)."""
         if n < 0:
             raise ValueError("node count must be nonnegative")
         self.n = int(n)
         self._dev = {}
         if _canonical:
             self._u, self._v, self._w = u, v, w
+            return
+        on_gpu = device is not None or any(isinstance(a, torch.Tensor) and a.is_cuda
+                                           for a in (u, v, w))
+        if on_gpu:
+            self._canonicalize_on_device(u, v, w, device)
             return
         u = np.asarray(u, dtype=np.int64)
         v = np.asarray(v, dtype=np.int64)
@@ -75,6 +83,42 @@ class Graph:
         if pair_ids.size and np.any(np.diff(pair_ids) == 0):
             raise ValueError("duplicate edge for an unordered node pair")
         self._u, self._v, self._w = lo, hi, w
+
+    def _canonicalize_on_device(self, u, v, w, device):
+        import ctypes as C
+        if device is None:
+            device = next(a.device for a in (u, v, w) if isinstance(a, torch.Tensor) and a.is_cuda)
+        dev = _lib.require_cuda(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+
+        def put(a, dt):
+            if isinstance(a, torch.Tensor):
+                return a.to(device=dev, dtype=dt).contiguous()
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt).contiguous()
+        u, v, w = put(u, torch.int64), put(v, torch.int64), put(w, torch.float64)
+        if not (u.shape == v.shape == w.shape) or u.dim() != 1:
+            raise ValueError("edge arrays must have identical length")
+        m = int(u.numel())
+        u2, v2, w2 = torch.empty_like(u), torch.empty_like(v), torch.empty_like(w)
+        mk, st = C.c_int64(0), C.c_int32(0)
+        lib = _lib.load()
+        rc = lib.sped_canonicalize_edges(self.n, m, _lib.ptr(u), _lib.ptr(v), _lib.ptr(w),
+                                         _lib.ptr(u2), _lib.ptr(v2), _lib.ptr(w2), C.byref(mk),
+                                         C.byref(st), _lib.stream_ptr(dev))
+        _lib.check(rc, "sped_canonicalize_edges")
+        st = int(st.value)
+        if st & 1:
+            raise ValueError("edge weights must be nonnegative")
+        if st & 2:
+            raise ValueError("self-loops are not allowed")
+        if st & 4:
+            raise ValueError("edge endpoint out of range")
+        if st & 8:
+            raise ValueError("duplicate edge for an unordered node pair")
+        k = int(mk.value)
+        self._u, self._v, self._w = u2[:k], v2[:k], w2[:k]
+        self._dev[torch.device(dev)] = (self._u, self._v, self._w)
 
     # -- construction ------------------------------------------------------
     @classmethod

@@ -303,3 +303,49 @@ def test_scaled_normalized_path(cuda, k, monkeypatch):
     # weighted graphs keep the stored values
     wg = sp.Graph(n, g.u, g.v, np.full(g.m, 2.0))
     assert sp.LaplacianOperator(wg, "normalized").row_scale is None
+
+
+def test_device_canonicalisation_matches_host(cuda):
+    """Graph(n, u, v, w, device=...) (sped_canonicalize_edges) returns the
+    host path's canonical edge list bit for bit -- orientation, lexsort,
+    dropped zero weights -- and raises the same ValueErrors in the same
+    order of precedence (graph.py:64-88)."""
+    import torch
+    import paper_2207_14589_b200 as sp
+    rng = np.random.default_rng(7)
+    for n, m in ((1, 0), (5, 4), (1000, 20000), (300_000, 2_000_000)):
+        a = rng.integers(0, n, m)
+        b = rng.integers(0, n, m)
+        keep = a != b
+        a, b = a[keep], b[keep]
+        key = np.unique(np.minimum(a, b) * n + np.maximum(a, b))
+        lo, hi = key // n, key % n
+        perm = rng.permutation(lo.size)
+        flip = rng.random(lo.size) < 0.5
+        u = np.where(flip, hi, lo)[perm]
+        v = np.where(flip, lo, hi)[perm]
+        w = rng.uniform(0.0, 2.0, lo.size)
+        w[rng.random(lo.size) < 0.05] = 0.0  # dropped, as on the host
+        host = sp.Graph(n, u, v, w)
+        dev = sp.Graph(n, u, v, w, device="cuda")
+        assert dev.m == host.m
+        assert np.array_equal(dev.u, host.u) and np.array_equal(dev.v, host.v)
+        assert np.array_equal(dev.w, host.w)
+        td = sp.Graph(n, torch.as_tensor(u, device="cuda"), torch.as_tensor(v, device="cuda"),
+                      torch.as_tensor(w, device="cuda"))
+        assert np.array_equal(td.u, host.u) and td.u.dtype == np.int64
+    cases = [  # (u, v, w, message) -- precedence as in the reference
+        ([0, 1], [1, 2], [1.0, -1.0], "nonnegative"),
+        ([0, 2, 1], [0, 9, 2], [1.0, 1.0, -0.5], "nonnegative"),
+        ([0, 2], [0, 9], [1.0, 1.0], "self-loops"),
+        ([0, 2], [1, 9], [1.0, 1.0], "out of range"),
+        ([0, 1, 2], [1, 0, 3], [1.0, 2.0, 1.0], "duplicate"),
+        ([3, 3], [3, 3], [0.0, 0.0], None),  # zero-weight self loops are dropped first
+    ]
+    for u, v, w, msg in cases:
+        for kw in ({}, {"device": "cuda"}):
+            if msg is None:
+                assert sp.Graph(5, u, v, w, **kw).m == 0
+            else:
+                with pytest.raises(ValueError, match=msg):
+                    sp.Graph(5, u, v, w, **kw)
