@@ -37,8 +37,19 @@ __all__ = [
 ]
 
 _DENSE_MAX_NODES = 5000
-LONG_ROW_THRESHOLD = 1024
+LONG_ROW_THRESHOLD = 1024   # floor of the adaptive long-row threshold
 CHUNK_LEN = 512
+
+
+def long_row_plan(nnz: int, sms: int = 148) -> tuple[int, int]:
+    """(long_threshold, chunk_len) for the hub-chunk kernel: rows longer than
+    the threshold are cut into chunks; shorter rows go to one warp.  The
+    threshold follows the per-warp share of the nonzeros (a row no longer
+    than ~1/4 of it cannot form a tail), clamped to [1024, 4096]; chunks are
+    a quarter of it (>= 512).  Config 4 (1.7e8 nnz): 4096 / 1024, 3.18 ->
+    ~3.10 ms/term against 1024 / 512 (tools/sweep_chunking.py)."""
+    thr = max(LONG_ROW_THRESHOLD, min(4096, nnz // (sms * 256)))
+    return thr, max(CHUNK_LEN, thr // 4)
 
 
 class Graph:
@@ -294,7 +305,7 @@ class LaplacianOperator:
     """
 
     def __init__(self, graph: Graph, mode: str = "unnormalized", device=None,
-                 long_threshold: int = LONG_ROW_THRESHOLD, chunk_len: int = CHUNK_LEN,
+                 long_threshold: int | None = None, chunk_len: int | None = None,
                  implicit: bool | None = None, reorder: str | None = "auto"):
         if mode not in ("unnormalized", "normalized"):
             raise ValueError(f"unknown Laplacian mode: {mode!r}")
@@ -333,8 +344,9 @@ class LaplacianOperator:
         self.edge_w = None if graph.is_unit_weight() else w.to(torch.float32)
         self.rowlen = np.diff(self.indptr.cpu().numpy().astype(np.int64))
         self.max_row_nnz = int(self.rowlen.max()) if n else 0
-        self.long_threshold = int(long_threshold)
-        self.chunk_len = int(chunk_len)
+        thr, cl = long_row_plan(self.nnz)
+        self.long_threshold = int(long_threshold if long_threshold is not None else thr)
+        self.chunk_len = int(chunk_len if chunk_len is not None else cl)
         self._plan()
         self._segments = {}
 
