@@ -9,6 +9,8 @@
 // (device-side, no host sync) so the n-row sum cannot overflow; each input is
 // rounded to 2^-s absolute (s >= 40 for n <= 2^20 and |X| < 1).
 
+#include <mutex>
+
 #include "sped_common.cuh"
 
 namespace {
@@ -89,9 +91,11 @@ __global__ void fixed_to_double_kernel(int64_t count, int64_t n, const unsigned 
 
 unsigned int* maxbits_scratch() {
   static unsigned int* p[16] = {};
+  static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 16) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
   if (!p[dev] && cudaMalloc(&p[dev], sizeof(unsigned int)) != cudaSuccess) {
     cudaGetLastError();
     p[dev] = nullptr;

@@ -679,11 +679,9 @@ struct L2Persist {
   size_t max_window = 0;
   bool on = false;
 };
-static L2Persist& l2_persist() {
-  static L2Persist p;
-  static bool init = false;
-  if (!init) {
-    init = true;
+static const L2Persist& l2_persist() {
+  static const L2Persist cfg = [] {  // initialised once (thread-safe static)
+    L2Persist p;
     const char* e = getenv("SPED_L2_PERSIST_MB");
     const double mb = e ? atof(e) : 40.0;
     if (mb > 0) {
@@ -700,8 +698,9 @@ static L2Persist& l2_persist() {
       }
       cudaGetLastError();  // no persisting L2 on this device: plain gathers
     }
-  }
-  return p;
+    return p;
+  }();
+  return cfg;
 }
 
 // Window [base, base + bytes) for the following launches on `s` (bytes = 0
