@@ -395,7 +395,7 @@ extern "C" int sped_spmm_plan(int64_t n, const int32_t* indptr, int32_t long_thr
 // Degree-descending node order (locality for power-law graphs) and edge
 // relabelling.  Hubs get the smallest ids, so the most-gathered rows of every
 // block form one contiguous prefix that the SpMM keeps L2-resident
-// (evict_last) while cold rows stream (evict_first); rows also come sorted by
+// (a persisting-L2 window over the prefix); rows also come sorted by
 // length, which lets the SpMM pick a lanes-per-row width per row range.
 
 namespace sped {

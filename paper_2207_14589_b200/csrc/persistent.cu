@@ -8,7 +8,7 @@
 // barriers instead of kernel boundaries:
 //
 //   term 0 .. T-1   w' = a x + b L w + g w   (final: lam_f x + s w')
-//                   -- grid barrier between terms (rows gather neighbours)
+//                   -- no barrier between terms: generation-tagged words (below)
 //   Gram partials   each CTA owns a contiguous, nnz-balanced row range for
 //                   EVERY phase, so after the final term it can form its
 //                   partial S = X^T X (upper), C = X^T M, diag Q = M^T M from

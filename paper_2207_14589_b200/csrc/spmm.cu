@@ -16,8 +16,10 @@
 //    chunk warps run in the FIRST blocks of the same launch, write partial
 //    rows, and the last chunk to arrive (ticket) folds the partials in chunk
 //    order and applies the epilogue -> deterministic, no float atomics;
-//  * index/value/x streams use L2::evict_first, gathered w rows
-//    L2::evict_last so the block being multiplied stays in the 126 MB L2;
+//  * degree-relabelled graphs: a persisting-L2 access-policy window over
+//    the hub prefix of the gathered block keeps the most-gathered rows in L2
+//    (per-instruction evict_last/evict_first hints: compile-time SPED_HINTS,
+//    slower);
 //  * unweighted combinatorial Laplacians use implicit values (-1 off the
 //    diagonal, row_len-1 on it): 4 B per nonzero instead of 8;
 //  * unweighted NORMALIZED Laplacians (no self loops) run every term after
