@@ -464,3 +464,52 @@ def test_power_law_graph_capture_with_l2_window(cuda):
     got = op.apply(torch.as_tensor(x, device="cuda")).cpu().numpy()
     ref = O.apply_transform(csr, "negexp-taylor", 6, 1e-6, op.lambda_star, x.astype(np.float64))
     assert rel_fro(got, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 1000])
+def test_k128_tensor_core_kernels_small_n(cuda, n):
+    """The k = 128 tcgen05 update and the mu-EG Gram at tile-edge sizes
+    (one partial tile, exactly one tile, one row over) against fp64."""
+    from paper_2207_14589_b200.solvers import StepWorkspace
+    k = 128
+    gen = torch.Generator(device="cuda").manual_seed(n)
+    P = torch.randn((n, k), device="cuda", generator=gen)
+    M = torch.randn((n, k), device="cuda", generator=gen)
+    A = torch.triu(torch.randn((k, k), device="cuda", generator=gen)).contiguous()
+    sc = torch.rand(k, device="cuda", generator=gen) + 0.5
+    ws = StepWorkspace(n, k, torch.device("cuda"))
+    out = torch.empty_like(P)
+    ws.update(P, A, M, None, 0.3, sc, out, upper=True)
+    ref = ((P.double() @ A.double() + 0.3 * M.double()) * sc.double()).cpu().numpy()
+    assert rel_fro(out.cpu().numpy(), ref) <= 3e-6
+    ws.gram(P, M, diag_q=True)
+    G = ws.G.cpu().numpy()
+    Ph, Mh = P.double().cpu().numpy(), M.double().cpu().numpy()
+    S, C = G[: k * k].reshape(k, k), G[k * k: 2 * k * k].reshape(k, k)
+    assert np.abs(S - Ph.T @ Ph).max() <= 1e-5 * np.abs(Ph.T @ Ph).max()
+    assert np.abs(C - Ph.T @ Mh).max() <= 1e-5 * np.abs(Ph.T @ Mh).max()
+    Q = G[2 * k * k:].reshape(k, k)
+    np.testing.assert_allclose(np.diag(Q), (Mh * Mh).sum(0), rtol=1e-12)
+
+
+@pytest.mark.parametrize("k,kind,ell", [(1, "negexp-limit", 1), (3, "negexp-taylor", 2),
+                                        (5, "identity", None)])
+def test_persistent_solver_tiny(cuda, golden, k, kind, ell):
+    """K7 at the small end (k = 1, one-term and identity transforms, a
+    6-node graph): whole steps equal the oracle's fp64 steps."""
+    sp = _sp()
+    from paper_2207_14589_b200.solvers import _PersistentStepper, persistent_solver_eligible
+    g = _graph(golden, "two_triangles_bridge")
+    op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell))
+    assert persistent_solver_eligible(op, k, "mu-eg")
+    V0 = O.init_state(g.n, k, 4)
+    st = _PersistentStepper(op, 0.2, op.laplacian.to_internal(
+        torch.as_tensor(V0, dtype=torch.float32, device="cuda")))
+    st.advance(5)
+    csr = O.laplacian_csr(g.n, g.u, g.v, g.w)
+    V = V0.copy()
+    for _ in range(5):
+        V = O.mu_eg_step(V, O.apply_transform(csr, kind, ell, 1e-6, op.lambda_star, V), 0.2)
+    got = op.laplacian.from_internal(st.V).cpu().numpy()
+    assert rel_fro(got, V) <= 1e-4
+    assert not st.ws.take_flag()
