@@ -1,0 +1,115 @@
+"""Device mirrors of the reference's solver behaviour tests
+(tests/test_solvers.py:95-262 of specgap): the same scenarios, run through
+this package on the GPU (fp32, so 1e-8 equalities become 1e-5)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _sp():
+    import paper_2207_14589_b200 as sp
+    return sp
+
+
+def _embedded_operator(vals, seed):
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((len(vals), len(vals))))
+    M = (q * np.asarray(vals)) @ q.T
+    return torch.as_tensor(M, dtype=torch.float32, device="cuda"), q
+
+
+def _connected_random_graph(rng, n, p):
+    while True:
+        iu, ju = np.triu_indices(n, k=1)
+        keep = rng.random(iu.size) < p
+        u, v = iu[keep], ju[keep]
+        # connectivity by union-find
+        parent = list(range(n))
+
+        def find(a):
+            while parent[a] != a:
+                parent[a] = parent[parent[a]]
+                a = parent[a]
+            return a
+        for a, b in zip(u, v):
+            parent[find(a)] = find(b)
+        if len({find(a) for a in range(n)}) == 1:
+            w = rng.uniform(0.1, 2.0, u.size).astype(np.float32).astype(np.float64)
+            return n, u, v, w
+
+
+def test_mu_eg_k1_matches_power_direction(cuda):
+    """specgap tests/test_solvers.py:120-126"""
+    sp = _sp()
+    g = sp.Graph(2, [0], [1], [1.0])
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("identity"))
+    st = sp.init_state(2, 1, seed=10)
+    for _ in range(300):
+        st = sp.mu_eg_step(st, op.apply, eta=0.3)
+    target = np.array([1.0, 1.0]) / np.sqrt(2)
+    assert abs(abs(st.V.cpu().numpy()[:, 0] @ target) - 1) < 1e-5
+
+
+def test_mu_eg_alignment_grows_after_burn_in(cuda):
+    """specgap tests/test_solvers.py:129-137"""
+    sp = _sp()
+    M, q = _embedded_operator([4.0, 1.0, 0.5, 0.25], seed=11)
+    st = sp.init_state(4, 1, seed=12)
+    aligns = []
+    for _ in range(400):
+        st = sp.mu_eg_step(st, lambda V: M @ V, eta=0.05)
+        aligns.append(abs(float(st.V.cpu().numpy()[:, 0] @ q[:, 0])))
+    tail = np.array(aligns[50:])
+    assert np.all(np.diff(tail) >= -1e-6)
+
+
+def test_stochastic_oracle_needs_polynomial(cuda):
+    """specgap tests/test_solvers.py:177-180"""
+    sp = _sp()
+    g = sp.Graph(3, [0, 0, 1], [1, 2, 2], [1.0, 1.0, 1.0])
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp"))
+    with pytest.raises(ValueError, match="polynomial"):
+        sp.make_stochastic_oracle(op, 4, seed=0)
+
+
+@pytest.mark.parametrize("solver,eta", [("oja", 1.0), ("mu-eg", 0.05)])
+def test_solver_correctness_random_graphs(cuda, solver, eta):
+    """specgap tests/test_solvers.py:216-227: four random connected weighted
+    graphs, k = 3, identity transform, subspace error <= 1e-3."""
+    sp = _sp()
+    rng = np.random.default_rng(33)
+    for _ in range(4):
+        n, u, v, w = _connected_random_graph(rng, int(rng.integers(8, 50)), 0.4)
+        g = sp.Graph(n, u, v, w)
+        cfg = sp.SolverConfig(solver=solver, k=3, eta=eta, steps=30000, eval_every=200, seed=7)
+        run = sp.run_solver(g, sp.SpectralTransform("identity"), cfg, subspace_target=1e-3,
+                            stop_on_targets=True, record_timing=False)
+        assert run.records[-1].subspace_error <= 1e-3, f"{solver} failed on n={n}"
+
+
+def test_transform_equivariance(cuda):
+    """specgap tests/test_solvers.py:230-242: transforms change the speed,
+    never the answer (identity, exact neg-exp, exact log)."""
+    sp = _sp()
+    g = sp.Graph.from_edges(6, [(0, 1), (0, 2), (1, 2), (3, 4), (3, 5), (4, 5), (2, 3)])
+    gt = sp.graph_ground_truth(g)
+    for t in (sp.SpectralTransform("identity"), sp.SpectralTransform("negexp"),
+              sp.SpectralTransform("log", epsilon=1e-6)):
+        cfg = sp.SolverConfig(solver="oja", k=2, eta=0.5, steps=4000, eval_every=100, seed=8)
+        run = sp.run_solver(g, t, cfg, subspace_target=1e-4, stop_on_targets=True,
+                            record_timing=False)
+        V = run.V.cpu().numpy() if isinstance(run.V, torch.Tensor) else run.V
+        assert sp.subspace_error(V, gt) <= 1e-3, t.kind
+
+
+def test_eta_schedule_invsqrt(cuda):
+    """specgap tests/test_solvers.py:245-249"""
+    sp = _sp()
+    g = sp.Graph(3, [0, 0, 1], [1, 2, 2], [1.0, 1.0, 1.0])
+    cfg = sp.SolverConfig(k=1, eta=0.5, steps=200, eval_every=50, seed=9, eta_schedule="invsqrt")
+    run = sp.run_solver(g, sp.SpectralTransform("identity"), cfg)
+    assert run.records[-1].streak >= 0
+    assert run.records[-1].step == 200
