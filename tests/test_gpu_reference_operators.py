@@ -114,3 +114,20 @@ def test_reversed_top_k_is_bottom_k(cuda):
             gaps = np.diff(gt.eigenvalues[:3])
             if np.all(gaps > 1e-3):  # well-defined bottom-2 subspace
                 assert sp.subspace_error(top, gt, k=2) <= 1e-4, t.kind
+
+
+def test_kmeans_reference_cases(cuda):
+    """specgap tests/test_metrics.py:127-152 on the device k-means (incl. the
+    degenerate identical-points case, where empty clusters are re-seeded at
+    the farthest point exactly as metrics.py:161-165)."""
+    sp = _sp()
+    rng = np.random.default_rng(0)
+    X = np.vstack([rng.normal(0, 0.1, (40, 2)), rng.normal(5, 0.1, (40, 2))])
+    truth = np.repeat([0, 1], 40)
+    assert sp.cluster_accuracy(sp.kmeans_cluster(X, 2, seed=1), truth) == 1.0
+    X0 = np.zeros((10, 2))
+    truth0 = np.array([0] * 7 + [1] * 3)
+    labels0 = sp.kmeans_cluster(X0, 2, seed=1)
+    assert sp.cluster_accuracy(labels0, truth0) == pytest.approx(0.7)
+    np.testing.assert_array_equal(labels0, O.kmeans_cluster(X0, 2, seed=1))
+    assert sp.cluster_accuracy(np.array([2, 2, 0, 0, 1, 1]), np.array([0, 0, 1, 1, 2, 2])) == 1.0
