@@ -113,3 +113,44 @@ def test_eta_schedule_invsqrt(cuda):
     run = sp.run_solver(g, sp.SpectralTransform("identity"), cfg)
     assert run.records[-1].streak >= 0
     assert run.records[-1].step == 200
+
+
+def _clique_clusters(sp, n=1000, c=5, bridges=25, seed=0):
+    size = n // c
+    us, vs = [], []
+    for b in range(c):
+        iu, ju = np.triu_indices(size, k=1)
+        us.append(iu + b * size)
+        vs.append(ju + b * size)
+    rng = np.random.default_rng(seed)
+    have = set()
+    while len(have) < bridges:
+        a, b = rng.integers(0, n, 2)
+        if a // size != b // size:
+            have.add((min(a, b), max(a, b)))
+    br = np.array(sorted(have))
+    u = np.concatenate(us + [br[:, 0]])
+    v = np.concatenate(vs + [br[:, 1]])
+    return sp.Graph(n, u, v, np.ones(u.size))
+
+
+def test_dilation_speedup_criterion(cuda):
+    """The paper's claim as the reference's acceptance criterion 6 states it
+    (tests/test_acceptance.py:196-220): on 5 cliques of 200 nodes joined by
+    25 edges, negexp-limit(251) reaches the streak k = 5 (Oja, eta 3) and the
+    identity transform needs at least 3x as many steps (run against the
+    capped budget 3 s + 500, as the criterion does for mu-EG)."""
+    sp = _sp()
+    g = _clique_clusters(sp)
+    gt = sp.graph_ground_truth(g)
+
+    def streak(t, steps, every):
+        cfg = sp.SolverConfig(solver="oja", k=5, eta=3.0, steps=steps, eval_every=every, seed=11)
+        return sp.run_solver(g, t, cfg, ground_truth=gt, stop_on_targets=True,
+                             record_timing=False).steps_to_streak
+
+    s251 = streak(sp.SpectralTransform("negexp-limit", 251), 20_000, 25)
+    assert s251 is not None
+    cap = 3 * s251 + 500
+    s_id = streak(sp.SpectralTransform("identity"), cap, 25)
+    assert s_id is None or s_id >= 3 * s251, (s_id, s251)
