@@ -207,7 +207,7 @@ int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, floa
  * around the Gram; state in HBM/L2).  V (n x k) is updated in place; flag
  * bit 0 is set when a column's norm vanishes (rank collapse,
  * solvers.py:136-143), bit 1 when a tagged wait timed out (a bug, never
- * expected); SPED_ERR_UNSUPPORTED for k > 32 or > 64 terms.  `nnz` =
+ * expected); SPED_ERR_UNSUPPORTED for k > 32 or > 256 terms.  `nnz` =
  * indptr[n] (host copy, sizes the launch); `workspace` of at least
  * sped_persistent_workspace_bytes(n, k) bytes, ZEROED before its first use
  * and kept across launches (two fp32 and two tagged n x k blocks, Gram

@@ -35,7 +35,8 @@
 //
 // 2 (or 3) grid barriers per step: Gram partials, [partials reduce,] update;
 // the T - 1 barriers between terms of the barrier version are gone
-// (config 1: 62 -> 50 us/step, config 2: 91 -> 72 us/step).
+// (config 1: 62 -> 50 us/step, config 2: 91 -> 72 us/step).  Up to 256 terms
+// (negexp-limit(251), the reference's high-degree transform).
 //
 // Same arithmetic as the multi-kernel path (spmm.cu term schedule; mu-EG in
 // Gram form, solvers.py:121-144 / SURVEY §8a; zero-norm columns flagged for
@@ -70,7 +71,7 @@ namespace sped {
 namespace {
 
 constexpr int PT_MAX_K = 32;
-constexpr int PT_MAX_TERMS = 64;
+constexpr int PT_MAX_TERMS = 256;  // term coefficients ride in the kernel parameters (3 KB)
 constexpr int PT_DYN_BYTES = 180 * 1024;  // dynamic smem: own rows + CSR slice
 constexpr int PT_NT = 512;                // threads per CTA
 #ifndef PT_REDUNDANT_MAX

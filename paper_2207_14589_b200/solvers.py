@@ -426,7 +426,7 @@ def persistent_solver_eligible(op, k: int, solver: str) -> bool:
     term)."""
     if not (solver == "mu-eg" and isinstance(op, TransformedOperator)
             and op.transform.is_polynomial and k <= 32 and op.n * k <= PERSISTENT_MAX_NK
-            and op.n_terms <= 64):
+            and op.n_terms <= 256):
         return False
     return op.laplacian.max_row_nnz <= 512
 

@@ -368,7 +368,8 @@ def test_persistent_solver_vs_reference(cuda, golden, name, mode, kind, ell, k):
 @pytest.mark.parametrize("graph,mode,kind,ell,eta,k", [
     ("cfg2", "normalized", "negexp-limit", 17, 1.0, 16),
     ("sbm20k", "normalized", "negexp-taylor", 12, 0.1, 32),
-    ("sbm20k", "unnormalized", "negexp-limit", 9, 0.3, 7)])
+    ("sbm20k", "unnormalized", "negexp-limit", 9, 0.3, 7),
+    ("sbm20k", "normalized", "negexp-limit", 151, 0.5, 8)])  # > 64 terms in the parameters
 def test_persistent_solver_multi_cta(cuda, graph, mode, kind, ell, eta, k):
     """K7 on graphs spread over every SM (config 2's 10^4-node grid; a 2x10^4
     node SBM with stored normalized values / implicit unit weights, odd k):
