@@ -19,7 +19,7 @@ from paper_2207_14589_b200 import generators as G, graph as GR  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--hot", type=float, nargs="*", default=[0.7])
+    ap.add_argument("--hot", type=float, nargs="*", default=[GR.HOT_FRACTION])
     ap.add_argument("--reorder", nargs="*", default=["auto"])
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--kind", default="negexp-taylor")
