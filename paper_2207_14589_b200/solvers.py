@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .arrays import as_device_block, from_device_block, is_device_array
+from .arrays import as_device_block, from_device_block
 from .graph import Graph
 from .metrics import GroundTruth, eigenvector_streak, graph_ground_truth, subspace_error
 from .sampling import EdgeBatchOracle

@@ -12,8 +12,6 @@ reference's thread count, never its result, and is accepted and ignored.
 
 from __future__ import annotations
 
-import ctypes
-import math
 from dataclasses import dataclass
 
 import numpy as np
