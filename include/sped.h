@@ -213,6 +213,16 @@ int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t with_m, floa
  * and kept across launches (two fp32 and two tagged n x k blocks, Gram
  * partials, the tag base). */
 int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* bytes);
+/* As sped_persistent_mueg, for oja_step (solvers.py:114-118): W = V + eta
+ * p(L)V orthonormalised by CholQR2 (two Gram / Cholesky / R^{-1} rounds, the
+ * MGS of _orthonormalize, solvers.py:84-102); flag set when a Cholesky pivot
+ * is not positive (rank collapse). */
+int sped_persistent_oja(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
+                        const int32_t* indices, const float* values, int32_t n_terms,
+                        const double* alpha, const double* beta, const double* gamma,
+                        double w0_scale, double lam_f, double s_final, double eta, int32_t steps,
+                        float* V, int32_t* flag, void* workspace, int64_t workspace_bytes,
+                        sped_stream_t stream);
 int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
                          const int32_t* indices, const float* values, int32_t n_terms, const double* alpha,
                          const double* beta, const double* gamma, double w0_scale,

@@ -57,6 +57,8 @@ SIGNATURES = {
     "sped_persistent_workspace_bytes": (C.c_int, [_i32, _i32, _p]),
     "sped_persistent_mueg": (C.c_int, [_i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64,
                                        _f64, _f64, _i32, _p, _p, _p, _i64, _p]),
+    "sped_persistent_oja": (C.c_int, [_i32, _i32, _i64, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64,
+                                      _f64, _f64, _i32, _p, _p, _p, _i64, _p]),
     "sped_walk_index_workspace_bytes": (_i64, [_i64, _i64]),
     "sped_walk_index_build": (C.c_int, [_i64, _i64, _p, _p, _p, _p, _p, _p, _i64, _p]),
     "sped_walk_workspace_bytes": (_i64, [_i64, _i32, _i64]),

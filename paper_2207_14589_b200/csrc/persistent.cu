@@ -158,7 +158,59 @@ __device__ __forceinline__ int row_lower_bound(const int32_t* indptr, int n, int
   return lo;
 }
 
+// Cholesky of the k x k fp64 Gram G (upper R, G = R^T R) and T = R^{-1}
+// (upper), CTA-wide; R lives in Rw (k x k fp64 scratch), T goes out as fp32.
+// Same arithmetic as oja_coeffs_kernel (solver.cu).  Returns nonzero when a
+// pivot is not positive (rank collapse; the host re-randomises).
 template <int PT_THREADS>
+__device__ int cta_chol_inverse(int k, const double* G, double* Rw, float* T) {
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < k * k; e += PT_THREADS) Rw[e] = G[e];
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      double djj = Rw[j * k + j];
+      for (int q = 0; q < j; ++q) djj -= Rw[q * k + j] * Rw[q * k + j];
+      if (!(djj > 1e-24)) {
+        bad = 1;
+        djj = 1.0;
+      }
+      Rw[j * k + j] = sqrt(djj);
+    }
+    __syncthreads();
+    const double rjj = Rw[j * k + j];
+    for (int l = j + 1 + tid; l < k; l += PT_THREADS) {
+      double v = Rw[j * k + l];
+      for (int q = 0; q < j; ++q) v -= Rw[q * k + j] * Rw[q * k + l];
+      Rw[j * k + l] = v / rjj;
+    }
+    __syncthreads();
+  }
+  // back substitution per column l; T[i][l] (i < l) parked at Rw[l][i]
+  for (int l = tid; l < k; l += PT_THREADS) {
+    const double tll = 1.0 / Rw[l * k + l];
+    for (int i = l - 1; i >= 0; --i) {
+      double acc = -Rw[i * k + l] * tll;
+      for (int q = i + 1; q < l; ++q) acc -= Rw[i * k + q] * Rw[l * k + q];
+      Rw[l * k + i] = acc / Rw[i * k + i];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += PT_THREADS) {
+    const int i = e / k, l = e % k;
+    T[e] = (float)(i == l ? 1.0 / Rw[i * k + i] : (i < l ? Rw[l * k + i] : 0.0));
+  }
+  __syncthreads();
+  return bad;
+}
+
+// OJA = false: mu-EigenGame steps (solvers.py:121-144, Gram form);
+// OJA = true: oja_step (solvers.py:114-118) with the MGS as CholQR2 -- W =
+// X + eta M, then twice: Gram of the own rows -> all-CTA sum -> Cholesky ->
+// rows times R^{-1}.
+template <int PT_THREADS, bool OJA>
 __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -355,6 +407,97 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
     float* Xn = (X == a.V) ? a.XB : a.V;  // X' goes to the other float buffer
     __syncthreads();                      // own rows of M complete
 
+    if constexpr (OJA) {
+      // W = X + eta M over the own rows, in place of M (smem or Mb)
+      float* Wb = resident ? sM : M;
+      float* W1b = resident ? sXn : Xn;
+      const int64_t wo = resident ? 0 : i0;  // element offset of own row 0
+      for (int i = tid; i < nr * k; i += PT_THREADS) {
+        const float xv = resident ? sX[i] : __ldcg(X + i0 + i);
+        const float mv = resident ? sM[i] : __ldcg(M + i0 + i);
+        Wb[wo + i] = fmaf(eta_f, mv, xv);
+      }
+      __syncthreads();
+      const int nSo = k * (k + 1) / 2;
+      const int parts_o = max(1, PT_THREADS / nSo), per_pass_o = PT_THREADS / parts_o;
+      const int passes_o = (nSo + per_pass_o - 1) / per_pass_o;
+      const bool redundant_o = (int64_t)nb * nSo <= PT_REDUNDANT_MAX;
+      for (int cq = 0; cq < 2; ++cq) {
+        const float* Bsrc = cq == 0 ? Wb : W1b;   // block whose Gram is taken
+        float* Bdst = cq == 0 ? W1b : Wb;         // block times R^{-1}
+        // Gram partial of the own rows (upper triangle, fixed order)
+        double acc[PT_MAX_PASSES];
+#pragma unroll
+        for (int q = 0; q < PT_MAX_PASSES; ++q) acc[q] = 0.0;
+        for (int pass = 0; pass < passes_o; ++pass) {
+          const int e = pass * per_pass_o + tid / parts_o, q = tid % parts_o;
+          double sum = 0.0;
+          if (tid < per_pass_o * parts_o && e < nSo) {
+            int ca, cb;
+            entry_cols(e, k, nSo, 0, ca, cb);
+            for (int r = q; r < nr; r += parts_o) {
+              const float pa = resident ? Bsrc[r * k + ca] : __ldcg(Bsrc + wo + r * k + ca);
+              const float pb = resident ? Bsrc[r * k + cb] : __ldcg(Bsrc + wo + r * k + cb);
+              sum += (double)pa * (double)pb;
+            }
+          }
+          red[tid] = sum;
+          __syncthreads();
+          if (tid < per_pass_o) {
+            double t2 = 0.0;
+            for (int qq = 0; qq < parts_o; ++qq) t2 += red[tid * parts_o + qq];
+            acc[pass] += t2;
+          }
+          __syncthreads();
+        }
+        for (int pass = 0; pass < passes_o; ++pass) {
+          const int e = pass * per_pass_o + tid;
+          if (tid < per_pass_o && e < nSo) a.partials[(size_t)b * nSo + e] = acc[pass];
+        }
+        grid.sync();
+        // sum the partials in CTA order into Gs (symmetric S)
+        if (redundant_o) {
+          for (int e = tid; e < nSo; e += PT_THREADS) {
+            double sum = 0.0;
+            for (int q = 0; q < nb; ++q) sum += __ldcg(a.partials + (size_t)q * nSo + e);
+            put_gram(Gs, e, k, nSo, 0, sum);
+          }
+        } else {
+          const int gw = b * (PT_THREADS / 32) + warp;
+          const int nwarps = nb * (PT_THREADS / 32);
+          for (int e = gw; e < nSo; e += nwarps) {
+            double sum = 0.0;
+            for (int q = lane; q < nb; q += 32) sum += __ldcg(a.partials + (size_t)q * nSo + e);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off);
+            if (lane == 0) a.G[e] = sum;
+          }
+          grid.sync();
+          for (int e = tid; e < nSo; e += PT_THREADS) put_gram(Gs, e, k, nSo, 0, __ldcg(a.G + e));
+        }
+        __syncthreads();
+        if (cta_chol_inverse<PT_THREADS>(k, Gs, Ad, Acoef) && b == 0 && tid == 0)
+          atomicExch(a.flag, 1);
+        // rows times R^{-1} (upper): Bdst[r][c] = sum_{q <= c} Bsrc[r][q] T[q][c]
+        for (int i = tid; i < nr * k; i += PT_THREADS) {
+          const int r = i / k, c = i - r * k;
+          float o = 0.f;
+          for (int q = 0; q <= c; ++q) {
+            const float bv = resident ? Bsrc[r * k + q] : __ldcg(Bsrc + wo + r * k + q);
+            o = fmaf(bv, Acoef[q * k + c], o);
+          }
+          Bdst[wo + i] = o;
+        }
+        __syncthreads();
+        if (cq == 0) grid.sync();  // the partials buffer is reused by pass 2
+      }
+      // X' = Wb (own rows) -> Xn (global) and the resident copy
+      for (int i = tid; i < nr * k; i += PT_THREADS) {
+        const float o = resident ? Wb[i] : __ldcg(Wb + wo + i);
+        Xn[i0 + i] = o;
+        if (resident) sXn[i] = o;
+      }
+    } else {
     // ---- Gram partials over own rows (fp64 accumulation, fixed order) ------
     {
       double acc[PT_MAX_PASSES];
@@ -488,6 +631,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
       Xn[i] = o;
       if (resident) sXn[i - i0] = o;
     }
+    }
     X = Xn;
     {
       float* tmp = sX;
@@ -542,12 +686,12 @@ extern "C" int sped_persistent_workspace_bytes(int32_t n, int32_t k, int64_t* by
   return SPED_OK;
 }
 
-extern "C" int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
-                                    const int32_t* indices, const float* values, int32_t n_terms,
-                                    const double* alpha, const double* beta, const double* gamma,
-                                    double w0_scale, double lam_f, double s_final, double eta,
-                                    int32_t steps, float* V, int32_t* flag, void* workspace,
-                                    int64_t workspace_bytes, sped_stream_t stream) {
+static int persistent_run(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
+                          const int32_t* indices, const float* values, int32_t n_terms,
+                          const double* alpha, const double* beta, const double* gamma,
+                          double w0_scale, double lam_f, double s_final, double eta,
+                          int32_t steps, float* V, int32_t* flag, void* workspace,
+                          int64_t workspace_bytes, sped_stream_t stream, bool oja) {
   SPED_CHECK_ARG(n >= 1 && k >= 1 && nnz >= 0 && V && flag && indptr && indices && workspace &&
                      steps >= 0,
                  "bad persistent_mueg arguments");
@@ -569,10 +713,13 @@ extern "C" int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int
   const int rw = 32 / (slots * k);
   const int sms = num_sms();
   constexpr int nt = PT_NT;
-  const void* fn = (const void*)persistent_mueg_kernel<PT_NT>;
+  const void* fn = oja ? (const void*)persistent_mueg_kernel<PT_NT, true>
+                       : (const void*)persistent_mueg_kernel<PT_NT, false>;
   static bool attr = false;
   if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT>,
+    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
+    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
     attr = true;
   }
@@ -620,4 +767,26 @@ extern "C" int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int
   SPED_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(nt), args, PT_DYN_BYTES,
                                         as_stream(stream)));
   return SPED_OK;
+}
+
+extern "C" int sped_persistent_mueg(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
+                                    const int32_t* indices, const float* values, int32_t n_terms,
+                                    const double* alpha, const double* beta, const double* gamma,
+                                    double w0_scale, double lam_f, double s_final, double eta,
+                                    int32_t steps, float* V, int32_t* flag, void* workspace,
+                                    int64_t workspace_bytes, sped_stream_t stream) {
+  return persistent_run(n, k, nnz, indptr, indices, values, n_terms, alpha, beta, gamma, w0_scale,
+                        lam_f, s_final, eta, steps, V, flag, workspace, workspace_bytes, stream,
+                        false);
+}
+
+extern "C" int sped_persistent_oja(int32_t n, int32_t k, int64_t nnz, const int32_t* indptr,
+                                   const int32_t* indices, const float* values, int32_t n_terms,
+                                   const double* alpha, const double* beta, const double* gamma,
+                                   double w0_scale, double lam_f, double s_final, double eta,
+                                   int32_t steps, float* V, int32_t* flag, void* workspace,
+                                   int64_t workspace_bytes, sped_stream_t stream) {
+  return persistent_run(n, k, nnz, indptr, indices, values, n_terms, alpha, beta, gamma, w0_scale,
+                        lam_f, s_final, eta, steps, V, flag, workspace, workspace_bytes, stream,
+                        true);
 }

@@ -419,12 +419,12 @@ PERSISTENT_MAX_NK = 1 << 22
 
 
 def persistent_solver_eligible(op, k: int, solver: str) -> bool:
-    """Graphs small enough that a mu-EG step is launch bound run whole steps
-    inside one grid-resident launch (sped_persistent_mueg, K7): polynomial
-    transforms, k <= 32, n*k <= 4M, no row longer than 512 nonzeros (one
-    thread per output entry walks its row, so a hub row would serialise the
-    term)."""
-    if not (solver == "mu-eg" and isinstance(op, TransformedOperator)
+    """Graphs small enough that a solver step is launch bound run whole steps
+    inside one grid-resident launch (sped_persistent_mueg / _oja, K7):
+    polynomial transforms, k <= 32, n*k <= 4M, no row longer than 512
+    nonzeros (one thread per output entry walks its row, so a hub row would
+    serialise the term)."""
+    if not (solver in ("mu-eg", "oja") and isinstance(op, TransformedOperator)
             and op.transform.is_polynomial and k <= 32 and op.n * k <= PERSISTENT_MAX_NK
             and op.n_terms <= 256):
         return False
@@ -432,10 +432,13 @@ def persistent_solver_eligible(op, k: int, solver: str) -> bool:
 
 
 class _PersistentStepper:
-    """Many whole mu-EG steps per cooperative launch (K7)."""
+    """Many whole mu-EG (or Oja) steps per cooperative launch (K7)."""
 
-    def __init__(self, op: TransformedOperator, eta: float, V0: torch.Tensor):
-        self.op, self.eta = op, eta
+    def __init__(self, op: TransformedOperator, eta: float, V0: torch.Tensor,
+                 solver: str = "mu-eg"):
+        if solver not in ("mu-eg", "oja"):
+            raise ValueError(f"persistent solver: unknown solver {solver!r}")
+        self.op, self.eta, self.solver = op, eta, solver
         self.V_ = V0.clone().contiguous()
         k = int(V0.shape[1])
         self.ws = StepWorkspace(op.n, k, V0.device)
@@ -455,14 +458,12 @@ class _PersistentStepper:
         lib = _lib.load()
         lap = self.op.laplacian
         nt, al, be, ga, w0, lf, s = self._coef
-        rc = lib.sped_persistent_mueg(lap.n, int(self.V_.shape[1]), int(lap.nnz),
-                                      _lib.ptr(lap.indptr),
-                                      _lib.ptr(lap.indices), _lib.ptr(lap.values), nt, al, be,
-                                      ga, w0, lf, s, float(self.eta), int(m),
-                                      _lib.ptr(self.V_), _lib.ptr(self.ws.flag),
-                                      _lib.ptr(self.scratch), self.scratch.numel(),
-                                      _lib.stream_ptr(self.V_.device))
-        _lib.check(rc, "sped_persistent_mueg")
+        fn = lib.sped_persistent_oja if self.solver == "oja" else lib.sped_persistent_mueg
+        rc = fn(lap.n, int(self.V_.shape[1]), int(lap.nnz), _lib.ptr(lap.indptr),
+                _lib.ptr(lap.indices), _lib.ptr(lap.values), nt, al, be, ga, w0, lf, s,
+                float(self.eta), int(m), _lib.ptr(self.V_), _lib.ptr(self.ws.flag),
+                _lib.ptr(self.scratch), self.scratch.numel(), _lib.stream_ptr(self.V_.device))
+        _lib.check(rc, "sped_persistent_" + self.solver.replace("-", ""))
 
     def step(self):
         self.advance(1)
@@ -547,7 +548,7 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
         persistent = (persistent_solver_eligible(op, config.k, config.solver)
                       if use_persistent_kernel is None else use_persistent_kernel)
         if persistent:
-            stepper = _PersistentStepper(op, config.eta, V)
+            stepper = _PersistentStepper(op, config.eta, V, config.solver)
         else:
             stepper = _GraphStepper(op, config.solver, config.eta, V)
         t = 0

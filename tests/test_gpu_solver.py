@@ -247,9 +247,15 @@ def test_run_solver_cuda_graph_equals_eager(cuda, golden):
     assert rel_fro(d.V.cpu().numpy(), b.V.cpu().numpy()) <= 1e-5
     assert torch.equal(d.V, e.V)
     cfg = sp.SolverConfig(solver="oja", k=10, eta=0.1, steps=40, eval_every=20, seed=1)
-    a = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=True)
+    a = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=True,
+                      use_persistent_kernel=False)
     b = sp.run_solver(g, t, cfg, record_timing=False, use_cuda_graphs=False)
     assert torch.equal(a.V, b.V)
+    # the grid-resident Oja (K7, CholQR2 in-kernel; the default here)
+    d = sp.run_solver(g, t, cfg, record_timing=False)
+    e = sp.run_solver(g, t, cfg, record_timing=False, use_persistent_kernel=True)
+    assert rel_fro(d.V.cpu().numpy(), b.V.cpu().numpy()) <= 1e-5
+    assert torch.equal(d.V, e.V)
 
 
 def test_reference_solver_accepts_device_operator(cuda, golden):
@@ -514,3 +520,45 @@ def test_persistent_solver_tiny(cuda, golden, k, kind, ell):
     got = op.laplacian.from_internal(st.V).cpu().numpy()
     assert rel_fro(got, V) <= 1e-4
     assert not st.ws.take_flag()
+
+
+
+@pytest.mark.parametrize("graph,mode,kind,ell,eta,k", [
+    ("cfg1", "unnormalized", "negexp-limit", 13, 0.1, 10),
+    ("cfg2", "normalized", "negexp-limit", 17, 1.0, 16),
+    ("sbm20k", "normalized", "negexp-taylor", 12, 0.5, 32)])
+def test_persistent_oja_vs_oracle(cuda, golden, graph, mode, kind, ell, eta, k):
+    """K7 Oja (sped_persistent_oja: CholQR2 inside the grid-resident launch)
+    over 20 steps against the oracle's fp64 oja_step (MGS, solvers.py:114-118)
+    and the multi-kernel path; bit-reproducible run to run."""
+    sp = _sp()
+    from paper_2207_14589_b200 import generators as G
+    from paper_2207_14589_b200.solvers import (_GraphStepper, _PersistentStepper,
+                                               persistent_solver_eligible)
+    if graph == "cfg1":
+        g = _graph(golden, "cfg1")
+    else:
+        n, u, v, w = G.config_graph(2) if graph == "cfg2" else G.sbm_sparse(20000, 100, 20.0, 0.9)
+        g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
+    op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell), mode)
+    assert persistent_solver_eligible(op, k, "oja")
+    V0 = sp.init_state(g.n, k, 5).V
+    Vi = op.laplacian.to_internal(V0)
+    p = _PersistentStepper(op, eta, Vi, "oja")
+    q = _GraphStepper(op, "oja", eta, Vi)
+    p.advance(20)
+    q.advance(20)
+    Vp = op.laplacian.from_internal(p.V).cpu().numpy()
+    assert rel_fro(Vp, op.laplacian.from_internal(q.V).cpu().numpy()) <= 1e-4
+    csr = O.laplacian_csr(g.n, g.u, g.v, g.w, mode)
+    lam = O.choose_lambda_star(kind, O.lambda_upper(g.n, g.u, g.v, g.w, mode))
+    Vo = V0.cpu().numpy().astype(np.float64)
+    for _ in range(20):
+        Vo = O.oja_step(Vo, O.apply_transform(csr, kind, ell, 1e-6, lam, Vo), eta)
+    assert rel_fro(Vp, Vo) <= 1e-4
+    np.testing.assert_allclose(np.linalg.norm(Vp, axis=0), 1.0, atol=1e-5)
+    p2 = _PersistentStepper(op, eta, Vi, "oja")
+    for m in (7, 13):
+        p2.advance(m)
+    assert torch.equal(p.V, p2.V)
+    assert not p.ws.take_flag()

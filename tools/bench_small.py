@@ -47,6 +47,9 @@ def main():
         row["cuda_graph_us_per_step"] = per_step_us(_GraphStepper(op, "mu-eg", eta, Vi), args.steps)
         t0 = time.perf_counter()
         row["persistent_us_per_step"] = per_step_us(_PersistentStepper(op, eta, Vi), args.steps)
+        row["oja_cuda_graph_us_per_step"] = per_step_us(_GraphStepper(op, "oja", eta, Vi), args.steps)
+        row["oja_persistent_us_per_step"] = per_step_us(_PersistentStepper(op, eta, Vi, "oja"),
+                                                        args.steps)
         print(json.dumps(row), flush=True)
 
 
