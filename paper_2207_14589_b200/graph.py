@@ -52,6 +52,28 @@ def long_row_plan(nnz: int, sms: int = 148) -> tuple[int, int]:
     return thr, max(CHUNK_LEN, thr // 4)
 
 
+AUTO_DEVICE_MIN_EDGES = 1 << 20  # host edge lists this long canonicalise on the GPU
+
+
+def _auto_device_canonical(u) -> bool:
+    """Large host edge lists take the device canonicalisation (bit-identical
+    edges, the same ValueErrors) when a GPU and the library are present;
+    SPED_GRAPH_HOST=1 keeps numpy."""
+    try:
+        m = len(u)
+    except TypeError:
+        return False
+    if m < AUTO_DEVICE_MIN_EDGES or os.environ.get("SPED_GRAPH_HOST") == "1":
+        return False
+    if not torch.cuda.is_available():
+        return False
+    try:
+        _lib.load()
+    except Exception:  # library not built: the reference's host path
+        return False
+    return True
+
+
 class Graph:
     """Undirected weighted graph stored as a canonical edge list (u < v,
     lexsorted, unique, w > 0).  Same contract as ``specgap.Graph``."""
@@ -69,6 +91,8 @@ class Graph:
             return
         on_gpu = device is not None or any(isinstance(a, torch.Tensor) and a.is_cuda
                                            for a in (u, v, w))
+        if not on_gpu and _auto_device_canonical(u):
+            on_gpu, device = True, "cuda"
         if on_gpu:
             self._canonicalize_on_device(u, v, w, device)
             return

@@ -305,7 +305,7 @@ def test_scaled_normalized_path(cuda, k, monkeypatch):
     assert sp.LaplacianOperator(wg, "normalized").row_scale is None
 
 
-def test_device_canonicalisation_matches_host(cuda):
+def test_device_canonicalisation_matches_host(cuda, monkeypatch):
     """Graph(n, u, v, w, device=...) (sped_canonicalize_edges) returns the
     host path's canonical edge list bit for bit -- orientation, lexsort,
     dropped zero weights -- and raises the same ValueErrors in the same
@@ -326,8 +326,14 @@ def test_device_canonicalisation_matches_host(cuda):
         v = np.where(flip, lo, hi)[perm]
         w = rng.uniform(0.0, 2.0, lo.size)
         w[rng.random(lo.size) < 0.05] = 0.0  # dropped, as on the host
+        monkeypatch.setenv("SPED_GRAPH_HOST", "1")  # the numpy path, whatever m is
         host = sp.Graph(n, u, v, w)
+        monkeypatch.delenv("SPED_GRAPH_HOST")
+        assert not isinstance(host._u, torch.Tensor)
         dev = sp.Graph(n, u, v, w, device="cuda")
+        auto = sp.Graph(n, u, v, w)  # >= 2^20 edges: device path by default
+        assert isinstance(auto._u, torch.Tensor) == (u.size >= sp.graph.AUTO_DEVICE_MIN_EDGES)
+        assert np.array_equal(auto.u, host.u) and np.array_equal(auto.w, host.w)
         assert dev.m == host.m
         assert np.array_equal(dev.u, host.u) and np.array_equal(dev.v, host.v)
         assert np.array_equal(dev.w, host.w)

@@ -43,9 +43,12 @@ def main():
     L = sp.LaplacianOperator(gd, spec["mode"], reorder=None)
     torch.cuda.synchronize()
     t_csr = time.perf_counter() - t0
+    import os
+    os.environ["SPED_GRAPH_HOST"] = "1"  # the reference's numpy path
     t0 = time.perf_counter()
     gh = sp.Graph(n, uh, vh, wh)
     t_host = time.perf_counter() - t0
+    del os.environ["SPED_GRAPH_HOST"]
     same = (np.array_equal(gh.u, gd.u) and np.array_equal(gh.v, gd.v)
             and np.array_equal(gh.w, gd.w))
     print(json.dumps({"config": spec["name"], "n": n, "m": int(gh.m),
