@@ -17,12 +17,15 @@
  *                              (ell x LaplacianOperator.matvec   graph.py:205-211)
  *   sped_edge_batch_poly_apply make_stochastic_oracle identity   solvers.py:166-178
  *                              (+ restated per-term composition)
- *   sped_gram / sped_mueg_coeffs / sped_block_update
+ *   sped_csr_term_split        one term of the apply on a row shard (own-column
+ *                              pass overlapping the halo exchange)
+ *   sped_gram_mueg / sped_mueg_coeffs / sped_block_update
  *                              mu_eg_step                        solvers.py:121-144
- *   sped_persistent_mueg
- *                              run_solver's step loop (mu-eg)    solvers.py:227-292
- *                              (whole steps per launch)          solvers.py:121-144
- *   sped_oja_coeffs (+ gram/update)  oja_step + _orthonormalize  solvers.py:84-118
+ *   sped_persistent_mueg / sped_persistent_oja
+ *                              run_solver's step loop            solvers.py:227-292
+ *                              (whole steps per launch)          solvers.py:114-144
+ *   sped_gram / sped_oja_coeffs (+ update)
+ *                              oja_step + _orthonormalize        solvers.py:84-118
  *   sped_pcg64_integers        Generator(PCG64).integers(0,m,B)  solvers.py:171
  *   sped_kmeans_*              kmeans_cluster                    metrics.py:143-176
  *   sped_walk_index_build / sped_walk_poly_estimate
