@@ -197,3 +197,18 @@ def test_product_does_not_import_oracle():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_bench_max_angle_matches_scipy():
+    """bench.max_angle (the time-to-angle criterion, truth factored once)
+    equals scipy's largest principal angle -- the oracle's definition --
+    from 1e-6 rad to pi/2, numpy path."""
+    import scipy.linalg as sla
+    import bench
+    rng = np.random.default_rng(3)
+    n, k = 400, 6
+    Q = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    for eps in (1e-6, 1e-3, 0.1, 1.0, 10.0):
+        V = Q @ rng.standard_normal((k, k)) + eps * rng.standard_normal((n, k))
+        ref = float(np.max(sla.subspace_angles(V, Q)))
+        assert abs(bench.max_angle(V, Q) - ref) <= 1e-9 + 1e-7 * ref
