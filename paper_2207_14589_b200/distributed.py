@@ -227,7 +227,7 @@ class SplitCSR:
         self.indices = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int32)).to(device)
         self.values = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(device)
         self.long_threshold, self.chunk_len = long_threshold, chunk_len
-        self.n_chunks, self.chunk_desc, self.tickets = _plan_chunks(
+        self.n_chunks, self.chunk_desc = _plan_chunks(
             self.n, self.nnz, self.indptr, long_threshold, chunk_len, device)
         self._segments = {}
 
@@ -244,10 +244,12 @@ class SplitCSR:
         nseg, seg = self.segments(k)
         partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=E.device)
                     if self.n_chunks else None)
+        tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=E.device)
+                   if self.n_chunks else None)
         rc = lib.sped_csr_term_split(
             self.n, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
             self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
-            _lib.ptr(partials), _lib.ptr(self.tickets if self.n_chunks else None), seg, nseg,
+            _lib.ptr(partials), _lib.ptr(tickets), seg, nseg,
             _lib.ptr(x_own), _lib.ptr(E), _lib.ptr(partial_in), int(raw_out), _lib.ptr(out),
             float(alpha), float(beta), float(gamma), float(w0), float(lam_f), float(s_final),
             _lib.stream_ptr(E.device))
@@ -255,7 +257,8 @@ class SplitCSR:
 
 
 def _plan_chunks(n, nnz, indptr_dev, long_threshold, chunk_len, device):
-    """Long-row chunk plan (sped_spmm_plan) of a CSR: (n_chunks, desc, tickets)."""
+    """Long-row chunk plan (sped_spmm_plan) of a CSR: (n_chunks, desc).  The
+    arrival tickets are allocated zeroed per call (thread safety)."""
     import ctypes as C
     lib = _lib.load()
     maxc = int(lib.sped_spmm_plan_max_chunks(n, nnz, long_threshold, chunk_len))
@@ -266,8 +269,7 @@ def _plan_chunks(n, nnz, indptr_dev, long_threshold, chunk_len, device):
     _lib.check(rc, "sped_spmm_plan")
     n_chunks = int(nch.value)
     chunk_desc = desc[: max(4 * n_chunks, 4)].clone() if n_chunks else None
-    tickets = torch.zeros(max(n_chunks, 1), dtype=torch.int32, device=device)
-    return n_chunks, chunk_desc, tickets
+    return n_chunks, chunk_desc
 
 
 def split_local_csr(indptr: np.ndarray, local_indices: np.ndarray, values, n_own: int):
@@ -333,7 +335,7 @@ class ShardedLaplacian:
         self._plan_chunks()
 
     def _plan_chunks(self):
-        self.n_chunks, self.chunk_desc, self.tickets = _plan_chunks(
+        self.n_chunks, self.chunk_desc = _plan_chunks(
             self.n_own, self.nnz_local, self.indptr, self.long_threshold, self.chunk_len,
             self.device)
 
@@ -375,10 +377,12 @@ class ShardedLaplacian:
         nseg, seg = self.segments(k)
         partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=self.device)
                     if self.n_chunks else None)
+        tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=self.device)
+                   if self.n_chunks else None)
         rc = lib.sped_csr_poly_apply(
             self.n_own, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
             self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
-            _lib.ptr(partials), _lib.ptr(self.tickets if self.n_chunks else None), seg, nseg,
+            _lib.ptr(partials), _lib.ptr(tickets), seg, nseg,
             self.n_own + self.plan.n_halo, None, _lib.ptr(x_own), _lib.ptr(E),
             None, None, _lib.ptr(out), 1, _lib.dbl_array([alpha]), _lib.dbl_array([beta]),
             _lib.dbl_array([gamma]), float(w0), float(lam_f), float(s_final),

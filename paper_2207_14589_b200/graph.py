@@ -436,8 +436,7 @@ class LaplacianOperator:
         self.n_chunks = int(nch.value)
         self.n_long_rows = int(nlong.value)
         self.chunk_desc = desc[: max(4 * self.n_chunks, 4)].clone() if self.n_chunks else None
-        self._tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=self.device)
-                         if self.n_chunks else None)
+
 
     @property
     def reordered(self) -> bool:
@@ -522,14 +521,18 @@ class LaplacianOperator:
             out = torch.empty_like(xd)
         wa = torch.empty_like(xd) if nt >= 2 else None
         wb = torch.empty_like(xd) if nt >= 3 else None
+        # per-call chunk scratch (partial rows and arrival tickets), so one
+        # operator can be applied from several threads / streams at once
         partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=self.device)
                     if self.n_chunks else None)
+        tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=self.device)
+                   if self.n_chunks else None)
         nseg, seg = self.segments(k)
         with torch.cuda.device(self.device):
             rc = lib.sped_csr_poly_apply(
                 n, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
                 self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
-                _lib.ptr(partials), _lib.ptr(self._tickets), seg, nseg, self.hot_rows(k),
+                _lib.ptr(partials), _lib.ptr(tickets), seg, nseg, self.hot_rows(k),
                 _lib.ptr(self.row_scale), _lib.ptr(xd), None, _lib.ptr(wa), _lib.ptr(wb),
                 _lib.ptr(out), nt,
                 _lib.dbl_array(alpha), _lib.dbl_array(beta), _lib.dbl_array(gamma), float(w0),

@@ -355,3 +355,39 @@ def test_device_canonicalisation_matches_host(cuda, monkeypatch):
             else:
                 with pytest.raises(ValueError, match=msg):
                     sp.Graph(5, u, v, w, **kw)
+
+
+def test_operator_shared_across_threads(cuda):
+    """The reference's operators are immutable and safe to share across
+    threads (transforms.py:207-208): two host threads applying one
+    relabelled operator (hub chunks in play) on their own streams get the
+    single-thread result bit for bit."""
+    import threading
+    import torch
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.chung_lu(200_000, cap=20000.0, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    L = sp.LaplacianOperator(g, "normalized", long_threshold=256, chunk_len=128)
+    assert L.n_chunks > 0
+    op = sp.TransformedOperator(L, sp.SpectralTransform("negexp-limit", 9), 0.0, 2.0)
+    xs = [torch.randn((n, 32), device="cuda", generator=torch.Generator(device="cuda").manual_seed(s))
+          for s in (1, 2)]
+    ref = [op.apply_internal(x) for x in xs]
+    torch.cuda.synchronize()
+    got = [None, None]
+
+    def work(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(20):
+                y = op.apply_internal(xs[i])
+            s.synchronize()
+            got[i] = y
+    ts = [threading.Thread(target=work, args=(i,)) for i in (0, 1)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in (0, 1):
+        assert torch.equal(got[i], ref[i])
