@@ -212,3 +212,27 @@ def test_bench_max_angle_matches_scipy():
         V = Q @ rng.standard_normal((k, k)) + eps * rng.standard_normal((n, k))
         ref = float(np.max(sla.subspace_angles(V, Q)))
         assert abs(bench.max_angle(V, Q) - ref) <= 1e-9 + 1e-7 * ref
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the reference's CPU algorithm, host
+    cores) prints one JSON line with the driver's keys; runs on CPU."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference",
+                        "--scale", "0.01", "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
