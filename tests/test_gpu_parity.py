@@ -391,3 +391,31 @@ def test_operator_shared_across_threads(cuda):
         t.join()
     for i in (0, 1):
         assert torch.equal(got[i], ref[i])
+
+
+def test_bench_sped_arm_contract(cuda):
+    """`bench.py` (default arm, scaled-down graph) prints one JSON line with
+    the driver's keys plus roofline / cpu_baseline / e2e / gpu_launches /
+    clocks, and W >= 3 warm-up steps."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--scale", "0.02", "--steps", "3",
+                        "--warmup", "3", "--cpu-seconds", "1", "--no-extra"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3
+    rf = d["roofline"]
+    assert rf["bound"] in ("hbm", "tensor") and 0 < rf["frac"] < 1.5 and rf["peak"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0 and d["cpu_baseline"]["cores"] >= 1
+    assert "workload" in d["config"]
