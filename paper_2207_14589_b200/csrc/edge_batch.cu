@@ -23,6 +23,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
+#include <initializer_list>
 
 #include "sped_common.cuh"
 
@@ -79,6 +81,7 @@ struct BatchArgs {
   float* wout;
   float alpha, beta, gamma, lamf, sfin;  // beta already includes m/B
   int flags;   // bit0 alpha, bit1 gamma, bit2 final, bit3 lamf
+  int spare_per_sm;  // resident blocks per SM left free (the concurrent sort)
 };
 
 template <int LPR, int CPL, bool VEC>
@@ -208,7 +211,8 @@ void launch_rows(const BatchArgs& a, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_row_kernel<LPR, CPL, VEC>, 256, 0);
     if (per_sm < 1) per_sm = 1;
   }
-  const int64_t blocks = std::min<int64_t>((a.n + 7) / 8, (int64_t)num_sms() * per_sm);
+  const int64_t blocks = std::min<int64_t>(
+      (a.n + 7) / 8, (int64_t)num_sms() * std::max(1, per_sm - a.spare_per_sm));
   batch_row_kernel<LPR, CPL, VEC><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(a);
 }
 
@@ -279,12 +283,27 @@ BatchWs batch_ws_layout(char* base, int64_t n, int64_t B) {
 int launch_axpby(int64_t count, double a, const float* x, double b, const float* y, float* out,
                  cudaStream_t s);
 
+// Per-device side stream for the record/sort stage (created once; the
+// stochastic oracle is single-threaded by contract, it carries its RNG).
+static cudaStream_t batch_side_stream() {
+  static cudaStream_t st[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  if (!st[dev] && cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    st[dev] = nullptr;
+  }
+  return st[dev];
+}
+
 }  // namespace sped
 
 using namespace sped;
 
+// two record / sort sets: term t+1's records are built and sorted (side
+// stream) while term t's row sweep runs
 extern "C" int64_t sped_edge_batch_workspace_bytes(int64_t n, int64_t B) {
-  return (int64_t)batch_ws_layout(nullptr, n, std::max<int64_t>(B, 1)).bytes;
+  return 2 * (int64_t)align256(batch_ws_layout(nullptr, n, std::max<int64_t>(B, 1)).bytes) + 256;
 }
 
 extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
@@ -307,27 +326,71 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
   if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0_scale, x, 0.0, nullptr, out, s);
   SPED_CHECK_ARG(m > 0 && indices && epos && batch && workspace, "null graph/batch array");
   char* base = (char*)(((uintptr_t)workspace + 255) & ~uintptr_t(255));
-  BatchWs ws = batch_ws_layout(base, n, B);
-  SPED_CHECK_ARG(workspace_bytes >= (int64_t)ws.bytes, "edge batch workspace too small");
+  BatchWs wsv[2];
+  wsv[0] = batch_ws_layout(base, n, B);
+  wsv[1] = batch_ws_layout(base + align256(wsv[0].bytes), n, B);
+  SPED_CHECK_ARG(workspace_bytes >= (int64_t)(2 * align256(wsv[0].bytes)),
+                 "edge batch workspace too small");
   const double scale = (double)m / (double)B;
   const int32_t slabs = (k + 127) / 128;
   const int64_t R = 2 * B;
   int end_bit = 1;
   while (end_bit < 31 && ((int64_t)1 << end_bit) <= n) ++end_bit;  // keys in [0, n]
+  // Pipeline: the records + stable sort + run starts of term t+1 (side
+  // stream, double-buffered workspace) overlap the row sweep of term t; the
+  // sweep fills the SMs (SPED_STO_SPARE=j leaves j block slots per SM free
+  // for the side stream; 1, 2, 4 measured slower).  SPED_STO_OVERLAP=0
+  // runs everything in order on `s`.  Same kernels, same order of summation:
+  // the result does not depend on the overlap.
+  static const bool overlap_env = [] {
+    const char* e = getenv("SPED_STO_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  static const int spare_env = [] {
+    const char* e = getenv("SPED_STO_SPARE");
+    return e ? atoi(e) : 0;
+  }();
+  cudaStream_t s2 = (overlap_env && n_terms > 1) ? batch_side_stream() : nullptr;
+  const bool overlap = s2 != nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ready[2] = {nullptr, nullptr},
+              freed[2] = {nullptr, nullptr};
+  if (overlap) {
+    for (cudaEvent_t* e : {&ev_fork, &ev_join, &ready[0], &ready[1], &freed[0], &freed[1]})
+      SPED_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    SPED_CUDA(cudaEventRecord(ev_fork, s));
+    SPED_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
+  }
+  cudaStream_t sp = overlap ? s2 : s;  // the record/sort stream
+  auto prep = [&](int32_t t) -> int {
+    BatchWs& w = wsv[t & 1];
+    if (overlap && t >= 2) SPED_CUDA(cudaStreamWaitEvent(sp, freed[t & 1], 0));
+    records_kernel<<<grid_for(B, 256), 256, 0, sp>>>(B, n, batch + (int64_t)t * B, epos, erow,
+                                                     indices, edge_w, w.kin, w.vin);
+    SPED_LAUNCH_CHECK();
+    size_t tb = w.tmp_bytes;
+    // stable: a row's records keep sample order -> fixed summation order
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.kin, w.kout, w.vin, w.vout, (int)R, 0,
+                                              end_bit, sp));
+    row_starts_kernel<<<grid_for(R + 1, 256), 256, 0, sp>>>(R, n, w.kout, w.start);
+    SPED_LAUNCH_CHECK();
+    if (overlap) SPED_CUDA(cudaEventRecord(ready[t & 1], sp));
+    return SPED_OK;
+  };
+  int rc0 = prep(0);
+  if (rc0 != SPED_OK) return rc0;
   const float* cur = w_init ? w_init : x;
   for (int32_t t = 0; t < n_terms; ++t) {
     const bool final = (t == n_terms - 1);
     float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);
     SPED_CHECK_ARG(dst != nullptr, "scratch buffer for term %d is NULL", t);
-    records_kernel<<<grid_for(B, 256), 256, 0, s>>>(B, n, batch + (int64_t)t * B, epos, erow,
-                                                    indices, edge_w, ws.kin, ws.vin);
-    SPED_LAUNCH_CHECK();
-    size_t tb = ws.tmp_bytes;
-    // stable: a row's records keep sample order -> fixed summation order
-    SPED_CUDA(cub::DeviceRadixSort::SortPairs(ws.tmp, tb, ws.kin, ws.kout, ws.vin, ws.vout,
-                                              (int)R, 0, end_bit, s));
-    row_starts_kernel<<<grid_for(R + 1, 256), 256, 0, s>>>(R, n, ws.kout, ws.start);
-    SPED_LAUNCH_CHECK();
+    if (t + 1 < n_terms) {
+      if (overlap) {
+        int rc = prep(t + 1);
+        if (rc != SPED_OK) return rc;
+      }
+    }
+    if (overlap) SPED_CUDA(cudaStreamWaitEvent(s, ready[t & 1], 0));
+    const BatchWs& ws = wsv[t & 1];
     const double sc = (t == 0) ? w0_scale : 1.0;
     for (int32_t sl = 0; sl < slabs; ++sl) {
       const int32_t c0 = sl * 128;
@@ -348,13 +411,25 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
       a.sfin = (float)s_final;
       a.flags = (alpha[t] != 0.0 ? 1 : 0) | (gamma[t] != 0.0 ? 2 : 0) | (final ? 4 : 0) |
                 (lam_f != 0.0 ? 8 : 0);
+      a.spare_per_sm = (overlap && !final) ? spare_env : 0;
       const bool aligned = (k % 4 == 0) &&
                            ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(cur) |
                              reinterpret_cast<uintptr_t>(dst)) % 16 == 0);
       int rc = launch_batch_slab(a, aligned, s);
       if (rc != SPED_OK) return rc;
     }
+    if (overlap) SPED_CUDA(cudaEventRecord(freed[t & 1], s));
+    if (!overlap && t + 1 < n_terms) {
+      int rc = prep(t + 1);
+      if (rc != SPED_OK) return rc;
+    }
     cur = dst;
+  }
+  if (overlap) {
+    SPED_CUDA(cudaEventRecord(ev_join, sp));
+    SPED_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    for (cudaEvent_t e : {ev_fork, ev_join, ready[0], ready[1], freed[0], freed[1]})
+      cudaEventDestroy(e);  // released once the recorded work completes
   }
   return SPED_OK;
 }

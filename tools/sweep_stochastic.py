@@ -4,6 +4,7 @@ device PCG64 draw of ell*B edge ids + the per-term batch kernels.
     python tools/sweep_stochastic.py --config 3
 """
 import argparse
+import hashlib
 import json
 import sys
 from pathlib import Path
@@ -29,6 +30,7 @@ def main():
     t = sp.SpectralTransform("negexp-limit", ell + 1)
     op = sp.make_reversed_operator(g, t, spec["mode"], device=dev)
     orc = sp.make_stochastic_oracle(op, B, seed=7)
+    torch.manual_seed(0)
     X = torch.randn((n, k), device=dev)
     nt = op.n_terms
     for _ in range(2):
@@ -40,7 +42,7 @@ def main():
         ev[0].record()
         batch = orc.draw(nt * B)
         ev[1].record()
-        orc.apply_internal(X, batch=batch)
+        Y = orc.apply_internal(X, batch=batch)
         ev[2].record()
         torch.cuda.synchronize()
         draw_ms += ev[0].elapsed_time(ev[1])
@@ -50,7 +52,10 @@ def main():
     print(json.dumps({"config": a.config, "n": n, "nnz": op.laplacian.nnz, "k": k, "terms": nt,
                       "batch": B, "draw_ms_per_apply": draw_ms, "apply_ms": apply_ms,
                       "ms_per_term": apply_ms / nt,
-                      "sampled_edges_k_per_s": nt * B * k / (apply_ms / 1e3)}), flush=True)
+                      "sampled_edges_k_per_s": nt * B * k / (apply_ms / 1e3),
+                      # bit pattern of the last apply (A/B builds must agree)
+                      "out_hash": hashlib.sha1(Y.cpu().numpy().tobytes()).hexdigest()[:16]}),
+          flush=True)
 
 
 if __name__ == "__main__":
