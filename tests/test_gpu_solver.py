@@ -173,6 +173,29 @@ def test_edge_batch_poly_vs_restated_oracle(cuda, kind, ell, k):
     assert torch.equal(oracle.apply_device(xd, batch=bd), oracle.apply_device(xd, batch=bd))
 
 
+@pytest.mark.parametrize("B", [31, 33, 700, 4000])
+def test_edge_batch_hub_runs_vs_restated_oracle(cuda, B):
+    """Rows whose record run spans several 32-record chunks of the sweep
+    (a star's hub) next to short runs (a path)."""
+    sp = _sp()
+    hub = [(0, j) for j in range(1, 301)]
+    tail = [(300 + j, 301 + j) for j in range(40)]
+    wts = np.linspace(0.5, 2.0, len(hub) + len(tail))
+    g = sp.Graph.from_edges(341, [(a, b, c) for (a, b), c in zip(hub + tail, wts)])
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 5))
+    oracle = sp.make_stochastic_oracle(op, B, seed=11)
+    x = np.random.default_rng(B).standard_normal((g.n, 8)).astype(np.float32).astype(np.float64)
+    y = oracle(x)
+    batch = oracle.last_batch.cpu().numpy().astype(np.int64)
+    batches = [batch[t * B:(t + 1) * B] for t in range(op.n_terms)]
+    ref = O.edge_batch_poly_apply(g.u, g.v, g.w, "negexp-limit", 5, 1e-6, op.lambda_star,
+                                  batches, x)
+    assert rel_fro(y, ref) <= 1e-5
+    xd = torch.as_tensor(x, dtype=torch.float32, device="cuda")
+    bd = oracle.last_batch
+    assert torch.equal(oracle.apply_device(xd, batch=bd), oracle.apply_device(xd, batch=bd))
+
+
 def test_edge_batch_unbiased_on_device(cuda):
     sp = _sp()
     g = sp.Graph.from_edges(3, [(0, 1), (1, 2)])
