@@ -173,6 +173,14 @@ int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr, const int32
  * may alias out / w_a / w_b.  Deterministic (sorted records, no float
  * atomics). */
 int64_t sped_edge_batch_workspace_bytes(int64_t n, int64_t B);
+/* Workspace for sorting all n_terms terms' records at once (one
+ * bandwidth-bound radix sort by (term, row) instead of n_terms small ones;
+ * same summation order, bit-identical output).  sped_edge_batch_poly_apply
+ * takes that path whenever workspace_bytes is at least this size and the
+ * keys fit in int32; otherwise it sorts per term, overlapping term t+1's
+ * sort with term t's sweep on a side stream.  SPED_STO_ALLTERMS=0 /
+ * SPED_STO_OVERLAP=0 switch either off. */
+int64_t sped_edge_batch_workspace_bytes_terms(int64_t n, int64_t B, int32_t n_terms);
 int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
                                const float* edge_w, const int32_t* epos, const int32_t* erow,
                                const int32_t* batch, int64_t B, void* workspace,

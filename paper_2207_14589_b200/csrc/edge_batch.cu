@@ -33,8 +33,10 @@ namespace {
 
 // one record per owned endpoint of each sampled edge: key = row, value =
 // (float weight bits << 32) | neighbour column (the entry's CSR column: the
-// node id, or the [own | halo] index of a row shard); unowned -> key n
-__global__ void records_kernel(int64_t B, int64_t n, const int32_t* __restrict__ batch,
+// node id, or the [own | halo] index of a row shard); unowned -> key n.
+// Records of several terms at once (total = terms * Bt): term t's keys are
+// offset by t * (n + 1).
+__global__ void records_kernel(int64_t B, int64_t Bt, int64_t n, const int32_t* __restrict__ batch,
                                const int32_t* __restrict__ epos, const int32_t* __restrict__ erow,
                                const int32_t* __restrict__ indices,
                                const float* __restrict__ edge_w, int32_t* __restrict__ keys,
@@ -55,7 +57,7 @@ __global__ void records_kernel(int64_t B, int64_t n, const int32_t* __restrict__
       row = erow ? erow[2 * e + s] : indices[s ? p0 : p1];
       val = ((uint64_t)__float_as_uint(we) << 32) | (uint32_t)indices[p];
     }
-    keys[2 * b + s] = row;
+    keys[2 * b + s] = row + (int32_t)((b / Bt) * (n + 1));
     vals[2 * b + s] = val;
   }
 }
@@ -255,9 +257,10 @@ struct BatchWs {
   size_t tmp_bytes, bytes;
 };
 
-BatchWs batch_ws_layout(char* base, int64_t n, int64_t B) {
+// T terms' records (T > 1: one sort for all of them)
+BatchWs batch_ws_layout(char* base, int64_t n, int64_t B, int64_t T = 1) {
   BatchWs w{};
-  const int64_t R = 2 * B;
+  const int64_t R = 2 * B * T;
   size_t off = 0;
   auto take = [&](size_t b) {
     char* p = base ? base + off : nullptr;
@@ -268,7 +271,7 @@ BatchWs batch_ws_layout(char* base, int64_t n, int64_t B) {
   w.kout = (int32_t*)take(sizeof(int32_t) * R);
   w.vin = (uint64_t*)take(sizeof(uint64_t) * R);
   w.vout = (uint64_t*)take(sizeof(uint64_t) * R);
-  w.start = (int32_t*)take(sizeof(int32_t) * (n + 2));
+  w.start = (int32_t*)take(sizeof(int32_t) * (T * (n + 1) + 1));
   size_t t = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t, (int32_t*)nullptr, (int32_t*)nullptr,
                                   (uint64_t*)nullptr, (uint64_t*)nullptr, (int)R);
@@ -306,6 +309,18 @@ extern "C" int64_t sped_edge_batch_workspace_bytes(int64_t n, int64_t B) {
   return 2 * (int64_t)align256(batch_ws_layout(nullptr, n, std::max<int64_t>(B, 1)).bytes) + 256;
 }
 
+// all terms' records sorted at once (one bandwidth-bound sort instead of
+// n_terms latency-bound ones) when the keys fit; else the per-term size
+static bool all_terms_fit(int64_t n, int64_t B, int64_t T) {
+  return T > 1 && 2 * B * T < INT32_MAX && T * (n + 1) < INT32_MAX;
+}
+extern "C" int64_t sped_edge_batch_workspace_bytes_terms(int64_t n, int64_t B, int32_t n_terms) {
+  const int64_t per = sped_edge_batch_workspace_bytes(n, B);
+  B = std::max<int64_t>(B, 1);
+  if (!all_terms_fit(n, B, n_terms)) return per;
+  return std::max<int64_t>(per, (int64_t)batch_ws_layout(nullptr, n, B, n_terms).bytes + 256);
+}
+
 extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
                                           const float* edge_w, const int32_t* epos,
                                           const int32_t* erow, const int32_t* batch, int64_t B,
@@ -333,6 +348,71 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
                  "edge batch workspace too small");
   const double scale = (double)m / (double)B;
   const int32_t slabs = (k + 127) / 128;
+  auto sweep = [&](int32_t t, const int32_t* start, const uint64_t* rec, const float* cur,
+                   float* dst, int spare) -> int {
+    const bool final = (t == n_terms - 1);
+    const double sc = (t == 0) ? w0_scale : 1.0;
+    for (int32_t sl = 0; sl < slabs; ++sl) {
+      const int32_t c0 = sl * 128;
+      BatchArgs a;
+      a.n = n;
+      a.k = min(128, k - c0);
+      a.ld = k;
+      a.start = start;
+      a.rec = rec;
+      a.x = x + c0;
+      a.win = cur + c0;
+      a.wout = dst + c0;
+      a.alpha = (float)alpha[t];
+      // est is built from the term input w_t = sc * (stored input)
+      a.beta = (float)(beta[t] * scale * sc);
+      a.gamma = (float)(gamma[t] * sc);
+      a.lamf = (float)lam_f;
+      a.sfin = (float)s_final;
+      a.flags = (alpha[t] != 0.0 ? 1 : 0) | (gamma[t] != 0.0 ? 2 : 0) | (final ? 4 : 0) |
+                (lam_f != 0.0 ? 8 : 0);
+      a.spare_per_sm = spare;
+      const bool aligned = (k % 4 == 0) &&
+                           ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(cur) |
+                             reinterpret_cast<uintptr_t>(dst)) % 16 == 0);
+      int rc = launch_batch_slab(a, aligned, s);
+      if (rc != SPED_OK) return rc;
+    }
+    return SPED_OK;
+  };
+  static const bool all_env = [] {
+    const char* e = getenv("SPED_STO_ALLTERMS");
+    return !(e && e[0] == '0');
+  }();
+  if (all_env && all_terms_fit(n, B, n_terms)) {
+    BatchWs wa = batch_ws_layout(base, n, B, n_terms);
+    if (workspace_bytes >= (int64_t)wa.bytes) {
+      // every term's records in one launch, one stable sort by (term, row)
+      // -- a row's records keep sample order, as in the per-term sort -- and
+      // the run starts of all terms; then the row sweeps
+      const int64_t RT = 2 * B * n_terms, keys = (int64_t)n_terms * (n + 1);
+      int eb = 1;
+      while (eb < 31 && ((int64_t)1 << eb) < keys) ++eb;  // keys in [0, T(n+1))
+      records_kernel<<<grid_for(B * n_terms, 256), 256, 0, s>>>(B * n_terms, B, n, batch, epos,
+                                                                erow, indices, edge_w, wa.kin,
+                                                                wa.vin);
+      SPED_LAUNCH_CHECK();
+      size_t tb = wa.tmp_bytes;
+      SPED_CUDA(cub::DeviceRadixSort::SortPairs(wa.tmp, tb, wa.kin, wa.kout, wa.vin, wa.vout,
+                                                (int)RT, 0, eb, s));
+      row_starts_kernel<<<grid_for(RT + 1, 256), 256, 0, s>>>(RT, keys, wa.kout, wa.start);
+      SPED_LAUNCH_CHECK();
+      const float* cur = w_init ? w_init : x;
+      for (int32_t t = 0; t < n_terms; ++t) {
+        float* dst = (t == n_terms - 1) ? out : ((t & 1) == 0 ? w_a : w_b);
+        SPED_CHECK_ARG(dst != nullptr, "scratch buffer for term %d is NULL", t);
+        int rc = sweep(t, wa.start + (int64_t)t * (n + 1), wa.vout, cur, dst, 0);
+        if (rc != SPED_OK) return rc;
+        cur = dst;
+      }
+      return SPED_OK;
+    }
+  }
   const int64_t R = 2 * B;
   int end_bit = 1;
   while (end_bit < 31 && ((int64_t)1 << end_bit) <= n) ++end_bit;  // keys in [0, n]
@@ -364,7 +444,7 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
   auto prep = [&](int32_t t) -> int {
     BatchWs& w = wsv[t & 1];
     if (overlap && t >= 2) SPED_CUDA(cudaStreamWaitEvent(sp, freed[t & 1], 0));
-    records_kernel<<<grid_for(B, 256), 256, 0, sp>>>(B, n, batch + (int64_t)t * B, epos, erow,
+    records_kernel<<<grid_for(B, 256), 256, 0, sp>>>(B, B, n, batch + (int64_t)t * B, epos, erow,
                                                      indices, edge_w, w.kin, w.vin);
     SPED_LAUNCH_CHECK();
     size_t tb = w.tmp_bytes;
@@ -391,33 +471,8 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
     }
     if (overlap) SPED_CUDA(cudaStreamWaitEvent(s, ready[t & 1], 0));
     const BatchWs& ws = wsv[t & 1];
-    const double sc = (t == 0) ? w0_scale : 1.0;
-    for (int32_t sl = 0; sl < slabs; ++sl) {
-      const int32_t c0 = sl * 128;
-      BatchArgs a;
-      a.n = n;
-      a.k = min(128, k - c0);
-      a.ld = k;
-      a.start = ws.start;
-      a.rec = ws.vout;
-      a.x = x + c0;
-      a.win = cur + c0;
-      a.wout = dst + c0;
-      a.alpha = (float)alpha[t];
-      // est is built from the term input w_t = sc * (stored input)
-      a.beta = (float)(beta[t] * scale * sc);
-      a.gamma = (float)(gamma[t] * sc);
-      a.lamf = (float)lam_f;
-      a.sfin = (float)s_final;
-      a.flags = (alpha[t] != 0.0 ? 1 : 0) | (gamma[t] != 0.0 ? 2 : 0) | (final ? 4 : 0) |
-                (lam_f != 0.0 ? 8 : 0);
-      a.spare_per_sm = (overlap && !final) ? spare_env : 0;
-      const bool aligned = (k % 4 == 0) &&
-                           ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(cur) |
-                             reinterpret_cast<uintptr_t>(dst)) % 16 == 0);
-      int rc = launch_batch_slab(a, aligned, s);
-      if (rc != SPED_OK) return rc;
-    }
+    int rc = sweep(t, ws.start, ws.vout, cur, dst, (overlap && !final) ? spare_env : 0);
+    if (rc != SPED_OK) return rc;
     if (overlap) SPED_CUDA(cudaEventRecord(freed[t & 1], s));
     if (!overlap && t + 1 < n_terms) {
       int rc = prep(t + 1);

@@ -124,7 +124,9 @@ class EdgeBatchOracle:
         self.device = lap.device
         self.m = lap.graph.m
         lib = _lib.load()
-        self.ws_bytes = int(lib.sped_edge_batch_workspace_bytes(lap.n, self.batch_size))
+        # room for every term's records (one sort per apply, not per term)
+        self.ws_bytes = int(lib.sped_edge_batch_workspace_bytes_terms(
+            lap.n, self.batch_size, max(int(op.n_terms), 1)))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.last_batch = None
 
