@@ -271,7 +271,7 @@ BatchWs batch_ws_layout(char* base, int64_t n, int64_t B, int64_t T = 1) {
   w.kout = (int32_t*)take(sizeof(int32_t) * R);
   w.vin = (uint64_t*)take(sizeof(uint64_t) * R);
   w.vout = (uint64_t*)take(sizeof(uint64_t) * R);
-  w.start = (int32_t*)take(sizeof(int32_t) * (T * (n + 1) + 1));
+  w.start = (int32_t*)take(sizeof(int32_t) * (T * (n + 1) + 4));  // <= 4 sort groups
   size_t t = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t, (int32_t*)nullptr, (int32_t*)nullptr,
                                   (uint64_t*)nullptr, (uint64_t*)nullptr, (int)R);
@@ -390,23 +390,54 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
       // every term's records in one launch, one stable sort by (term, row)
       // -- a row's records keep sample order, as in the per-term sort -- and
       // the run starts of all terms; then the row sweeps
-      const int64_t RT = 2 * B * n_terms, keys = (int64_t)n_terms * (n + 1);
-      int eb = 1;
-      while (eb < 31 && ((int64_t)1 << eb) < keys) ++eb;  // keys in [0, T(n+1))
-      records_kernel<<<grid_for(B * n_terms, 256), 256, 0, s>>>(B * n_terms, B, n, batch, epos,
-                                                                erow, indices, edge_w, wa.kin,
-                                                                wa.vin);
-      SPED_LAUNCH_CHECK();
-      size_t tb = wa.tmp_bytes;
-      SPED_CUDA(cub::DeviceRadixSort::SortPairs(wa.tmp, tb, wa.kin, wa.kout, wa.vin, wa.vout,
-                                                (int)RT, 0, eb, s));
-      row_starts_kernel<<<grid_for(RT + 1, 256), 256, 0, s>>>(RT, keys, wa.kout, wa.start);
-      SPED_LAUNCH_CHECK();
+      // Terms are split into G equal groups (one sort each) when that drops
+      // the key width to one fewer 8-bit onesweep pass and each group still
+      // holds >= 2^22 records (bandwidth-bound); SPED_STO_SPLIT=0: one group.
+      static const bool split_env = [] {
+        const char* e = getenv("SPED_STO_SPLIT");
+        return !(e && e[0] == '0');
+      }();
+      auto key_bits = [&](int64_t terms) {
+        int eb = 1;
+        while (eb < 31 && ((int64_t)1 << eb) < terms * (n + 1)) ++eb;  // keys in [0, T(n+1))
+        return eb;
+      };
+      int32_t G = 1;
+      if (split_env) {
+        const int passes1 = (key_bits(n_terms) + 7) / 8;
+        for (int32_t g = 2; g <= 4 && g <= n_terms; ++g) {
+          const int64_t tg = (n_terms + g - 1) / g;
+          if ((key_bits(tg) + 7) / 8 < passes1 && 2 * B * tg >= (int64_t(1) << 22)) {
+            G = g;
+            break;
+          }
+        }
+      }
+      const int32_t tper = (n_terms + G - 1) / G;
+      for (int32_t t0 = 0; t0 < n_terms; t0 += tper) {
+        const int32_t tn = min(tper, n_terms - t0);
+        const int64_t off = 2 * B * t0, RT = 2 * B * tn, keys = (int64_t)tn * (n + 1);
+        records_kernel<<<grid_for(B * tn, 256), 256, 0, s>>>(
+            B * tn, B, n, batch + (int64_t)t0 * B, epos, erow, indices, edge_w, wa.kin + off,
+            wa.vin + off);
+        SPED_LAUNCH_CHECK();
+        size_t tb = wa.tmp_bytes;
+        SPED_CUDA(cub::DeviceRadixSort::SortPairs(wa.tmp, tb, wa.kin + off, wa.kout + off,
+                                                  wa.vin + off, wa.vout + off, (int)RT, 0,
+                                                  key_bits(tn), s));
+        row_starts_kernel<<<grid_for(RT + 1, 256), 256, 0, s>>>(
+            RT, keys, wa.kout + off, wa.start + (int64_t)t0 * (n + 1) + (t0 / tper));
+        SPED_LAUNCH_CHECK();
+      }
       const float* cur = w_init ? w_init : x;
       for (int32_t t = 0; t < n_terms; ++t) {
         float* dst = (t == n_terms - 1) ? out : ((t & 1) == 0 ? w_a : w_b);
         SPED_CHECK_ARG(dst != nullptr, "scratch buffer for term %d is NULL", t);
-        int rc = sweep(t, wa.start + (int64_t)t * (n + 1), wa.vout, cur, dst, 0);
+        // group g's run starts follow the previous groups' (one extra end
+        // entry per group); positions are relative to the group's records
+        const int32_t g = t / tper;
+        int rc = sweep(t, wa.start + (int64_t)t * (n + 1) + g, wa.vout + 2 * B * (g * tper), cur,
+                       dst, 0);
         if (rc != SPED_OK) return rc;
         cur = dst;
       }
