@@ -196,6 +196,32 @@ def test_edge_batch_hub_runs_vs_restated_oracle(cuda, B):
     assert torch.equal(oracle.apply_device(xd, batch=bd), oracle.apply_device(xd, batch=bd))
 
 
+@pytest.mark.parametrize("k", [16, 200])
+def test_edge_batch_all_terms_sort_equals_per_term(cuda, k):
+    """The all-terms (grouped) sort and the per-term overlapped sorts -- the
+    path a workspace of sped_edge_batch_workspace_bytes(n, B) takes -- give
+    bit-identical output."""
+    sp = _sp()
+    from paper_2207_14589_b200 import _lib
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.lp_sbm(3000, 12, 20.0, 0.1, 7, 0.8)
+    g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 9))
+    orc = sp.make_stochastic_oracle(op, 4000, seed=5)
+    x = torch.randn((n, k), device="cuda", generator=torch.Generator("cuda").manual_seed(k))
+    y_all = orc.apply_internal(x).clone()
+    batch = orc.last_batch
+    per = int(_lib.load().sped_edge_batch_workspace_bytes(op.laplacian.n, 4000))
+    assert per < orc.ws_bytes
+    full = orc.ws_bytes
+    try:
+        orc.ws_bytes = per
+        y_per = orc.apply_internal(x, batch=batch)
+    finally:
+        orc.ws_bytes = full
+    assert torch.equal(y_all, y_per)
+
+
 def test_edge_batch_unbiased_on_device(cuda):
     sp = _sp()
     g = sp.Graph.from_edges(3, [(0, 1), (1, 2)])
