@@ -15,8 +15,8 @@ N > 1 (torchrun): rows are sharded across ranks (strong scaling: the same
 graph), halo rows exchanged per term over NCCL, one Gram all-reduce per step.
 
 ``--impl reference`` times the reference's CPU algorithm (the oracle port:
-scipy csr_matvecs, fp64) on all host cores, on a bounded row sample of the
-same workload.
+scipy csr_matvecs + numpy, fp64) on all host cores: whole mu-EG steps on the
+same graph (at most 3 timed steps; the line reports the steps it ran).
 """
 
 from __future__ import annotations
@@ -37,6 +37,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "p(L)V nnz*k/s (mu-EG step incl. Gram+update)"
 UNIT = "nnz*k/s"
+REF_MAX_STEPS = 3  # reference arm: whole host steps are ~10 s at config 4
 
 
 def parse():
@@ -47,7 +48,6 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["sped", "reference"], default="sped")
     ap.add_argument("--scale", type=float, default=1.0, help="node-count scale (debug only)")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
@@ -65,6 +65,41 @@ def cfg_spec(c):
 def transform_for(spec):
     import paper_2207_14589_b200 as sp
     return sp.SpectralTransform("negexp-taylor", spec["ell"])
+
+
+def workload_config(spec, cfg_index, n, m, nnz, world, eta):
+    """The ``config`` dict both arms print (identical keys and values)."""
+    return {"workload": f"{spec['name']} (BASELINE configs[{cfg_index - 1}])",
+            "n": n, "m": m, "nnz": nnz, "k": spec["k"], "mode": spec["mode"],
+            "transform": f"negexp-taylor({spec['ell']})", "terms": spec["ell"],
+            "solver": "mu-eg", "eta": eta,
+            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+            "l2": "inputs (V 4nk B, CSR) larger than the 126 MB L2; no flush"}
+
+
+def cpu_mueg_steps(n, u, v, w, mode, k, ell, eta, steps, warmup, threads, csr=None):
+    """Whole reference mu-EG steps on the host: ``MV = apply_transform(V)``
+    (transforms.py:229-262, negexp-taylor(ell): ell Horner terms of scipy
+    ``csr @ w`` in fp64, row blocks on ``threads`` threads) then
+    ``mu_eg_step`` (solvers.py:121-144, numpy/BLAS).  Returns (seconds per
+    step, steps timed, csr)."""
+    import oracle as O
+    if csr is None:
+        csr = O.laplacian_csr(n, u, v, w, mode)
+    lam = O.choose_lambda_star("negexp-taylor", O.lambda_upper(n, u, v, w, mode)
+                               if mode != "normalized" else 2.0)
+    rng = np.random.default_rng(1234)
+    V = rng.standard_normal((n, k))
+    V /= np.linalg.norm(V, axis=0)
+    for _ in range(warmup):
+        V = O.mu_eg_step(V, O.apply_transform(csr, "negexp-taylor", ell, 1e-6, lam, V,
+                                              threads=threads), eta)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        V = O.mu_eg_step(V, O.apply_transform(csr, "negexp-taylor", ell, 1e-6, lam, V,
+                                              threads=threads), eta)
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    return dt, steps, csr
 
 
 def bytes_per_term(n, nnz, k, stored_values, x_term, final_x):
@@ -155,47 +190,6 @@ def cpu_threads():
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
-
-
-def cpu_term_sample(n, u, v, w, mode, k, seconds, threads, alpha=1.0, beta=1.0):
-    """One p(L)V term (``w' = alpha*x + beta*L w``, the Horner term of
-    transforms.py:249-254) over a row sample of the CSR, fp64, scipy
-    csr_matvecs split over ``threads`` row blocks.  Rows are grown until one
-    term takes ~seconds/4; returns (nnz*k/s, description)."""
-    import oracle as O
-    from concurrent.futures import ThreadPoolExecutor
-    rng = np.random.default_rng(0)
-    W = rng.standard_normal((n, k))
-    rows = max(1000, min(n, 200_000))
-    while True:
-        csr = O.laplacian_csr_rows(n, u, v, w, mode, 0, rows)
-        X = W[:rows]
-        bounds = np.linspace(0, rows, threads + 1).astype(np.int64)
-        blocks = [csr[bounds[i]:bounds[i + 1]] for i in range(threads)]
-        out = np.empty((rows, k))
-
-        def term():
-            def work(i):
-                a, b = bounds[i], bounds[i + 1]
-                out[a:b] = alpha * X[a:b] + beta * (blocks[i] @ W)
-            with ThreadPoolExecutor(threads) as ex:
-                list(ex.map(work, range(threads)))
-
-        t0 = time.perf_counter()
-        term()
-        dt = time.perf_counter() - t0
-        if dt > seconds / 4 or rows == n:
-            break
-        rows = min(n, int(rows * max(2.0, (seconds / 4) / max(dt, 1e-3))))
-    reps = max(1, int(seconds / max(dt, 1e-3)))
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        term()
-    dt = (time.perf_counter() - t0) / reps
-    rate = csr.nnz * k / dt
-    desc = (f"one Horner term w'=x+L w over rows [0,{rows}) = {csr.nnz} nnz of the same CSR, "
-            f"k={k}, fp64 scipy csr_matvecs on {threads} threads, {reps} reps")
-    return rate, desc, dt, csr.nnz
 
 
 def max_angle(V, Qu):
@@ -380,7 +374,7 @@ def stochastic_line(cfg=3, reps=5):
     k, B = spec["k"], spec["batch"]
     t = sp.SpectralTransform("negexp-limit", spec["ell"] + 1)  # SURVEY 8d note (i)
     op = sp.make_reversed_operator(g, t, spec["mode"], device=dev)
-    orc = sp.make_stochastic_oracle(op, B, seed=7)
+    orc = sp.make_stochastic_oracle(op, B, seed=7, estimator="edge-batch")
     X = torch.randn((n, k), device=dev)
     nt = op.n_terms
     for _ in range(2):
@@ -583,11 +577,14 @@ def run_sped(args):
 
     cpu = None
     if rank == 0 and not sharded and not args.no_cpu:
-        uh, vh, wh = g.u, g.v, g.w
         thr = cpu_threads()
-        rate, desc, dt, snnz = cpu_term_sample(n, uh, vh, wh, mode, k, args.cpu_seconds, thr)
-        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port", "sample": desc,
-               "seconds_per_term": dt}
+        dt, nst, csr_h = cpu_mueg_steps(n, g.u, g.v, g.w, mode, k, ell, eta, 1, 0, thr)
+        cpu = {"value": n_terms * csr_h.nnz * k / dt, "unit": UNIT, "cores": thr, "kind": "port",
+               "sample": (f"1 whole mu-EG step of the reference algorithm on the same graph: "
+                          f"negexp-taylor({ell}) = {n_terms} fp64 scipy csr_matvecs terms over "
+                          f"all {n} rows ({csr_h.nnz} nnz), k={k}, {thr} threads, + mu_eg_step"),
+               "seconds_per_step": dt}
+        del csr_h
 
     conv = None
     if rank == 0 and not sharded and not args.no_cpu:
@@ -600,7 +597,7 @@ def run_sped(args):
     sto = None
     extra = None
     if rank == 0 and not sharded and not args.no_extra:
-        sto = stochastic_line(3)
+        sto = [stochastic_line(3), stochastic_line(5)]
         extra = [exact_step_line(3), exact_step_line(5)]
 
     if rank == 0:
@@ -609,13 +606,8 @@ def run_sped(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, BASELINE shape)",
-            "config": {"workload": f"{spec['name']} (BASELINE configs[{args.config - 1}])",
-                       "n": n, "m": g.m, "nnz": nnz, "k": k, "mode": mode,
-                       "transform": f"negexp-taylor({ell})", "terms": n_terms,
-                       "solver": "mu-eg", "eta": eta,
-                       "parallelism": f"row-shard x{world}" if sharded else "single GPU",
-                       "l2": "inputs (V 4nk B, CSR) larger than the 126 MB L2; no flush",
-                       "setup_s": setup_s},
+            "config": workload_config(spec, args.config, n, g.m, nnz, world, eta),
+            "setup_s": setup_s,
             "pLV_nnz_k_per_s": work * args.steps / (apply_ms / 1e3),
             "breakdown_ms_per_step": {"p(L)V": apply_ms / args.steps,
                                       "gram+coeffs+update": solve_ms / args.steps,
@@ -647,6 +639,12 @@ def run_sped(args):
 # ------------------------------------------------------------------------- reference arm
 
 def run_reference(args):
+    """The reference's own CPU algorithm on the box's host cores: whole mu-EG
+    steps (the oracle port of transforms.py:229-262 + solvers.py:121-144,
+    fp64, scipy csr_matvecs on all threads) on the SAME graph, k, transform
+    and eta as the GPU arm.  A step takes ~10 s at config 4, so at most
+    ``REF_MAX_STEPS`` timed steps and one warm-up step run; the line reports
+    the steps it actually ran (``steps_requested`` keeps --steps)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -654,22 +652,29 @@ def run_reference(args):
     import torch
     from paper_2207_14589_b200 import generators as G
     spec = cfg_spec(args.config)
-    k, mode = spec["k"], spec["mode"]
+    k, mode, ell = spec["k"], spec["mode"], spec["ell"]
+    eta = 0.1
     device = "cuda" if torch.cuda.is_available() else "cpu"
-    n, u, v, w = G.config_graph(args.config, device=device, scale=args.scale)  # input synthesis
+    # input synthesis only (the same seeded generator as the GPU arm)
+    n, u, v, w = G.config_graph(args.config, device=device, scale=args.scale)
     u, v, w = u.cpu().numpy(), v.cpu().numpy(), w.cpu().numpy()
     thr = cpu_threads()
-    budget = max(10.0, min(60.0, 4.0 * (args.steps + args.warmup)))
-    rate, desc, dt, snnz = cpu_term_sample(n, u, v, w, mode, k, budget, thr)
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
+    warm = min(args.warmup, 1)
+    dt, steps, csr = cpu_mueg_steps(n, u, v, w, mode, k, ell, eta, steps, warm, thr)
+    rate = ell * csr.nnz * k / dt
+    sample = (f"{steps} whole mu-EG steps (+{warm} warm-up): negexp-taylor({ell}) apply = "
+              f"{ell} Horner terms of fp64 scipy csr_matvecs over all {n} rows "
+              f"({csr.nnz} nnz), k={k}, on {thr} threads, then mu_eg_step (numpy/BLAS)")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * dt * spec["ell"], "higher_is_better": True,
+            "n_gpus": world, "steps": steps, "warmup": warm, "steps_requested": args.steps,
+            "warmup_requested": args.warmup, "extrapolated": False,
+            "ms_per_step": 1e3 * dt, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, BASELINE shape)",
-            "config": {"workload": f"{spec['name']} (BASELINE configs[{args.config - 1}])",
-                       "n": n, "m": int(u.size), "k": k, "mode": mode},
+            "config": workload_config(spec, args.config, n, int(u.size), int(csr.nnz), world, eta),
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
-                             "sample": desc},
+                             "sample": sample},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -244,32 +244,39 @@ def scalar_map(kind, lam, ell=None, epsilon=1e-6):
     raise AssertionError(kind)
 
 
-def apply_transform(csr, kind, ell, epsilon, lam_star, x):
+def apply_transform(csr, kind, ell, epsilon, lam_star, x, threads=1):
     """Reversed polynomial apply; restates ``TransformedOperator.apply``
-    (transforms.py:229-262) with ``L.matvec = csr @ w`` (graph.py:211)."""
+    (transforms.py:229-262) with ``L.matvec = csr @ w`` (graph.py:211).
+    ``threads > 1`` splits each ``csr @ w`` into row blocks on a thread pool
+    (``threaded_csr_matmul``: the same scipy kernel per row, so the same
+    fp64 result) for the full-size parity tests."""
     x = np.asarray(x, dtype=np.float64)
     if x.shape[0] != csr.shape[0]:
         raise ValueError("dimension mismatch in transformed matvec")
+
+    def L(w):
+        return csr @ w if threads <= 1 else threaded_csr_matmul(csr, w, threads)
+
     if kind == "identity":                                  # :241-242
-        return lam_star * x - csr @ x
+        return lam_star * x - L(x)
     if kind == "negexp-limit":                              # :243-248
         w = x.copy()
         inv = 1.0 / ell
         for _ in range(ell):
-            w -= inv * (csr @ w)
+            w -= inv * L(w)
         return lam_star * x + w
     if kind == "negexp-taylor":                             # :249-254
         c = [-((-1.0) ** i) / math.factorial(i) for i in range(ell + 1)]
         w = c[-1] * x
         for i in range(ell - 1, -1, -1):
-            w = c[i] * x + csr @ w
+            w = c[i] * x + L(w)
         return lam_star * x - w
     if kind == "log-taylor":                                # :255-262
         shift = epsilon - 1.0
         c = [0.0] + [(1.0 if i % 2 == 1 else -1.0) / i for i in range(1, ell + 1)]
         w = c[-1] * x
         for i in range(ell - 1, -1, -1):
-            w = c[i] * x + csr @ w + shift * w
+            w = c[i] * x + L(w) + shift * w
         return lam_star * x - w
     raise ValueError(f"{kind} is not a polynomial transform")
 
@@ -303,10 +310,23 @@ def draw_batches(rng: np.random.Generator, m: int, batch: int, count: int):
     return [rng.integers(0, m, size=batch) for _ in range(count)]
 
 
-def sampled_laplacian_apply(u, v, w, batch, x):
+def sampled_laplacian_apply(u, v, w, batch, x, threads=1):
     """Unscaled sampled-edge Laplacian product ``est`` of solvers.py:172-176:
-    ``diff = (x[u_b]-x[v_b])*w_b; est[u_b] += diff; est[v_b] -= diff``."""
+    ``diff = (x[u_b]-x[v_b])*w_b; est[u_b] += diff; est[v_b] -= diff``.
+
+    ``threads > 1`` (full-size tests): the same sum written as the sampled
+    Laplacian ``sum_b w_b (e_u - e_v)(e_u - e_v)^T`` in scipy CSR (duplicate
+    samples summed) times ``x`` on a thread pool -- equal to the ``np.add.at``
+    form up to fp64 summation order."""
     x = np.asarray(x, dtype=np.float64)
+    if threads > 1:
+        ub, vb = u[batch], v[batch]
+        wb = np.asarray(w, dtype=np.float64)[batch]
+        n = x.shape[0]
+        S = sp.coo_matrix((np.concatenate([wb, -wb, -wb, wb]),
+                           (np.concatenate([ub, ub, vb, vb]), np.concatenate([ub, vb, ub, vb]))),
+                          shape=(n, n)).tocsr()
+        return threaded_csr_matmul(S, x, threads)
     diff = (x[u[batch]] - x[v[batch]]) * (w[batch] if x.ndim == 1 else w[batch][:, None])
     est = np.zeros_like(x)
     np.add.at(est, u[batch], diff)
@@ -322,7 +342,7 @@ def identity_minibatch_apply(u, v, w, lam_star, batch, x):
     return lam_star * np.asarray(x, dtype=np.float64) - est
 
 
-def edge_batch_poly_apply(u, v, w, kind, ell, epsilon, lam_star, batches, x):
+def edge_batch_poly_apply(u, v, w, kind, ell, epsilon, lam_star, batches, x, threads=1):
     """RESTATED (no reference implementation): the reversed
     polynomial recurrence of transforms.py:241-262 with term t's ``L w``
     replaced by the unbiased minibatch estimate of solvers.py:171-177 drawn
@@ -337,7 +357,7 @@ def edge_batch_poly_apply(u, v, w, kind, ell, epsilon, lam_star, batches, x):
         return identity_minibatch_apply(u, v, w, lam_star, batches[0], x)
     cur = w0 * x
     for t in range(len(al)):
-        est = sampled_laplacian_apply(u, v, w, batches[t], cur) * (m / batches[t].size)
+        est = sampled_laplacian_apply(u, v, w, batches[t], cur, threads) * (m / batches[t].size)
         cur = al[t] * x + be[t] * est + ga[t] * cur
     return lam_f * x + s * cur
 

@@ -139,14 +139,7 @@ size_t gram_tc_workspace(int64_t n, int32_t k);
 int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, void* ws,
             cudaStream_t s, bool diag_q);
 
-static bool use_tc(int32_t k, bool with_m) {
-  static int force_simt = -1;
-  if (force_simt < 0) {
-    const char* e = getenv("SPED_GRAM_SIMT");
-    force_simt = (e && e[0] == '1') ? 1 : 0;
-  }
-  return !force_simt && gram_tc_supported(k, with_m);
-}
+static bool use_tc(int32_t k, bool with_m) { return gram_tc_supported(k, with_m); }
 
 }  // namespace sped
 

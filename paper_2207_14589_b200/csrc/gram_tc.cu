@@ -31,8 +31,6 @@
 // rows 0..127 x cols 0..255 (TMEM cols 0..255) and rows 128..255 x cols
 // 128..255 (TMEM cols 256..383).
 
-#include <cstdlib>
-
 #include "async_copy.cuh"
 #include "sped_common.cuh"
 #include "tcgen05.cuh"
@@ -42,34 +40,8 @@ namespace tc {
 
 using namespace ::sped::async;
 
-constexpr int THREADS = 128;
-
-
 constexpr int SBO_B = 272;   // column-group (8 MN) stride, bytes
 constexpr int LBO_B = 128;   // second 4-row K half, bytes
-
-template <int K2>
-struct Cfg {
-  static constexpr int NACC = (K2 == 64) ? 4 : (K2 == 128) ? 2 : 1;  // accumulator sets
-  static constexpr int SPLIT = (K2 == 64) ? 1024 : 512;              // rows per drain
-  static constexpr int KC = (K2 == 256) ? 32 : 64;                   // rows per chunk
-  static constexpr int NR = (K2 == 64) ? 3 : 2;                      // raw (bulk copy) stages
-  static constexpr int RAW_FLOATS = KC * K2;                         // KC rows of V then of M
-  static constexpr int KSTEP_FLOATS = (K2 / 8) * (SBO_B / 4);        // one 8-row K step
-  static constexpr int TILE_FLOATS = (KC / 8) * KSTEP_FLOATS;        // one of hi / lo
-  static constexpr int TMEM_COLS = (K2 == 64) ? 256 : (K2 == 128) ? 256 : 512;
-  static constexpr int SMEM = NR * RAW_FLOATS * 4 + 2 * 2 * TILE_FLOATS * 4 + 1024;
-  static constexpr int CPS = SPLIT / KC;                             // chunks per slice
-};
-
-template <int K2>
-__device__ __forceinline__ int kmaj_offset(int r, int c) {
-  // float offset of element (row r of the chunk, column c): K-major core
-  // matrices (8 columns x 4 rows), LBO between the 4-row halves, SBO between
-  // 8-column groups
-  return (r >> 3) * Cfg<K2>::KSTEP_FLOATS + ((r >> 2) & 1) * (LBO_B / 4) + (c >> 3) * (SBO_B / 4) +
-         (c & 7) * 4 + (r & 3);
-}
 
 template <int TC>  // TC = columns of the K-major tile
 __device__ __forceinline__ int kmaj_offset2(int r, int c) {
@@ -77,192 +49,6 @@ __device__ __forceinline__ int kmaj_offset2(int r, int c) {
          (c & 7) * 4 + (r & 3);
 }
 
-
-// Gram partials: one fp64 K2 x K2 block (upper triangle meaningful) per CTA.
-// 256 threads: all convert raw fp32 rows into the hi/lo K-major tiles;
-// thread 0 also issues the bulk copies (cp.async.bulk, NR chunks ahead) and
-// the MMAs; warps 0-3 drain TMEM (one TMEM lane quarter each).
-template <int K2>
-__global__ void __launch_bounds__(256, 1) gram_tc_kernel(int64_t n, int32_t k,
-                                                         const float* __restrict__ V,
-                                                         const float* __restrict__ M,
-                                                         double* __restrict__ partial,
-                                                         int64_t nslices) {
-  using C = Cfg<K2>;
-  constexpr int NT = 256;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  float* raw = reinterpret_cast<float*>(smem);
-  float* tiles = raw + C::NR * C::RAW_FLOATS;
-  __shared__ uint64_t full_bar[C::NR];
-  __shared__ uint64_t mma_bar[2];
-  __shared__ uint64_t done_bar;
-  __shared__ uint32_t tmem_base_sh;
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base_sh)),
-                 "r"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int i = 0; i < C::NR; ++i) mbar_init(&full_bar[i], 1);
-    mbar_init(&mma_bar[0], 1);
-    mbar_init(&mma_bar[1], 1);
-    mbar_init(&done_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  double* out = partial + (int64_t)blockIdx.x * K2 * K2;
-  for (int e = tid; e < K2 * K2; e += NT) out[e] = 0.0;
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_base_sh;
-
-  // chunks of this CTA: q = j*CPS + ch for its j-th slice
-  const int64_t my_slices = (nslices - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t nq = my_slices * C::CPS;
-  auto chunk_rows = [&](int64_t q, int64_t& r0) -> int {
-    const int64_t sl = blockIdx.x + (q / C::CPS) * gridDim.x;
-    r0 = sl * C::SPLIT + (q % C::CPS) * C::KC;
-    const int64_t v = n - r0;
-    return (int)(v < 0 ? 0 : (v > C::KC ? C::KC : v));
-  };
-  auto issue = [&](int64_t q) {
-    if (q >= nq) return;
-    const int rs = (int)(q % C::NR);
-    int64_t r0;
-    const int valid = chunk_rows(q, r0);
-    float* dst = raw + rs * C::RAW_FLOATS;
-    if (valid > 0) {
-      const uint32_t bytes = (uint32_t)valid * (uint32_t)k * 4u;
-      mbar_expect_tx(&full_bar[rs], 2 * bytes);
-      bulk_g2s(dst, V + r0 * k, bytes, &full_bar[rs]);
-      bulk_g2s(dst + C::KC * k, M + r0 * k, bytes, &full_bar[rs]);
-    } else {
-      mbar_arrive(&full_bar[rs]);
-    }
-  };
-  if (tid == 0)
-    for (int i = 0; i < C::NR; ++i) issue(i);
-
-  uint32_t mma_uses[2] = {0, 0};
-  uint32_t done_uses = 0;
-  constexpr uint32_t KSTEP_B = C::KSTEP_FLOATS * 4;
-  for (int64_t q = 0; q < nq; ++q) {
-    const int rs = (int)(q % C::NR);
-    const int ts = (int)(q & 1);
-    const int ch = (int)(q % C::CPS);
-    int64_t r0;
-    const int valid = chunk_rows(q, r0);
-    mbar_wait(&full_bar[rs], (uint32_t)((q / C::NR) & 1));
-    if (mma_uses[ts] > 0) mbar_wait(&mma_bar[ts], (mma_uses[ts] - 1) & 1);
-    float* hi = tiles + ts * (2 * C::TILE_FLOATS);
-    float* lo = hi + C::TILE_FLOATS;
-    const float* src = raw + rs * C::RAW_FLOATS;
-#pragma unroll 2
-    for (int f = tid; f < C::KC * (K2 / 4); f += NT) {
-      const int r = f / (K2 / 4);
-      const int c = (f % (K2 / 4)) * 4;
-      float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < valid)
-        z = *reinterpret_cast<const float4*>((c < k) ? (src + r * k + c)
-                                                     : (src + C::KC * k + r * k + (c - k)));
-      const float zz[4] = {z.x, z.y, z.z, z.w};
-      const int off = kmaj_offset<K2>(r, c);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t h = to_tf32(zz[j]);
-        hi[off + 4 * j] = __uint_as_float(h);
-        lo[off + 4 * j] = __uint_as_float(to_tf32(zz[j] - __uint_as_float(h)));
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      issue(q + C::NR);  // raw stage rs is consumed: refill it NR chunks ahead
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t hi_a = smem_u32(hi), lo_a = smem_u32(lo);
-#pragma unroll
-      for (int kb = 0; kb < C::KC / 8; ++kb) {
-        const int gk = ch * (C::KC / 8) + kb;              // K step within the slice
-        const uint32_t acc0 = (gk >= C::NACC) ? 1u : 0u;   // first use of this accumulator
-        const uint32_t tacc = tmem + (uint32_t)((gk % C::NACC) * K2);
-        if (K2 <= 128) {
-          constexpr uint32_t idesc = instr_desc_tf32(K2, K2);
-          const uint64_t dh = smem_desc(hi_a + kb * KSTEP_B, SBO_B, LBO_B);
-          const uint64_t dl = smem_desc(lo_a + kb * KSTEP_B, SBO_B, LBO_B);
-          mma_tf32(tacc, dh, dh, idesc, acc0);
-          mma_tf32(tacc, dh, dl, idesc, 1u);
-          mma_tf32(tacc, dl, dh, idesc, 1u);
-        } else {
-          constexpr uint32_t id0 = instr_desc_tf32(128, 256);
-          const uint64_t ah0 = smem_desc(hi_a + kb * KSTEP_B, SBO_B, LBO_B);
-          const uint64_t al0 = smem_desc(lo_a + kb * KSTEP_B, SBO_B, LBO_B);
-          mma_tf32(tmem, ah0, ah0, id0, acc0);
-          mma_tf32(tmem, ah0, al0, id0, 1u);
-          mma_tf32(tmem, al0, ah0, id0, 1u);
-          constexpr uint32_t id1 = instr_desc_tf32(128, 128);
-          const uint32_t goff = 16u * SBO_B;
-          const uint64_t ah1 = smem_desc(hi_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
-          const uint64_t al1 = smem_desc(lo_a + goff + kb * KSTEP_B, SBO_B, LBO_B);
-          mma_tf32(tmem + 256, ah1, ah1, id1, acc0);
-          mma_tf32(tmem + 256, ah1, al1, id1, 1u);
-          mma_tf32(tmem + 256, al1, ah1, id1, 1u);
-        }
-      }
-      mma_commit(&mma_bar[ts]);
-    }
-    mma_uses[ts] += 1;
-    if (ch == C::CPS - 1) {
-      // end of a slice: drain the accumulators into the fp64 partial
-      if (tid == 0) mma_commit(&done_bar);
-      mbar_wait(&done_bar, done_uses & 1);
-      done_uses += 1;
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (warp < 4) {
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-        const int64_t rows_in_slice = n - (r0 - (int64_t)ch * C::KC);
-        const int nk = (int)min((int64_t)C::NACC, (rows_in_slice + 7) / 8);
-        auto drain = [&](uint32_t tcol, int row, int col0, int ncols, bool ok) {
-          for (int c0 = 0; c0 < ncols; c0 += 16) {
-            double acc[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-            for (int a2 = 0; a2 < nk; ++a2) {
-              float v[16];
-              tmem_ld16(tmem + tcol + (uint32_t)(a2 * K2) + lane_base + c0, v);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) acc[i] += (double)v[i];
-            }
-            if (ok) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) out[row * K2 + col0 + c0 + i] += acc[i];
-            }
-          }
-        };
-        if (K2 == 64) {
-          drain(0, warp * 16 + lane, 0, K2, lane < 16);  // M=64: row m in lane m%16 + 32*(m/16)
-        } else if (K2 == 128) {
-          drain(0, warp * 32 + lane, 0, K2, true);
-        } else {
-          drain(0, warp * 32 + lane, 0, 256, true);
-          drain(256, 128 + warp * 32 + lane, 128, 128, true);
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncthreads();
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(C::TMEM_COLS));
-  }
-}
 
 // ---------------------------------------------------------------------------
 // v2 (K2 = 64, 128): warp-specialised pipeline, nothing CTA-synchronous in
@@ -623,7 +409,7 @@ __global__ void __launch_bounds__(Cfg2<K2, DQ>::NTHREADS, 1)
   }
 }
 
-// Sum the v2 partials (CTA order) into S / C / Q.
+// Sum the per-CTA partials (CTA order) into S / C / Q.
 __global__ void gram_tc2_reduce(int32_t k, int32_t nparts, const double* __restrict__ partial,
                                 double* __restrict__ G) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -646,58 +432,19 @@ template <int K2, bool DQ = false>
 int launch2(int64_t n, int32_t k, const float* V, const float* M, double* G, double* partial,
             cudaStream_t s) {
   using C = Cfg2<K2, DQ>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  const int rc = attr([]() -> int {
     SPED_CUDA(cudaFuncSetAttribute(gram_tc2_kernel<K2, DQ>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
-  }
+    return SPED_OK;
+  });
+  if (rc != SPED_OK) return rc;
   const int64_t nslices = (n + C::SPLIT - 1) / C::SPLIT;
   const unsigned grid = (unsigned)std::min<int64_t>(nslices, (int64_t)num_sms());
   gram_tc2_kernel<K2, DQ><<<grid, C::NTHREADS, C::SMEM, s>>>(n, k, V, M, partial, nslices);
   SPED_LAUNCH_CHECK();
   const int per = k * K2 + k * k;
   gram_tc2_reduce<<<(per + 255) / 256, 256, 0, s>>>(k, (int)grid, partial, G);
-  SPED_LAUNCH_CHECK();
-  return SPED_OK;
-}
-
-// Sum the per-CTA fp64 partials (CTA order) and scatter into S / C / Q.
-__global__ void gram_tc_reduce(int32_t k, int32_t K2, int64_t nslices,
-                               const double* __restrict__ partial, double* __restrict__ G) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= K2 * K2) return;
-  const int i = e / K2, j = e % K2;
-  if (j < i) return;
-  double s = 0.0;
-  for (int64_t sl = 0; sl < nslices; ++sl) s += partial[sl * K2 * K2 + e];
-  auto put = [&](int a, int b) {
-    if (a < k && b < k) G[a * k + b] = s;
-    else if (a < k) G[k * k + a * k + (b - k)] = s;
-    else if (b >= k) G[2 * k * k + (a - k) * k + (b - k)] = s;
-  };
-  put(i, j);
-  if (i != j) put(j, i);
-}
-
-template <int K2>
-constexpr int grid_per_sm() { return 1; }
-
-template <int K2>
-int launch(int64_t n, int32_t k, const float* V, const float* M, double* G, double* partial,
-           cudaStream_t s) {
-  using C = Cfg<K2>;
-  static bool attr = false;
-  if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(gram_tc_kernel<K2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   C::SMEM));
-    attr = true;
-  }
-  const int64_t nslices = (n + C::SPLIT - 1) / C::SPLIT;
-  const unsigned grid = (unsigned)std::min<int64_t>(nslices, (int64_t)num_sms() * grid_per_sm<K2>());
-  gram_tc_kernel<K2><<<grid, 256, C::SMEM, s>>>(n, k, V, M, partial, nslices);
-  SPED_LAUNCH_CHECK();
-  gram_tc_reduce<<<(K2 * K2 + 255) / 256, 256, 0, s>>>(k, K2, (int64_t)grid, partial, G);
   SPED_LAUNCH_CHECK();
   return SPED_OK;
 }
@@ -715,17 +462,10 @@ size_t gram_tc_workspace(int64_t n, int32_t k) {
 int gram_tc(int64_t n, int32_t k, const float* V, const float* M, double* G, void* ws,
             cudaStream_t s, bool diag_q) {
   double* partial = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
-  static const bool v1 = [] {
-    const char* e = getenv("SPED_GRAM_V1");
-    return e && e[0] == '1';
-  }();
   switch (k) {
-    case 32: return v1 ? tc::launch<64>(n, k, V, M, G, partial, s)
-                       : tc::launch2<64>(n, k, V, M, G, partial, s);
-    case 64: return v1 ? tc::launch<128>(n, k, V, M, G, partial, s)
-                       : tc::launch2<128>(n, k, V, M, G, partial, s);
+    case 32: return tc::launch2<64>(n, k, V, M, G, partial, s);
+    case 64: return tc::launch2<128>(n, k, V, M, G, partial, s);
     case 128:
-      if (v1) return tc::launch<256>(n, k, V, M, G, partial, s);
       return diag_q ? tc::launch2<256, true>(n, k, V, M, G, partial, s)
                     : tc::launch2<256>(n, k, V, M, G, partial, s);
     default: set_error("gram_tc: unsupported k=%d", k); return SPED_ERR_UNSUPPORTED;

@@ -715,13 +715,16 @@ static int persistent_run(int32_t n, int32_t k, int64_t nnz, const int32_t* indp
   constexpr int nt = PT_NT;
   const void* fn = oja ? (const void*)persistent_mueg_kernel<PT_NT, true>
                        : (const void*)persistent_mueg_kernel<PT_NT, false>;
-  static bool attr = false;
-  if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT, false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
-    SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
-    attr = true;
+  static PerDeviceOnce attr;  // per device: function attributes are per context
+  {
+    const int rc_ = attr([&]() -> int {
+      SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
+      SPED_CUDA(cudaFuncSetAttribute(persistent_mueg_kernel<PT_NT, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, PT_DYN_BYTES));
+      return SPED_OK;
+    });
+    if (rc_ != SPED_OK) return rc_;
   }
   int per_sm = 0;
   SPED_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, PT_DYN_BYTES));

@@ -442,14 +442,17 @@ int launch_v2(int64_t n, const float* P, const float* A, const float* M, const f
   const int tr = C::STAGE_BYTES / (K * 4 * (mode == 0 ? 1 : 2));
   const size_t smem = (size_t)C::NSTAGE * C::STAGE_BYTES;
   // register budget: A (and B) columns live in registers, so k = 64 with
-  // M*B (Oja) takes the v1 kernel
-  static bool attr = false;
-  if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if constexpr (K == 32)
-      SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  // M*B (Oja) takes the row-streaming kernel
+  static PerDeviceOnce attr;  // per device: function attributes are per context
+  {
+    const int rc_ = attr([&]() -> int {
+      SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if constexpr (K == 32)
+        SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      return SPED_OK;
+    });
+    if (rc_ != SPED_OK) return rc_;
   }
   const int64_t ntiles = (n + tr - 1) / tr;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * 2));
@@ -468,150 +471,22 @@ int launch_v2(int64_t n, const float* P, const float* A, const float* M, const f
   return SPED_OK;
 }
 
-// k = 128 update: A (64 KB) in shared memory; a warp computes an 8-row x
-// 128-column tile, lane l owning columns 4l..4l+3, so every float4 of A read
-// from shared memory feeds 8 rows x 4 columns of FMAs (FMA-issue bound).  P
-// (and M) stream through a two-stage cp.async.bulk ring (warp 8).  Modes 0/1
-// only (the M*B form of Oja would need 256 KB of shared memory).
-constexpr int U128_ROWS = 64;  // rows per stage (8 warps x 8 rows)
-
-template <int MODE>  // 0: P A; 1: P A + eta M; 2: P A + M B
-__global__ void __launch_bounds__(288, 1) block_update_k128(int64_t n, const float* __restrict__ P,
-                                                           const float* __restrict__ A,
-                                                           const float* __restrict__ M,
-                                                           const float* __restrict__ B, float eta,
-                                                           const float* __restrict__ scale,
-                                                           float* __restrict__ out) {
-  using namespace ::sped::async;
-  constexpr int K = 128, NS = 2, TR = U128_ROWS;
-  constexpr int STAGE = TR * K * (MODE == 0 ? 1 : 2);
-  extern __shared__ __align__(128) float sm[];
-  float* As = sm;                  // K x K
-  float* Bs = As + K * K;          // K x K (MODE 2)
-  float* stage = Bs + (MODE == 2 ? K * K : 0);
-  __shared__ uint64_t full[NS], empty[NS];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t ntiles = (n + TR - 1) / TR;
-  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  for (int e = tid; e < K * K / 4; e += blockDim.x) {
-    reinterpret_cast<float4*>(As)[e] = __ldg(reinterpret_cast<const float4*>(A) + e);
-    if (MODE == 2) reinterpret_cast<float4*>(Bs)[e] = __ldg(reinterpret_cast<const float4*>(B) + e);
-  }
-  if (tid == 0) {
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 256);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == 8) {
-    if (lane == 0) {
-      for (int64_t j = 0; j < my_tiles; ++j) {
-        const int st = (int)(j % NS);
-        if (j >= NS) mbar_wait(&empty[st], (uint32_t)(((j / NS) - 1) & 1));
-        const int64_t r0 = (blockIdx.x + j * gridDim.x) * (int64_t)TR;
-        const int rows = (int)min((int64_t)TR, n - r0);
-        const uint32_t bytes = (uint32_t)rows * K * 4u;
-        float* dst = stage + (size_t)st * STAGE;
-        mbar_expect_tx(&full[st], (MODE == 0 ? 1u : 2u) * bytes);
-        bulk_g2s(dst, P + r0 * K, bytes, &full[st]);
-        if (MODE != 0) bulk_g2s(dst + TR * K, M + r0 * K, bytes, &full[st]);
-      }
-    }
-    return;
-  }
-  float4 sc = make_float4(1.f, 1.f, 1.f, 1.f);
-  if (scale) sc = __ldg(reinterpret_cast<const float4*>(scale) + lane);
-  for (int64_t j = 0; j < my_tiles; ++j) {
-    const int st = (int)(j % NS);
-    const int64_t r0 = (blockIdx.x + j * gridDim.x) * (int64_t)TR;
-    const int rows = (int)min((int64_t)TR, n - r0);
-    mbar_wait(&full[st], (uint32_t)((j / NS) & 1));
-    const float* ps = stage + (size_t)st * STAGE;
-    const float* ms = ps + TR * K;
-    const int rbase = warp * 8;  // this warp's 8 rows of the stage
-    float acc[8][4];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
-    auto accumulate = [&](const float* X, const float* W) {
-#pragma unroll 2
-      for (int i4 = 0; i4 < K / 4; ++i4) {
-        float4 w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) w[q] = reinterpret_cast<const float4*>(W + (4 * i4 + q) * K)[lane];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const float4 x = reinterpret_cast<const float4*>(X + (rbase + r) * K)[i4];  // broadcast
-          const float xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            acc[r][0] = fmaf(xv[q], w[q].x, acc[r][0]);
-            acc[r][1] = fmaf(xv[q], w[q].y, acc[r][1]);
-            acc[r][2] = fmaf(xv[q], w[q].z, acc[r][2]);
-            acc[r][3] = fmaf(xv[q], w[q].w, acc[r][3]);
-          }
-        }
-      }
-    };
-    accumulate(ps, As);
-    if (MODE == 2) accumulate(ms, Bs);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (rbase + r < rows) {
-        float4 o = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
-        if (MODE == 1) {
-          const float4 mv = reinterpret_cast<const float4*>(ms + (rbase + r) * K)[lane];
-          o = make_float4(fmaf(eta, mv.x, o.x), fmaf(eta, mv.y, o.y), fmaf(eta, mv.z, o.z),
-                          fmaf(eta, mv.w, o.w));
-        }
-        o = make_float4(o.x * sc.x, o.y * sc.y, o.z * sc.z, o.w * sc.w);
-        __stcs(reinterpret_cast<float4*>(out + (r0 + rbase + r) * K) + lane, o);
-      }
-    }
-    mbar_arrive(&empty[st]);
-  }
-}
-
-int launch_k128(int64_t n, const float* P, const float* A, const float* M, const float* B,
-                float eta, const float* scale, float* out, cudaStream_t s) {
-  constexpr int K = 128;
-  const int mode = M ? (B ? 2 : 1) : 0;
-  auto smem_for = [](int md) {
-    return (size_t)4 * (K * K * (md == 2 ? 2 : 1) + 2 * U128_ROWS * K * (md == 0 ? 1 : 2));
-  };
-  static bool attr = false;
-  if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(block_update_k128<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(0)));
-    SPED_CUDA(cudaFuncSetAttribute(block_update_k128<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(1)));
-    attr = true;
-  }
-  const int64_t ntiles = (n + U128_ROWS - 1) / U128_ROWS;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms()));
-  switch (mode) {
-    case 0: block_update_k128<0><<<grid, 288, smem_for(0), s>>>(n, P, A, M, B, eta, scale, out); break;
-    case 1: block_update_k128<1><<<grid, 288, smem_for(1), s>>>(n, P, A, M, B, eta, scale, out); break;
-    default:  // M*B (Oja): A and B plus two stages exceed shared memory
-      set_error("update k128: M*B takes the v1 kernel");
-      return SPED_ERR_UNSUPPORTED;
-  }
-  SPED_LAUNCH_CHECK();
-  return SPED_OK;
-}
-
 template <int K>
 int launch_rows(int64_t n, const float* P, const float* A, const float* M, const float* B,
                 float eta, const float* scale, float* out, bool upper, cudaStream_t s) {
   const int64_t total = n * (K / 32);
   const size_t smem = sizeof(float) * K * K * (B ? 2 : 1);
-  static bool attr = false;
-  if (!attr) {
-    const int maxb = (int)(sizeof(float) * K * K * 2);
-    SPED_CUDA(cudaFuncSetAttribute(block_update_rows<K, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, maxb));
-    SPED_CUDA(cudaFuncSetAttribute(block_update_rows<K, false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, maxb));
-    attr = true;
+  static PerDeviceOnce attr;  // per device: function attributes are per context
+  {
+    const int rc_ = attr([&]() -> int {
+      const int maxb = (int)(sizeof(float) * K * K * 2);
+      SPED_CUDA(cudaFuncSetAttribute(block_update_rows<K, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, maxb));
+      SPED_CUDA(cudaFuncSetAttribute(block_update_rows<K, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, maxb));
+      return SPED_OK;
+    });
+    if (rc_ != SPED_OK) return rc_;
   }
   int per_sm = (int)((200 * 1024) / (smem + 1024));
   per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
@@ -654,11 +529,14 @@ int launch_update(int64_t n, const float* P, const float* A, const float* M, con
   constexpr int TR = 64;
   size_t smem = sizeof(float) * (K * K * (B ? 2 : 1) + TR * (K + 1) * ((M && B) ? 2 : 1));
   auto kern = block_update_kernel<K>;
-  static bool attr_set = false;  // once, so the launch is graph-capturable
-  if (!attr_set) {
-    SPED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(float) * (2 * K * K + 2 * TR * (K + 1)))));
-    attr_set = true;
+  static PerDeviceOnce attr_set;  // per device: function attributes are per context
+  {
+    const int rc_ = attr_set([&]() -> int {
+      SPED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(float) * (2 * K * K + 2 * TR * (K + 1)))));
+      return SPED_OK;
+    });
+    if (rc_ != SPED_OK) return rc_;
   }
   const int64_t ntiles = (n + TR - 1) / TR;
   int per_sm = (int)((220 * 1024) / smem);
@@ -694,11 +572,14 @@ extern "C" int sped_oja_coeffs(int32_t k, const double* G, double eta, int32_t w
   SPED_CHECK_ARG(k >= 1 && k <= 160 && G && T && flag, "bad oja_coeffs arguments (k <= 160)");
   cudaStream_t s = as_stream(stream);
   const size_t smem = sizeof(double) * (size_t)k * k;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SPED_CUDA(cudaFuncSetAttribute(oja_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * 160 * 160)));
-    attr_set = true;
+  static PerDeviceOnce attr_set;  // per device: function attributes are per context
+  {
+    const int rc_ = attr_set([&]() -> int {
+      SPED_CUDA(cudaFuncSetAttribute(oja_coeffs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * 160 * 160)));
+      return SPED_OK;
+    });
+    if (rc_ != SPED_OK) return rc_;
   }
   oja_coeffs_kernel<<<1, 256, smem, s>>>(k, G, eta, with_m, T, flag);
   SPED_LAUNCH_CHECK();
@@ -717,26 +598,15 @@ extern "C" int sped_block_update(int64_t n, int32_t k, const float* P, const flo
                         16) == 0;
   if (aligned) {
     const bool upper = (upper_flag != 0);
-    static const bool v1 = [] {
-      const char* e = getenv("SPED_UPDATE_V1");
-      return e && e[0] == '1';
-    }();
     switch (k) {
       case 16: return launch_update<16>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 32: return v1 ? launch_rows<32>(n, P, A, M, B, (float)eta, scale, out, upper, s)
-                         : launch_v2<32>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 64: return (v1 || (M && B)) ? launch_rows<64>(n, P, A, M, B, (float)eta, scale, out, upper, s)
-                                       : launch_v2<64>(n, P, A, M, B, (float)eta, scale, out, s);
-      case 128: {
-        // tcgen05 3xTF32 GEMM (update_tc.cu); SPED_UPDATE_TC=0 keeps the SIMT kernel
-        static const bool tc = [] {
-          const char* e = getenv("SPED_UPDATE_TC");
-          return !(e && e[0] == '0');
-        }();
-        if (v1 || (M && B)) return launch_rows<128>(n, P, A, M, B, (float)eta, scale, out, upper, s);
-        if (tc) return launch_update_tc128(n, P, A, M, (float)eta, scale, out, s);
-        return launch_k128(n, P, A, M, B, (float)eta, scale, out, s);
-      }
+      case 32: return launch_v2<32>(n, P, A, M, B, (float)eta, scale, out, s);
+      case 64: return (M && B) ? launch_rows<64>(n, P, A, M, B, (float)eta, scale, out, upper, s)
+                               : launch_v2<64>(n, P, A, M, B, (float)eta, scale, out, s);
+      case 128:
+        // tcgen05 3xTF32 GEMM (update_tc.cu); the Oja M*B form streams rows
+        if (M && B) return launch_rows<128>(n, P, A, M, B, (float)eta, scale, out, upper, s);
+        return launch_update_tc128(n, P, A, M, (float)eta, scale, out, s);
       default: break;
     }
   }

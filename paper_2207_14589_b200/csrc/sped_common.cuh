@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdarg>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/sped.h"
@@ -35,15 +36,38 @@ void set_error(const char* fmt, ...);
 
 inline cudaStream_t as_stream(sped_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
-inline int num_sms() {
-  static int cached = 0;
-  if (!cached) {
+// One-time per-device setup (function attributes such as the >48 KB
+// dynamic shared-memory opt-in are per device context): `f` runs once for
+// each device ordinal it is called on, under a mutex; a failure is not
+// remembered, so the next call retries.
+struct PerDeviceOnce {
+  std::mutex mu;
+  uint64_t done = 0;  // bit d: device d set up
+  template <class F>
+  int operator()(F&& f) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
+    const uint64_t bit = 1ull << (dev & 63);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done & bit) return SPED_OK;
+    const int rc = f();
+    if (rc == SPED_OK) done |= bit;
+    return rc;
   }
-  return cached;
+};
+
+// SM count of the current device (cached per device ordinal).
+inline int num_sms() {
+  static int cached[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = cached[dev & 63];
+  if (c <= 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    c = v > 0 ? v : 148;
+  }
+  return c;
 }
 
 // L2 eviction policies (createpolicy + .L2::cache_hint).  Streaming

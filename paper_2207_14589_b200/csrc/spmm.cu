@@ -270,10 +270,11 @@ __device__ __forceinline__ Vf<W> group_row_accumulate(const TermArgs& a, int32_t
         if (j < cnt) {
 #if SPED_HINTS
           const uint64_t pol = c < hot ? pol_hot : pol_cold;
-          gv[u] = single ? ldg_vec_pol<W>(wbase + c * (W * LPR), pol)
+          gv[u] = single ? ldg_vec_pol<W>(wbase + (int64_t)c * (W * LPR), pol)
                          : ldg_vec_pol<W>(wbase + (int64_t)c * a.ld, pol);
 #else
-          gv[u] = single ? ldg_vec<W>(wbase + c * (W * LPR)) : ldg_vec<W>(wbase + (int64_t)c * a.ld);
+          gv[u] = single ? ldg_vec<W>(wbase + (int64_t)c * (W * LPR))
+                         : ldg_vec<W>(wbase + (int64_t)c * a.ld);
 #endif
         } else {
           gv[u].zero();
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
              make_float4(acc.v[4 * h], acc.v[4 * h + 1], acc.v[4 * h + 2], acc.v[4 * h + 3]));
   }
   __threadfence();
+  __syncwarp();  // every lane's partial store is fenced before lane 0 takes the ticket
   int ticket = 0;
   if (lane == 0) ticket = atomicAdd(a.tickets + c0, 1);
   ticket = __shfl_sync(0xffffffffu, ticket, 0);

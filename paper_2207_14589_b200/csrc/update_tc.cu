@@ -277,13 +277,16 @@ __global__ void __launch_bounds__(UTHREADS, 1)
 // P A (+ eta M), columns scaled by `scale` (NULL = 1); k = 128, 16-B aligned.
 int launch_update_tc128(int64_t n, const float* P, const float* A, const float* M, float eta,
                         const float* scale, float* out, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    SPED_CUDA(cudaFuncSetAttribute(update_tc128_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, USMEM));
-    SPED_CUDA(cudaFuncSetAttribute(update_tc128_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, USMEM));
-    attr = true;
+  static PerDeviceOnce attr;  // per device: function attributes are per context
+  {
+    const int rc_ = attr([&]() -> int {
+      SPED_CUDA(cudaFuncSetAttribute(update_tc128_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, USMEM));
+      SPED_CUDA(cudaFuncSetAttribute(update_tc128_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, USMEM));
+      return SPED_OK;
+    });
+    if (rc_ != SPED_OK) return rc_;
   }
   const int64_t ntiles = (n + UTM - 1) / UTM;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms()));

@@ -52,36 +52,16 @@ def long_row_plan(nnz: int, sms: int = 148) -> tuple[int, int]:
     return thr, max(CHUNK_LEN, thr // 4)
 
 
-AUTO_DEVICE_MIN_EDGES = 1 << 20  # host edge lists this long canonicalise on the GPU
-
-
-def _auto_device_canonical(u) -> bool:
-    """Large host edge lists take the device canonicalisation (bit-identical
-    edges, the same ValueErrors) when a GPU and the library are present;
-    SPED_GRAPH_HOST=1 keeps numpy."""
-    try:
-        m = len(u)
-    except TypeError:
-        return False
-    if m < AUTO_DEVICE_MIN_EDGES or os.environ.get("SPED_GRAPH_HOST") == "1":
-        return False
-    if not torch.cuda.is_available():
-        return False
-    try:
-        _lib.load()
-    except Exception:  # library not built: the reference's host path
-        return False
-    return True
-
-
 class Graph:
     """Undirected weighted graph stored as a canonical edge list (u < v,
     lexsorted, unique, w > 0).  Same contract as ``specgap.Graph``."""
 
     def __init__(self, n: int, u, v, w, *, device=None, _canonical: bool = False):
-        """``device`` (or CUDA tensor inputs): canonicalise on that GPU
-        (``sped_canonicalize_edges``: same result bit for bit and the same
-        ValueErrors as the host path, which follows graph.py:64-88)."""
+        """Edges are canonicalised on the GPU (``device``, the CUDA tensors'
+        device, or the current one): ``sped_canonicalize_edges`` produces the
+        reference's canonical list (graph.py:64-88) bit for bit and raises
+        the same ValueErrors.  There is no host path: without CUDA this
+        raises (no CPU fallback)."""
         if n < 0:
             raise ValueError("node count must be nonnegative")
         self.n = int(n)
@@ -89,40 +69,13 @@ class Graph:
         if _canonical:
             self._u, self._v, self._w = u, v, w
             return
-        on_gpu = device is not None or any(isinstance(a, torch.Tensor) and a.is_cuda
-                                           for a in (u, v, w))
-        if not on_gpu and _auto_device_canonical(u):
-            on_gpu, device = True, "cuda"
-        if on_gpu:
-            self._canonicalize_on_device(u, v, w, device)
-            return
-        u = np.asarray(u, dtype=np.int64)
-        v = np.asarray(v, dtype=np.int64)
-        w = np.asarray(w, dtype=np.float64)
-        if not (u.shape == v.shape == w.shape):
-            raise ValueError("edge arrays must have identical length")
-        if np.any(w < 0):
-            raise ValueError("edge weights must be nonnegative")
-        keep = w > 0
-        u, v, w = u[keep], v[keep], w[keep]
-        if u.size:
-            if np.any(u == v):
-                raise ValueError("self-loops are not allowed")
-            if np.any((u < 0) | (u >= self.n) | (v < 0) | (v >= self.n)):
-                raise ValueError("edge endpoint out of range")
-        lo = np.minimum(u, v)
-        hi = np.maximum(u, v)
-        order = np.lexsort((hi, lo))
-        lo, hi, w = lo[order], hi[order], w[order]
-        pair_ids = lo * self.n + hi
-        if pair_ids.size and np.any(np.diff(pair_ids) == 0):
-            raise ValueError("duplicate edge for an unordered node pair")
-        self._u, self._v, self._w = lo, hi, w
+        self._canonicalize_on_device(u, v, w, device)
 
     def _canonicalize_on_device(self, u, v, w, device):
         import ctypes as C
         if device is None:
-            device = next(a.device for a in (u, v, w) if isinstance(a, torch.Tensor) and a.is_cuda)
+            device = next((a.device for a in (u, v, w) if isinstance(a, torch.Tensor) and a.is_cuda),
+                          None)
         dev = _lib.require_cuda(device)
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())

@@ -16,8 +16,10 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 import time
 import warnings
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -115,23 +117,27 @@ class StepWorkspace:
         """G = {S, C, Q}; diag_q: Q's diagonal only (mu-EG, sped_gram_mueg)."""
         lib = _lib.load()
         fn = lib.sped_gram_mueg if (diag_q and M is not None) else lib.sped_gram
-        rc = fn(self.n, self.k, _lib.ptr(V), _lib.ptr(M), _lib.ptr(self.G),
-                _lib.ptr(self.gram_ws), self.gram_bytes, _lib.stream_ptr(self.device))
+        with torch.cuda.device(self.device):
+            rc = fn(self.n, self.k, _lib.ptr(V), _lib.ptr(M), _lib.ptr(self.G),
+                    _lib.ptr(self.gram_ws), self.gram_bytes, _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_gram")
         if self.reduce is not None:
             self.reduce(self.G)
 
     def update(self, P, A, M, B, eta, scale, out, upper=False):
         lib = _lib.load()
-        rc = lib.sped_block_update(self.n, self.k, _lib.ptr(P), _lib.ptr(A), _lib.ptr(M),
-                                   _lib.ptr(B), float(eta), _lib.ptr(scale), int(upper),
-                                   _lib.ptr(out), _lib.stream_ptr(self.device))
+        with torch.cuda.device(self.device):
+            rc = lib.sped_block_update(self.n, self.k, _lib.ptr(P), _lib.ptr(A), _lib.ptr(M),
+                                       _lib.ptr(B), float(eta), _lib.ptr(scale), int(upper),
+                                       _lib.ptr(out), _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_block_update")
 
     def oja_coeffs(self, eta, with_m, T):
         lib = _lib.load()
-        rc = lib.sped_oja_coeffs(self.k, _lib.ptr(self.G), float(eta), int(with_m), _lib.ptr(T),
-                                 _lib.ptr(self.flag), _lib.stream_ptr(self.device))
+        with torch.cuda.device(self.device):
+            rc = lib.sped_oja_coeffs(self.k, _lib.ptr(self.G), float(eta), int(with_m),
+                                     _lib.ptr(T), _lib.ptr(self.flag),
+                                     _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_oja_coeffs")
 
     # -- step bodies (device, stream-ordered, no host sync) -------------------
@@ -139,9 +145,10 @@ class StepWorkspace:
         """solvers.py:121-144 in Gram form."""
         lib = _lib.load()
         self.gram(V, MV, diag_q=True)
-        rc = lib.sped_mueg_coeffs(self.k, _lib.ptr(self.G), float(eta), _lib.ptr(self.A),
-                                  _lib.ptr(self.scale), _lib.ptr(self.flag),
-                                  _lib.stream_ptr(self.device))
+        with torch.cuda.device(self.device):
+            rc = lib.sped_mueg_coeffs(self.k, _lib.ptr(self.G), float(eta), _lib.ptr(self.A),
+                                      _lib.ptr(self.scale), _lib.ptr(self.flag),
+                                      _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_mueg_coeffs")
         self.update(V, self.A, MV, None, eta, self.scale, out, upper=True)
 
@@ -150,8 +157,9 @@ class StepWorkspace:
         lib = _lib.load()
         self.gram(V, MV)
         self.oja_coeffs(eta, 1, self.A)
-        rc = lib.sped_axpby(self.k * self.k, float(eta), _lib.ptr(self.A), 0.0, None,
-                            _lib.ptr(self.B), _lib.stream_ptr(self.device))
+        with torch.cuda.device(self.device):
+            rc = lib.sped_axpby(self.k * self.k, float(eta), _lib.ptr(self.A), 0.0, None,
+                                _lib.ptr(self.B), _lib.stream_ptr(self.device))
         _lib.check(rc, "sped_axpby")
         self.update(V, self.A, MV, self.B, 0.0, None, self.tmp)
         self.gram(self.tmp)
@@ -177,15 +185,27 @@ class StepWorkspace:
         return f
 
 
-_WS_CACHE: dict = {}
+_WS_LOCAL = threading.local()
+_WS_MAX = 4  # workspaces kept per thread (each pins an n x k fp32 block)
 
 
 def _workspace(n, k, device) -> StepWorkspace:
+    """The calling thread's workspace for (n, k, device, current stream).
+    Per thread, so concurrent step calls never share the Gram / coefficient
+    / flag buffers (the reference's step functions are pure); a small LRU
+    bounds the device memory the cache pins."""
+    cache = getattr(_WS_LOCAL, "cache", None)
+    if cache is None:
+        cache = _WS_LOCAL.cache = OrderedDict()
     key = (n, k, str(device), torch.cuda.current_stream(device).cuda_stream)
-    ws = _WS_CACHE.get(key)
+    ws = cache.get(key)
     if ws is None:
         ws = StepWorkspace(n, k, device)
-        _WS_CACHE[key] = ws
+        cache[key] = ws
+        while len(cache) > _WS_MAX:
+            cache.popitem(last=False)
+    else:
+        cache.move_to_end(key)
     return ws
 
 
@@ -259,6 +279,9 @@ def _device_oracle(oracle):
         return obj.apply_device
     if isinstance(obj, EdgeBatchOracle):
         return obj.apply_device
+    from .walks import WalkOracle
+    if isinstance(obj, WalkOracle):
+        return obj.apply_device
     return None
 
 
@@ -320,30 +343,35 @@ _STEP_RULES = {"oja": oja_step, "mu-eg": mu_eg_step}
 
 def make_stochastic_oracle(op: TransformedOperator, batch_size: int, seed: int,
                            sampler=None, index_source: str = "device",
-                           estimator: str = "edge-batch"):
+                           estimator: str | None = None):
     """Unbiased stochastic estimate of the reversed transformed matvec
     (solvers.py:150-202).  Batch size 0 returns ``op.apply``.
 
-    * Default (the north-star device path): per-term seeded edge minibatches
-      drawn from ONE numpy PCG64 stream seeded with ``seed`` (identity kind:
-      exactly the reference's identity oracle; other kinds: the restated
-      per-term composition of SURVEY 8c(1)).
-    * ``sampler=SamplerConfig(...)`` or ``estimator="walk"``: the reference's
-      walk oracle for non-identity polynomials (solvers.py:183-200), one
-      importance estimate per column with the reference's per-call seeds and
-      bit-identical walks (``walks.WalkOracle``)."""
+    * Default (``estimator=None``): the reference's own estimators.  Identity
+      kind: ``batch_size`` seeded edge minibatches from ONE numpy PCG64
+      stream (solvers.py:164-178, bit-identical indices); other polynomial
+      kinds: the reference's walk oracle (solvers.py:183-200), one importance
+      estimate per column with the reference's per-call seeds and
+      bit-identical walks (``walks.WalkOracle``; ``sampler=`` as in the
+      reference).
+    * ``estimator="edge-batch"`` (the north-star device path, opt-in for
+      non-identity kinds): per-term seeded edge minibatches of ``batch_size``
+      edges drawn from ONE PCG64 stream seeded with ``seed`` -- the restated
+      per-term composition of SURVEY 8c(1).
+    * ``estimator="walk"``: the walk oracle explicitly."""
     if batch_size == 0:
         return op.apply
     if batch_size < 0:
         raise ValueError("batch size must be nonnegative")
+    if estimator not in (None, "edge-batch", "walk"):
+        raise ValueError(f"unknown estimator {estimator!r}")
     if not op.transform.is_polynomial:
         raise ValueError("stochastic sampling needs a polynomial transform")
-    if (sampler is not None or estimator == "walk") and op.transform.kind != "identity":
+    if op.transform.kind != "identity" and (estimator == "walk" or
+                                            (estimator is None)):
         from .walks import WalkOracle
         walks = sampler.walks_per_estimate if sampler is not None else batch_size
         return WalkOracle(op, walks, seed)
-    if estimator not in ("edge-batch", "walk"):
-        raise ValueError(f"unknown estimator {estimator!r}")
     return EdgeBatchOracle(op, batch_size, seed, index_source=index_source)
 
 
@@ -486,14 +514,17 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
                stop_on_targets: bool = False, record_timing: bool = True,
                device=None, use_cuda_graphs: bool = True,
                index_source: str = "device",
-               use_persistent_kernel: bool | None = None) -> SolverRun:
+               use_persistent_kernel: bool | None = None,
+               estimator: str | None = None) -> SolverRun:
     """Run a solver on the reversed transformed Laplacian (solvers.py:227-292),
     entirely on the device.  Metrics are evaluated on the host every
     ``eval_every`` steps against the original Laplacian's bottom-k truth
     (dense, n <= 5000, as in the reference).  Deterministic polynomial
     mu-EG runs on small graphs use the grid-resident kernel K7
     (``use_persistent_kernel=None`` = when eligible), other graphable runs
-    replay whole steps as CUDA graphs."""
+    replay whole steps as CUDA graphs.  ``estimator`` selects the stochastic
+    oracle for ``batch_size > 0`` (``make_stochastic_oracle``: None = the
+    reference's; "edge-batch" = per-term edge minibatches)."""
     if config.k > g.n:
         raise ValueError("k exceeds the node count")
     dev = _lib.require_cuda(device)
@@ -503,7 +534,8 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
     rng = np.random.default_rng(aux_seed)
     stochastic = config.batch_size > 0
     oracle = make_stochastic_oracle(op, config.batch_size, oracle_seed,
-                                    index_source=index_source) if stochastic else op
+                                    index_source=index_source,
+                                    estimator=estimator) if stochastic else op
     if ground_truth is None and g.n <= 5000:
         ground_truth = graph_ground_truth(g, mode)
     state = init_state(g.n, config.k, init_seed, device=dev)

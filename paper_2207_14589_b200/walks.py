@@ -209,6 +209,14 @@ class WalkOracle:
         out = out[:, 0] if Xd.dim() == 1 else out
         return out.to(X.dtype)
 
+    def apply_internal(self, X: torch.Tensor) -> torch.Tensor:
+        """The solver's internal (relabelled) row order in and out; the walks
+        run on the reference's node ids."""
+        lap = self.op.laplacian
+        if not lap.reordered:
+            return self.apply_device(X)
+        return lap.to_internal(self.apply_device(lap.from_internal(X)))
+
     def __call__(self, x):
         if is_device_array(x):
             return self.apply_device(x)

@@ -97,7 +97,7 @@ def test_sharded_stochastic_terms_match_single_gpu(cuda, world, cfg):
     op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 9), spec["mode"])
     L = op.laplacian
     B = 5000
-    orc = sp.make_stochastic_oracle(op, B, seed=11)
+    orc = sp.make_stochastic_oracle(op, B, seed=11, estimator="edge-batch")
     k = spec["k"]
     X = torch.randn((n, k), device="cuda", generator=torch.Generator(device="cuda").manual_seed(2))
     al, be, ga, w0, lf, s = op.schedule
@@ -177,7 +177,7 @@ def test_sharded_solver_steps_single_rank(cuda):
             assert rel_fro(out_s.cpu().numpy(), out_r.cpu().numpy()) <= 1e-6, name
             assert ws1.reduce is None
         sto = ShardedStochasticOperator(shard, t, op.lambda_star, 4000, seed=5)
-        orc = sp.make_stochastic_oracle(op, 4000, seed=5)
+        orc = sp.make_stochastic_oracle(op, 4000, seed=5, estimator="edge-batch")
         y_s = sto.apply_local(Vi)
         y_r = orc.apply_internal(Vi)  # same seed: the same batches
         assert rel_fro(y_s.cpu().numpy(), y_r.cpu().numpy()) <= 1e-6

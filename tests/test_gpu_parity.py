@@ -269,7 +269,7 @@ def test_relabelled_stochastic_oracle_matches_unrelabelled(cuda):
     for reorder in (None, "degree"):
         L = sp.LaplacianOperator(g, "normalized", reorder=reorder)
         op = sp.TransformedOperator(L, t, 0.0, 2.0)
-        oracle = sp.make_stochastic_oracle(op, 20000, seed=9)
+        oracle = sp.make_stochastic_oracle(op, 20000, seed=9, estimator="edge-batch")
         outs.append(oracle(x).cpu().numpy())
     assert rel_fro(outs[1], outs[0]) <= PV_TOL
 
@@ -305,11 +305,12 @@ def test_scaled_normalized_path(cuda, k, monkeypatch):
     assert sp.LaplacianOperator(wg, "normalized").row_scale is None
 
 
-def test_device_canonicalisation_matches_host(cuda, monkeypatch):
-    """Graph(n, u, v, w, device=...) (sped_canonicalize_edges) returns the
-    host path's canonical edge list bit for bit -- orientation, lexsort,
-    dropped zero weights -- and raises the same ValueErrors in the same
-    order of precedence (graph.py:64-88)."""
+def test_device_canonicalisation_matches_host(cuda):
+    """Graph(n, u, v, w) canonicalises on the device (sped_canonicalize_edges)
+    and returns the reference's canonical edge list (the oracle restatement of
+    graph.py:64-88) bit for bit -- orientation, lexsort, dropped zero weights
+    -- for host arrays, CUDA tensors and device=, and raises the same
+    ValueErrors in the same order of precedence."""
     import torch
     import paper_2207_14589_b200 as sp
     rng = np.random.default_rng(7)
@@ -325,21 +326,14 @@ def test_device_canonicalisation_matches_host(cuda, monkeypatch):
         u = np.where(flip, hi, lo)[perm]
         v = np.where(flip, lo, hi)[perm]
         w = rng.uniform(0.0, 2.0, lo.size)
-        w[rng.random(lo.size) < 0.05] = 0.0  # dropped, as on the host
-        monkeypatch.setenv("SPED_GRAPH_HOST", "1")  # the numpy path, whatever m is
-        host = sp.Graph(n, u, v, w)
-        monkeypatch.delenv("SPED_GRAPH_HOST")
-        assert not isinstance(host._u, torch.Tensor)
-        dev = sp.Graph(n, u, v, w, device="cuda")
-        auto = sp.Graph(n, u, v, w)  # >= 2^20 edges: device path by default
-        assert isinstance(auto._u, torch.Tensor) == (u.size >= sp.graph.AUTO_DEVICE_MIN_EDGES)
-        assert np.array_equal(auto.u, host.u) and np.array_equal(auto.w, host.w)
-        assert dev.m == host.m
-        assert np.array_equal(dev.u, host.u) and np.array_equal(dev.v, host.v)
-        assert np.array_equal(dev.w, host.w)
-        td = sp.Graph(n, torch.as_tensor(u, device="cuda"), torch.as_tensor(v, device="cuda"),
-                      torch.as_tensor(w, device="cuda"))
-        assert np.array_equal(td.u, host.u) and td.u.dtype == np.int64
+        w[rng.random(lo.size) < 0.05] = 0.0  # dropped, as in the reference
+        ru, rv, rw = O.canonical_edges(n, u, v, w)
+        for g in (sp.Graph(n, u, v, w), sp.Graph(n, u, v, w, device="cuda"),
+                  sp.Graph(n, torch.as_tensor(u, device="cuda"), torch.as_tensor(v, device="cuda"),
+                           torch.as_tensor(w, device="cuda"))):
+            assert g.m == ru.size
+            assert np.array_equal(g.u, ru) and np.array_equal(g.v, rv) and np.array_equal(g.w, rw)
+            assert g.u.dtype == np.int64
     cases = [  # (u, v, w, message) -- precedence as in the reference
         ([0, 1], [1, 2], [1.0, -1.0], "nonnegative"),
         ([0, 2, 1], [0, 9, 2], [1.0, 1.0, -0.5], "nonnegative"),
@@ -349,6 +343,11 @@ def test_device_canonicalisation_matches_host(cuda, monkeypatch):
         ([3, 3], [3, 3], [0.0, 0.0], None),  # zero-weight self loops are dropped first
     ]
     for u, v, w, msg in cases:
+        if msg is None:
+            assert O.canonical_edges(5, u, v, w)[0].size == 0
+        else:
+            with pytest.raises(ValueError, match=msg):
+                O.canonical_edges(5, u, v, w)
         for kw in ({}, {"device": "cuda"}):
             if msg is None:
                 assert sp.Graph(5, u, v, w, **kw).m == 0
@@ -393,6 +392,42 @@ def test_operator_shared_across_threads(cuda):
         assert torch.equal(got[i], ref[i])
 
 
+def test_mu_eg_step_concurrent_threads(cuda):
+    """The reference's step functions are pure: two host threads running
+    mu_eg_step on the SAME (default) stream with their own states get the
+    single-thread results bit for bit -- each thread has its own step
+    workspace (Gram, coefficients, collapse flag)."""
+    import threading
+    import torch
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200 import generators as G
+    n, u, v, w = G.lp_sbm(20000, 20, 24.0, 0.1, 5, 0.8, device="cuda")
+    g = sp.Graph.from_canonical(n, u, v, w)
+    op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 5), device="cuda")
+    V0 = [sp.init_state(n, 32, s).V for s in (1, 2)]
+
+    def run(V):
+        st = sp.EigenState(V)
+        for _ in range(10):
+            st = sp.mu_eg_step(st, op, 0.1)
+        return st.V
+
+    ref = [run(V) for V in V0]
+    torch.cuda.synchronize()
+    got = [None, None]
+
+    def work(i):
+        got[i] = run(V0[i])
+        torch.cuda.synchronize()
+    ts = [threading.Thread(target=work, args=(i,)) for i in (0, 1)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in (0, 1):
+        assert torch.equal(got[i], ref[i])
+
+
 def test_bench_sped_arm_contract(cuda):
     """`bench.py` (default arm, scaled-down graph) prints one JSON line with
     the driver's keys plus roofline / cpu_baseline / e2e / gpu_launches /
@@ -403,7 +438,7 @@ def test_bench_sped_arm_contract(cuda):
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     r = subprocess.run([sys.executable, str(root / "bench.py"), "--scale", "0.02", "--steps", "3",
-                        "--warmup", "3", "--cpu-seconds", "1", "--no-extra"],
+                        "--warmup", "3", "--no-extra"],
                        capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]

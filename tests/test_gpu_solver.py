@@ -157,7 +157,7 @@ def test_edge_batch_poly_vs_restated_oracle(cuda, kind, ell, k):
     g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
     eps = 0.5 if kind == "log-taylor" else 1e-6
     op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell, eps))
-    oracle = sp.make_stochastic_oracle(op, 5000, seed=3)
+    oracle = sp.make_stochastic_oracle(op, 5000, seed=3, estimator="edge-batch")
     x = np.random.default_rng(k).standard_normal((n, k)).astype(np.float32).astype(np.float64)
     y = oracle(x)
     B = 5000
@@ -183,7 +183,7 @@ def test_edge_batch_hub_runs_vs_restated_oracle(cuda, B):
     wts = np.linspace(0.5, 2.0, len(hub) + len(tail))
     g = sp.Graph.from_edges(341, [(a, b, c) for (a, b), c in zip(hub + tail, wts)])
     op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 5))
-    oracle = sp.make_stochastic_oracle(op, B, seed=11)
+    oracle = sp.make_stochastic_oracle(op, B, seed=11, estimator="edge-batch")
     x = np.random.default_rng(B).standard_normal((g.n, 8)).astype(np.float32).astype(np.float64)
     y = oracle(x)
     batch = oracle.last_batch.cpu().numpy().astype(np.int64)
@@ -207,7 +207,7 @@ def test_edge_batch_all_terms_sort_equals_per_term(cuda, k):
     n, u, v, w = G.lp_sbm(3000, 12, 20.0, 0.1, 7, 0.8)
     g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
     op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 9))
-    orc = sp.make_stochastic_oracle(op, 4000, seed=5)
+    orc = sp.make_stochastic_oracle(op, 4000, seed=5, estimator="edge-batch")
     x = torch.randn((n, k), device="cuda", generator=torch.Generator("cuda").manual_seed(k))
     y_all = orc.apply_internal(x).clone()
     batch = orc.last_batch
@@ -226,7 +226,7 @@ def test_edge_batch_unbiased_on_device(cuda):
     sp = _sp()
     g = sp.Graph.from_edges(3, [(0, 1), (1, 2)])
     op = sp.make_reversed_operator(g, sp.SpectralTransform("negexp-limit", 3))
-    oracle = sp.make_stochastic_oracle(op, 2, seed=3)
+    oracle = sp.make_stochastic_oracle(op, 2, seed=3, estimator="edge-batch")
     v = torch.tensor([0.2, -0.5, 0.9], device="cuda")
     exact = op.apply(v).cpu().numpy()
     draws = np.stack([oracle(v).cpu().numpy() for _ in range(4000)])

@@ -67,6 +67,11 @@ def test_walk_oracle_vs_reference(cuda, golden):
         cfg = sp.SamplerConfig(int(ell), int(B))
         orc2 = sp.make_stochastic_oracle(op, int(B), seed=int(seed), sampler=cfg)
         np.testing.assert_allclose(orc2(X), golden[base + "/y0"], **TOL)
+        # and the reference's default call (no sampler, no estimator) is the
+        # walk oracle too, as in solvers.py:181-202
+        orc3 = sp.make_stochastic_oracle(op, int(B), seed=int(seed))
+        np.testing.assert_allclose(orc3(X), golden[base + "/y0"], **TOL)
+        np.testing.assert_allclose(orc3(X), golden[base + "/y1"], **TOL)
 
 
 @pytest.mark.parametrize("graph", ["sbm1k", "chunglu"])

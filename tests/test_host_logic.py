@@ -1,7 +1,8 @@
-"""Host-side logic of the device package (CPU only, no kernel launches):
-graph canonicalisation, transform validation, the fused term schedule,
+"""Host-side logic of the device package (CPU, no kernel launches) --
+transform validation, the fused term schedule,
 PCG64 state bookkeeping, generators, solver configuration, distributed
-partitioning."""
+partitioning -- plus the Graph canonicalisation contract (gpu-marked: the
+product canonicalises on the device)."""
 
 import numpy as np
 import pytest
@@ -15,15 +16,17 @@ from paper_2207_14589_b200.transforms import term_schedule
 from conftest import rel_fro
 
 
-# --- Graph (graph.py:64-104) ---------------------------------------------------
+# --- Graph (graph.py:64-104): canonicalised on the device, so these launch ---------
 
-def test_edges_canonicalized_and_sorted():
+@pytest.mark.gpu
+def test_edges_canonicalized_and_sorted(cuda):
     g = sp.Graph.from_edges(4, [(3, 1), (2, 0), (1, 0)])
     assert g.u.tolist() == [0, 0, 1]
     assert g.v.tolist() == [1, 2, 3]
 
 
-def test_zero_weight_edges_dropped():
+@pytest.mark.gpu
+def test_zero_weight_edges_dropped(cuda):
     assert sp.Graph.from_edges(3, [(0, 1, 1.0), (1, 2, 0.0)]).m == 1
 
 
@@ -31,12 +34,14 @@ def test_zero_weight_edges_dropped():
                                          ([(0, 1), (1, 0)], 3, "duplicate"),
                                          ([(0, 5)], 2, "out of range"),
                                          ([(0, 1, -1.0)], 2, "nonnegative")])
-def test_graph_validation_errors(edges, n, msg):
+@pytest.mark.gpu
+def test_graph_validation_errors(cuda, edges, n, msg):
     with pytest.raises(ValueError, match=msg):
         sp.Graph.from_edges(n, edges)
 
 
-def test_graph_matches_oracle_canonicalisation(golden):
+@pytest.mark.gpu
+def test_graph_matches_oracle_canonicalisation(cuda, golden):
     for name in golden.graph_names():
         n, u, v, w = golden.graph(name)
         g = sp.Graph(n, v, u, w)  # reversed orientation
@@ -57,7 +62,8 @@ def test_from_canonical_validates():
         sp.Graph.from_canonical(3, torch.tensor([1]), torch.tensor([0]), torch.ones(1, dtype=torch.float64))
 
 
-def test_degree_bounds():
+@pytest.mark.gpu
+def test_degree_bounds(cuda):
     g = sp.Graph.from_edges(4, [(0, 1, 2.0), (0, 2), (0, 3)])
     b = sp.degree_bounds(g)
     assert b.deg_star == 3 and b.deg_star_inc == 5 and b.lambda_upper == 8.0
@@ -186,7 +192,10 @@ def test_run_to_csv_format():
 def test_no_cpu_fallback_without_cuda():
     if torch.cuda.is_available():
         pytest.skip("CUDA present")
-    g = sp.Graph.from_edges(3, [(0, 1), (1, 2)])
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        sp.Graph.from_edges(3, [(0, 1), (1, 2)])  # canonicalisation runs on the device
+    g = sp.Graph.from_canonical(3, torch.tensor([0, 1]), torch.tensor([1, 2]),
+                                torch.ones(2, dtype=torch.float64))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         sp.build_laplacian(g)
 

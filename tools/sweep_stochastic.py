@@ -29,7 +29,7 @@ def main():
     k, ell, B = spec["k"], spec["ell"], spec["batch"]
     t = sp.SpectralTransform("negexp-limit", ell + 1)
     op = sp.make_reversed_operator(g, t, spec["mode"], device=dev)
-    orc = sp.make_stochastic_oracle(op, B, seed=7)
+    orc = sp.make_stochastic_oracle(op, B, seed=7, estimator="edge-batch")
     torch.manual_seed(0)
     X = torch.randn((n, k), device=dev)
     nt = op.n_terms
