@@ -108,9 +108,12 @@ __device__ __forceinline__ float entry_value(const float* values, int64_t p, int
 __device__ __forceinline__ float4 ldg_f4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
+// column indices are read once per term: evict_first, so they do not displace
+// gathered rows (config 4: -1.5 %/term, profiles/r02_ab_cachepolicy.log)
 __device__ __forceinline__ int32_t ld_idx(const int32_t* p) {
   int32_t r;
-  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+      : "=r"(r) : "l"(p), "l"(policy_evict_first()));
   return r;
 }
 __device__ __forceinline__ float ld_val(const float* p) {
@@ -618,13 +621,20 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
 #endif
     const bool w8 = wide && (k % 8 == 0) && aligned32 && k >= W8_MIN_K;
     const int lpr = k / (w8 ? 8 : 4);
-    if (a.n_chunks > 0) {
-      // hub chunks keep 128-bit gathers at k = 32 (0.78 vs 0.87 ms at config 4)
-      if (w8 && k >= 64) launch_chunks_w<8>(lpr, a, vm, s);
-      else launch_chunks_w<4>(k / 4, a, vm, s);
-      SPED_LAUNCH_CHECK();
-    }
-    for (int i = 0; i < nseg; ++i) {
+    // rows in descending segment order, hub chunks last: the hub prefix of
+    // the output is then the most recently written data when the next term
+    // starts gathering from it (config 4: -0.3 %/term, r02_ab_cachepolicy)
+    auto chunks = [&]() -> int {
+      if (a.n_chunks > 0) {
+        // hub chunks keep 128-bit gathers at k = 32 (0.78 vs 0.87 ms at config 4)
+        if (w8 && k >= 64) launch_chunks_w<8>(lpr, a, vm, s);
+        else launch_chunks_w<4>(k / 4, a, vm, s);
+        SPED_LAUNCH_CHECK();
+      }
+      return SPED_OK;
+    };
+    for (int j = 0; j < nseg; ++j) {
+      const int i = nseg - 1 - j;
       a.row_begin = segs[i].begin;
       a.row_end = segs[i].end;
       int sub = segs[i].sub;
@@ -634,6 +644,8 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       else launch_rows_w<4>(lpr, sub, a, vm, s);
       SPED_LAUNCH_CHECK();
     }
+    const int rc = chunks();
+    if (rc != SPED_OK) return rc;
   } else {
     a.chunk_blocks = 0;
     a.long_thresh = INT32_MAX;
