@@ -287,6 +287,16 @@ int sped_pcg64_integers(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                         uint64_t inc_lo, int32_t has_uint32, uint32_t uinteger,
                         uint64_t m, int64_t count, int32_t* out, int64_t* draws32_out,
                         void* workspace, size_t workspace_bytes, sped_stream_t stream);
+/* The same draw with the generator state resident in DEVICE memory:
+ * state_words[6] = {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger}
+ * (numpy's bit_generator.state), advanced in place on the stream; nothing
+ * waits on the host, so the call is CUDA-graph capturable.  *status (device,
+ * may be NULL) gets bit 0 if the candidate pool ran out (state unchanged).
+ * Replaces the per-call rng.integers of solvers.py:171 with the stream kept
+ * on the GPU; the host Generator is re-synchronised from the words lazily. */
+int sped_pcg64_integers_device(uint64_t* state_words, uint64_t m, int64_t count,
+                               int32_t* out, int32_t* status, void* workspace,
+                               size_t workspace_bytes, sped_stream_t stream);
 
 /* ---- k-means on the embedding (metrics.py:143-176) ----------------------- */
 int sped_kmeans_assign(int64_t n, int32_t d, int32_t c, const float* X,

@@ -69,6 +69,7 @@ SIGNATURES = {
     "sped_pcg64_workspace_bytes": (_sz, [_i64]),
     "sped_pcg64_integers": (C.c_int, [_u64, _u64, _u64, _u64, _i32, _u32, _u64, _i64, _p,
                                       C.POINTER(_i64), _p, _sz, _p]),
+    "sped_pcg64_integers_device": (C.c_int, [_p, _u64, _i64, _p, _p, _p, _sz, _p]),
     "sped_kmeans_assign": (C.c_int, [_i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "sped_row_dist2": (C.c_int, [_i64, _i32, _p, _p, _p, _i32, _p]),
     "sped_gather_rows": (C.c_int, [_i64, _i32, _p, _p, _p, _p]),

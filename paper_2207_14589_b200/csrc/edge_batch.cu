@@ -206,6 +206,88 @@ __global__ void __launch_bounds__(256) batch_row_kernel(const BatchArgs a) {
   }
 }
 
+// Aligned slabs (k % 4 == 0, 16-B rows): G = k/4 lanes per row, one float4
+// column slice per lane, 32/G rows per warp.  Every lane of a group reads the
+// row's records itself (the group's lanes load the same 8-B word: one
+// broadcast request), so there are no shuffles and no fold: per record one
+// broadcast load, one 16-B gather and 4 FMAs per lane; U records are in
+// flight per group.  Records are folded in sorted (= sample) order, so the
+// result is deterministic.  (The warp-per-row kernel below spent most of its
+// issue slots on shuffles and folds: config 3s has ~2 records per row.)
+// G <= 16: U = 2 records in flight and 8 resident blocks (32 registers);
+// G = 32 (k = 128, one row per warp): U = 4 at the natural register count
+// (config 3s 0.33 -> 0.23 ms/term, 5s 1.26 -> 1.17 ms/term against the
+// warp-per-row kernel, profiles/r02_ab_sto_group.log)
+template <int G, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) batch_group_kernel(const BatchArgs a) {
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int c = 4 * (lane % G);
+  const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x >> 5) * RPW;
+  const bool need_x = (a.flags & 1) || ((a.flags & 4) && (a.flags & 8));
+  const unsigned long long* rec = reinterpret_cast<const unsigned long long*>(a.rec);
+  for (int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW + lane / G;
+       row < a.n; row += ngroups) {
+    const int32_t b = __ldg(a.start + row), e = __ldg(a.start + row + 1);
+    const float4 wr = ld_gather_f4(a.win + row * a.ld + c);
+    const float4 xr = need_x ? ld_stream_f4(a.x + row * a.ld + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float hsum = 0.f;
+    for (int32_t p = b; p < e; p += U) {
+      unsigned long long r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) r[u] = (p + u < e) ? __ldg(rec + p + u) : 0ull;
+      float4 g[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        g[u] = (p + u < e) ? ld_gather_f4(a.win + (int64_t)(int32_t)(uint32_t)r[u] * a.ld + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float h = __uint_as_float((uint32_t)(r[u] >> 32));  // 0 for padding
+        hsum += h;
+        acc = f4_fma(-h, g[u], acc);
+      }
+    }
+    float o[4] = {acc.x, acc.y, acc.z, acc.w};
+    const float wv[4] = {wr.x, wr.y, wr.z, wr.w};
+    const float xv[4] = {xr.x, xr.y, xr.z, xr.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float r = a.beta * fmaf(hsum, wv[i], o[i]);
+      if (a.flags & 1) r = fmaf(a.alpha, xv[i], r);
+      if (a.flags & 2) r = fmaf(a.gamma, wv[i], r);
+      if (a.flags & 4) {
+        r *= a.sfin;
+        if (a.flags & 8) r = fmaf(a.lamf, xv[i], r);
+      }
+      o[i] = r;
+    }
+    st_stream_f4(a.wout + row * a.ld + c, make_float4(o[0], o[1], o[2], o[3]));
+  }
+}
+
+template <int G>
+void launch_groups(const BatchArgs& a, cudaStream_t s) {
+  constexpr int U = G == 32 ? 4 : 2;
+  constexpr int MINB = G == 32 ? 1 : 8;
+  static PerDeviceOnce once;
+  static int per_sm[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once([&]() -> int {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, batch_group_kernel<G, U, MINB>, 256, 0);
+    per_sm[dev & 63] = v < 1 ? 1 : v;
+    return SPED_OK;
+  });
+  const int64_t rows_per_block = 8 * (32 / G);
+  const int64_t blocks = std::min<int64_t>(
+      (a.n + rows_per_block - 1) / rows_per_block,
+      (int64_t)num_sms() * std::max(1, per_sm[dev & 63] - a.spare_per_sm));
+  batch_group_kernel<G, U, MINB><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(a);
+}
+
 template <int LPR, int CPL, bool VEC>
 void launch_rows(const BatchArgs& a, cudaStream_t s) {
   static int per_sm = 0;  // grid = resident capacity; warps stride over rows
@@ -222,12 +304,12 @@ int launch_batch_slab(const BatchArgs& a, bool aligned, cudaStream_t s) {
   const int k = a.k;
   if (aligned && k % 4 == 0) {
     switch (k) {
-      case 4: launch_rows<1, 1, true>(a, s); break;
-      case 8: launch_rows<2, 1, true>(a, s); break;
-      case 16: launch_rows<4, 1, true>(a, s); break;
-      case 32: launch_rows<8, 1, true>(a, s); break;
-      case 64: launch_rows<16, 1, true>(a, s); break;
-      case 128: launch_rows<32, 1, true>(a, s); break;
+      case 4: launch_groups<1>(a, s); break;
+      case 8: launch_groups<2>(a, s); break;
+      case 16: launch_groups<4>(a, s); break;
+      case 32: launch_groups<8>(a, s); break;
+      case 64: launch_groups<16>(a, s); break;
+      case 128: launch_groups<32>(a, s); break;
       default: aligned = false;
     }
     if (aligned) {

@@ -11,6 +11,12 @@
 // one call of ell*B draws, so a whole polynomial's batches come from one
 // launch sequence.
 //
+// The generator state can live on the device (sped_pcg64_integers_device:
+// words state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger): the
+// kernels read it there and a one-thread finalize kernel advances it by the
+// number of 32-bit draws consumed, so a draw never waits on the host and a
+// whole stochastic solver step can be captured in a CUDA graph.
+//
 // Parallelisation: thread t owns 64-bit outputs [t*G, (t+1)*G) and jumps its
 // LCG state ahead with the O(log n) affine-power method (128-bit arithmetic).
 // Pass 1 counts accepted candidates per block, a scan gives block offsets,
@@ -68,6 +74,15 @@ struct Params {
   int64_t n_out64;      // 64-bit outputs generated in total
 };
 
+// the generator words of the device-resident state
+__device__ __forceinline__ Params with_state(Params P, const uint64_t* __restrict__ sw) {
+  P.state = mk128(sw[0], sw[1]);
+  P.inc = mk128(sw[2], sw[3]);
+  P.has = sw[4] ? 1 : 0;
+  P.uinteger = (uint32_t)sw[5];
+  return P;
+}
+
 __device__ __forceinline__ bool accept(uint32_t d, uint32_t m, uint32_t thresh, uint32_t* val) {
   const uint64_t p = (uint64_t)d * (uint64_t)m;
   *val = (uint32_t)(p >> 32);
@@ -92,7 +107,9 @@ __device__ __forceinline__ int thread_count(const Params& P, int64_t j0) {
   return c;
 }
 
-__global__ void __launch_bounds__(PT) pcg_count_kernel(Params P, int32_t* block_counts) {
+__global__ void __launch_bounds__(PT) pcg_count_kernel(Params P0, const uint64_t* sw,
+                                                       int32_t* block_counts) {
+  const Params P = with_state(P0, sw);
   typedef cub::BlockReduce<int, PT> BR;
   __shared__ typename BR::TempStorage tmp;
   const int64_t t = (int64_t)blockIdx.x * PT + threadIdx.x;
@@ -101,9 +118,11 @@ __global__ void __launch_bounds__(PT) pcg_count_kernel(Params P, int32_t* block_
   if (threadIdx.x == 0) block_counts[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(PT) pcg_emit_kernel(Params P, const int32_t* block_offsets,
+__global__ void __launch_bounds__(PT) pcg_emit_kernel(Params P0, const uint64_t* sw,
+                                                      const int32_t* block_offsets,
                                                       int64_t count, int32_t* out,
                                                       int64_t* last_draw) {
+  const Params P = with_state(P0, sw);
   typedef cub::BlockScan<int, PT> BS;
   __shared__ typename BS::TempStorage tmp;
   const int64_t t = (int64_t)blockIdx.x * PT + threadIdx.x;
@@ -140,6 +159,78 @@ __global__ void __launch_bounds__(PT) pcg_emit_kernel(Params P, const int32_t* b
   }
 }
 
+// numpy's state after `last_draw + 1` 32-bit draws (sampling.py's
+// pcg64_advance_state on the device); an exhausted candidate pool leaves the
+// state unchanged and sets status bit 0.
+__global__ void pcg_finalize_kernel(uint64_t* sw, const int64_t* last_draw, int32_t* status) {
+  const int64_t l = *last_draw;
+  if (l < 0) {
+    if (status) atomicOr(status, 1);
+    return;
+  }
+  const int64_t r = (l + 1) - (sw[4] ? 1 : 0);
+  if (r <= 0) {
+    sw[4] = 0;
+    return;
+  }
+  const u128 st = pcg_advance(mk128(sw[0], sw[1]), mk128(sw[2], sw[3]), (uint64_t)((r + 1) / 2));
+  sw[0] = (uint64_t)(st >> 64);
+  sw[1] = (uint64_t)st;
+  sw[4] = (uint64_t)(r % 2);
+  sw[5] = pcg_output(st) >> 32;
+}
+
+struct PcgWs {
+  int32_t *counts, *offsets;
+  int64_t* last;
+  uint64_t* words;  // host-state entry point: the state staged here
+  void* scan_tmp;
+  size_t scan_bytes;
+};
+
+PcgWs pcg_ws(void* workspace, size_t workspace_bytes, int64_t blocks) {
+  PcgWs w;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  w.counts = reinterpret_cast<int32_t*>(ws);
+  w.offsets = w.counts + (blocks + 1);
+  w.last = reinterpret_cast<int64_t*>(
+      (reinterpret_cast<uintptr_t>(w.offsets + blocks + 1) + 15) & ~uintptr_t(15));
+  w.words = reinterpret_cast<uint64_t*>(w.last + 1);
+  w.scan_tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(w.words + 6) + 255) &
+                                       ~uintptr_t(255));
+  w.scan_bytes = workspace_bytes - (reinterpret_cast<uint8_t*>(w.scan_tmp) - ws);
+  return w;
+}
+
+// draws `count` integers with the state in device memory `sw`, all on stream
+// `s` (no host synchronisation); advances `sw`.
+int pcg_draw_device(uint64_t* sw, uint64_t m, int64_t count, int32_t* out, int32_t* status,
+                    void* workspace, size_t workspace_bytes, cudaStream_t s, int64_t** last_out) {
+  Params P{};
+  P.m = (uint32_t)m;
+  P.thresh = (uint32_t)((0x100000000ULL - m) % m);
+  // candidates: the rejection rate is thresh/2^32 < m/2^32
+  const double prej = (double)P.thresh / 4294967296.0;
+  int64_t need = count + (int64_t)(count * prej * 2.0) + 4096;
+  if (need > count + count / 8 + 4096) need = count + count / 8 + 4096;
+  P.n_out64 = need / 2 + 1;
+  const int64_t blocks = (P.n_out64 + (int64_t)PT * PG - 1) / ((int64_t)PT * PG);
+  SPED_CHECK_ARG(blocks < INT32_MAX, "count too large");
+  PcgWs w = pcg_ws(workspace, workspace_bytes, blocks);
+  SPED_CUDA(cudaMemsetAsync(w.counts + blocks, 0, sizeof(int32_t), s));
+  SPED_CUDA(cudaMemsetAsync(w.last, 0xff, sizeof(int64_t), s));
+  pcg_count_kernel<<<(unsigned)blocks, PT, 0, s>>>(P, sw, w.counts);
+  SPED_LAUNCH_CHECK();
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(w.scan_tmp, w.scan_bytes, w.counts, w.offsets,
+                                          (int)(blocks + 1), s));
+  pcg_emit_kernel<<<(unsigned)blocks, PT, 0, s>>>(P, sw, w.offsets, count, out, w.last);
+  SPED_LAUNCH_CHECK();
+  pcg_finalize_kernel<<<1, 1, 0, s>>>(sw, w.last, status);
+  SPED_LAUNCH_CHECK();
+  if (last_out) *last_out = w.last;
+  return SPED_OK;
+}
+
 }  // namespace
 }  // namespace sped
 
@@ -152,7 +243,25 @@ extern "C" size_t sped_pcg64_workspace_bytes(int64_t count) {
   size_t scan_tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (int32_t*)nullptr, (int32_t*)nullptr,
                                 (int)(blocks + 1));
-  return 512 + sizeof(int32_t) * 2 * (blocks + 1) + sizeof(int64_t) + scan_tmp;
+  return 512 + sizeof(int32_t) * 2 * (blocks + 1) + sizeof(int64_t) * 7 + scan_tmp;
+}
+
+extern "C" int sped_pcg64_integers_device(uint64_t* state_words, uint64_t m, int64_t count,
+                                          int32_t* out, int32_t* status, void* workspace,
+                                          size_t workspace_bytes, sped_stream_t stream) {
+  SPED_CHECK_ARG(count >= 0 && state_words, "bad pcg64 arguments");
+  SPED_CHECK_ARG(m >= 1 && m <= (uint64_t)INT32_MAX, "m must be in [1, 2^31-1]");
+  if (count == 0) return SPED_OK;
+  SPED_CHECK_ARG(out != nullptr, "null output");
+  cudaStream_t s = as_stream(stream);
+  if (m == 1) {  // numpy: rng == 0 fills `off` without drawing
+    SPED_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t) * count, s));
+    return SPED_OK;
+  }
+  SPED_CHECK_ARG(workspace && workspace_bytes >= sped_pcg64_workspace_bytes(count),
+                 "pcg64 workspace too small");
+  return pcg_draw_device(state_words, m, count, out, status, workspace, workspace_bytes, s,
+                         nullptr);
 }
 
 extern "C" int sped_pcg64_integers(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
@@ -171,35 +280,23 @@ extern "C" int sped_pcg64_integers(uint64_t state_hi, uint64_t state_lo, uint64_
   }
   SPED_CHECK_ARG(workspace && workspace_bytes >= sped_pcg64_workspace_bytes(count),
                  "pcg64 workspace too small");
-  Params P;
-  P.state = mk128(state_hi, state_lo);
-  P.inc = mk128(inc_hi, inc_lo);
-  P.has = has_uint32 ? 1 : 0;
-  P.uinteger = uinteger;
+  // stage the host state in the workspace, draw, read back the last draw
+  uint64_t words[6] = {state_hi, state_lo, inc_hi, inc_lo, (uint64_t)(has_uint32 ? 1 : 0),
+                       (uint64_t)uinteger};
+  // the staging words follow the block table: the same layout pcg_draw_device uses
+  Params P{};
   P.m = (uint32_t)m;
   P.thresh = (uint32_t)((0x100000000ULL - m) % m);
-  // candidates: the rejection rate is thresh/2^32 < m/2^32
   const double prej = (double)P.thresh / 4294967296.0;
   int64_t need = count + (int64_t)(count * prej * 2.0) + 4096;
   if (need > count + count / 8 + 4096) need = count + count / 8 + 4096;
-  P.n_out64 = need / 2 + 1;
-  const int64_t blocks = (P.n_out64 + (int64_t)PT * PG - 1) / ((int64_t)PT * PG);
-  SPED_CHECK_ARG(blocks < INT32_MAX, "count too large");
-  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  int32_t* counts = reinterpret_cast<int32_t*>(ws);
-  int32_t* offsets = counts + (blocks + 1);
-  int64_t* last = reinterpret_cast<int64_t*>(
-      (reinterpret_cast<uintptr_t>(offsets + blocks + 1) + 15) & ~uintptr_t(15));
-  void* scan_tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(last + 1) + 255) &
-                                           ~uintptr_t(255));
-  size_t scan_bytes = workspace_bytes - (reinterpret_cast<uint8_t*>(scan_tmp) - ws);
-  SPED_CUDA(cudaMemsetAsync(counts + blocks, 0, sizeof(int32_t), s));
-  SPED_CUDA(cudaMemsetAsync(last, 0xff, sizeof(int64_t), s));
-  pcg_count_kernel<<<(unsigned)blocks, PT, 0, s>>>(P, counts);
-  SPED_LAUNCH_CHECK();
-  SPED_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, offsets, (int)(blocks + 1), s));
-  pcg_emit_kernel<<<(unsigned)blocks, PT, 0, s>>>(P, offsets, count, out, last);
-  SPED_LAUNCH_CHECK();
+  const int64_t blocks = (need / 2 + 1 + (int64_t)PT * PG - 1) / ((int64_t)PT * PG);
+  PcgWs w = pcg_ws(workspace, workspace_bytes, blocks);
+  SPED_CUDA(cudaMemcpyAsync(w.words, words, sizeof(words), cudaMemcpyHostToDevice, s));
+  int64_t* last = nullptr;
+  const int rc = pcg_draw_device(w.words, m, count, out, nullptr, workspace, workspace_bytes, s,
+                                 &last);
+  if (rc != SPED_OK) return rc;
   int64_t last_h = -1;
   SPED_CUDA(cudaMemcpyAsync(&last_h, last, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   SPED_CUDA(cudaStreamSynchronize(s));

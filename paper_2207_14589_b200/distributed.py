@@ -503,18 +503,23 @@ class ShardedStochasticOperator(ShardedOperator):
         if index_source not in ("device", "host"):
             raise ValueError("index_source must be 'device' or 'host'")
         self.batch_size = int(batch_size)
-        self.rng = np.random.default_rng(seed)
+        from .sampling import DeviceGenerator
+        self.gen = DeviceGenerator(np.random.default_rng(seed), shard.device)
         self.index_source = index_source
         self.batch_fn = term_fn or shard.local_batch_term
         self._batch = None
         self.overlap = False  # edge-minibatch terms: one pass after the exchange
 
+    @property
+    def rng(self) -> np.random.Generator:
+        return self.gen.rng
+
     def draw(self, count: int) -> torch.Tensor:
-        from .sampling import host_draw, pcg64_draw
+        from .sampling import host_draw
         m = self.shard.full.graph.m
         if self.index_source == "device":
-            return pcg64_draw(self.rng, m, count, self.shard.device)
-        return host_draw(self.rng, m, count, self.shard.device)
+            return self.gen.integers(m, count)
+        return host_draw(self.gen.rng, m, count, self.shard.device)
 
     def apply_local(self, x_own: torch.Tensor, out: torch.Tensor | None = None,
                     batch: torch.Tensor | None = None) -> torch.Tensor:

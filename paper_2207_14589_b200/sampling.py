@@ -4,9 +4,10 @@ The reference draws ``rng.integers(0, m, size=B)`` from a numpy PCG64
 generator created once per oracle (solvers.py:167,171).  Here the same
 indices are produced either
 
-* on the device by ``sped_pcg64_integers`` (bit-exact numpy PCG64 + Lemire,
-  the default), after which the host ``Generator``'s state is advanced to
-  exactly where numpy would be, or
+* on the device by ``sped_pcg64_integers_device`` (bit-exact numpy PCG64 +
+  Lemire, the default) with the generator state kept in device memory and
+  advanced there (no host synchronisation, CUDA-graph capturable); the host
+  ``Generator`` is re-synchronised from it lazily (``DeviceGenerator``), or
 * on the host by the numpy generator itself (``index_source="host"``),
   uploaded through pinned memory.
 
@@ -25,7 +26,8 @@ import torch
 from . import _lib
 from .arrays import as_device_block, from_device_block
 
-__all__ = ["pcg64_draw", "host_draw", "EdgeBatchOracle", "pcg64_advance_state"]
+__all__ = ["pcg64_draw", "host_draw", "EdgeBatchOracle", "pcg64_advance_state",
+           "DeviceGenerator"]
 
 _MULT = (2549297995355413924 << 64) | 4865540595714422341
 _M128 = (1 << 128) - 1
@@ -98,6 +100,85 @@ def pcg64_draw(rng: np.random.Generator, m: int, count: int, device) -> torch.Te
     return out[:count]
 
 
+def _state_words(st: dict) -> np.ndarray:
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    return np.array([s >> 64, s & _M64, inc >> 64, inc & _M64, int(st["has_uint32"]),
+                     int(st["uinteger"])], dtype=np.uint64)
+
+
+def _words_state(w: np.ndarray) -> dict:
+    w = [int(x) for x in np.asarray(w, dtype=np.uint64)]
+    return {"bit_generator": "PCG64", "state": {"state": (w[0] << 64) | w[1],
+                                                "inc": (w[2] << 64) | w[3]},
+            "has_uint32": int(w[4]), "uinteger": int(w[5])}
+
+
+class DeviceGenerator:
+    """A numpy ``Generator(PCG64)`` whose state lives on the device between
+    draws.  ``integers(m, count)`` runs ``sped_pcg64_integers_device``: the
+    same values and the same state evolution as ``rng.integers(0, m, count)``
+    (solvers.py:171), with no host round trip.  ``rng`` returns the host
+    Generator re-synchronised from the device words (one small D2H copy);
+    touching it hands authority back to the host until the next draw."""
+
+    def __init__(self, rng: np.random.Generator, device):
+        if rng.bit_generator.state.get("bit_generator") != "PCG64":
+            raise ValueError("device draws need a PCG64 generator")
+        self._rng = rng
+        self.device = torch.device(device)
+        self._words = torch.empty(6, dtype=torch.int64, device=self.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._where = "host"  # which copy of the state is current
+
+    @property
+    def rng(self) -> np.random.Generator:
+        if self._where == "device":
+            self._rng.bit_generator.state = _words_state(self._words.cpu().numpy().view(np.uint64))
+            self.check()
+        self._where = "host"
+        return self._rng
+
+    def to_device(self):
+        """Make the device words the current state (upload if the host copy
+        is current)."""
+        if self._where == "host":
+            w = _state_words(self._rng.bit_generator.state).view(np.int64)
+            self._words.copy_(torch.from_numpy(w))
+            self._where = "device"
+
+    def snapshot(self) -> torch.Tensor:
+        self.to_device()
+        return self._words.clone()
+
+    def restore(self, words: torch.Tensor):
+        self._words.copy_(words)
+        self._where = "device"
+
+    def check(self):
+        if int(self.status.item()) & 1:
+            raise RuntimeError("pcg64: candidate pool exhausted")
+
+    def integers(self, m: int, count: int) -> torch.Tensor:
+        if m <= 0:
+            raise ValueError("high <= 0")
+        if m > np.iinfo(np.int32).max:
+            raise ValueError("edge count exceeds int32 indices")
+        self.to_device()
+        lib = _lib.load()
+        out = torch.empty(max(count, 1), dtype=torch.int32, device=self.device)
+        nbytes = int(lib.sped_pcg64_workspace_bytes(count))
+        if self._ws.numel() < nbytes:
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            rc = lib.sped_pcg64_integers_device(_lib.ptr(self._words), int(m), int(count),
+                                                _lib.ptr(out), _lib.ptr(self.status),
+                                                _lib.ptr(self._ws), self._ws.numel(),
+                                                _lib.stream_ptr(self.device))
+        _lib.check(rc, "sped_pcg64_integers_device")
+        return out[:count]
+
+
 def host_draw(rng: np.random.Generator, m: int, count: int, device) -> torch.Tensor:
     """The reference's own host draw, uploaded through pinned memory."""
     idx = rng.integers(0, m, size=count)
@@ -118,10 +199,10 @@ class EdgeBatchOracle:
             raise ValueError("index_source must be 'device' or 'host'")
         self.op = op
         self.batch_size = int(batch_size)
-        self.rng = np.random.default_rng(seed)
         self.index_source = index_source
         lap = op.laplacian
         self.device = lap.device
+        self.gen = DeviceGenerator(np.random.default_rng(seed), self.device)
         self.m = lap.graph.m
         lib = _lib.load()
         # room for every term's records (one sort per apply, not per term)
@@ -134,10 +215,26 @@ class EdgeBatchOracle:
     def n(self) -> int:
         return self.op.n
 
+    @property
+    def rng(self) -> np.random.Generator:
+        """The oracle's numpy stream (solvers.py:167), current as of the last
+        draw (re-synchronised from the device on access)."""
+        return self.gen.rng
+
     def draw(self, count: int) -> torch.Tensor:
         if self.index_source == "device":
-            return pcg64_draw(self.rng, self.m, count, self.device)
-        return host_draw(self.rng, self.m, count, self.device)
+            return self.gen.integers(self.m, count)
+        return host_draw(self.gen.rng, self.m, count, self.device)
+
+    @property
+    def graph_capturable(self) -> bool:
+        """Whole applies can be captured in a CUDA graph: device-resident
+        draws, and one stream (all terms sorted at once, or a single term)."""
+        if self.index_source != "device":
+            return False
+        per_term = int(_lib.load().sped_edge_batch_workspace_bytes(self.op.laplacian.n,
+                                                                   self.batch_size))
+        return self.op.n_terms <= 1 or self.ws_bytes > per_term
 
     def apply_device(self, xd: torch.Tensor, batch: torch.Tensor | None = None,
                      out: torch.Tensor | None = None) -> torch.Tensor:

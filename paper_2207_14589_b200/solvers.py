@@ -398,9 +398,12 @@ class SolverRun:
 
 
 class _GraphStepper:
-    """Whole solver steps captured as CUDA graphs (ping-pong buffers)."""
+    """Whole solver steps captured as CUDA graphs (ping-pong buffers).
+    ``op`` is the exact operator or an edge-minibatch oracle whose draws run
+    on the device (each replay draws the next batches from the device-resident
+    PCG64 state, so replays continue the reference's stream)."""
 
-    def __init__(self, op: TransformedOperator, solver: str, eta: float, V0: torch.Tensor):
+    def __init__(self, op, solver: str, eta: float, V0: torch.Tensor):
         self.dev = V0.device
         n, k = V0.shape
         self.bufs = [V0.clone(), torch.empty_like(V0)]
@@ -409,6 +412,9 @@ class _GraphStepper:
         self.op, self.solver, self.eta = op, solver, eta
         self.cur = 0
         self.graphs = [None, None]
+        gen = getattr(op, "gen", None)
+        if gen is not None:  # the warm-up must not consume the oracle's stream
+            saved = gen.snapshot()
         s = torch.cuda.Stream(self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
@@ -416,6 +422,8 @@ class _GraphStepper:
                 self._body(self.bufs[i], self.bufs[1 - i])
         torch.cuda.current_stream(self.dev).wait_stream(s)
         torch.cuda.synchronize(self.dev)
+        if gen is not None:
+            gen.restore(saved)
         self.bufs[0].copy_(V0)
         for i in (0, 1):
             g = torch.cuda.CUDAGraph()
@@ -567,9 +575,11 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
         return True
 
     evaluate(state.V, 0)
-    graphable = (use_cuda_graphs and not stochastic and config.eta_schedule == "constant"
+    graphable = (use_cuda_graphs and config.eta_schedule == "constant"
                  and isinstance(op, TransformedOperator) and op.transform.is_polynomial
-                 and config.steps > 0)
+                 and config.steps > 0
+                 and (not stochastic or (isinstance(oracle, EdgeBatchOracle)
+                                         and oracle.graph_capturable)))
     lap = op.laplacian if isinstance(op, TransformedOperator) else None
     internal = lap is not None and lap.reordered
     # the solver state lives in the operator's internal (relabelled) order
@@ -577,12 +587,13 @@ def run_solver(g: Graph, transform: SpectralTransform, config: SolverConfig,
     out_order = (lambda X: lap.from_internal(X)) if internal else (lambda X: X)
     steps_done = 0
     if graphable:
-        persistent = (persistent_solver_eligible(op, config.k, config.solver)
-                      if use_persistent_kernel is None else use_persistent_kernel)
+        persistent = not stochastic and (persistent_solver_eligible(op, config.k, config.solver)
+                                         if use_persistent_kernel is None
+                                         else use_persistent_kernel)
         if persistent:
             stepper = _PersistentStepper(op, config.eta, V, config.solver)
         else:
-            stepper = _GraphStepper(op, config.solver, config.eta, V)
+            stepper = _GraphStepper(oracle if stochastic else op, config.solver, config.eta, V)
         t = 0
         while t < config.steps:
             m = min(config.eval_every - t % config.eval_every, config.steps - t)

@@ -117,6 +117,45 @@ def test_device_pcg64_large_streams(cuda, m, count):
         assert rng.bit_generator.state == mirror.bit_generator.state
 
 
+def test_device_generator_stream_and_state(cuda):
+    """DeviceGenerator (state resident on the device, no host sync per draw):
+    successive draws equal numpy's integers(0, m, count) stream, the host
+    Generator re-synchronised from the device words equals numpy's state,
+    and host/device hand-over in both directions keeps one stream."""
+    from paper_2207_14589_b200.sampling import DeviceGenerator
+    for m, sizes in ((5, [7, 1, 300]), (80_296_541, [1_000_001, 3, 17_000_000]),
+                     (2**31 - 1, [999, 1000])):
+        gen = DeviceGenerator(np.random.default_rng(11), "cuda")
+        mirror = np.random.default_rng(11)
+        for c in sizes:
+            got = gen.integers(m, c).cpu().numpy()
+            np.testing.assert_array_equal(got, mirror.integers(0, m, size=c))
+        assert gen.rng.bit_generator.state == mirror.bit_generator.state
+        # the host takes over, then the device again
+        np.testing.assert_array_equal(gen.rng.integers(0, m, size=5), mirror.integers(0, m, size=5))
+        np.testing.assert_array_equal(gen.integers(m, 9).cpu().numpy(),
+                                      mirror.integers(0, m, size=9))
+        assert gen.rng.bit_generator.state == mirror.bit_generator.state
+
+
+def test_stochastic_run_solver_cuda_graph_equals_eager(cuda, golden):
+    """Stochastic mu-EG / Oja steps replayed as CUDA graphs (device draws from
+    the resident PCG64 state inside the graph) are bit-identical to the eager
+    steps, and the oracle's stream ends where numpy's does."""
+    sp = _sp()
+    g = _graph(golden, "cfg1")
+    t = sp.SpectralTransform("negexp-limit", 13)
+    for solver in ("mu-eg", "oja"):
+        cfg = sp.SolverConfig(solver=solver, k=10, eta=0.1, steps=30, eval_every=10, seed=4,
+                              batch_size=3 * g.m)
+        a = sp.run_solver(g, t, cfg, record_timing=False, estimator="edge-batch",
+                          use_cuda_graphs=True)
+        b = sp.run_solver(g, t, cfg, record_timing=False, estimator="edge-batch",
+                          use_cuda_graphs=False)
+        assert torch.equal(a.V, b.V), solver
+        assert [r.subspace_error for r in a.records] == [r.subspace_error for r in b.records]
+
+
 @pytest.mark.parametrize("source", ["device", "host"])
 def test_identity_stochastic_oracle_vs_reference(cuda, golden, source):
     sp = _sp()
