@@ -70,8 +70,10 @@ enum TermFlags : int {
 
 struct TermArgs {
   int64_t n;
-  int32_t k;    // columns in this slab
-  int64_t ld;   // row stride (floats)
+  int32_t k;    // columns in this slab / panel
+  int64_t ld;   // row stride of the gathered block win (floats)
+  int64_t ldx;  // row stride of x
+  int64_t ldo;  // row stride of wout (and acc_in)
   const int32_t* indptr;
   const int32_t* indices;
   const float* values;
@@ -377,10 +379,11 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
       }
     }
     const int64_t off = (int64_t)row * a.ld + lcl * W;
+    const int64_t offo = (int64_t)row * a.ldo + lcl * W;
     if (VM == 3) {
-      if (a.acc_in) y.add(ldg_vec<W>(a.acc_in + off));
+      if (a.acc_in) y.add(ldg_vec<W>(a.acc_in + offo));
       if (a.flags & TF_RAW_OUT) {
-        st_stream_vec<W>(a.wout + off, y);
+        st_stream_vec<W>(a.wout + offo, y);
         y.zero();
       }
     }
@@ -388,9 +391,9 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
       Vf<W> xr, wr;
       xr.zero();
       wr.zero();
-      if (need_x) xr = ld_stream_vec<W>(a.x + off);
+      if (need_x) xr = ld_stream_vec<W>(a.x + (int64_t)row * a.ldx + lcl * W);
       if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
-      st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, y, xr, wr, row_ds(a, row)));
+      st_stream_vec<W>(a.wout + offo, term_epilogue<W>(a, y, xr, wr, row_ds(a, row)));
     }
   }
   if (lane == 0) a.tickets[c0] = 0;
@@ -417,10 +420,11 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? TE
   Vf<W> acc = group_row_accumulate<W, LPR, SUB, U, VM>(a, row, valid, b, e, e - b, lane);
   if (valid && sub == 0) {
     const int64_t off = (int64_t)row * a.ld + cl * W;
+    const int64_t offo = (int64_t)row * a.ldo + cl * W;
     if (VM == 3) {
-      if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + off));
+      if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + offo));
       if (a.flags & TF_RAW_OUT) {
-        st_stream_vec<W>(a.wout + off, acc);
+        st_stream_vec<W>(a.wout + offo, acc);
         return;
       }
     }
@@ -428,9 +432,9 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? TE
     Vf<W> xr, wr;
     xr.zero();
     wr.zero();
-    if (need_x) xr = ld_stream_vec<W>(a.x + off);
+    if (need_x) xr = ld_stream_vec<W>(a.x + (int64_t)row * a.ldx + cl * W);
     if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
-    st_stream_vec<W>(a.wout + off, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
+    st_stream_vec<W>(a.wout + offo, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
   }
 }
 
@@ -494,23 +498,24 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
     const int cc = q * LPR + cl;
     if (cc >= a.k) continue;
     const int64_t off = row * a.ld + cc;
+    const int64_t offo = row * a.ldo + cc;
     if (VM == 3) {
-      if (a.acc_in) acc[q] += a.acc_in[off];
+      if (a.acc_in) acc[q] += a.acc_in[offo];
       if (a.flags & TF_RAW_OUT) {
-        a.wout[off] = acc[q];
+        a.wout[offo] = acc[q];
         continue;
       }
     }
     float r = a.beta * acc[q];
     const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
-    const float xv = need_x ? a.x[off] : 0.f;
+    const float xv = need_x ? a.x[row * a.ldx + cc] : 0.f;
     if (a.flags & TF_ALPHA) r = fmaf(a.alpha, xv, r);
     if (a.flags & TF_GAMMA) r = fmaf(a.gamma, a.win[off], r);
     if (a.flags & TF_FINAL) {
       r *= a.sfin;
       if (a.flags & TF_LAMF) r = fmaf(a.lamf, xv, r);
     }
-    a.wout[off] = r;
+    a.wout[offo] = r;
   }
 }
 
@@ -737,16 +742,19 @@ static void l2_window(cudaStream_t s, const void* base, size_t bytes) {
 
 // Shared driver for the exact and stochastic applies: runs the schedule,
 // calling `term(t, win, wout, args)` for each term.
+// With `panel` set, the schedule runs one column panel starting at column
+// c0: the initial block and the output are offset by c0 (row-major), the
+// ping-pong intermediates are used from their start (panel-contiguous).
 template <class TermFn>
 int run_schedule(int64_t n, int32_t k, const float* x, const float* w_init, float* w_a, float* w_b,
                  float* out, int32_t n_terms, const double* alpha, const double* beta,
                  const double* gamma, double w0, double lam_f, double s_final, cudaStream_t s,
-                 TermFn&& term) {
+                 TermFn&& term, int32_t c0 = 0, bool panel = false) {
   if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0, x, 0.0, nullptr, out, s);
-  const float* cur = w_init ? w_init : x;
+  const float* cur = (w_init ? w_init : x) + (panel ? c0 : 0);
   for (int32_t t = 0; t < n_terms; ++t) {
     const bool final = (t == n_terms - 1);
-    float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);
+    float* dst = final ? out + (panel ? c0 : 0) : ((t & 1) == 0 ? w_a : w_b);
     if (!dst) {
       set_error("scratch buffer for term %d is NULL", t);
       return SPED_ERR_ARG;
@@ -765,6 +773,23 @@ int run_schedule(int64_t n, int32_t k, const float* x, const float* w_init, floa
     cur = dst;
   }
   return SPED_OK;
+}
+
+// Panel width for the exact apply (SPED_PANEL_K overrides; 0 or k = off).
+// Default: off until measured.
+static int32_t panel_width(int64_t n, int32_t k, int64_t hot_rows, int32_t n_terms, bool ok) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("SPED_PANEL_K");
+    env = e ? atoi(e) : -1;
+  }
+  if (!ok || n_terms < 2 || k > 128) return k;
+  int32_t kp = k;
+  if (env >= 0) kp = env;
+  (void)n;
+  (void)hot_rows;
+  if (kp <= 0 || kp >= k || k % kp != 0 || kp % 4 != 0) return k;
+  return kp;
 }
 
 }  // namespace sped
@@ -824,68 +849,97 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
     SPED_CHECK_ARG(segs[i].begin >= 0 && segs[i].end <= n && segs[i].begin <= segs[i].end,
                    "segment %d out of range", i);
   }
-  auto term = [&](int32_t t, const float* win, float* wout, float al, float be, float ga,
-                  float lf, float sf, int flags) -> int {
-    int vm = implicit ? 1 : 0;
-    if (norm) {
-      if (t > 0) {
-        vm = 2;
-        flags |= TF_NORM_IN;
+  Segment fixed[8];
+  int ns = nseg;
+  for (int i = 0; i < ns; ++i) fixed[i] = segs[i];
+  if (ns == 0) {
+    fixed[0].begin = 0;
+    fixed[0].end = n;
+    fixed[0].sub = 32;
+    ns = 1;
+  }
+  // Column panels: the polynomial acts on every column independently, so a
+  // k-wide block can run as k/kp independent kp-wide chains whose
+  // intermediates are stored panel-contiguous ([n x kp] each).  Every term
+  // then gathers kp*4-byte rows from an n*kp*4-byte block: twice the rows
+  // per byte of L2 for the hub prefix of a power-law graph, at the price of
+  // re-streaming the CSR indices once per panel.  x and out stay row-major
+  // (row stride k).
+  const int32_t kp = panel_width(n, k, hot_rows, n_terms, norm || implicit || values != nullptr);
+  const int32_t npan = (kp < k) ? k / kp : 1;
+  const int64_t hot_bytes = hot_rows * (int64_t)k * (int64_t)sizeof(float);
+  int rc = SPED_OK;
+  for (int32_t pan = 0; pan < npan && rc == SPED_OK; ++pan) {
+    const int32_t pc0 = pan * (npan > 1 ? kp : 0);
+    const int32_t pw = npan > 1 ? kp : k;
+    const float* xin = w_init ? w_init : x;
+    auto term = [&](int32_t t, const float* win, float* wout, float al, float be, float ga,
+                    float lf, float sf, int flags) -> int {
+      int vm = implicit ? 1 : 0;
+      if (norm) {
+        if (t > 0) {
+          vm = 2;
+          flags |= TF_NORM_IN;
+        }
+        if (!(flags & TF_FINAL)) flags |= TF_SCALE_OUT;
       }
-      if (!(flags & TF_FINAL)) flags |= TF_SCALE_OUT;
-    }
-    for (int32_t sl = 0; sl < slabs; ++sl) {
-      const int32_t c0 = sl * 128;
-      const int32_t kw = min(128, k - c0);
-      TermArgs a;
-      a.n = n;
-      a.k = kw;
-      a.ld = k;
-      a.indptr = indptr;
-      a.indices = indices;
-      a.values = values;
-      a.x = x + c0;
-      a.win = win + c0;
-      a.wout = wout + c0;
-      a.alpha = al;
-      a.beta = be;
-      a.gamma = ga;
-      a.lamf = lf;
-      a.sfin = sf;
-      a.flags = flags;
-      a.long_thresh = n_chunks > 0 ? long_threshold : INT32_MAX;
-      a.chunk_desc = chunk_desc;
-      a.n_chunks = (int32_t)n_chunks;
-      a.chunk_blocks = 0;
-      a.chunk_len = chunk_len > 0 ? chunk_len : 1;
-      a.partials = partials;
-      a.tickets = tickets;
-      a.row_begin = 0;
-      a.row_end = n;
-      a.hot_rows = hot_rows;
-      a.rscale = row_scale;
-      a.acc_in = nullptr;
-      Segment fixed[8];
-      int ns = nseg;
-      for (int i = 0; i < ns; ++i) fixed[i] = segs[i];
-      if (ns == 0) {
-        fixed[0].begin = 0;
-        fixed[0].end = n;
-        fixed[0].sub = 32;
-        ns = 1;
+      // strides: x, the initial block and the output are row-major (k);
+      // panel intermediates are panel-contiguous (pw)
+      const bool win_rm = (npan == 1) || (win == xin + pc0);
+      const bool out_rm = (npan == 1) || (flags & TF_FINAL);
+      const int64_t ldw = win_rm ? k : pw, ldo = out_rm ? k : pw;
+      const int32_t slabs = (pw + 127) / 128;
+      for (int32_t sl = 0; sl < slabs; ++sl) {
+        const int32_t c0 = sl * 128;
+        const int32_t kw = min(128, pw - c0);
+        TermArgs a;
+        a.n = n;
+        a.k = kw;
+        a.ld = ldw;
+        a.ldx = k;
+        a.ldo = ldo;
+        a.indptr = indptr;
+        a.indices = indices;
+        a.values = values;
+        a.x = x + pc0 + c0;
+        a.win = win + c0;
+        a.wout = wout + c0;
+        a.alpha = al;
+        a.beta = be;
+        a.gamma = ga;
+        a.lamf = lf;
+        a.sfin = sf;
+        a.flags = flags;
+        a.long_thresh = n_chunks > 0 ? long_threshold : INT32_MAX;
+        a.chunk_desc = chunk_desc;
+        a.n_chunks = (int32_t)n_chunks;
+        a.chunk_blocks = 0;
+        a.chunk_len = chunk_len > 0 ? chunk_len : 1;
+        a.partials = partials;
+        a.tickets = tickets;
+        a.row_begin = 0;
+        a.row_end = n;
+        a.hot_rows = hot_rows;
+        a.rscale = row_scale;
+        a.acc_in = nullptr;
+        const uintptr_t pbits = reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.win) |
+                                reinterpret_cast<uintptr_t>(a.wout);
+        const bool aligned = (kw % 4 == 0) && (k % 4 == 0) && (pbits % 16 == 0);
+        const bool aligned32 = (kw % 8 == 0) && (k % 8 == 0) && (pw % 8 == 0) && (pbits % 32 == 0);
+        // the same number of bytes of the gathered block stays persisting:
+        // hot_rows * k / ldw rows of it
+        if (hot_rows > 0 && hot_rows < n) {
+          const int64_t span = min(hot_bytes, n * ldw * (int64_t)sizeof(float));
+          l2_window(s, win, (size_t)span);
+        }
+        int r = launch_term_slab(a, vm, aligned, aligned32, fixed, ns, s);
+        if (r != SPED_OK) return r;
       }
-      const uintptr_t pbits = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(win) |
-                              reinterpret_cast<uintptr_t>(wout);
-      const bool aligned = (k % 4 == 0) && (pbits % 16 == 0);
-      const bool aligned32 = (k % 8 == 0) && (pbits % 32 == 0);
-      if (hot_rows > 0 && hot_rows < n) l2_window(s, win, (size_t)hot_rows * k * sizeof(float));
-      int rc = launch_term_slab(a, vm, aligned, aligned32, fixed, ns, s);
-      if (rc != SPED_OK) return rc;
-    }
-    return SPED_OK;
-  };
-  const int rc = run_schedule(n, k, x, w_init, w_a, w_b, out, n_terms, alpha, beta, gamma,
-                              w0_scale, lam_f, s_final, s, term);
+      return SPED_OK;
+    };
+    rc = run_schedule(n, k, x, w_init, w_a, w_b, out, n_terms, alpha, beta, gamma, w0_scale, lam_f,
+                      s_final, s, term, pc0, npan > 1);
+  }
   if (hot_rows > 0 && hot_rows < n) l2_window(s, nullptr, 0);
   return rc;
 }
@@ -946,6 +1000,8 @@ extern "C" int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr,
     a.n = n;
     a.k = min(128, k - c0);
     a.ld = k;
+    a.ldx = k;
+    a.ldo = k;
     a.indptr = indptr;
     a.indices = indices;
     a.values = values;

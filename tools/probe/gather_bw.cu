@@ -60,7 +60,7 @@ int main() {
     cudaFree(a); cudaFree(b);
   }
   std::mt19937_64 rng(1);
-  for (int row_floats : {32, 64, 128}) {
+  for (int row_floats : {8, 16, 32, 64, 128}) {
     for (int64_t table_mb : {64LL, 1280LL}) {
       int64_t trows = table_mb * 1024 * 1024 / (row_floats * 4);
       int per = 16;

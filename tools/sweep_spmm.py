@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reorder", nargs="*", default=["auto"])
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--kind", default="negexp-taylor")
+    ap.add_argument("--k", type=int, nargs="*", default=None, help="block widths (default: the config's k)")
     a = ap.parse_args()
     spec = G.CONFIGS[a.config]
     dev = torch.device("cuda")
@@ -31,8 +32,9 @@ def main():
     k, ell = spec["k"], spec["ell"]
     t = sp.SpectralTransform(a.kind, ell if a.kind != "negexp-limit" else ell + 1)
     for ro in a.reorder:
-        L = sp.LaplacianOperator(g, spec["mode"], reorder=None if ro == "none" else ro)
-        op = sp.TransformedOperator(L, t, 0.0, 2.0)
+      L = sp.LaplacianOperator(g, spec["mode"], reorder=None if ro == "none" else ro)
+      op = sp.TransformedOperator(L, t, 0.0, 2.0)
+      for k in (a.k or [spec["k"]]):
         X = torch.randn((n, k), device=dev)
         out = torch.empty_like(X)
         for hot in a.hot:
@@ -47,12 +49,13 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.reps
-            print(json.dumps({"config": a.config, "reorder": ro, "reordered": L.reordered,
+            print(json.dumps({"config": a.config, "k": k, "reorder": ro, "reordered": L.reordered,
                               "hot_fraction": hot, "hot_rows": L.hot_rows(k), "terms": op.n_terms,
                               "ms_per_apply": ms, "ms_per_term": ms / op.n_terms,
                               "segments": [list(L.segments(k)[1])[:3 * L.segments(k)[0]]]}),
                   flush=True)
-        del L, op
+        del X, out
+      del L, op
 
 
 if __name__ == "__main__":
