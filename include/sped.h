@@ -75,6 +75,24 @@ int sped_laplacian_build(int64_t n, int64_t m, const int64_t* u, const int64_t* 
                          double* degrees, int32_t* epos, int64_t* nnz_out,
                          sped_stream_t stream);
 
+/* ---- one row shard of the same CSR (replaces slicing the
+ * LaplacianOperator of graph.py:182-199 built whole on every rank) --------
+ * Rows [row_begin, row_end) of sped_laplacian_build's CSR, bit for bit, from
+ * any lexsorted subsequence of the canonical edge list that contains every
+ * edge incident to those rows (other edges are ignored).  indices hold
+ * GLOBAL column ids.  normalized + store_values needs col_degrees = every
+ * node's degree (fp64[n]; the all-gather of the shards' `degrees`).
+ *   indptr  int32[nr+1], indices/values capacity 2m+nr, degrees fp64[nr]
+ *   (own rows, Graph.degrees order), epos int32[2m] (local CSR position of
+ *   each input edge's two entries, -1 where the row is not in the shard).
+ * Synchronises `stream`. */
+int sped_laplacian_build_rows(int64_t n, int64_t row_begin, int64_t row_end, int64_t m,
+                              const int64_t* u, const int64_t* v, const double* w,
+                              const double* col_degrees, int normalized, int store_values,
+                              int32_t* indptr, int32_t* indices, float* values,
+                              double* degrees, int32_t* epos, int64_t* nnz_out,
+                              sped_stream_t stream);
+
 /* ---- graph canonicalisation (Graph.__post_init__, graph.py:64-88) -------
  * Drops w == 0 edges, orients u < v and sorts by (u, v) on the device (the
  * reference's lexsort, bit for bit: a radix sort of the unique keys u*n+v).
@@ -189,6 +207,21 @@ int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* i
                                const double* alpha, const double* beta, const double* gamma,
                                double w0_scale, double lam_f, double s_final,
                                sped_stream_t stream);
+
+/* As sped_edge_batch_poly_apply with the estimator scale given explicitly:
+ * a row shard passes its COMPACTED batch (only the samples with an endpoint
+ * in the shard, in sample order, as indices into its local edge arrays of
+ * m local edges) and scale = m_global / B_global, so its rows get the
+ * single-GPU arithmetic while sorting O(B / P) records.  B may be 0 (no
+ * sampled endpoint in the shard: epilogues only); B > 0 needs n_terms <= 1. */
+int sped_edge_batch_poly_apply_scaled(int64_t n, int32_t k, int64_t m, const int32_t* indices,
+                                      const float* edge_w, const int32_t* epos,
+                                      const int32_t* erow, const int32_t* batch, int64_t B,
+                                      double scale, void* workspace, int64_t workspace_bytes,
+                                      const float* x, const float* w_init, float* w_a, float* w_b,
+                                      float* out, int32_t n_terms, const double* alpha,
+                                      const double* beta, const double* gamma, double w0_scale,
+                                      double lam_f, double s_final, sped_stream_t stream);
 
 /* ---- solver step pieces (solvers.py:84-144) -----------------------------
  * sped_gram: G fp64[3*k*k] = {S = V^T V, C = V^T M, Q = M^T M} (M may be

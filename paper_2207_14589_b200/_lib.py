@@ -31,6 +31,8 @@ SIGNATURES = {
     "sped_abi_version": (C.c_int, []),
     "sped_laplacian_build": (C.c_int, [_i64, _i64, _p, _p, _p, C.c_int, C.c_int, _p, _p, _p, _p,
                                        _p, C.POINTER(_i64), _p]),
+    "sped_laplacian_build_rows": (C.c_int, [_i64, _i64, _i64, _i64, _p, _p, _p, _p, C.c_int,
+                                            C.c_int, _p, _p, _p, _p, _p, C.POINTER(_i64), _p]),
     "sped_canonicalize_edges": (C.c_int, [_i64, _i64, _p, _p, _p, _p, _p, _p, C.POINTER(_i64),
                                           C.POINTER(_i32), _p]),
     "sped_degree_order": (C.c_int, [_i64, _p, _p, _p, _p]),
@@ -49,6 +51,9 @@ SIGNATURES = {
     "sped_edge_batch_poly_apply": (C.c_int, [_i64, _i32, _i64, _p, _p, _p, _p, _p, _i64, _p, _i64,
                                              _p, _p, _p, _p, _p, _i32, _p, _p, _p, _f64, _f64, _f64,
                                              _p]),
+    "sped_edge_batch_poly_apply_scaled": (C.c_int, [_i64, _i32, _i64, _p, _p, _p, _p, _p, _i64,
+                                                    _f64, _p, _i64, _p, _p, _p, _p, _p, _i32, _p,
+                                                    _p, _p, _f64, _f64, _f64, _p]),
     "sped_gram_workspace_bytes": (_sz, [_i64, _i32]),
     "sped_gram": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _sz, _p]),
     "sped_gram_mueg": (C.c_int, [_i64, _i32, _p, _p, _p, _p, _sz, _p]),

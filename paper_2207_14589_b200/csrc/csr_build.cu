@@ -72,6 +72,11 @@ __global__ void rowlen_kernel(int64_t n, const int32_t* __restrict__ up_start,
   rowlen[i] = d + (d > 0 ? 1 : 0);
 }
 
+__global__ void count_zero_kernel(int64_t n, const double* __restrict__ d, int32_t* flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && d[i] == 0.0) atomicExch(flag, 1);
+}
+
 // np.bincount(u, w) + np.bincount(v, w): per bin a sequential fold in edge
 // order; with unit weights that is the exact integer count
 __global__ void degree_kernel(int64_t n, const int32_t* __restrict__ up_start,
@@ -605,5 +610,269 @@ extern "C" int sped_canonicalize_edges(int64_t n, int64_t m, const int64_t* u, c
   }
   *m_out = mk;
   *status_out = st;
+  return SPED_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Row-range build for one row shard: rows [b, e) of the same
+// CSR, from the edges incident to those rows only.  Input: any lexsorted
+// subsequence of the canonical edge list that contains every edge with an
+// endpoint in [b, e) (other edges are ignored), so a rank never holds the
+// whole graph.  The entries of row i are built exactly as in
+// sped_laplacian_build (lower run by a stable sort on v, diagonal, upper run
+// = the contiguous u-run of the lexsorted list), so the shard rows are
+// bit-identical to rows [b, e) of the full build.  Normalized values need
+// d^-1/2 of the halo columns too: the caller passes every node's degree
+// (the all-gather of the shards' own degrees).
+
+namespace sped {
+namespace {
+__device__ __forceinline__ int64_t clamp_row(int64_t x, int64_t b, int64_t nr) {
+  const int64_t r = x - b;
+  return r < 0 ? -1 : (r > nr ? nr : r);
+}
+
+// up_start[i] = first edge whose u - b >= i, i in [0, nr]
+__global__ void range_up_starts_kernel(int64_t m, int64_t nr, int64_t b,
+                                       const int64_t* __restrict__ u, int32_t* __restrict__ start) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > m) return;
+  const int64_t lo = (t == 0) ? -1 : clamp_row(u[t - 1], b, nr);
+  const int64_t hi = (t == m) ? nr : clamp_row(u[t], b, nr);
+  for (int64_t i = lo + 1; i <= hi; ++i) start[i] = (int32_t)t;
+}
+
+// lower-run sort keys: local row of v (nr = not in this shard)
+__global__ void range_keys_kernel(int64_t m, int64_t nr, int64_t b, const int64_t* __restrict__ v,
+                                  int32_t* __restrict__ vkey, int32_t* __restrict__ eval) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const int64_t r = v[e] - b;
+  vkey[e] = (r >= 0 && r < nr) ? (int32_t)r : (int32_t)nr;
+  eval[e] = (int32_t)e;
+}
+
+__device__ __forceinline__ double dinv_of(const double* deg, int64_t c) { return 1.0 / sqrt(deg[c]); }
+
+__global__ void range_degree_kernel(int64_t nr, const int32_t* __restrict__ up_start,
+                                    const int32_t* __restrict__ lo_start,
+                                    const int32_t* __restrict__ sorted_e,
+                                    const double* __restrict__ w, const int32_t* __restrict__ nonunit,
+                                    double* __restrict__ degrees) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nr) return;
+  double d;
+  if (*nonunit) {
+    double su = 0.0;
+    for (int32_t e = up_start[i]; e < up_start[i + 1]; ++e) su += w[e];
+    double sv = 0.0;
+    for (int32_t j = lo_start[i]; j < lo_start[i + 1]; ++j) sv += w[sorted_e[j]];
+    d = su + sv;
+  } else {
+    d = (double)((up_start[i + 1] - up_start[i]) + (lo_start[i + 1] - lo_start[i]));
+  }
+  degrees[i] = d;
+}
+
+__global__ void range_fill_lower_kernel(int64_t n_lo, int64_t b, const int64_t* __restrict__ u,
+                                        const int32_t* __restrict__ sorted_v,
+                                        const int32_t* __restrict__ sorted_e,
+                                        const double* __restrict__ w,
+                                        const int32_t* __restrict__ lo_start,
+                                        const int32_t* __restrict__ indptr,
+                                        const double* __restrict__ col_deg, int normalized,
+                                        int32_t* __restrict__ indices, float* __restrict__ values,
+                                        int32_t* __restrict__ epos) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n_lo) return;
+  const int32_t i = sorted_v[j];  // local row
+  const int32_t e = sorted_e[j];
+  const int64_t c = u[e];
+  const int32_t p = indptr[i] + ((int32_t)j - lo_start[i]);
+  indices[p] = (int32_t)c;
+  if (values) {
+    double val = -w[e];
+    if (normalized) val = (dinv_of(col_deg, b + i) * val) * dinv_of(col_deg, c);
+    values[p] = (float)val;
+  }
+  epos[2 * (int64_t)e + 1] = p;
+}
+
+__global__ void range_fill_upper_kernel(int64_t e0, int64_t e1, int64_t b,
+                                        const int64_t* __restrict__ u, const int64_t* __restrict__ v,
+                                        const double* __restrict__ w,
+                                        const int32_t* __restrict__ up_start,
+                                        const int32_t* __restrict__ lo_start,
+                                        const int32_t* __restrict__ indptr,
+                                        const double* __restrict__ col_deg, int normalized,
+                                        int32_t* __restrict__ indices, float* __restrict__ values,
+                                        int32_t* __restrict__ epos) {
+  const int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= e1) return;
+  const int32_t i = (int32_t)(u[e] - b);
+  const int64_t c = v[e];
+  const int32_t p = indptr[i] + (lo_start[i + 1] - lo_start[i]) + 1 + ((int32_t)e - up_start[i]);
+  indices[p] = (int32_t)c;
+  if (values) {
+    double val = -w[e];
+    if (normalized) val = (dinv_of(col_deg, b + i) * val) * dinv_of(col_deg, c);
+    values[p] = (float)val;
+  }
+  epos[2 * e] = p;
+}
+
+__global__ void range_fill_diag_kernel(int64_t nr, int64_t b, const double* __restrict__ w,
+                                       const int32_t* __restrict__ up_start,
+                                       const int32_t* __restrict__ lo_start,
+                                       const int32_t* __restrict__ sorted_e,
+                                       const int32_t* __restrict__ indptr,
+                                       const double* __restrict__ col_deg,
+                                       const int32_t* __restrict__ nonunit, int normalized,
+                                       int32_t* __restrict__ indices, float* __restrict__ values) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nr) return;
+  const int32_t up0 = up_start[i], up1 = up_start[i + 1];
+  const int32_t lo0 = lo_start[i], lo1 = lo_start[i + 1];
+  if (up1 == up0 && lo1 == lo0) return;
+  const int32_t p = indptr[i] + (lo1 - lo0);
+  indices[p] = (int32_t)(b + i);
+  if (!values) return;
+  double acc;
+  if (*nonunit) {
+    acc = 0.0;
+    bool first = true;
+    for (int32_t e = up0; e < up1; ++e) {
+      acc = first ? w[e] : acc + w[e];
+      first = false;
+    }
+    for (int32_t j = lo0; j < lo1; ++j) {
+      const double x = w[sorted_e[j]];
+      acc = first ? x : acc + x;
+      first = false;
+    }
+  } else {
+    acc = (double)((up1 - up0) + (lo1 - lo0));
+  }
+  if (normalized) {
+    const double di = dinv_of(col_deg, b + i);
+    acc = (di * acc) * di;
+  }
+  values[p] = (float)acc;
+}
+}  // namespace
+}  // namespace sped
+
+extern "C" int sped_laplacian_build_rows(int64_t n, int64_t row_begin, int64_t row_end, int64_t m,
+                                         const int64_t* u, const int64_t* v, const double* w,
+                                         const double* col_degrees, int normalized,
+                                         int store_values, int32_t* indptr, int32_t* indices,
+                                         float* values, double* degrees, int32_t* epos,
+                                         int64_t* nnz_out, sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && m >= 0 && row_begin >= 0 && row_begin <= row_end && row_end <= n,
+                 "bad row range [%lld, %lld) of n=%lld", (long long)row_begin, (long long)row_end,
+                 (long long)n);
+  const int64_t nr = row_end - row_begin;
+  SPED_CHECK_ARG(n < (int64_t)INT32_MAX && 2 * m + nr < (int64_t)INT32_MAX,
+                 "shard too large for int32 CSR (rows=%lld, m=%lld)", (long long)nr, (long long)m);
+  SPED_CHECK_ARG(indptr && nnz_out, "null output");
+  SPED_CHECK_ARG(!normalized || !store_values || col_degrees,
+                 "normalized values need every node's degree (col_degrees)");
+  cudaStream_t s = as_stream(stream);
+  *nnz_out = 0;
+  if (nr == 0) {
+    SPED_CUDA(cudaMemsetAsync(indptr, 0, sizeof(int32_t), s));
+    if (m > 0 && epos) SPED_CUDA(cudaMemsetAsync(epos, 0xFF, sizeof(int32_t) * 2 * m, s));
+    SPED_CUDA(cudaStreamSynchronize(s));
+    return SPED_OK;
+  }
+  SPED_CHECK_ARG(m == 0 || (u && v && w && indices && epos && degrees), "null edge/output array");
+  SPED_CHECK_ARG(!store_values || values, "values requested but NULL");
+  SPED_CHECK_ARG(degrees, "null degrees");
+
+  AsyncBuf b_len(s), b_up(s), b_lo(s), b_keys(s), b_vals(s), b_keys2(s), b_vals2(s), b_flag(s),
+      b_tmp(s);
+  SPED_CUDA(b_len.alloc(sizeof(int32_t) * (nr + 1)));
+  SPED_CUDA(b_up.alloc(sizeof(int32_t) * (nr + 1)));
+  SPED_CUDA(b_lo.alloc(sizeof(int32_t) * (nr + 1)));
+  SPED_CUDA(b_keys.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_vals.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_keys2.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_vals2.alloc(sizeof(int32_t) * m));
+  SPED_CUDA(b_flag.alloc(sizeof(int32_t)));
+  SPED_CUDA(cudaMemsetAsync(b_flag.p, 0, sizeof(int32_t), s));
+  int32_t* nonunit_d = (int32_t*)b_flag.p;
+  int32_t* rowlen = (int32_t*)b_len.p;
+  int32_t* up_start = (int32_t*)b_up.p;
+  int32_t* lo_start = (int32_t*)b_lo.p;
+  int32_t* keys = (int32_t*)b_keys.p;
+  int32_t* vals = (int32_t*)b_vals.p;
+  int32_t* sorted_v = (int32_t*)b_keys2.p;
+  int32_t* sorted_e = (int32_t*)b_vals2.p;
+
+  size_t tmp_scan = 0, tmp_sort = 0;
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, rowlen, indptr, (int)(nr + 1), s));
+  int end_bit = 1;
+  while (end_bit < 31 && ((int64_t)1 << end_bit) <= nr) ++end_bit;  // keys in [0, nr]
+  if (m > 0)
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, keys, sorted_v, vals, sorted_e,
+                                              (int)m, 0, end_bit, s));
+  SPED_CUDA(b_tmp.alloc(tmp_scan > tmp_sort ? tmp_scan : tmp_sort));
+  if (m > 0) {
+    SPED_CUDA(cudaMemsetAsync(epos, 0xFF, sizeof(int32_t) * 2 * m, s));  // -1: row not in shard
+    unit_check_kernel<<<grid_for(m, 256, num_sms() * 8), 256, 0, s>>>(m, w, nonunit_d);
+    range_keys_kernel<<<grid_for(m, 256), 256, 0, s>>>(m, nr, row_begin, v, keys, vals);
+    SPED_LAUNCH_CHECK();
+    size_t sb = tmp_sort;
+    SPED_CUDA(cub::DeviceRadixSort::SortPairs(b_tmp.p, sb, keys, sorted_v, vals, sorted_e, (int)m,
+                                              0, end_bit, s));
+  }
+  range_up_starts_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(m, nr, row_begin, u, up_start);
+  run_starts_kernel<int32_t><<<grid_for(m + 1, 256), 256, 0, s>>>(m, nr, sorted_v, lo_start);
+  rowlen_kernel<<<grid_for(nr + 1, 256), 256, 0, s>>>(nr, up_start, lo_start, rowlen);
+  SPED_LAUNCH_CHECK();
+  size_t tmp_bytes = tmp_scan;
+  SPED_CUDA(cub::DeviceScan::ExclusiveSum(b_tmp.p, tmp_bytes, rowlen, indptr, (int)(nr + 1), s));
+  range_degree_kernel<<<grid_for(nr, 256), 256, 0, s>>>(nr, up_start, lo_start, sorted_e, w,
+                                                          nonunit_d, degrees);
+  SPED_LAUNCH_CHECK();
+  int32_t bounds[3] = {0, 0, 0};  // up_start[0], up_start[nr], lo_start[nr]
+  SPED_CUDA(cudaMemcpyAsync(&bounds[0], up_start, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaMemcpyAsync(&bounds[1], up_start + nr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaMemcpyAsync(&bounds[2], lo_start + nr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaStreamSynchronize(s));
+  if (normalized) {
+    // the shard's own rows: a zero degree is the reference's ValueError
+    // (graph.py:187-188); callers check the gathered degree vector globally
+    AsyncBuf b_z(s);
+    SPED_CUDA(b_z.alloc(sizeof(int32_t)));
+    SPED_CUDA(cudaMemsetAsync(b_z.p, 0, sizeof(int32_t), s));
+    count_zero_kernel<<<grid_for(nr, 256), 256, 0, s>>>(nr, degrees, (int32_t*)b_z.p);
+    SPED_LAUNCH_CHECK();
+    int32_t z = 0;
+    SPED_CUDA(cudaMemcpyAsync(&z, b_z.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SPED_CUDA(cudaStreamSynchronize(s));
+    if (z) {
+      set_error("normalized Laplacian requires all degrees > 0");
+      return SPED_ERR_ZERO_DEGREE;
+    }
+  }
+  float* vout = store_values ? values : nullptr;
+  const int64_t n_lo = bounds[2];
+  if (n_lo > 0)
+    range_fill_lower_kernel<<<grid_for(n_lo, 256), 256, 0, s>>>(
+        n_lo, row_begin, u, sorted_v, sorted_e, w, lo_start, indptr, col_degrees, normalized,
+        indices, vout, epos);
+  if (bounds[1] > bounds[0])
+    range_fill_upper_kernel<<<grid_for(bounds[1] - bounds[0], 256), 256, 0, s>>>(
+        bounds[0], bounds[1], row_begin, u, v, w, up_start, lo_start, indptr, col_degrees,
+        normalized, indices, vout, epos);
+  range_fill_diag_kernel<<<grid_for(nr, 256), 256, 0, s>>>(nr, row_begin, w, up_start, lo_start,
+                                                             sorted_e, indptr, col_degrees,
+                                                             nonunit_d, normalized, indices, vout);
+  SPED_LAUNCH_CHECK();
+  int32_t nnz = 0;
+  SPED_CUDA(cudaMemcpyAsync(&nnz, indptr + nr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SPED_CUDA(cudaStreamSynchronize(s));
+  *nnz_out = nnz;
   return SPED_OK;
 }

@@ -403,6 +403,17 @@ extern "C" int64_t sped_edge_batch_workspace_bytes_terms(int64_t n, int64_t B, i
   return std::max<int64_t>(per, (int64_t)batch_ws_layout(nullptr, n, B, n_terms).bytes + 256);
 }
 
+// Edge-minibatch apply with an explicit estimator scale (m/B of the global
+// batch).  B == 0 (a row shard owning no endpoint of this term's samples):
+// every estimate is 0 and only the term epilogues run.
+static int edge_batch_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
+                            const float* edge_w, const int32_t* epos, const int32_t* erow,
+                            const int32_t* batch, int64_t B, double scale, void* workspace,
+                            int64_t workspace_bytes, const float* x, const float* w_init,
+                            float* w_a, float* w_b, float* out, int32_t n_terms,
+                            const double* alpha, const double* beta, const double* gamma,
+                            double w0_scale, double lam_f, double s_final, sped_stream_t stream);
+
 extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
                                           const float* edge_w, const int32_t* epos,
                                           const int32_t* erow, const int32_t* batch, int64_t B,
@@ -413,6 +424,31 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
                                           const double* gamma, double w0_scale, double lam_f,
                                           double s_final, sped_stream_t stream) {
   SPED_CHECK_ARG(n >= 0 && k >= 1 && m >= 0 && B >= 1, "bad sizes");
+  return edge_batch_apply(n, k, m, indices, edge_w, epos, erow, batch, B, (double)m / (double)B,
+                          workspace, workspace_bytes, x, w_init, w_a, w_b, out, n_terms, alpha,
+                          beta, gamma, w0_scale, lam_f, s_final, stream);
+}
+
+extern "C" int sped_edge_batch_poly_apply_scaled(
+    int64_t n, int32_t k, int64_t m, const int32_t* indices, const float* edge_w,
+    const int32_t* epos, const int32_t* erow, const int32_t* batch, int64_t B, double scale,
+    void* workspace, int64_t workspace_bytes, const float* x, const float* w_init, float* w_a,
+    float* w_b, float* out, int32_t n_terms, const double* alpha, const double* beta,
+    const double* gamma, double w0_scale, double lam_f, double s_final, sped_stream_t stream) {
+  SPED_CHECK_ARG(n >= 0 && k >= 1 && m >= 0 && B >= 0, "bad sizes");
+  SPED_CHECK_ARG(B == 0 || n_terms <= 1, "a compacted shard batch carries one term");
+  return edge_batch_apply(n, k, m, indices, edge_w, epos, erow, batch, B, scale, workspace,
+                          workspace_bytes, x, w_init, w_a, w_b, out, n_terms, alpha, beta, gamma,
+                          w0_scale, lam_f, s_final, stream);
+}
+
+static int edge_batch_apply(int64_t n, int32_t k, int64_t m, const int32_t* indices,
+                            const float* edge_w, const int32_t* epos, const int32_t* erow,
+                            const int32_t* batch, int64_t B, double scale, void* workspace,
+                            int64_t workspace_bytes, const float* x, const float* w_init,
+                            float* w_a, float* w_b, float* out, int32_t n_terms,
+                            const double* alpha, const double* beta, const double* gamma,
+                            double w0_scale, double lam_f, double s_final, sped_stream_t stream) {
   SPED_CHECK_ARG(n_terms >= 0 && (n_terms == 0 || (alpha && beta && gamma)), "bad schedule");
   SPED_CHECK_ARG(x != out && x != w_a && x != w_b, "x must not alias outputs");
   SPED_CHECK_ARG(w_init == nullptr || (w_init != out && w_init != w_a && w_init != w_b),
@@ -421,14 +457,14 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
   if (n == 0) return SPED_OK;
   cudaStream_t s = as_stream(stream);
   if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0_scale, x, 0.0, nullptr, out, s);
-  SPED_CHECK_ARG(m > 0 && indices && epos && batch && workspace, "null graph/batch array");
+  SPED_CHECK_ARG(workspace && (B == 0 || (m > 0 && indices && epos && batch)),
+                 "null graph/batch array");
   char* base = (char*)(((uintptr_t)workspace + 255) & ~uintptr_t(255));
   BatchWs wsv[2];
-  wsv[0] = batch_ws_layout(base, n, B);
-  wsv[1] = batch_ws_layout(base + align256(wsv[0].bytes), n, B);
+  wsv[0] = batch_ws_layout(base, n, std::max<int64_t>(B, 1));
+  wsv[1] = batch_ws_layout(base + align256(wsv[0].bytes), n, std::max<int64_t>(B, 1));
   SPED_CHECK_ARG(workspace_bytes >= (int64_t)(2 * align256(wsv[0].bytes)),
                  "edge batch workspace too small");
-  const double scale = (double)m / (double)B;
   const int32_t slabs = (k + 127) / 128;
   auto sweep = [&](int32_t t, const int32_t* start, const uint64_t* rec, const float* cur,
                    float* dst, int spare) -> int {
@@ -462,6 +498,19 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
     }
     return SPED_OK;
   };
+  if (B == 0) {
+    // no sampled endpoint in this shard: empty runs, epilogue only
+    SPED_CUDA(cudaMemsetAsync(wsv[0].start, 0, sizeof(int32_t) * (n + 1), s));
+    const float* cur = w_init ? w_init : x;
+    for (int32_t t = 0; t < n_terms; ++t) {
+      float* dst = (t == n_terms - 1) ? out : ((t & 1) == 0 ? w_a : w_b);
+      SPED_CHECK_ARG(dst != nullptr, "scratch buffer for term %d is NULL", t);
+      int rc = sweep(t, wsv[0].start, wsv[0].vout, cur, dst, 0);
+      if (rc != SPED_OK) return rc;
+      cur = dst;
+    }
+    return SPED_OK;
+  }
   static const bool all_env = [] {
     const char* e = getenv("SPED_STO_ALLTERMS");
     return !(e && e[0] == '0');

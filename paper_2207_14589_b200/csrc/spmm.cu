@@ -30,6 +30,7 @@
 #include <cstdlib>
 
 #include "sped_common.cuh"
+#include "async_copy.cuh"
 
 #ifndef TERM_MIN_BLOCKS
 #define TERM_MIN_BLOCKS 6
@@ -42,6 +43,16 @@
 #endif
 #ifndef W8_U
 #define W8_U 1  // one 256-bit gather in flight per lane, more rows resident instead
+#endif
+// k = 128 short rows (16 lanes x 256 bit per row, 2 rows per warp): four
+// gathers in flight per lane at 4 blocks/SM (config 5: 2.94 -> 2.80
+// ms/term; k = 64 stays at one gather in flight and 8 blocks/SM, where the
+// same change is slower: 0.539 -> 0.571; profiles/r02_ab_mlp_cfg*.log)
+#ifndef W8_K128_U
+#define W8_K128_U 4
+#endif
+#ifndef W8_K128_MINB
+#define W8_K128_MINB 4
 #endif
 #ifndef CHUNK_MIN_BLOCKS
 #define CHUNK_MIN_BLOCKS 4
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
 }
 
 template <int W, int LPR, int SUB, int U, int VM>
-__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? TERM_MIN_BLOCKS_W8 : TERM_MIN_BLOCKS))) spmm_term_kernel(const TermArgs a) {
+__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? (LPR >= 16 ? W8_K128_MINB : TERM_MIN_BLOCKS_W8) : TERM_MIN_BLOCKS))) spmm_term_kernel(const TermArgs a) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -438,6 +449,125 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? TE
   }
 }
 
+
+// Short rows through a shared-memory ring (SUB = 1, 256-bit lane slices):
+// every lane keeps D gathered 32-B slices of the row's next neighbours in
+// flight as cp.async copies into its own ring slots, so the bytes in flight
+// per SM are set by shared memory (D * 32 B per thread) instead of by the
+// registers a register-held unroll needs (which halves the resident warps).
+// A lane consumes exactly the bytes it copied, so no cross-lane barrier:
+// per-thread cp.async groups (commit / wait_group D-1) order the ring.
+// Column indices (and stored values) of the row are read through L1 (the
+// LPR lanes of a row group read the same words).
+#ifndef RING_D
+#define RING_D 4
+#endif
+#ifndef RING_MIN_BLOCKS
+#define RING_MIN_BLOCKS 6
+#endif
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int LPR, int D, int VM>
+__global__ void __launch_bounds__(256, RING_MIN_BLOCKS) spmm_ring_kernel(const TermArgs a) {
+  constexpr int W = 8;
+  constexpr int RPW = 32 / LPR;
+  extern __shared__ float4 ring_smem[];  // [256 threads][D][2]
+  const int lane = threadIdx.x & 31;
+  const int cl = lane % LPR;
+  const int32_t wglobal = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int32_t row = (int32_t)a.row_begin + wglobal * RPW + lane / LPR;
+  bool valid = row < a.row_end;
+  int32_t b = 0, e = 0;
+  if (valid) {
+    b = __ldg(a.indptr + row);
+    e = __ldg(a.indptr + row + 1);
+    if (e - b > a.long_thresh) valid = false;
+  }
+  if (__all_sync(0xffffffffu, !valid)) return;
+  const int32_t len = valid ? e - b : 0;
+  float4* my = ring_smem + threadIdx.x * (2 * D);
+  const uint32_t my_s = async::smem_u32(my);
+  const float* wbase = a.win + cl * W;
+  const int64_t ldw = a.ld;
+  int32_t cols[D];
+  float vals[D];
+  auto fetch = [&](int d, int32_t j) {
+    if (j < len) {
+      const int32_t c = __ldg(a.indices + b + j);
+      cols[d] = c;
+      if (VM == 0 || VM == 3) vals[d] = __ldg(a.values + b + j);
+      const float* src = wbase + (int64_t)c * ldw;
+      cp_async16(my_s + d * 32, src);
+      cp_async16(my_s + d * 32 + 16, src + 4);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < D; ++d) fetch(d, d);
+  Vf<W> acc;
+  acc.zero();
+  for (int32_t j0 = 0; j0 < len; j0 += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int32_t j = j0 + d;
+      if (j < len) {
+        cp_async_wait<D - 1>();
+        const float4 lo = my[2 * d], hi = my[2 * d + 1];
+        float v;
+        if (VM == 1) v = cols[d] == row ? (float)(len - 1) : -1.0f;
+        else if (VM == 2) v = cols[d] == row ? 0.0f : 1.0f;
+        else v = vals[d];
+        acc.v[0] = fmaf(v, lo.x, acc.v[0]); acc.v[1] = fmaf(v, lo.y, acc.v[1]);
+        acc.v[2] = fmaf(v, lo.z, acc.v[2]); acc.v[3] = fmaf(v, lo.w, acc.v[3]);
+        acc.v[4] = fmaf(v, hi.x, acc.v[4]); acc.v[5] = fmaf(v, hi.y, acc.v[5]);
+        acc.v[6] = fmaf(v, hi.z, acc.v[6]); acc.v[7] = fmaf(v, hi.w, acc.v[7]);
+        fetch(d, j + D);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (!valid) return;
+  const int64_t off = (int64_t)row * a.ld + cl * W;
+  const int64_t offo = (int64_t)row * a.ldo + cl * W;
+  if (VM == 3) {
+    if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + offo));
+    if (a.flags & TF_RAW_OUT) {
+      st_stream_vec<W>(a.wout + offo, acc);
+      return;
+    }
+  }
+  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
+  Vf<W> xr, wr;
+  xr.zero();
+  wr.zero();
+  if (need_x) xr = ld_stream_vec<W>(a.x + (int64_t)row * a.ldx + cl * W);
+  if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
+  st_stream_vec<W>(a.wout + offo, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
+}
+
+template <int LPR>
+static void launch_ring(const TermArgs& a, int vm, cudaStream_t s) {
+  constexpr int RPW = 32 / LPR;
+  const int threads = 256;
+  const int64_t rows = a.row_end - a.row_begin;
+  const int64_t warps = (rows + RPW - 1) / RPW;
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  if (grid == 0) return;
+  static_assert(256 * RING_D * 32 <= 48 * 1024, "ring above the default dynamic smem limit");
+  const size_t smem = (size_t)threads * RING_D * 32;
+  auto go = [&](auto kern) { kern<<<grid, threads, smem, s>>>(a); };
+  if (vm == 1) go(spmm_ring_kernel<LPR, RING_D, 1>);
+  else if (vm == 2) go(spmm_ring_kernel<LPR, RING_D, 2>);
+  else if (vm == 3) go(spmm_ring_kernel<LPR, RING_D, 3>);
+  else go(spmm_ring_kernel<LPR, RING_D, 0>);
+}
 
 // Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
 // lanes over columns (CPL columns each), SUB groups over nonzeros.  Handles
@@ -522,7 +652,8 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
 constexpr int UNROLL = 4;
 
 template <int W, int LPR, int SUB,
-          int U = (SUB > 1 ? (W == 8 ? W8_LONG_U : LONG_U) : (W == 8 ? W8_U : SUB1_U))>
+          int U = (SUB > 1 ? (W == 8 ? W8_LONG_U : LONG_U)
+                           : (W == 8 ? (LPR >= 16 ? W8_K128_U : W8_U) : SUB1_U))>
 static void launch_fast(const TermArgs& a, int vm, cudaStream_t s) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
@@ -609,6 +740,18 @@ struct Segment {
   int sub;
 };
 
+// shared-memory ring for the short-row launches (SPED_RING: 1 = every k,
+// 0 = off, unset = default set)
+static bool ring_enabled(int k) {
+  static const int env = [] {
+    const char* e = getenv("SPED_RING");
+    return e ? atoi(e) : -1;
+  }();
+  if (env >= 0) return env == 1;
+  (void)k;
+  return false;
+}
+
 // Launch one term over one column slab: one launch per row segment, the
 // long-row chunks riding in the leading blocks of the first launch.
 static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
@@ -645,8 +788,17 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       int sub = segs[i].sub;
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
-      if (w8) launch_rows_w<8>(lpr, sub, a, vm, s);
-      else launch_rows_w<4>(lpr, sub, a, vm, s);
+      if (w8 && sub == 1 && ring_enabled(k)) {
+        switch (lpr) {
+          case 4: launch_ring<4>(a, vm, s); break;
+          case 8: launch_ring<8>(a, vm, s); break;
+          default: launch_ring<16>(a, vm, s); break;
+        }
+      } else if (w8) {
+        launch_rows_w<8>(lpr, sub, a, vm, s);
+      } else {
+        launch_rows_w<4>(lpr, sub, a, vm, s);
+      }
       SPED_LAUNCH_CHECK();
     }
     const int rc = chunks();
@@ -742,19 +894,16 @@ static void l2_window(cudaStream_t s, const void* base, size_t bytes) {
 
 // Shared driver for the exact and stochastic applies: runs the schedule,
 // calling `term(t, win, wout, args)` for each term.
-// With `panel` set, the schedule runs one column panel starting at column
-// c0: the initial block and the output are offset by c0 (row-major), the
-// ping-pong intermediates are used from their start (panel-contiguous).
 template <class TermFn>
 int run_schedule(int64_t n, int32_t k, const float* x, const float* w_init, float* w_a, float* w_b,
                  float* out, int32_t n_terms, const double* alpha, const double* beta,
                  const double* gamma, double w0, double lam_f, double s_final, cudaStream_t s,
-                 TermFn&& term, int32_t c0 = 0, bool panel = false) {
+                 TermFn&& term) {
   if (n_terms == 0) return launch_axpby(n * k, lam_f + s_final * w0, x, 0.0, nullptr, out, s);
-  const float* cur = (w_init ? w_init : x) + (panel ? c0 : 0);
+  const float* cur = w_init ? w_init : x;
   for (int32_t t = 0; t < n_terms; ++t) {
     const bool final = (t == n_terms - 1);
-    float* dst = final ? out + (panel ? c0 : 0) : ((t & 1) == 0 ? w_a : w_b);
+    float* dst = final ? out : ((t & 1) == 0 ? w_a : w_b);
     if (!dst) {
       set_error("scratch buffer for term %d is NULL", t);
       return SPED_ERR_ARG;
@@ -773,23 +922,6 @@ int run_schedule(int64_t n, int32_t k, const float* x, const float* w_init, floa
     cur = dst;
   }
   return SPED_OK;
-}
-
-// Panel width for the exact apply (SPED_PANEL_K overrides; 0 or k = off).
-// Default: off until measured.
-static int32_t panel_width(int64_t n, int32_t k, int64_t hot_rows, int32_t n_terms, bool ok) {
-  static int env = -2;
-  if (env == -2) {
-    const char* e = getenv("SPED_PANEL_K");
-    env = e ? atoi(e) : -1;
-  }
-  if (!ok || n_terms < 2 || k > 128) return k;
-  int32_t kp = k;
-  if (env >= 0) kp = env;
-  (void)n;
-  (void)hot_rows;
-  if (kp <= 0 || kp >= k || k % kp != 0 || kp % 4 != 0) return k;
-  return kp;
 }
 
 }  // namespace sped
@@ -858,21 +990,8 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
     fixed[0].sub = 32;
     ns = 1;
   }
-  // Column panels: the polynomial acts on every column independently, so a
-  // k-wide block can run as k/kp independent kp-wide chains whose
-  // intermediates are stored panel-contiguous ([n x kp] each).  Every term
-  // then gathers kp*4-byte rows from an n*kp*4-byte block: twice the rows
-  // per byte of L2 for the hub prefix of a power-law graph, at the price of
-  // re-streaming the CSR indices once per panel.  x and out stay row-major
-  // (row stride k).
-  const int32_t kp = panel_width(n, k, hot_rows, n_terms, norm || implicit || values != nullptr);
-  const int32_t npan = (kp < k) ? k / kp : 1;
   const int64_t hot_bytes = hot_rows * (int64_t)k * (int64_t)sizeof(float);
-  int rc = SPED_OK;
-  for (int32_t pan = 0; pan < npan && rc == SPED_OK; ++pan) {
-    const int32_t pc0 = pan * (npan > 1 ? kp : 0);
-    const int32_t pw = npan > 1 ? kp : k;
-    const float* xin = w_init ? w_init : x;
+  {
     auto term = [&](int32_t t, const float* win, float* wout, float al, float be, float ga,
                     float lf, float sf, int flags) -> int {
       int vm = implicit ? 1 : 0;
@@ -883,25 +1002,19 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
         }
         if (!(flags & TF_FINAL)) flags |= TF_SCALE_OUT;
       }
-      // strides: x, the initial block and the output are row-major (k);
-      // panel intermediates are panel-contiguous (pw)
-      const bool win_rm = (npan == 1) || (win == xin + pc0);
-      const bool out_rm = (npan == 1) || (flags & TF_FINAL);
-      const int64_t ldw = win_rm ? k : pw, ldo = out_rm ? k : pw;
-      const int32_t slabs = (pw + 127) / 128;
       for (int32_t sl = 0; sl < slabs; ++sl) {
         const int32_t c0 = sl * 128;
-        const int32_t kw = min(128, pw - c0);
+        const int32_t kw = min(128, k - c0);
         TermArgs a;
         a.n = n;
         a.k = kw;
-        a.ld = ldw;
+        a.ld = k;
         a.ldx = k;
-        a.ldo = ldo;
+        a.ldo = k;
         a.indptr = indptr;
         a.indices = indices;
         a.values = values;
-        a.x = x + pc0 + c0;
+        a.x = x + c0;
         a.win = win + c0;
         a.wout = wout + c0;
         a.alpha = al;
@@ -925,23 +1038,19 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
         const uintptr_t pbits = reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.win) |
                                 reinterpret_cast<uintptr_t>(a.wout);
         const bool aligned = (kw % 4 == 0) && (k % 4 == 0) && (pbits % 16 == 0);
-        const bool aligned32 = (kw % 8 == 0) && (k % 8 == 0) && (pw % 8 == 0) && (pbits % 32 == 0);
-        // the same number of bytes of the gathered block stays persisting:
-        // hot_rows * k / ldw rows of it
-        if (hot_rows > 0 && hot_rows < n) {
-          const int64_t span = min(hot_bytes, n * ldw * (int64_t)sizeof(float));
-          l2_window(s, win, (size_t)span);
-        }
+        const bool aligned32 = (kw % 8 == 0) && (k % 8 == 0) && (pbits % 32 == 0);
+        // persisting window over the hub prefix of the gathered block
+        if (hot_rows > 0 && hot_rows < n && sl == 0) l2_window(s, win, (size_t)hot_bytes);
         int r = launch_term_slab(a, vm, aligned, aligned32, fixed, ns, s);
         if (r != SPED_OK) return r;
       }
       return SPED_OK;
     };
-    rc = run_schedule(n, k, x, w_init, w_a, w_b, out, n_terms, alpha, beta, gamma, w0_scale, lam_f,
-                      s_final, s, term, pc0, npan > 1);
+    const int rc = run_schedule(n, k, x, w_init, w_a, w_b, out, n_terms, alpha, beta, gamma,
+                                w0_scale, lam_f, s_final, s, term);
+    if (hot_rows > 0 && hot_rows < n) l2_window(s, nullptr, 0);
+    return rc;
   }
-  if (hot_rows > 0 && hot_rows < n) l2_window(s, nullptr, 0);
-  return rc;
 }
 
 // One term of a row shard whose CSR is split into own-column entries and

@@ -259,7 +259,8 @@ def segment_table(rowlen: np.ndarray, k: int, sorted_desc: bool, long_threshold)
             seg.append((r_64, n, 1))              # medium/short rows: LPR lanes per row
     else:
         mean = float(rowlen.sum()) / n
-        seg = [(0, n, smax if mean >= 64 else 1)]
+        sub = int(os.environ.get("SPED_SUB", "0")) or (smax if mean >= 64 else 1)
+        seg = [(0, n, min(sub, smax))]
     flat = [x for t in seg for x in t]
     return len(seg), _lib.i64_array(flat)
 

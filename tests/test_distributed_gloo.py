@@ -179,3 +179,102 @@ def test_split_local_csr_partitions_entries():
     (_, c0, v0), (_, c1, v1) = split_local_csr(indptr, cols, None, 3)
     np.testing.assert_array_equal(v0, [2, -1, 1, -1, 3])  # diag = row length - 1
     np.testing.assert_array_equal(v1, [-1, -1, -1, -1])
+
+
+def _route_worker(rank, world, port, n, u, v, w, reorder, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2207_14589_b200.distributed import plan_shard_edges
+        sl = np.arange(rank, u.size, world)  # a strided slice of the edge list per rank
+        se = plan_shard_edges(n, torch.from_numpy(u[sl]), torch.from_numpy(v[sl]),
+                              torch.from_numpy(w[sl]), torch.from_numpy(sl), rank, world,
+                              reorder=reorder)
+        parts = [None] * world
+        dist.all_gather_object(parts, (rank, se.offsets, se.lo.numpy(), se.hi.numpy(),
+                                       se.w.numpy(), se.eid.numpy(), se.m, se.unit_weight,
+                                       None if se.perm is None else se.perm.numpy()))
+        if rank == 0:
+            result_q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,graph,reorder", [(2, "cfg4s", None), (3, "cfg4s", "degree"),
+                                                 (3, "cfg5s", None), (2, "cfg3s", "degree")])
+def test_plan_shard_edges_routes_incident_edges(golden, world, graph, reorder):
+    """Edge routing without the whole graph on any rank: from strided edge
+    slices, every rank ends up with exactly the edges incident to its rows
+    (lexsorted in the agreed internal labels, original ids and weights
+    kept), the nnz-balanced offsets of the whole graph, and -- with
+    reorder -- the degree-descending relabelling of the single-GPU operator."""
+    from paper_2207_14589_b200.distributed import partition_rows
+    n, u, v, w = golden.graph(graph)
+    u, v, w = O.canonical_edges(n, u, v, w)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_route_worker, args=(r, world, port, n, u, v, w, reorder, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cnt = np.bincount(u, minlength=n) + np.bincount(v, minlength=n)
+    rowlen = cnt + (cnt > 0)
+    lo, hi = u.copy(), v.copy()
+    if reorder == "degree":
+        perm = np.argsort(-rowlen, kind="stable")
+        iperm = np.empty(n, dtype=np.int64)
+        iperm[perm] = np.arange(n)
+        a, b = iperm[u], iperm[v]
+        lo, hi = np.minimum(a, b), np.maximum(a, b)
+        rowlen = rowlen[perm]
+    offsets = partition_rows(np.concatenate([[0], np.cumsum(rowlen)]), world)
+    eid = np.arange(u.size)
+    for r, off, plo, phi, pw, peid, m, unit, pperm in parts:
+        np.testing.assert_array_equal(off, offsets)
+        assert m == u.size and unit == bool(np.all(w == 1.0))
+        if reorder == "degree":
+            np.testing.assert_array_equal(pperm, perm)
+        else:
+            assert pperm is None
+        b, e = offsets[r], offsets[r + 1]
+        sel = ((lo >= b) & (lo < e)) | ((hi >= b) & (hi < e))
+        order = np.lexsort((hi[sel], lo[sel]))
+        np.testing.assert_array_equal(plo, lo[sel][order])
+        np.testing.assert_array_equal(phi, hi[sel][order])
+        np.testing.assert_array_equal(peid, eid[sel][order])
+        np.testing.assert_array_equal(pw, w[sel][order])
+
+
+def test_exchange_bytes_per_term_model():
+    """Predicted halo bytes (SURVEY 8e): deduplicated off-shard rows x 4k;
+    hub-prefix replication moves the prefix rows out of the point-to-point
+    halos into one all-gather."""
+    from paper_2207_14589_b200.distributed import exchange_bytes_per_term, partition_rows
+    # path 0-1-2-3-4-5 plus a hub 0 joined to everything
+    n = 6
+    edges = sorted({(i, i + 1) for i in range(5)} | {(0, j) for j in range(2, 6)})
+    rows = [[] for _ in range(n)]
+    for a, b in edges:
+        rows[a].append(b)
+        rows[b].append(a)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    cols = []
+    for i in range(n):
+        r = sorted(rows[i] + [i])
+        cols += r
+        indptr[i + 1] = indptr[i] + len(r)
+    cols = np.array(cols, dtype=np.int64)
+    off = np.array([0, 3, 6])
+    d = exchange_bytes_per_term(indptr, cols, off, k=4)
+    # rank 0 (rows 0-2) references 3, 4, 5; rank 1 (rows 3-5) references 0, 2
+    assert [x["halo_rows"] for x in d["ranks"]] == [3, 2]
+    assert d["max_bytes_per_rank"] == 3 * 16
+    h = exchange_bytes_per_term(indptr, cols, off, k=4, replicate_rows=1)
+    assert [x["p2p_rows"] for x in h["ranks"]] == [3, 1]
+    assert [x["allgather_rows"] for x in h["ranks"]] == [0, 1]
