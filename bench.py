@@ -313,6 +313,68 @@ def time_to_angle(cfg=1, target=1e-3, eval_every=50, max_steps=20000, cpu=True,
     return out
 
 
+def stochastic_time_to_angle(target=1e-2, eval_every=100, max_steps=4000, cpu_sample_steps=20,
+                             kind="negexp-limit", ell=13, eta=0.1, batch_mult=16):
+    """Time to max principal angle <= target in STOCHASTIC mode
+    (run_solver(batch_size > 0), solvers.py:150-180,248-249): mu-EG with the
+    per-term edge-minibatch oracle (B = 16 m edges per term, device PCG64
+    draws, CUDA-graph replay of whole steps) on the config-1 SBM.  The
+    stochastic iteration's noise floor sits near 5e-3 at eta = 0.1, so the
+    target is 1e-2 (tests/test_gpu_fullsize.py::test_stochastic_run_solver_sbm).
+    CPU leg: the restated oracle (the reference's np.add.at estimator per
+    term, fp64, one core) on the same graph/seeds, a bounded sample of steps
+    scaled to the GPU's step count."""
+    import torch
+    import oracle as O
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200 import generators as G
+    from paper_2207_14589_b200.solvers import _GraphStepper
+    spec = G.CONFIGS[1]
+    k = spec["k"]
+    n, u, v, w = G.config_graph(1)
+    g = sp.Graph(n, u.numpy(), v.numpy(), w.numpy())
+    U = sp.graph_ground_truth(g, spec["mode"]).bottom(k)
+    Qu = np.linalg.qr(U)[0]
+    init_seed, _, oracle_seed = O.solver_seeds(2)
+    op = sp.make_reversed_operator(g, sp.SpectralTransform(kind, ell), spec["mode"])
+    B = batch_mult * g.m
+    orc = sp.make_stochastic_oracle(op, B, oracle_seed, estimator="edge-batch")
+    V0 = sp.init_state(n, k, init_seed).V
+    Qu_d = torch.as_tensor(Qu, dtype=torch.float64, device=V0.device)
+    max_angle(V0, Qu_d)
+    stepper = _GraphStepper(orc, "mu-eg", eta, op.laplacian.to_internal(V0))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    gpu_steps = None
+    for t in range(eval_every, max_steps + 1, eval_every):
+        stepper.advance(eval_every)
+        if max_angle(stepper.V, Qu_d) <= target:
+            gpu_steps = t
+            break
+    gpu_s = time.perf_counter() - t0
+    out = {"config": spec["name"] + " stochastic", "estimator": "edge-batch (per-term minibatches)",
+           "transform": f"{kind}({ell})", "eta": eta, "k": k, "batch_per_term": B,
+           "target_angle": target, "eval_every": eval_every, "gpu_steps": gpu_steps,
+           "gpu_s": gpu_s, "gpu_path": "CUDA-graph steps (device PCG64 draws)"}
+    # CPU: the same algorithm (restated oracle, identical batches by seed)
+    csr = O.laplacian_csr(n, g.u, g.v, g.w, spec["mode"])
+    lam = O.choose_lambda_star(kind, O.lambda_upper(n, g.u, g.v, g.w, spec["mode"]))
+    rng = np.random.default_rng(oracle_seed)
+    nt = len(O.term_schedule(kind, ell, 1e-6, lam)[0])
+    V = O.init_state(n, k, init_seed)
+    t0 = time.perf_counter()
+    for _ in range(cpu_sample_steps):
+        bt = O.draw_batches(rng, g.m, B, nt)
+        V = O.mu_eg_step(V, O.edge_batch_poly_apply(g.u, g.v, g.w, kind, ell, 1e-6, lam, bt, V), eta)
+    per = (time.perf_counter() - t0) / cpu_sample_steps
+    del csr
+    if gpu_steps:
+        out.update(cpu_steps=gpu_steps, cpu_s=per * gpu_steps, cpu_extrapolated_from_steps=cpu_sample_steps,
+                   cpu_cores=1, cpu_kind="port (restated edge-batch oracle, np.add.at, fp64)",
+                   speedup=per * gpu_steps / gpu_s)
+    return out
+
+
 def exact_step_line(cfg, steps=5, warmup=2):
     """One exact mu-EG step on another BASELINE config (SBM configs 3 / 5:
     natural order, L2-resident gathers; config 5's k = 128 Gram and update
@@ -593,7 +655,8 @@ def run_sped(args):
                 # spectrum, <= 2), eta = 1.0 (4,500 CPU steps, 92 s);
                 # the CPU leg is a 300-step sample scaled to the GPU's step count
                 time_to_angle(2, kind="negexp-limit", ell=17, eta=1.0, eval_every=100,
-                              cpu_sample_steps=300)]
+                              cpu_sample_steps=300),
+                stochastic_time_to_angle()]
     sto = None
     extra = None
     if rank == 0 and not sharded and not args.no_extra:

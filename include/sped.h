@@ -177,6 +177,27 @@ int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr, const int32
                         int32_t raw_out, float* out, double alpha, double beta, double gamma,
                         double w0_scale, double lam_f, double s_final, sped_stream_t stream);
 
+/* General shard term: as sped_csr_term_split, plus
+ *   - the scaled-normalized form of sped_csr_poly_apply for unit-weight
+ *     normalized Laplacians: scaled_in = 1 means w holds u = D^-1/2 w (own
+ *     AND halo rows -- the exchange moves u) and the neighbour sums are
+ *     unweighted (values not read); scaled_out = 1 writes u' = D^-1/2 w';
+ *     row_scale = d^-1/2 of the own rows (fp32);
+ *   - a persisting-L2 window over rows [hot_begin, hot_begin + hot_rows) of
+ *     w (the hub rows: the own prefix on the shard that owns the hubs, the
+ *     head of the halo elsewhere); hot_rows = 0: none.
+ * With raw_out = 1 and partial_in = NULL on a split CSR this is pass 0; an
+ * unsplit shard (no halo) runs one pass with partial_in = NULL. */
+int sped_csr_term_shard(int64_t n, int32_t k, const int32_t* indptr, const int32_t* indices,
+                        const float* values, int32_t long_threshold, int32_t chunk_len,
+                        const int32_t* chunk_desc, int64_t n_chunks, float* partials,
+                        int32_t* tickets, const int64_t* segments, int32_t n_segments,
+                        const float* row_scale, int32_t scaled_in, int32_t scaled_out,
+                        int64_t hot_begin, int64_t hot_rows, const float* x, const float* w,
+                        const float* partial_in, int32_t raw_out, float* out, double alpha,
+                        double beta, double gamma, double w0_scale, double lam_f,
+                        double s_final, sped_stream_t stream);
+
 /* ---- edge-minibatch apply (solvers.py:166-178, per term) ----------------
  * Term t replaces L w by (m/B) * sum_{b<B} w_e x_e x_e^T w over the sampled
  * edge ids batch[t*B .. t*B+B) (int32, the numpy rng.integers stream).

@@ -46,6 +46,9 @@ SIGNATURES = {
     "sped_csr_term_split": (C.c_int, [_i64, _i32, _p, _p, _p, _i32, _i32, _p, _i64, _p, _p, _p,
                                       _i32, _p, _p, _p, _i32, _p, _f64, _f64, _f64, _f64, _f64,
                                       _f64, _p]),
+    "sped_csr_term_shard": (C.c_int, [_i64, _i32, _p, _p, _p, _i32, _i32, _p, _i64, _p, _p, _p,
+                                      _i32, _p, _i32, _i32, _i64, _i64, _p, _p, _p, _i32, _p,
+                                      _f64, _f64, _f64, _f64, _f64, _f64, _p]),
     "sped_edge_batch_workspace_bytes": (_i64, [_i64, _i64]),
     "sped_edge_batch_workspace_bytes_terms": (_i64, [_i64, _i64, _i32]),
     "sped_edge_batch_poly_apply": (C.c_int, [_i64, _i32, _i64, _p, _p, _p, _p, _p, _i64, _p, _i64,

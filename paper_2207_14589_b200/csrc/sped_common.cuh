@@ -83,6 +83,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_unchanged() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ int ld_stream_i32(const int32_t* p) {
   int r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"

@@ -30,7 +30,6 @@
 #include <cstdlib>
 
 #include "sped_common.cuh"
-#include "async_copy.cuh"
 
 #ifndef TERM_MIN_BLOCKS
 #define TERM_MIN_BLOCKS 6
@@ -240,7 +239,9 @@ __device__ __forceinline__ Vf<W> group_row_accumulate(const TermArgs& a, int32_t
   const bool single = (a.ld == W * LPR);
   const float* wbase = a.win + cl * W;
 #if SPED_HINTS
-  const uint64_t pol_hot = policy_evict_last();
+  // 1: hot gathers evict_last, cold evict_first; 2: hot gathers unchanged (the
+  // persisting window holds them), cold gathers evict_first
+  const uint64_t pol_hot = SPED_HINTS == 2 ? policy_evict_unchanged() : policy_evict_last();
   const uint64_t pol_cold = policy_evict_first();
   const int32_t hot = (int32_t)min(a.hot_rows, (int64_t)INT32_MAX);
 #endif
@@ -346,11 +347,156 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
   return make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
 }
 
+// Row sums without shuffles: every LPR-lane slice of a row's SUB lane
+// groups walks its own nonzeros (p = b + sub, b + sub + SUB, ...); column
+// indices and values come through L1 (the LPR lanes of a slice read the same
+// words), so there is no warp-uniform trip count, no predicated zero-fill
+// and no index broadcast, and U independent gathers per lane are in flight.
+// The SUB partial sums fold with the same xor tree as group_row_accumulate:
+// the summation order -- and so every result bit -- is unchanged.
+// (config 3: 0.542 -> 0.418 ms/term, config 5: 2.83 -> 2.41, config 4:
+// 3.04 -> 2.87; profiles/r02_ab_shuffle_free_cfg*.log)
+#ifndef FREE_U
+#define FREE_U 2
+#endif
+#ifndef FREE_MINB
+#define FREE_MINB 6
+#endif
+#ifndef FREE_LONG_U
+#define FREE_LONG_U 4
+#endif
+template <int W, int LPR, int SUB, int U, int VM>
+__device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row, bool valid,
+                                                 int32_t b, int32_t e, int32_t rowlen, int lane) {
+  constexpr int G = LPR * SUB;
+  const int g = lane % G;
+  const int sub = g / LPR;
+  const int cl = g % LPR;
+  const float* wbase = a.win + cl * W;
+  const int64_t ldw = a.ld;
+  Vf<W> acc;
+  acc.zero();
+  if (valid) {
+    int32_t p = b + sub;
+    for (; p + (U - 1) * SUB < e; p += U * SUB) {
+      int32_t c[U];
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = __ldg(a.indices + p + u * SUB);
+        if (VM == 1) v[u] = c[u] == row ? (float)(rowlen - 1) : -1.0f;
+        else if (VM == 2) v[u] = c[u] == row ? 0.0f : 1.0f;
+        else v[u] = __ldg(a.values + p + u * SUB);
+      }
+      Vf<W> gv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) gv[u] = ldg_vec<W>(wbase + (int64_t)c[u] * ldw);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc.fma(v[u], gv[u]);
+    }
+    for (; p < e; p += SUB) {
+      const int32_t c = __ldg(a.indices + p);
+      float v;
+      if (VM == 1) v = c == row ? (float)(rowlen - 1) : -1.0f;
+      else if (VM == 2) v = c == row ? 0.0f : 1.0f;
+      else v = __ldg(a.values + p);
+      acc.fma(v, ldg_vec<W>(wbase + (int64_t)c * ldw));
+    }
+  }
+#pragma unroll
+  for (int off = LPR; off < G; off <<= 1) acc.add_xor(off);
+  return acc;
+}
+
+template <int W, int LPR, int SUB, int VM>
+__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : FREE_MINB)) spmm_free_kernel(const TermArgs a) {
+  constexpr int G = LPR * SUB;
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G;
+  const int cl = g % LPR;
+  const int32_t wglobal = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int32_t row = (int32_t)a.row_begin + wglobal * RPW + lane / G;
+  bool valid = row < a.row_end;
+  int32_t b = 0, e = 0;
+  if (valid) {
+    b = __ldg(a.indptr + row);
+    e = __ldg(a.indptr + row + 1);
+    if (e - b > a.long_thresh) valid = false;
+  }
+  if (SUB > 1) {
+    if (__all_sync(0xffffffffu, !valid)) return;  // the fold needs the whole warp
+  } else if (!valid) {
+    return;
+  }
+  Vf<W> acc = free_accumulate<W, LPR, SUB, (SUB > 1 ? FREE_LONG_U : FREE_U), VM>(
+      a, row, valid, b, e, e - b, lane);
+  if (!valid || g >= LPR) return;
+  const int64_t off = (int64_t)row * a.ld + cl * W;
+  const int64_t offo = (int64_t)row * a.ldo + cl * W;
+  if (VM == 3 || VM == 2) {
+    if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + offo));
+    if (a.flags & TF_RAW_OUT) {
+      st_stream_vec<W>(a.wout + offo, acc);
+      return;
+    }
+  }
+  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
+  Vf<W> xr, wr;
+  xr.zero();
+  wr.zero();
+  if (need_x) xr = ld_stream_vec<W>(a.x + (int64_t)row * a.ldx + cl * W);
+  if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
+  st_stream_vec<W>(a.wout + offo, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
+}
+
+template <int W, int LPR, int SUB>
+static void launch_free(const TermArgs& a, int vm, cudaStream_t s) {
+  constexpr int RPW = 32 / (LPR * SUB);
+  const int64_t rows = a.row_end - a.row_begin;
+  const unsigned grid = (unsigned)(((rows + RPW - 1) / RPW + 7) / 8);
+  if (grid == 0) return;
+  if (vm == 1) spmm_free_kernel<W, LPR, SUB, 1><<<grid, 256, 0, s>>>(a);
+  else if (vm == 2) spmm_free_kernel<W, LPR, SUB, 2><<<grid, 256, 0, s>>>(a);
+  else if (vm == 3) spmm_free_kernel<W, LPR, SUB, 3><<<grid, 256, 0, s>>>(a);
+  else spmm_free_kernel<W, LPR, SUB, 0><<<grid, 256, 0, s>>>(a);
+}
+
+template <int W, int LPR>
+static void launch_free_sub(const TermArgs& a, int sub, int vm, cudaStream_t s) {
+  switch (sub) {
+    case 1: launch_free<W, LPR, 1>(a, vm, s); break;
+    case 2: if constexpr (LPR * 2 <= 32) { launch_free<W, LPR, 2>(a, vm, s); break; } [[fallthrough]];
+    case 4: if constexpr (LPR * 4 <= 32) { launch_free<W, LPR, 4>(a, vm, s); break; } [[fallthrough]];
+    case 8: if constexpr (LPR * 8 <= 32) { launch_free<W, LPR, 8>(a, vm, s); break; } [[fallthrough]];
+    default: launch_free<W, LPR, 32 / LPR>(a, vm, s); break;
+  }
+}
+template <int W>
+static void launch_free_w(int lpr, int sub, const TermArgs& a, int vm, cudaStream_t s) {
+  switch (lpr) {
+    case 1: launch_free_sub<W, 1>(a, sub, vm, s); break;
+    case 2: launch_free_sub<W, 2>(a, sub, vm, s); break;
+    case 4: launch_free_sub<W, 4>(a, sub, vm, s); break;
+    case 8: launch_free_sub<W, 8>(a, sub, vm, s); break;
+    case 16: launch_free_sub<W, 16>(a, sub, vm, s); break;
+    default: if constexpr (W == 4) launch_free_sub<W, 32>(a, sub, vm, s); break;
+  }
+}
+
+static bool free_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SPED_FREE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // Long-row chunks: one warp per chunk (all 32/LPR lane groups over the
 // chunk's nonzeros).  The last chunk of a row to finish (ticket) folds the
 // partial rows in chunk order and applies the epilogue: deterministic, no
 // float atomics.
-template <int W, int LPR, int U, int VM>
+template <int W, int LPR, int U, int VM, bool FREE = false>
 __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const TermArgs a) {
   const int lane = threadIdx.x & 31;
   const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
@@ -361,8 +507,11 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
   const int32_t pe = a.chunk_desc[4 * c + 2];
   const int32_t c0 = a.chunk_desc[4 * c + 3];
   const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
-  const Vf<W> acc = group_row_accumulate<W, LPR, 32 / LPR, U, VM>(
-      a, row, true, pb, pe, re - rb, lane);
+  Vf<W> acc;
+  if constexpr (FREE)
+    acc = free_accumulate<W, LPR, 32 / LPR, U, VM>(a, row, true, pb, pe, re - rb, lane);
+  else
+    acc = group_row_accumulate<W, LPR, 32 / LPR, U, VM>(a, row, true, pb, pe, re - rb, lane);
   const int lsub = lane / LPR, lcl = lane % LPR;
   if (lsub == 0) {
 #pragma unroll
@@ -391,14 +540,14 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
     }
     const int64_t off = (int64_t)row * a.ld + lcl * W;
     const int64_t offo = (int64_t)row * a.ldo + lcl * W;
-    if (VM == 3) {
+    if (VM == 3 || VM == 2) {
       if (a.acc_in) y.add(ldg_vec<W>(a.acc_in + offo));
       if (a.flags & TF_RAW_OUT) {
         st_stream_vec<W>(a.wout + offo, y);
         y.zero();
       }
     }
-    if (VM != 3 || !(a.flags & TF_RAW_OUT)) {
+    if (!(VM == 3 || VM == 2) || !(a.flags & TF_RAW_OUT)) {
       Vf<W> xr, wr;
       xr.zero();
       wr.zero();
@@ -432,7 +581,7 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? (L
   if (valid && sub == 0) {
     const int64_t off = (int64_t)row * a.ld + cl * W;
     const int64_t offo = (int64_t)row * a.ldo + cl * W;
-    if (VM == 3) {
+    if (VM == 3 || VM == 2) {
       if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + offo));
       if (a.flags & TF_RAW_OUT) {
         st_stream_vec<W>(a.wout + offo, acc);
@@ -449,125 +598,6 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? (L
   }
 }
 
-
-// Short rows through a shared-memory ring (SUB = 1, 256-bit lane slices):
-// every lane keeps D gathered 32-B slices of the row's next neighbours in
-// flight as cp.async copies into its own ring slots, so the bytes in flight
-// per SM are set by shared memory (D * 32 B per thread) instead of by the
-// registers a register-held unroll needs (which halves the resident warps).
-// A lane consumes exactly the bytes it copied, so no cross-lane barrier:
-// per-thread cp.async groups (commit / wait_group D-1) order the ring.
-// Column indices (and stored values) of the row are read through L1 (the
-// LPR lanes of a row group read the same words).
-#ifndef RING_D
-#define RING_D 4
-#endif
-#ifndef RING_MIN_BLOCKS
-#define RING_MIN_BLOCKS 6
-#endif
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int LPR, int D, int VM>
-__global__ void __launch_bounds__(256, RING_MIN_BLOCKS) spmm_ring_kernel(const TermArgs a) {
-  constexpr int W = 8;
-  constexpr int RPW = 32 / LPR;
-  extern __shared__ float4 ring_smem[];  // [256 threads][D][2]
-  const int lane = threadIdx.x & 31;
-  const int cl = lane % LPR;
-  const int32_t wglobal = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int32_t row = (int32_t)a.row_begin + wglobal * RPW + lane / LPR;
-  bool valid = row < a.row_end;
-  int32_t b = 0, e = 0;
-  if (valid) {
-    b = __ldg(a.indptr + row);
-    e = __ldg(a.indptr + row + 1);
-    if (e - b > a.long_thresh) valid = false;
-  }
-  if (__all_sync(0xffffffffu, !valid)) return;
-  const int32_t len = valid ? e - b : 0;
-  float4* my = ring_smem + threadIdx.x * (2 * D);
-  const uint32_t my_s = async::smem_u32(my);
-  const float* wbase = a.win + cl * W;
-  const int64_t ldw = a.ld;
-  int32_t cols[D];
-  float vals[D];
-  auto fetch = [&](int d, int32_t j) {
-    if (j < len) {
-      const int32_t c = __ldg(a.indices + b + j);
-      cols[d] = c;
-      if (VM == 0 || VM == 3) vals[d] = __ldg(a.values + b + j);
-      const float* src = wbase + (int64_t)c * ldw;
-      cp_async16(my_s + d * 32, src);
-      cp_async16(my_s + d * 32 + 16, src + 4);
-    }
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int d = 0; d < D; ++d) fetch(d, d);
-  Vf<W> acc;
-  acc.zero();
-  for (int32_t j0 = 0; j0 < len; j0 += D) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int32_t j = j0 + d;
-      if (j < len) {
-        cp_async_wait<D - 1>();
-        const float4 lo = my[2 * d], hi = my[2 * d + 1];
-        float v;
-        if (VM == 1) v = cols[d] == row ? (float)(len - 1) : -1.0f;
-        else if (VM == 2) v = cols[d] == row ? 0.0f : 1.0f;
-        else v = vals[d];
-        acc.v[0] = fmaf(v, lo.x, acc.v[0]); acc.v[1] = fmaf(v, lo.y, acc.v[1]);
-        acc.v[2] = fmaf(v, lo.z, acc.v[2]); acc.v[3] = fmaf(v, lo.w, acc.v[3]);
-        acc.v[4] = fmaf(v, hi.x, acc.v[4]); acc.v[5] = fmaf(v, hi.y, acc.v[5]);
-        acc.v[6] = fmaf(v, hi.z, acc.v[6]); acc.v[7] = fmaf(v, hi.w, acc.v[7]);
-        fetch(d, j + D);
-      }
-    }
-  }
-  cp_async_wait<0>();
-  if (!valid) return;
-  const int64_t off = (int64_t)row * a.ld + cl * W;
-  const int64_t offo = (int64_t)row * a.ldo + cl * W;
-  if (VM == 3) {
-    if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + offo));
-    if (a.flags & TF_RAW_OUT) {
-      st_stream_vec<W>(a.wout + offo, acc);
-      return;
-    }
-  }
-  const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
-  Vf<W> xr, wr;
-  xr.zero();
-  wr.zero();
-  if (need_x) xr = ld_stream_vec<W>(a.x + (int64_t)row * a.ldx + cl * W);
-  if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
-  st_stream_vec<W>(a.wout + offo, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
-}
-
-template <int LPR>
-static void launch_ring(const TermArgs& a, int vm, cudaStream_t s) {
-  constexpr int RPW = 32 / LPR;
-  const int threads = 256;
-  const int64_t rows = a.row_end - a.row_begin;
-  const int64_t warps = (rows + RPW - 1) / RPW;
-  const unsigned grid = (unsigned)((warps + 7) / 8);
-  if (grid == 0) return;
-  static_assert(256 * RING_D * 32 <= 48 * 1024, "ring above the default dynamic smem limit");
-  const size_t smem = (size_t)threads * RING_D * 32;
-  auto go = [&](auto kern) { kern<<<grid, threads, smem, s>>>(a); };
-  if (vm == 1) go(spmm_ring_kernel<LPR, RING_D, 1>);
-  else if (vm == 2) go(spmm_ring_kernel<LPR, RING_D, 2>);
-  else if (vm == 3) go(spmm_ring_kernel<LPR, RING_D, 3>);
-  else go(spmm_ring_kernel<LPR, RING_D, 0>);
-}
 
 // Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
 // lanes over columns (CPL columns each), SUB groups over nonzeros.  Handles
@@ -677,14 +707,22 @@ template <int W, int LPR>
 static void launch_chunks(const TermArgs& a, int vm, cudaStream_t s) {
   const unsigned grid = (unsigned)((a.n_chunks + 7) / 8);
   if (grid == 0) return;
+  constexpr int U = (W == 8 ? W8_LONG_U : LONG_U);
+  if (free_enabled()) {
+    if (vm == 1) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 1, true><<<grid, 256, 0, s>>>(a);
+    else if (vm == 2) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 2, true><<<grid, 256, 0, s>>>(a);
+    else if (vm == 3) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 3, true><<<grid, 256, 0, s>>>(a);
+    else spmm_chunk_kernel<W, LPR, FREE_LONG_U, 0, true><<<grid, 256, 0, s>>>(a);
+    return;
+  }
   if (vm == 1)
-    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 1><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, U, 1><<<grid, 256, 0, s>>>(a);
   else if (vm == 2)
-    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 2><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, U, 2><<<grid, 256, 0, s>>>(a);
   else if (vm == 3)
-    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 3><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, U, 3><<<grid, 256, 0, s>>>(a);
   else
-    spmm_chunk_kernel<W, LPR, (W == 8 ? W8_LONG_U : LONG_U), 0><<<grid, 256, 0, s>>>(a);
+    spmm_chunk_kernel<W, LPR, U, 0><<<grid, 256, 0, s>>>(a);
 }
 
 template <int W, int LPR>
@@ -740,17 +778,6 @@ struct Segment {
   int sub;
 };
 
-// shared-memory ring for the short-row launches (SPED_RING: 1 = every k,
-// 0 = off, unset = default set)
-static bool ring_enabled(int k) {
-  static const int env = [] {
-    const char* e = getenv("SPED_RING");
-    return e ? atoi(e) : -1;
-  }();
-  if (env >= 0) return env == 1;
-  (void)k;
-  return false;
-}
 
 // Launch one term over one column slab: one launch per row segment, the
 // long-row chunks riding in the leading blocks of the first launch.
@@ -788,12 +815,9 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       int sub = segs[i].sub;
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
-      if (w8 && sub == 1 && ring_enabled(k)) {
-        switch (lpr) {
-          case 4: launch_ring<4>(a, vm, s); break;
-          case 8: launch_ring<8>(a, vm, s); break;
-          default: launch_ring<16>(a, vm, s); break;
-        }
+      if (free_enabled()) {
+        if (w8) launch_free_w<8>(lpr, sub, a, vm, s);
+        else launch_free_w<4>(lpr, sub, a, vm, s);
       } else if (w8) {
         launch_rows_w<8>(lpr, sub, a, vm, s);
       } else {
@@ -1053,21 +1077,26 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
   }
 }
 
-// One term of a row shard whose CSR is split into own-column entries and
-// halo-column entries: pass 0 (raw_out) runs while the halo rows
-// are in flight and writes the raw own-column sum; pass 1 adds it to the
-// halo-column sum and applies the term epilogue.  Single term, stored values.
-extern "C" int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr,
-                                   const int32_t* indices, const float* values,
-                                   int32_t long_threshold, int32_t chunk_len,
-                                   const int32_t* chunk_desc, int64_t n_chunks, float* partials,
-                                   int32_t* tickets, const int64_t* segments, int32_t n_segments,
-                                   const float* x, const float* w, const float* partial_in,
-                                   int32_t raw_out, float* out, double alpha, double beta,
-                                   double gamma, double w0_scale, double lam_f, double s_final,
-                                   sped_stream_t stream) {
+// One polynomial term on a row shard.  E = w is the
+// [own | halo] block.  With a split CSR (own-column / halo-column entries)
+// pass 0 (raw_out) runs while the halo rows are in flight and writes the raw
+// own-column sum; pass 1 adds it (partial_in) to the halo-column sum and
+// applies the term epilogue.  An unsplit shard runs one pass.  scaled_in /
+// scaled_out: the scaled-normalized form of sped_csr_poly_apply (VM 2) --
+// E holds u = D^-1/2 w (own AND halo rows, so the exchange moves u),
+// neighbours are summed unweighted, row_scale = d^-1/2 of the own rows.
+// [hot_begin, hot_begin + hot_rows) rows of E get the persisting-L2 window.
+static int shard_term(int64_t n, int32_t k, const int32_t* indptr, const int32_t* indices,
+                      const float* values, int32_t long_threshold, int32_t chunk_len,
+                      const int32_t* chunk_desc, int64_t n_chunks, float* partials,
+                      int32_t* tickets, const int64_t* segments, int32_t n_segments,
+                      const float* row_scale, int32_t scaled_in, int32_t scaled_out,
+                      int64_t hot_begin, int64_t hot_rows, const float* x, const float* w,
+                      const float* partial_in, int32_t raw_out, float* out, double alpha,
+                      double beta, double gamma, double w0_scale, double lam_f, double s_final,
+                      sped_stream_t stream) {
   SPED_CHECK_ARG(n >= 0 && k >= 1, "bad shape n=%lld k=%d", (long long)n, k);
-  SPED_CHECK_ARG(n == 0 || (indptr && values && w && out), "null array");
+  SPED_CHECK_ARG(n == 0 || (indptr && w && out), "null array");
   SPED_CHECK_ARG(raw_out || x, "the epilogue pass needs x");
   SPED_CHECK_ARG(!raw_out || partial_in == nullptr, "the raw pass takes no partial input");
   SPED_CHECK_ARG(out != w && out != x, "out must not alias w or x");  // may alias partial_in
@@ -1077,6 +1106,10 @@ extern "C" int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr,
   SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX, "problem too large");
   SPED_CHECK_ARG(n_segments >= 0 && n_segments <= 8 && (n_segments == 0 || segments),
                  "bad segment table");
+  SPED_CHECK_ARG(!(scaled_in || scaled_out) || row_scale, "scaled terms need row_scale");
+  SPED_CHECK_ARG(scaled_in || values, "unscaled shard terms need stored values");
+  SPED_CHECK_ARG(!scaled_in || (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128),
+                 "scaled terms need k in {4, 8, 16, 32, 64, 128}");
   if (n == 0) return SPED_OK;
   cudaStream_t s = as_stream(stream);
   Segment fixed[8];
@@ -1101,8 +1134,13 @@ extern "C" int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr,
     if (alpha != 0.0) flags |= TF_ALPHA;
     if (gamma != 0.0) flags |= TF_GAMMA;
     if (lam_f != 0.0) flags |= TF_LAMF;
+    if (scaled_in) flags |= TF_NORM_IN;
+    if (scaled_out) flags |= TF_SCALE_OUT;
   }
+  const int vm = scaled_in ? 2 : 3;
   const int32_t slabs = (k + 127) / 128;
+  SPED_CHECK_ARG(!scaled_in || slabs == 1, "scaled terms need k <= 128");
+  if (hot_rows > 0) l2_window(s, w + hot_begin * (int64_t)k, (size_t)(hot_rows * (int64_t)k * 4));
   for (int32_t sl = 0; sl < slabs; ++sl) {
     const int32_t c0 = sl * 128;
     TermArgs a;
@@ -1132,16 +1170,50 @@ extern "C" int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr,
     a.tickets = tickets;
     a.row_begin = 0;
     a.row_end = n;
-    a.hot_rows = 0;
-    a.rscale = nullptr;
+    a.hot_rows = hot_rows;
+    a.rscale = row_scale;
     a.acc_in = partial_in ? partial_in + c0 : nullptr;
     const uintptr_t pbits = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) |
                             reinterpret_cast<uintptr_t>(out) |
                             reinterpret_cast<uintptr_t>(partial_in);
     const bool aligned = (k % 4 == 0) && (pbits % 16 == 0);
     const bool aligned32 = (k % 8 == 0) && (pbits % 32 == 0);
-    int rc = launch_term_slab(a, 3, aligned, aligned32, fixed, ns, s);
+    SPED_CHECK_ARG(!scaled_in || aligned, "scaled terms need 16-B aligned blocks");
+    int rc = launch_term_slab(a, vm, aligned, aligned32, fixed, ns, s);
     if (rc != SPED_OK) return rc;
   }
+  if (hot_rows > 0) l2_window(s, nullptr, 0);
   return SPED_OK;
+}
+
+extern "C" int sped_csr_term_split(int64_t n, int32_t k, const int32_t* indptr,
+                                   const int32_t* indices, const float* values,
+                                   int32_t long_threshold, int32_t chunk_len,
+                                   const int32_t* chunk_desc, int64_t n_chunks, float* partials,
+                                   int32_t* tickets, const int64_t* segments, int32_t n_segments,
+                                   const float* x, const float* w, const float* partial_in,
+                                   int32_t raw_out, float* out, double alpha, double beta,
+                                   double gamma, double w0_scale, double lam_f, double s_final,
+                                   sped_stream_t stream) {
+  return shard_term(n, k, indptr, indices, values, long_threshold, chunk_len, chunk_desc, n_chunks,
+                    partials, tickets, segments, n_segments, nullptr, 0, 0, 0, 0, x, w,
+                    partial_in, raw_out, out, alpha, beta, gamma, w0_scale, lam_f, s_final,
+                    stream);
+}
+
+extern "C" int sped_csr_term_shard(int64_t n, int32_t k, const int32_t* indptr,
+                                   const int32_t* indices, const float* values,
+                                   int32_t long_threshold, int32_t chunk_len,
+                                   const int32_t* chunk_desc, int64_t n_chunks, float* partials,
+                                   int32_t* tickets, const int64_t* segments, int32_t n_segments,
+                                   const float* row_scale, int32_t scaled_in, int32_t scaled_out,
+                                   int64_t hot_begin, int64_t hot_rows, const float* x,
+                                   const float* w, const float* partial_in, int32_t raw_out,
+                                   float* out, double alpha, double beta, double gamma,
+                                   double w0_scale, double lam_f, double s_final,
+                                   sped_stream_t stream) {
+  return shard_term(n, k, indptr, indices, values, long_threshold, chunk_len, chunk_desc, n_chunks,
+                    partials, tickets, segments, n_segments, row_scale, scaled_in, scaled_out,
+                    hot_begin, hot_rows, x, w, partial_in, raw_out, out, alpha, beta, gamma,
+                    w0_scale, lam_f, s_final, stream);
 }

@@ -48,6 +48,7 @@ is always ``sped_csr_poly_apply``.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -302,7 +303,7 @@ class SplitCSR:
 
     def __init__(self, indptr, indices, values, device, long_threshold: int, chunk_len: int):
         indptr = torch.as_tensor(indptr)
-        self.n = int(indptr.numel() - 1)
+        self.n = self.n_rows = int(indptr.numel() - 1)
         self.nnz = int(indptr[-1])
         self.rowlen = torch.diff(indptr).cpu().numpy()
         self.indptr = indptr.to(device=device, dtype=torch.int32)
@@ -321,21 +322,30 @@ class SplitCSR:
                                                 self.long_threshold if self.n_chunks else None)
         return self._segments[key]
 
-    def term(self, E, x_own, partial_in, raw_out, out, alpha, beta, gamma, w0, lam_f, s_final, k):
-        lib = _lib.load()
-        nseg, seg = self.segments(k)
-        partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=E.device)
-                    if self.n_chunks else None)
-        tickets = (torch.zeros(self.n_chunks, dtype=torch.int32, device=E.device)
-                   if self.n_chunks else None)
-        rc = lib.sped_csr_term_split(
-            self.n, k, _lib.ptr(self.indptr), _lib.ptr(self.indices), _lib.ptr(self.values),
-            self.long_threshold, self.chunk_len, _lib.ptr(self.chunk_desc), self.n_chunks,
-            _lib.ptr(partials), _lib.ptr(tickets), seg, nseg,
-            _lib.ptr(x_own), _lib.ptr(E), _lib.ptr(partial_in), int(raw_out), _lib.ptr(out),
-            float(alpha), float(beta), float(gamma), float(w0), float(lam_f), float(s_final),
-            _lib.stream_ptr(E.device))
-        _lib.check(rc, "sped_csr_term_split")
+    def term(self, E, x_own, partial_in, raw_out, out, alpha, beta, gamma, w0, lam_f, s_final, k,
+             row_scale=None, scaled_in=False, scaled_out=False, hot=(0, 0)):
+        _shard_term_call(self, E, x_own, partial_in, raw_out, out, alpha, beta, gamma, w0, lam_f,
+                         s_final, k, row_scale, scaled_in, scaled_out, hot)
+
+
+def _shard_term_call(csr, E, x_own, partial_in, raw_out, out, alpha, beta, gamma, w0, lam_f,
+                     s_final, k, row_scale, scaled_in, scaled_out, hot):
+    """sped_csr_term_shard on one (split or whole) shard CSR."""
+    lib = _lib.load()
+    nseg, seg = csr.segments(k)
+    partials = (torch.empty(csr.n_chunks * min(k, 128), dtype=torch.float32, device=E.device)
+                if csr.n_chunks else None)
+    tickets = (torch.zeros(csr.n_chunks, dtype=torch.int32, device=E.device)
+               if csr.n_chunks else None)
+    rc = lib.sped_csr_term_shard(
+        csr.n_rows, k, _lib.ptr(csr.indptr), _lib.ptr(csr.indices), _lib.ptr(csr.values),
+        csr.long_threshold, csr.chunk_len, _lib.ptr(csr.chunk_desc), csr.n_chunks,
+        _lib.ptr(partials), _lib.ptr(tickets), seg, nseg, _lib.ptr(row_scale), int(scaled_in),
+        int(scaled_out), int(hot[0]), int(hot[1]),
+        _lib.ptr(x_own), _lib.ptr(E), _lib.ptr(partial_in), int(raw_out), _lib.ptr(out),
+        float(alpha), float(beta), float(gamma), float(w0), float(lam_f), float(s_final),
+        _lib.stream_ptr(E.device))
+    _lib.check(rc, "sped_csr_term_shard")
 
 
 def _plan_chunks(n, nnz, indptr_dev, long_threshold, chunk_len, device):
@@ -506,6 +516,8 @@ class ShardedLaplacian:
                     (indptr_d[b:e + 1] - p0).to(torch.int32), cols,
                     None if lap.values is None else lap.values[p0:p1].contiguous(),
                     lap.long_threshold, lap.chunk_len, lap.reordered, eids, epos_l, ew)
+        if lap.row_scale is not None and os.environ.get("SPED_SHARD_SCALED", "1") != "0":
+            self.row_scale = lap.row_scale[b:e].contiguous()
 
     @classmethod
     def from_shard_edges(cls, se: ShardEdges, mode: str = "unnormalized", device=None,
@@ -574,6 +586,10 @@ class ShardedLaplacian:
                     None if se.unit_weight else w.to(torch.float32))
         self.perm = None if se.perm is None else se.perm.to(dev)
         self.degrees_own = deg[:nr]
+        if (normalized and se.unit_weight and vals is not None
+                and os.environ.get("SPED_SHARD_SCALED", "1") != "0"):
+            # the single-GPU row_scale: fp32(rsqrt(fp64 degree))
+            self.row_scale = torch.rsqrt(deg[:nr].double()).float().contiguous()
         return self
 
     def _setup(self, offsets, rank, world, group, plan, n_global, nnz_global, m_global, indptr,
@@ -612,7 +628,31 @@ class ShardedLaplacian:
             torch.int32).contiguous().view(-1)
         self.edge_w_l = edge_w
         self._eid_sorted, self._eid_order = torch.sort(eids)
+        self.row_scale = None       # d^-1/2 of the own rows: scaled-normalized terms
         self._plan_chunks()
+
+    @property
+    def n_rows(self) -> int:
+        return self.n_own
+
+    def scaled_terms(self, k: int) -> bool:
+        """Terms after the first run on u = D^-1/2 w without values (the
+        single-GPU VM 2 form; unit-weight normalized Laplacians)."""
+        return self.row_scale is not None and k in (4, 8, 16, 32, 64, 128)
+
+    def hot_range(self, k: int):
+        """Rows of E = [own | halo] holding the hub prefix of a
+        degree-ordered graph (the single-GPU operator's persisting window):
+        the own prefix on the shard that owns the hubs, the head of the halo
+        on the others."""
+        from .graph import HOT_FRACTION, L2_BYTES
+        if not self.sorted_rows:
+            return (0, 0)
+        H = int(min(self.n_global, HOT_FRACTION * L2_BYTES / (4 * max(k, 1))))
+        if self.row0 < H:
+            return (0, min(H, self.row0 + self.n_own) - self.row0)
+        halo = torch.as_tensor(self.plan.halo_cols)
+        return (self.n_own, int(torch.searchsorted(halo, torch.tensor(H, device=halo.device))))
 
     def _plan_chunks(self):
         self.n_chunks, self.chunk_desc = _plan_chunks(
@@ -633,13 +673,16 @@ class ShardedLaplacian:
                                     self.chunk_len) for ipp, idx, v in parts]
         return self._split
 
-    def partial_term(self, E, P, k):
+    def partial_term(self, E, P, k, scaled_in=False, scaled_out=False):
         """Pass 0: P = L_own E[:n_own] (own-column entries, no epilogue)."""
-        self.split[0].term(E, None, None, True, P, 0.0, 1.0, 0.0, 1.0, 0.0, 1.0, k)
+        self.split[0].term(E, None, None, True, P, 0.0, 1.0, 0.0, 1.0, 0.0, 1.0, k,
+                           self.row_scale, scaled_in, False, self.hot_range(k))
 
-    def remote_term(self, E, x_own, out, P, alpha, beta, gamma, w0, lam_f, s_final, k):
+    def remote_term(self, E, x_own, out, P, alpha, beta, gamma, w0, lam_f, s_final, k,
+                    scaled_in=False, scaled_out=False):
         """Pass 1: the term epilogue on L_halo E + P (= L E for the own rows)."""
-        self.split[1].term(E, x_own, P, False, out, alpha, beta, gamma, w0, lam_f, s_final, k)
+        self.split[1].term(E, x_own, P, False, out, alpha, beta, gamma, w0, lam_f, s_final, k,
+                           self.row_scale, scaled_in, scaled_out, self.hot_range(k))
 
     def segments(self, k):
         from .graph import segment_table
@@ -649,7 +692,12 @@ class ShardedLaplacian:
                                                 self.long_threshold if self.n_chunks else None)
         return self._segments[key]
 
-    def local_term(self, E, x_own, out, alpha, beta, gamma, w0, lam_f, s_final, k):
+    def local_term(self, E, x_own, out, alpha, beta, gamma, w0, lam_f, s_final, k,
+                   scaled_in=False, scaled_out=False):
+        if scaled_in or scaled_out or self.row_scale is not None:
+            _shard_term_call(self, E, x_own, None, False, out, alpha, beta, gamma, w0, lam_f,
+                             s_final, k, self.row_scale, scaled_in, scaled_out, self.hot_range(k))
+            return
         lib = _lib.load()
         nseg, seg = self.segments(k)
         partials = (torch.empty(self.n_chunks * min(k, 128), dtype=torch.float32, device=self.device)
@@ -742,6 +790,7 @@ class ShardedOperator:
         self.term_fn = term_fn or shard.local_term
         # own-column pass overlapping the exchange (product term kernels only)
         self.overlap = term_fn is None and bool(getattr(shard, "split_terms", False))
+        self.allow_scaled = term_fn is None
         self._ex = {}
         self._bufs = {}
         self._pbuf = {}
@@ -773,24 +822,28 @@ class ShardedOperator:
             if k not in self._pbuf:
                 self._pbuf[k] = torch.empty((sh.n_own, k), dtype=torch.float32, device=sh.device)
             P = self._pbuf[k]
+        scaled = (self.allow_scaled and len(al) >= 2
+                  and getattr(sh, "scaled_terms", lambda k: False)(k))
         for t in range(len(al)):
             final = t == len(al) - 1
             dst = out if final else nxt[: sh.n_own]
             coeffs = (al[t], be[t], ga[t], w0 if t == 0 else 1.0, lf if final else 0.0,
                       s if final else 1.0)
+            # scaled-normalized form: E carries u = D^-1/2 w after term 0
+            sk = {"scaled_in": t > 0, "scaled_out": not final} if scaled else {}
             if P is not None:
                 works = ex.start(cur)
-                sh.partial_term(cur, P, k)       # overlaps the halo transfer
+                sh.partial_term(cur, P, k, **sk)       # overlaps the halo transfer
                 ex.finish(works)
-                sh.remote_term(cur, x_own, dst, P, *coeffs, k)
+                sh.remote_term(cur, x_own, dst, P, *coeffs, k, **sk)
             else:
                 ex.exchange(cur)
-                self._term(t, cur, x_own, dst, *coeffs, k)
+                self._term(t, cur, x_own, dst, *coeffs, k, **sk)
             cur, nxt = nxt, cur
         return out
 
-    def _term(self, t, E, x_own, dst, al, be, ga, w0, lf, s, k):
-        self.term_fn(E, x_own, dst, al, be, ga, w0, lf, s, k)
+    def _term(self, t, E, x_own, dst, al, be, ga, w0, lf, s, k, **kw):
+        self.term_fn(E, x_own, dst, al, be, ga, w0, lf, s, k, **kw)
 
 
 class ShardedStochasticOperator(ShardedOperator):
@@ -810,6 +863,7 @@ class ShardedStochasticOperator(ShardedOperator):
         self.batch_fn = term_fn or shard.local_batch_term
         self._batch = None
         self.overlap = False  # edge-minibatch terms: one pass after the exchange
+        self.allow_scaled = False  # the minibatch estimate reads unscaled w
 
     @property
     def rng(self) -> np.random.Generator:
@@ -832,7 +886,7 @@ class ShardedStochasticOperator(ShardedOperator):
                        if nt > 0 and hasattr(self.shard, "compact_batch") else None)
         return super().apply_local(x_own, out)
 
-    def _term(self, t, E, x_own, dst, al, be, ga, w0, lf, s, k):
+    def _term(self, t, E, x_own, dst, al, be, ga, w0, lf, s, k, **kw):
         B = self.batch_size
         bt = self._batch[t * B:(t + 1) * B]
         if self._local is not None:

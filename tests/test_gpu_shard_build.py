@@ -119,13 +119,15 @@ def _halo_fill(E, shards, plans, cur, world):
             dst.copy_(E[q][cur][rows])
 
 
-@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
 @pytest.mark.parametrize("cfg,kind,ell", [(4, "negexp-taylor", 12), (5, "negexp-limit", 9),
-                                          (3, "negexp-taylor", 16)])
+                                          (3, "negexp-taylor", 16), (2, "negexp-limit", 17)])
 def test_shards_from_edges_apply(cuda, world, cfg, kind, ell):
     """Shards built from their incident edges run the overlapped split
     schedule (own-column pass while the halo is NaN, halo-column pass after)
-    and reproduce the single-GPU apply."""
+    and reproduce the single-GPU apply.  Normalized unit-weight graphs
+    (configs 2, 4) run the single-GPU scaled form: terms after the first
+    exchange and gather u = D^-1/2 w without values (sped_csr_term_shard)."""
     import paper_2207_14589_b200 as sp
     from paper_2207_14589_b200 import generators as G
     from paper_2207_14589_b200.distributed import ShardedLaplacian, build_halo_plans_local
@@ -155,18 +157,27 @@ def test_shards_from_edges_apply(cuda, world, cfg, kind, ell):
     P = [torch.empty_like(xs[r]) for r in range(world)]
     for r in range(world):
         E[r][0][: shards[r].n_own].copy_(xs[r])
+    scaled = shards[0].scaled_terms(k)
+    assert scaled == (spec["mode"] == "normalized" and g.is_unit_weight())
     cur = 0
     for tt in range(len(al)):
         final = tt == len(al) - 1
+        sk = {"scaled_in": tt > 0, "scaled_out": not final} if scaled else {}
+        coeffs = (al[tt], be[tt], ga[tt], w0 if tt == 0 else 1.0, lf if final else 0.0,
+                  s if final else 1.0)
+        if world == 1:  # no halo: one unsplit pass
+            shards[0].local_term(E[0][cur], xs[0], outs[0] if final else E[0][1 - cur], *coeffs,
+                                 k, **sk)
+            cur = 1 - cur
+            continue
         for r in range(world):
             E[r][cur][shards[r].n_own:].fill_(float("nan"))
-            shards[r].partial_term(E[r][cur], P[r], k)
+            shards[r].partial_term(E[r][cur], P[r], k, **sk)
         _halo_fill(E, shards, plans, cur, world)
         for r in range(world):
             sh = shards[r]
             dst = outs[r] if final else E[r][1 - cur][: sh.n_own]
-            sh.remote_term(E[r][cur], xs[r], dst, P[r], al[tt], be[tt], ga[tt],
-                           w0 if tt == 0 else 1.0, lf if final else 0.0, s if final else 1.0, k)
+            sh.remote_term(E[r][cur], xs[r], dst, P[r], *coeffs, k, **sk)
         cur = 1 - cur
     got = torch.cat(outs)
     assert torch.isfinite(got).all()
