@@ -177,6 +177,69 @@ def measured_traffic(workload):
     return float(d["dram_bytes_per_term"]), d["source"]
 
 
+class GpmDram:
+    """In-run DRAM traffic from the GPU's performance monitor (NVML GPM,
+    NVML_GPM_METRIC_DRAM_BW_UTIL = % of the device's DRAM bandwidth over a
+    sample interval).  The percentage's reference bandwidth is calibrated in
+    the same run against a device copy whose bytes are known (read + write
+    of a 2 GiB buffer), so ``bytes(fn)`` = util x calibrated bandwidth x
+    elapsed: the DRAM bytes a region moved, measured while it runs (no
+    profiler replay).  ``ok`` is False where GPM is unsupported."""
+
+    def __init__(self, device_index=0):
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(device_index)
+            sup = N.nvmlGpmQueryDeviceSupport(self.h)
+            if not getattr(sup, "isSupportedDevice", 0):
+                return
+            self.s = [N.nvmlGpmSampleAlloc(), N.nvmlGpmSampleAlloc()]
+            self.ok = True
+            self.ref_gbs = None
+        except Exception as exc:  # no NVML / GPM: report nothing, never guess
+            self.err = repr(exc)
+
+    def _util(self, fn):
+        import torch
+        N = self.N
+        torch.cuda.synchronize()
+        N.nvmlGpmSampleGet(self.h, self.s[0])
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        N.nvmlGpmSampleGet(self.h, self.s[1])
+        mg = N.c_nvmlGpmMetricsGet_t()
+        mg.version = N.NVML_GPM_METRICS_GET_VERSION
+        mg.numMetrics = 1
+        mg.sample1 = self.s[0]
+        mg.sample2 = self.s[1]
+        mg.metrics[0].metricId = N.NVML_GPM_METRIC_DRAM_BW_UTIL
+        N.nvmlGpmMetricsGet(mg)
+        return float(mg.metrics[0].value), dt
+
+    def calibrate(self):
+        import torch
+        a = torch.empty(1 << 29, dtype=torch.float32, device="cuda")  # 2 GiB
+        b = torch.empty_like(a)
+        a.fill_(1.0)
+        reps = 40
+        util, dt = self._util(lambda: [b.copy_(a) for _ in range(reps)])
+        moved = 2.0 * a.numel() * 4 * reps
+        self.ref_gbs = moved / dt / 1e9 / (util / 100.0) if util > 0 else None
+        self.calib = {"copy_GBps": moved / dt / 1e9, "gpm_util_pct": util,
+                      "reference_GBps": self.ref_gbs}
+        del a, b
+        return self.ref_gbs
+
+    def bytes(self, fn):
+        util, dt = self._util(fn)
+        return util / 100.0 * self.ref_gbs * 1e9 * dt, util, dt
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -590,7 +653,26 @@ def run_sped(args):
         bpt = (bpt + (n_terms - 1) * b_scaled) / n_terms
     peak, peak_src = measured_peak()
     achieved = bpt / t_term_s / 1e9
-    traffic, traffic_src = measured_traffic(spec["name"]) if not sharded else (None, None)
+    traffic, traffic_src, traffic_ncu = None, None, None
+    if not sharded:
+        ncu_bytes, ncu_src = measured_traffic(spec["name"])
+        traffic_ncu = {"bytes_per_term": ncu_bytes, "source": ncu_src} if ncu_bytes else None
+        gpm = GpmDram(torch.cuda.current_device())
+        if gpm.ok and gpm.calibrate():
+            reps = 8
+            xb = torch.randn((n, k), device=dev)
+            ob = torch.empty_like(xb)
+            op.apply_internal(xb, out=ob)
+            moved, util, dt = gpm.bytes(lambda: [op.apply_internal(xb, out=ob) for _ in range(reps)])
+            traffic = moved / (reps * n_terms)
+            traffic_src = ("in-run NVML GPM DRAM_BW_UTIL over %d applies (%.1f %% of %.0f GB/s "
+                           "for %.3f s), reference bandwidth calibrated on a 2 GiB device copy "
+                           "(%.0f GB/s at %.1f %%); per term = bytes / (applies x %d terms)"
+                           % (reps, util, gpm.ref_gbs, dt, gpm.calib["copy_GBps"],
+                              gpm.calib["gpm_util_pct"], n_terms))
+            del xb, ob
+        elif traffic_ncu:
+            traffic, traffic_src = ncu_bytes, ncu_src + " (GPM unavailable: %s)" % getattr(gpm, "err", "unsupported")
     # our kernels per step: per term one launch per row segment (+ the hub
     # chunk launch); Gram (tcgen05 partials + fp64 reduce), coefficients,
     # update.  Sharded: + the halo pack per term (NCCL's own kernels excluded).
@@ -685,6 +767,7 @@ def run_sped(args):
                          "stored values every term",
                          "peak_source": peak_src,
                          "traffic_source": traffic_src,
+                         "traffic_ncu": traffic_ncu,
                          "dram_frac_actual": (traffic / t_term_s / 1e9 / peak) if traffic else None},
             "cpu_baseline": cpu,
             "time_to_angle": conv,

@@ -7,19 +7,19 @@
 // so every intermediate block is written exactly once.
 //
 // Mapping (sm_100a, HBM/L2-gather bound):
-//  * one warp per row; the row's k columns are covered by LPR = k/4 lanes
-//    with 128-bit loads, and the SUB = 32/LPR lane groups split the row's
-//    nonzeros (a row's 32 column indices are fetched by one coalesced load
-//    and broadcast by shuffles), then a shuffle tree folds the SUB partials;
-//  * four gathers of w rows are kept in flight per lane (unrolled);
+//  * a row is owned by G = LPR*SUB lanes: LPR lanes cover its k columns with
+//    W-float (256-bit when k >= 32 and rows are 32-B aligned) loads, SUB
+//    lane slices split its nonzeros; lanes per row and SUB are chosen per
+//    row RANGE (degree-sorted rows) from a segment table;
+//  * shuffle-free: every lane slice walks its own nonzeros, reading column
+//    indices (and values) through L1, with U independent row gathers in
+//    flight -- no warp-uniform trip count, no index broadcast; the SUB
+//    partials fold with an xor tree (free_accumulate);
 //  * rows longer than `long_thresh` are cut into chunks (sped_spmm_plan);
-//    chunk warps run in the FIRST blocks of the same launch, write partial
-//    rows, and the last chunk to arrive (ticket) folds the partials in chunk
+//    the last chunk of a row to arrive (ticket) folds the partials in chunk
 //    order and applies the epilogue -> deterministic, no float atomics;
 //  * degree-relabelled graphs: a persisting-L2 access-policy window over
-//    the hub prefix of the gathered block keeps the most-gathered rows in L2
-//    (per-instruction evict_last/evict_first hints: compile-time SPED_HINTS,
-//    slower);
+//    the hub prefix of the gathered block keeps the most-gathered rows in L2;
 //  * unweighted combinatorial Laplacians use implicit values (-1 off the
 //    diagonal, row_len-1 on it): 4 B per nonzero instead of 8;
 //  * unweighted NORMALIZED Laplacians (no self loops) run every term after
@@ -31,39 +31,11 @@
 
 #include "sped_common.cuh"
 
-#ifndef TERM_MIN_BLOCKS
-#define TERM_MIN_BLOCKS 6
-#endif
-#ifndef TERM_MIN_BLOCKS_W8
-#define TERM_MIN_BLOCKS_W8 8  // full occupancy for the 256-bit one-group-per-row kernels (r01 sweep)
-#endif
-#ifndef SUB1_U
-#define SUB1_U 4
-#endif
-#ifndef W8_U
-#define W8_U 1  // one 256-bit gather in flight per lane, more rows resident instead
-#endif
-// k = 128 short rows (16 lanes x 256 bit per row, 2 rows per warp): four
-// gathers in flight per lane at 4 blocks/SM (config 5: 2.94 -> 2.80
-// ms/term; k = 64 stays at one gather in flight and 8 blocks/SM, where the
-// same change is slower: 0.539 -> 0.571; profiles/r02_ab_mlp_cfg*.log)
-#ifndef W8_K128_U
-#define W8_K128_U 4
-#endif
-#ifndef W8_K128_MINB
-#define W8_K128_MINB 4
-#endif
 #ifndef CHUNK_MIN_BLOCKS
 #define CHUNK_MIN_BLOCKS 4
 #endif
-#ifndef W8_LONG_U
-#define W8_LONG_U 4
-#endif
 #ifndef LONG_MIN_BLOCKS
 #define LONG_MIN_BLOCKS 4
-#endif
-#ifndef LONG_U
-#define LONG_U 8
 #endif
 
 namespace sped {
@@ -80,7 +52,7 @@ enum TermFlags : int {
 
 struct TermArgs {
   int64_t n;
-  int32_t k;    // columns in this slab / panel
+  int32_t k;    // columns in this slab
   int64_t ld;   // row stride of the gathered block win (floats)
   int64_t ldx;  // row stride of x
   int64_t ldo;  // row stride of wout (and acc_in)
@@ -100,9 +72,9 @@ struct TermArgs {
   float* partials;         // [n_chunks][k]
   int32_t* tickets;
   int64_t row_begin, row_end;  // this launch's row segment
-  int64_t hot_rows;        // hub prefix kept in L2 (persisting window; evict_last with SPED_HINTS)
+  int64_t hot_rows;        // hub prefix kept in L2 (persisting window)
   const float* rscale;     // d^-1/2 per row (TF_NORM_IN / TF_SCALE_OUT)
-  const float* acc_in;     // VM 3: partial neighbour sum added before the epilogue (or NULL)
+  const float* acc_in;     // VM 2/3: partial neighbour sum added before the epilogue (or NULL)
 };
 
 // VM 0: stored values; 1: implicit combinatorial (-1, row_len-1 on the
@@ -117,21 +89,24 @@ __device__ __forceinline__ float entry_value(const float* values, int64_t p, int
   return ld_stream_f32(values + p);
 }
 
-__device__ __forceinline__ float4 ldg_f4(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
-// column indices are read once per term: evict_first, so they do not displace
-// gathered rows (config 4: -1.5 %/term, profiles/r02_ab_cachepolicy.log)
-__device__ __forceinline__ int32_t ld_idx(const int32_t* p) {
-  int32_t r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
-      : "=r"(r) : "l"(p), "l"(policy_evict_first()));
-  return r;
-}
-__device__ __forceinline__ float ld_val(const float* p) {
-  float r;
-  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
-  return r;
+// CSR stream of the row sums: through L1 (the LPR lanes of a slice and the
+// next nonzeros of the same row share sectors); FREE_IDX_EF=1 also marks
+// the lines evict_first in L2 (read once per term)
+#ifndef FREE_IDX_EF
+#define FREE_IDX_EF 0
+#endif
+template <class T>
+__device__ __forceinline__ T ld_csr(const T* p) {
+#if FREE_IDX_EF
+  if constexpr (sizeof(T) == 4) {
+    uint32_t r;
+    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(policy_evict_first()));
+    T t;
+    memcpy(&t, &r, 4);
+    return t;
+  }
+#endif
+  return __ldg(p);
 }
 
 // W-float lane vectors: W = 4 (128-bit loads) or W = 8 (256-bit loads,
@@ -156,38 +131,6 @@ struct Vf {
     for (int i = 0; i < W; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
   }
 };
-
-#ifndef SPED_HINTS
-#define SPED_HINTS 0  // L2 policy hints: -14% DRAM bytes but +3-6% time (r01 sweep)
-#endif
-
-// gathers of hot rows (index < hot_rows, the degree-ordered prefix) are kept
-// in L2 (evict_last); cold rows and the streamed CSR arrays are evict_first
-template <int W>
-__device__ __forceinline__ Vf<W> ldg_vec_pol(const float* p, uint64_t pol) {
-  Vf<W> r;
-  if constexpr (W == 8) {
-    asm("ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
-        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
-          "=f"(r.v[6]), "=f"(r.v[7])
-        : "l"(p), "l"(pol));
-  } else {
-    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
-        : "l"(p), "l"(pol));
-  }
-  return r;
-}
-__device__ __forceinline__ int32_t ld_idx_pol(const int32_t* p, uint64_t pol) {
-  int32_t r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ float ld_val_pol(const float* p, uint64_t pol) {
-  float r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
-  return r;
-}
 
 template <int W>
 __device__ __forceinline__ Vf<W> ldg_vec(const float* p) {
@@ -218,93 +161,6 @@ __device__ __forceinline__ void st_stream_vec(float* p, const Vf<W>& x) {
 #pragma unroll
   for (int h = 0; h < W / 4; ++h)
     st_stream_f4(p + 4 * h, make_float4(x.v[4 * h], x.v[4 * h + 1], x.v[4 * h + 2], x.v[4 * h + 3]));
-}
-
-// One row per group of G = LPR*SUB lanes (32/G rows per warp).  Within a
-// group, LPR lanes cover the k = W*LPR columns with W-float loads and SUB
-// lane subgroups split the row's nonzeros; U gathers per lane are in flight
-// per round.  Loop bounds are warp-uniform (max over the warp's rows) so the
-// shuffles stay convergent; rows are predicated.  Returns the folded row sum
-// in the sub==0 lanes of each group.
-template <int W, int LPR, int SUB, int U, int VM>
-__device__ __forceinline__ Vf<W> group_row_accumulate(const TermArgs& a, int32_t row, bool valid,
-                                                      int32_t b, int32_t e, int32_t rowlen,
-                                                      int lane) {
-  constexpr int G = LPR * SUB;
-  const int g = lane % G;
-  const int gbase = lane - g;
-  const int sub = g / LPR;
-  const int cl = g % LPR;
-  // single-slab rows are exactly W*LPR floats: compile-time stride
-  const bool single = (a.ld == W * LPR);
-  const float* wbase = a.win + cl * W;
-#if SPED_HINTS
-  // 1: hot gathers evict_last, cold evict_first; 2: hot gathers unchanged (the
-  // persisting window holds them), cold gathers evict_first
-  const uint64_t pol_hot = SPED_HINTS == 2 ? policy_evict_unchanged() : policy_evict_last();
-  const uint64_t pol_cold = policy_evict_first();
-  const int32_t hot = (int32_t)min(a.hot_rows, (int64_t)INT32_MAX);
-#endif
-  Vf<W> acc;
-  acc.zero();
-  const int32_t len = valid ? e - b : 0;
-  int32_t maxlen = len;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
-  for (int32_t o = 0; o < maxlen; o += G) {
-    const int32_t p = b + o + g;
-    int32_t col = 0;
-    float val = 0.f;
-    if (o + g < len) {
-#if SPED_HINTS
-      col = ld_idx_pol(a.indices + p, pol_cold);
-#else
-      col = ld_idx(a.indices + p);
-#endif
-      if (VM == 1)
-        val = col == row ? (float)(rowlen - 1) : -1.0f;
-      else if (VM == 2)
-        val = col == row ? 0.0f : 1.0f;
-      else
-#if SPED_HINTS
-        val = ld_val_pol(a.values + p, pol_cold);
-#else
-        val = ld_val(a.values + p);
-#endif
-    }
-    const int cnt = max(0, min(G, len - o));
-    const int mcnt = min(G, maxlen - o);
-    const int T = (mcnt + SUB - 1) / SUB;
-    for (int t = 0; t < T; t += U) {
-      Vf<W> gv[U];
-      float w[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = (t + u) * SUB + sub;
-        const int js = gbase + (j < G ? j : G - 1);
-        const int32_t c = __shfl_sync(0xffffffffu, col, js);
-        w[u] = __shfl_sync(0xffffffffu, val, js);
-        if (j < cnt) {
-#if SPED_HINTS
-          const uint64_t pol = c < hot ? pol_hot : pol_cold;
-          gv[u] = single ? ldg_vec_pol<W>(wbase + (int64_t)c * (W * LPR), pol)
-                         : ldg_vec_pol<W>(wbase + (int64_t)c * a.ld, pol);
-#else
-          gv[u] = single ? ldg_vec<W>(wbase + (int64_t)c * (W * LPR))
-                         : ldg_vec<W>(wbase + (int64_t)c * a.ld);
-#endif
-        } else {
-          gv[u].zero();
-          w[u] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc.fma(w[u], gv[u]);
-    }
-  }
-#pragma unroll
-  for (int off = LPR; off < G; off <<= 1) acc.add_xor(off);
-  return acc;
 }
 
 // ds = d_i^-1/2 (only read with TF_NORM_IN / TF_SCALE_OUT).  With TF_NORM_IN
@@ -365,6 +221,12 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
 #ifndef FREE_LONG_U
 #define FREE_LONG_U 4
 #endif
+#ifndef FREE_K128_U
+#define FREE_K128_U 3  // k = 128 rows (16 lanes): config 5 2.41 -> 2.36 ms/term
+#endif
+#ifndef FREE_K128_MINB
+#define FREE_K128_MINB 5
+#endif
 template <int W, int LPR, int SUB, int U, int VM>
 __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row, bool valid,
                                                  int32_t b, int32_t e, int32_t rowlen, int lane) {
@@ -383,10 +245,10 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        c[u] = __ldg(a.indices + p + u * SUB);
+        c[u] = ld_csr(a.indices + p + u * SUB);
         if (VM == 1) v[u] = c[u] == row ? (float)(rowlen - 1) : -1.0f;
         else if (VM == 2) v[u] = c[u] == row ? 0.0f : 1.0f;
-        else v[u] = __ldg(a.values + p + u * SUB);
+        else v[u] = ld_csr(a.values + p + u * SUB);
       }
       Vf<W> gv[U];
 #pragma unroll
@@ -395,11 +257,11 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       for (int u = 0; u < U; ++u) acc.fma(v[u], gv[u]);
     }
     for (; p < e; p += SUB) {
-      const int32_t c = __ldg(a.indices + p);
+      const int32_t c = ld_csr(a.indices + p);
       float v;
       if (VM == 1) v = c == row ? (float)(rowlen - 1) : -1.0f;
       else if (VM == 2) v = c == row ? 0.0f : 1.0f;
-      else v = __ldg(a.values + p);
+      else v = ld_csr(a.values + p);
       acc.fma(v, ldg_vec<W>(wbase + (int64_t)c * ldw));
     }
   }
@@ -409,7 +271,7 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
 }
 
 template <int W, int LPR, int SUB, int VM>
-__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : FREE_MINB)) spmm_free_kernel(const TermArgs a) {
+__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W * LPR >= 128 ? FREE_K128_MINB : FREE_MINB))) spmm_free_kernel(const TermArgs a) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31;
@@ -429,7 +291,8 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : FREE_MINB)) 
   } else if (!valid) {
     return;
   }
-  Vf<W> acc = free_accumulate<W, LPR, SUB, (SUB > 1 ? FREE_LONG_U : FREE_U), VM>(
+  Vf<W> acc = free_accumulate<W, LPR, SUB,
+                              (SUB > 1 ? FREE_LONG_U : (W * LPR >= 128 ? FREE_K128_U : FREE_U)), VM>(
       a, row, valid, b, e, e - b, lane);
   if (!valid || g >= LPR) return;
   const int64_t off = (int64_t)row * a.ld + cl * W;
@@ -484,19 +347,12 @@ static void launch_free_w(int lpr, int sub, const TermArgs& a, int vm, cudaStrea
   }
 }
 
-static bool free_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("SPED_FREE");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
 
 // Long-row chunks: one warp per chunk (all 32/LPR lane groups over the
 // chunk's nonzeros).  The last chunk of a row to finish (ticket) folds the
 // partial rows in chunk order and applies the epilogue: deterministic, no
 // float atomics.
-template <int W, int LPR, int U, int VM, bool FREE = false>
+template <int W, int LPR, int U, int VM>
 __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const TermArgs a) {
   const int lane = threadIdx.x & 31;
   const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
@@ -507,11 +363,7 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
   const int32_t pe = a.chunk_desc[4 * c + 2];
   const int32_t c0 = a.chunk_desc[4 * c + 3];
   const int32_t rb = a.indptr[row], re = a.indptr[row + 1];
-  Vf<W> acc;
-  if constexpr (FREE)
-    acc = free_accumulate<W, LPR, 32 / LPR, U, VM>(a, row, true, pb, pe, re - rb, lane);
-  else
-    acc = group_row_accumulate<W, LPR, 32 / LPR, U, VM>(a, row, true, pb, pe, re - rb, lane);
+  const Vf<W> acc = free_accumulate<W, LPR, 32 / LPR, U, VM>(a, row, true, pb, pe, re - rb, lane);
   const int lsub = lane / LPR, lcl = lane % LPR;
   if (lsub == 0) {
 #pragma unroll
@@ -558,46 +410,6 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
   }
   if (lane == 0) a.tickets[c0] = 0;
 }
-
-template <int W, int LPR, int SUB, int U, int VM>
-__global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W == 8 ? (LPR >= 16 ? W8_K128_MINB : TERM_MIN_BLOCKS_W8) : TERM_MIN_BLOCKS))) spmm_term_kernel(const TermArgs a) {
-  constexpr int G = LPR * SUB;
-  constexpr int RPW = 32 / G;
-  const int lane = threadIdx.x & 31;
-  const int g = lane % G;
-  const int sub = g / LPR;
-  const int cl = g % LPR;
-  const int32_t wglobal = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int32_t row = (int32_t)a.row_begin + wglobal * RPW + lane / G;
-  bool valid = row < a.row_end;
-  int32_t b = 0, e = 0;
-  if (valid) {
-    b = __ldg(a.indptr + row);
-    e = __ldg(a.indptr + row + 1);
-    if (e - b > a.long_thresh) valid = false;
-  }
-  if (__all_sync(0xffffffffu, !valid)) return;
-  Vf<W> acc = group_row_accumulate<W, LPR, SUB, U, VM>(a, row, valid, b, e, e - b, lane);
-  if (valid && sub == 0) {
-    const int64_t off = (int64_t)row * a.ld + cl * W;
-    const int64_t offo = (int64_t)row * a.ldo + cl * W;
-    if (VM == 3 || VM == 2) {
-      if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + offo));
-      if (a.flags & TF_RAW_OUT) {
-        st_stream_vec<W>(a.wout + offo, acc);
-        return;
-      }
-    }
-    const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
-    Vf<W> xr, wr;
-    xr.zero();
-    wr.zero();
-    if (need_x) xr = ld_stream_vec<W>(a.x + (int64_t)row * a.ldx + cl * W);
-    if (a.flags & (TF_GAMMA | TF_NORM_IN)) wr = ldg_vec<W>(a.win + off);
-    st_stream_vec<W>(a.wout + offo, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
-  }
-}
-
 
 // Generic slab (k not in {4,8,...,128} or unaligned): scalar loads, LPR
 // lanes over columns (CPL columns each), SUB groups over nonzeros.  Handles
@@ -679,61 +491,14 @@ __global__ void __launch_bounds__(256) spmm_term_generic(const TermArgs a) {
   }
 }
 
-constexpr int UNROLL = 4;
-
-template <int W, int LPR, int SUB,
-          int U = (SUB > 1 ? (W == 8 ? W8_LONG_U : LONG_U)
-                           : (W == 8 ? (LPR >= 16 ? W8_K128_U : W8_U) : SUB1_U))>
-static void launch_fast(const TermArgs& a, int vm, cudaStream_t s) {
-  constexpr int G = LPR * SUB;
-  constexpr int RPW = 32 / G;
-  const int threads = 256;
-  const int wpb = threads / 32;
-  const int64_t rows = a.row_end - a.row_begin;
-  const int64_t warps = (rows + RPW - 1) / RPW;
-  const unsigned grid = (unsigned)((warps + wpb - 1) / wpb);
-  if (grid == 0) return;
-  if (vm == 1)
-    spmm_term_kernel<W, LPR, SUB, U, 1><<<grid, threads, 0, s>>>(a);
-  else if (vm == 2)
-    spmm_term_kernel<W, LPR, SUB, U, 2><<<grid, threads, 0, s>>>(a);
-  else if (vm == 3)
-    spmm_term_kernel<W, LPR, SUB, U, 3><<<grid, threads, 0, s>>>(a);
-  else
-    spmm_term_kernel<W, LPR, SUB, U, 0><<<grid, threads, 0, s>>>(a);
-}
-
 template <int W, int LPR>
 static void launch_chunks(const TermArgs& a, int vm, cudaStream_t s) {
   const unsigned grid = (unsigned)((a.n_chunks + 7) / 8);
   if (grid == 0) return;
-  constexpr int U = (W == 8 ? W8_LONG_U : LONG_U);
-  if (free_enabled()) {
-    if (vm == 1) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 1, true><<<grid, 256, 0, s>>>(a);
-    else if (vm == 2) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 2, true><<<grid, 256, 0, s>>>(a);
-    else if (vm == 3) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 3, true><<<grid, 256, 0, s>>>(a);
-    else spmm_chunk_kernel<W, LPR, FREE_LONG_U, 0, true><<<grid, 256, 0, s>>>(a);
-    return;
-  }
-  if (vm == 1)
-    spmm_chunk_kernel<W, LPR, U, 1><<<grid, 256, 0, s>>>(a);
-  else if (vm == 2)
-    spmm_chunk_kernel<W, LPR, U, 2><<<grid, 256, 0, s>>>(a);
-  else if (vm == 3)
-    spmm_chunk_kernel<W, LPR, U, 3><<<grid, 256, 0, s>>>(a);
-  else
-    spmm_chunk_kernel<W, LPR, U, 0><<<grid, 256, 0, s>>>(a);
-}
-
-template <int W, int LPR>
-static void launch_fast_sub(const TermArgs& a, int sub, int vm, cudaStream_t s) {
-  switch (sub) {
-    case 1: launch_fast<W, LPR, 1>(a, vm, s); break;
-    case 2: if constexpr (LPR * 2 <= 32) { launch_fast<W, LPR, 2>(a, vm, s); break; } [[fallthrough]];
-    case 4: if constexpr (LPR * 4 <= 32) { launch_fast<W, LPR, 4>(a, vm, s); break; } [[fallthrough]];
-    case 8: if constexpr (LPR * 8 <= 32) { launch_fast<W, LPR, 8>(a, vm, s); break; } [[fallthrough]];
-    default: launch_fast<W, LPR, 32 / LPR>(a, vm, s); break;
-  }
+  if (vm == 1) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 1><<<grid, 256, 0, s>>>(a);
+  else if (vm == 2) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 2><<<grid, 256, 0, s>>>(a);
+  else if (vm == 3) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 3><<<grid, 256, 0, s>>>(a);
+  else spmm_chunk_kernel<W, LPR, FREE_LONG_U, 0><<<grid, 256, 0, s>>>(a);
 }
 
 // width dispatch: W = 8 (256-bit gathers) when k % 8 == 0 and rows are 32 B
@@ -749,18 +514,6 @@ static void launch_chunks_w(int lpr, const TermArgs& a, int vm, cudaStream_t s) 
     default: if constexpr (W == 4) launch_chunks<W, 32>(a, vm, s); break;
   }
 }
-template <int W>
-static void launch_rows_w(int lpr, int sub, const TermArgs& a, int vm, cudaStream_t s) {
-  switch (lpr) {
-    case 1: launch_fast_sub<W, 1>(a, sub, vm, s); break;
-    case 2: launch_fast_sub<W, 2>(a, sub, vm, s); break;
-    case 4: launch_fast_sub<W, 4>(a, sub, vm, s); break;
-    case 8: launch_fast_sub<W, 8>(a, sub, vm, s); break;
-    case 16: launch_fast_sub<W, 16>(a, sub, vm, s); break;
-    default: if constexpr (W == 4) launch_fast_sub<W, 32>(a, sub, vm, s); break;
-  }
-}
-
 template <int LPR, int CPL>
 static void launch_generic(const TermArgs& a, int vm, cudaStream_t s) {  // vm 0 / 1 / 3
   const int threads = 256;
@@ -815,14 +568,8 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       int sub = segs[i].sub;
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
-      if (free_enabled()) {
-        if (w8) launch_free_w<8>(lpr, sub, a, vm, s);
-        else launch_free_w<4>(lpr, sub, a, vm, s);
-      } else if (w8) {
-        launch_rows_w<8>(lpr, sub, a, vm, s);
-      } else {
-        launch_rows_w<4>(lpr, sub, a, vm, s);
-      }
+      if (w8) launch_free_w<8>(lpr, sub, a, vm, s);
+      else launch_free_w<4>(lpr, sub, a, vm, s);
       SPED_LAUNCH_CHECK();
     }
     const int rc = chunks();
