@@ -166,9 +166,11 @@ class ClockSampler:
 
 
 def measured_traffic(workload):
-    """DRAM bytes per term of the SpMM launches from the committed ncu
-    capture (profiles/r01_traffic.json), or None."""
-    p = ROOT / "profiles" / "r01_traffic.json"
+    """DRAM bytes per term of the SpMM launches from the latest committed
+    ncu capture (profiles/r02_traffic.json, else r01), or None."""
+    p = ROOT / "profiles" / "r02_traffic.json"
+    if not p.exists():
+        p = ROOT / "profiles" / "r01_traffic.json"
     if not p.exists():
         return None, None
     d = json.loads(p.read_text()).get(workload)
@@ -177,67 +179,42 @@ def measured_traffic(workload):
     return float(d["dram_bytes_per_term"]), d["source"]
 
 
-class GpmDram:
-    """In-run DRAM traffic from the GPU's performance monitor (NVML GPM,
-    NVML_GPM_METRIC_DRAM_BW_UTIL = % of the device's DRAM bandwidth over a
-    sample interval).  The percentage's reference bandwidth is calibrated in
-    the same run against a device copy whose bytes are known (read + write
-    of a 2 GiB buffer), so ``bytes(fn)`` = util x calibrated bandwidth x
-    elapsed: the DRAM bytes a region moved, measured while it runs (no
-    profiler replay).  ``ok`` is False where GPM is unsupported."""
+class DramMeter:
+    """In-run DRAM traffic: bench_support/libdram_meter.so runs the CUPTI
+    Range Profiler over one user range (single pass, no kernel replay) and
+    returns dram__bytes_read.sum + dram__bytes_write.sum of everything the
+    region launched -- the bytes the SpMM applies moved while they ran, on
+    the bench's own process and clocks.  ``ok`` is False (with ``err``) when
+    the library or the profiler is unavailable; nothing is guessed then."""
 
     def __init__(self, device_index=0):
-        self.ok = False
+        import ctypes as C
+        self.ok, self.err = False, None
+        path = ROOT / "bench_support" / "libdram_meter.so"
         try:
-            import pynvml as N
-            N.nvmlInit()
-            self.N = N
-            self.h = N.nvmlDeviceGetHandleByIndex(device_index)
-            sup = N.nvmlGpmQueryDeviceSupport(self.h)
-            if not getattr(sup, "isSupportedDevice", 0):
+            lib = C.CDLL(str(path))
+            lib.dm_error.restype = C.c_char_p
+            lib.dm_end.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
+            if lib.dm_init(int(device_index)) != 0:
+                self.err = lib.dm_error().decode()
                 return
-            self.s = [N.nvmlGpmSampleAlloc(), N.nvmlGpmSampleAlloc()]
+            self.lib, self.C = lib, C
             self.ok = True
-            self.ref_gbs = None
-        except Exception as exc:  # no NVML / GPM: report nothing, never guess
+        except OSError as exc:
             self.err = repr(exc)
 
-    def _util(self, fn):
+    def bytes(self, fn):
         import torch
-        N = self.N
+        C = self.C
         torch.cuda.synchronize()
-        N.nvmlGpmSampleGet(self.h, self.s[0])
-        t0 = time.perf_counter()
+        if self.lib.dm_begin() != 0:
+            raise RuntimeError(self.lib.dm_error().decode())
         fn()
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        N.nvmlGpmSampleGet(self.h, self.s[1])
-        mg = N.c_nvmlGpmMetricsGet_t()
-        mg.version = N.NVML_GPM_METRICS_GET_VERSION
-        mg.numMetrics = 1
-        mg.sample1 = self.s[0]
-        mg.sample2 = self.s[1]
-        mg.metrics[0].metricId = N.NVML_GPM_METRIC_DRAM_BW_UTIL
-        N.nvmlGpmMetricsGet(mg)
-        return float(mg.metrics[0].value), dt
-
-    def calibrate(self):
-        import torch
-        a = torch.empty(1 << 29, dtype=torch.float32, device="cuda")  # 2 GiB
-        b = torch.empty_like(a)
-        a.fill_(1.0)
-        reps = 40
-        util, dt = self._util(lambda: [b.copy_(a) for _ in range(reps)])
-        moved = 2.0 * a.numel() * 4 * reps
-        self.ref_gbs = moved / dt / 1e9 / (util / 100.0) if util > 0 else None
-        self.calib = {"copy_GBps": moved / dt / 1e9, "gpm_util_pct": util,
-                      "reference_GBps": self.ref_gbs}
-        del a, b
-        return self.ref_gbs
-
-    def bytes(self, fn):
-        util, dt = self._util(fn)
-        return util / 100.0 * self.ref_gbs * 1e9 * dt, util, dt
+        rd, wr = C.c_double(0), C.c_double(0)
+        if self.lib.dm_end(C.byref(rd), C.byref(wr)) != 0:
+            raise RuntimeError(self.lib.dm_error().decode())
+        return rd.value, wr.value
 
 
 def measured_peak():
@@ -657,22 +634,27 @@ def run_sped(args):
     if not sharded:
         ncu_bytes, ncu_src = measured_traffic(spec["name"])
         traffic_ncu = {"bytes_per_term": ncu_bytes, "source": ncu_src} if ncu_bytes else None
-        gpm = GpmDram(torch.cuda.current_device())
-        if gpm.ok and gpm.calibrate():
-            reps = 8
-            xb = torch.randn((n, k), device=dev)
-            ob = torch.empty_like(xb)
-            op.apply_internal(xb, out=ob)
-            moved, util, dt = gpm.bytes(lambda: [op.apply_internal(xb, out=ob) for _ in range(reps)])
-            traffic = moved / (reps * n_terms)
-            traffic_src = ("in-run NVML GPM DRAM_BW_UTIL over %d applies (%.1f %% of %.0f GB/s "
-                           "for %.3f s), reference bandwidth calibrated on a 2 GiB device copy "
-                           "(%.0f GB/s at %.1f %%); per term = bytes / (applies x %d terms)"
-                           % (reps, util, gpm.ref_gbs, dt, gpm.calib["copy_GBps"],
-                              gpm.calib["gpm_util_pct"], n_terms))
-            del xb, ob
-        elif traffic_ncu:
-            traffic, traffic_src = ncu_bytes, ncu_src + " (GPM unavailable: %s)" % getattr(gpm, "err", "unsupported")
+        meter = DramMeter(torch.cuda.current_device())
+        if meter.ok:
+            try:
+                reps = 4
+                xb = torch.randn((n, k), device=dev)
+                ob = torch.empty_like(xb)
+                op.apply_internal(xb, out=ob)
+                rd, wr = meter.bytes(lambda: [op.apply_internal(xb, out=ob) for _ in range(reps)])
+                traffic = (rd + wr) / (reps * n_terms)
+                traffic_src = ("in-run CUPTI range profiler (bench_support/libdram_meter.so): "
+                               "dram__bytes_read.sum + dram__bytes_write.sum over %d whole "
+                               "applies (%.2f + %.2f GB), per term = bytes / (%d x %d terms)"
+                               % (reps, rd / 1e9, wr / 1e9, reps, n_terms))
+                del xb, ob
+            except RuntimeError as exc:
+                meter.err = str(exc)
+                traffic = None
+            meter.lib.dm_close()
+        if traffic is None and traffic_ncu:
+            traffic, traffic_src = ncu_bytes, (ncu_src + " (in-run meter unavailable: %s)"
+                                               % meter.err)
     # our kernels per step: per term one launch per row segment (+ the hub
     # chunk launch); Gram (tcgen05 partials + fp64 reduce), coefficients,
     # update.  Sharded: + the halo pack per term (NCCL's own kernels excluded).

@@ -1,6 +1,6 @@
 #!/bin/bash
 # compute-sanitizer (memcheck / racecheck / synccheck) over the parity tests
-# of the riskiest kernels: SpMM hub-chunk tickets, the smem-ring SpMM, the
+# of the riskiest kernels: SpMM hub-chunk tickets, the
 # tcgen05 Gram/update mbarrier rings, the grid-resident K7 tag protocol,
 # the edge-minibatch sort/sweep and the row-shard build.  Logs -> gpurun_out/sanitize_*.log
 O=gpurun_out
@@ -10,7 +10,7 @@ FILES="tests/test_gpu_parity.py tests/test_gpu_solver.py tests/test_gpu_shard_bu
 for tool in memcheck racecheck synccheck; do
   extra=""
   [ $tool = memcheck ] && extra="--leak-check no"
-  SPED_RING=1 timeout 1500 $CS --tool $tool $extra --target-processes all --print-limit 50 \
+  timeout 1500 $CS --tool $tool $extra --target-processes all --print-limit 50 \
     python -m pytest -q -x -p no:cacheprovider $FILES -k "$SEL_MEM" > $O/sanitize_$tool.log 2>&1
   echo "exit=$?" >> $O/sanitize_$tool.log
 done
