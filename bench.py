@@ -539,24 +539,41 @@ def run_sped(args):
     k, ell, mode = spec["k"], spec["ell"], spec["mode"]
     t_setup = time.perf_counter()
     n, u, v, w = G.config_graph(args.config, device=dev, scale=args.scale)
-    g = sp.Graph.from_canonical(n, u, v, w, validate=False)
     t = transform_for(spec)
-    op = sp.make_reversed_operator(g, t, mode, device=dev)
-    lap = op.laplacian
-    nnz = lap.nnz
-    stored = lap.values is not None
-    al, be, ga, w0, lf, s = op.schedule
+    if sharded:
+        # no whole graph on any rank: each rank keeps a strided slice of the
+        # (seeded, identical) generator output, routes it to the row owners
+        # and builds only its rows (plan_shard_edges + from_shard_edges)
+        from paper_2207_14589_b200.distributed import (ShardedLaplacian, ShardedOperator,
+                                                       plan_shard_edges, sharded_mu_eg_step)
+        from paper_2207_14589_b200.transforms import choose_lambda_star, term_schedule
+        m_all = int(u.numel())
+        sel = torch.arange(rank, m_all, world, device=dev)
+        se = plan_shard_edges(n, u[sel], v[sel], w[sel], sel, rank, world)
+        del u, v, w, sel
+        shard = ShardedLaplacian.from_shard_edges(se, mode, device=dev)
+        lam_star = choose_lambda_star(t, shard.lambda_upper(mode))
+        sop = ShardedOperator(shard, t, lam_star)
+        n_loc = shard.n_own
+        g = None
+        lap = None
+        nnz = int(shard.nnz_global)
+        m_graph = int(se.m)
+        stored = shard.values is not None
+        al, be, ga, w0, lf, s = term_schedule(t, lam_star)
+        del se
+    else:
+        g = sp.Graph.from_canonical(n, u, v, w, validate=False)
+        op = sp.make_reversed_operator(g, t, mode, device=dev)
+        lap = op.laplacian
+        nnz = lap.nnz
+        m_graph = g.m
+        stored = lap.values is not None
+        al, be, ga, w0, lf, s = op.schedule
+        n_loc = n
     n_terms = len(al)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
-
-    if sharded:
-        from paper_2207_14589_b200.distributed import ShardedLaplacian, ShardedOperator, sharded_mu_eg_step
-        shard = ShardedLaplacian(lap, rank, world)
-        sop = ShardedOperator(shard, t, op.lambda_star)
-        n_loc = shard.n_own
-    else:
-        n_loc = n
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     V = torch.randn((n_loc, k), device=dev, generator=gen)
     V /= torch.linalg.norm(V, dim=0) * (world ** 0.5)
@@ -623,7 +640,7 @@ def run_sped(args):
     n_b, nnz_b = (n, nnz) if not sharded else (n_loc, shard.nnz_local)
     x_term = any(a != 0 for a in al)
     bpt = bytes_per_term(n_b, nnz_b, k, stored, x_term, lf != 0.0)
-    scaled = (not sharded) and lap.row_scale is not None and n_terms >= 2
+    scaled = n_terms >= 2 and (shard.scaled_terms(k) if sharded else lap.row_scale is not None)
     if scaled:
         # terms after the first run on u = D^-1/2 w: no values, + d^-1/2 per row
         b_scaled = bytes_per_term(n_b, nnz_b, k, False, x_term, lf != 0.0) + 4 * n_b
@@ -733,7 +750,7 @@ def run_sped(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, BASELINE shape)",
-            "config": workload_config(spec, args.config, n, g.m, nnz, world, eta),
+            "config": workload_config(spec, args.config, n, m_graph, nnz, world, eta),
             "setup_s": setup_s,
             "pLV_nnz_k_per_s": work * args.steps / (apply_ms / 1e3),
             "breakdown_ms_per_step": {"p(L)V": apply_ms / args.steps,

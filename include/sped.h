@@ -363,6 +363,15 @@ int sped_row_dist2(int64_t n, int32_t d, const float* X, const double* center,
 int sped_gather_rows(int64_t count, int32_t k, const int32_t* rows, const float* src,
                      float* dst, sped_stream_t stream);
 
+/* ---- debug-check builds (-DSPED_DEBUG_CHECKS=1) ----------------------------
+ * sped_debug_checks() is 1 in such a build; sped_debug_take() returns and
+ * clears the OR of the device-side check bits (gather out of the input
+ * block 1, hub-chunk ticket overflow 2, CSR position outside its row 4,
+ * stochastic record out of range 8).  Synchronises the device.  Always 0 in
+ * release builds. */
+int sped_debug_checks(void);
+unsigned int sped_debug_take(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,8 @@ SIGNATURES = {
     "sped_kmeans_assign": (C.c_int, [_i64, _i32, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "sped_row_dist2": (C.c_int, [_i64, _i32, _p, _p, _p, _i32, _p]),
     "sped_gather_rows": (C.c_int, [_i64, _i32, _p, _p, _p, _p]),
+    "sped_debug_checks": (C.c_int, []),
+    "sped_debug_take": (_u32, []),
 }
 
 _lib = None

@@ -63,3 +63,12 @@ extern "C" int sped_gather_rows(int64_t count, int32_t k, const int32_t* rows, c
   SPED_LAUNCH_CHECK();
   return SPED_OK;
 }
+
+// debug-check builds (sped_common.cuh): OR of every unit's check bits, cleared
+extern "C" unsigned int sped_debug_take_spmm(void);
+extern "C" unsigned int sped_debug_take_csr(void);
+extern "C" unsigned int sped_debug_take_edge_batch(void);
+extern "C" int sped_debug_checks(void) { return SPED_DEBUG_CHECKS; }
+extern "C" unsigned int sped_debug_take(void) {
+  return sped_debug_take_spmm() | sped_debug_take_csr() | sped_debug_take_edge_batch();
+}

@@ -124,6 +124,7 @@ __global__ void fill_lower_kernel(int64_t m, const int64_t* __restrict__ u,
   const int32_t e = sorted_e[j];
   const int32_t c = (int32_t)u[e];
   const int32_t p = indptr[i] + ((int32_t)j - lo_start[i]);
+  SPED_DCHECK(p >= indptr[i] && p < indptr[i + 1], DBG_CSR_POS);
   indices[p] = c;
   if (values) {
     double val = -w[e];
@@ -149,6 +150,7 @@ __global__ void fill_upper_kernel(int64_t m, const int64_t* __restrict__ u,
   const int32_t c = (int32_t)v[e];
   const int32_t p =
       indptr[i] + (lo_start[i + 1] - lo_start[i]) + 1 + ((int32_t)e - up_start[i]);
+  SPED_DCHECK(p >= indptr[i] && p < indptr[i + 1], DBG_CSR_POS);
   indices[p] = c;
   if (values) {
     double val = -w[e];
@@ -689,6 +691,7 @@ __global__ void range_fill_lower_kernel(int64_t n_lo, int64_t b, const int64_t* 
   const int32_t e = sorted_e[j];
   const int64_t c = u[e];
   const int32_t p = indptr[i] + ((int32_t)j - lo_start[i]);
+  SPED_DCHECK(p >= indptr[i] && p < indptr[i + 1], DBG_CSR_POS);
   indices[p] = (int32_t)c;
   if (values) {
     double val = -w[e];
@@ -712,6 +715,7 @@ __global__ void range_fill_upper_kernel(int64_t e0, int64_t e1, int64_t b,
   const int32_t i = (int32_t)(u[e] - b);
   const int64_t c = v[e];
   const int32_t p = indptr[i] + (lo_start[i + 1] - lo_start[i]) + 1 + ((int32_t)e - up_start[i]);
+  SPED_DCHECK(p >= indptr[i] && p < indptr[i + 1], DBG_CSR_POS);
   indices[p] = (int32_t)c;
   if (values) {
     double val = -w[e];
@@ -876,3 +880,5 @@ extern "C" int sped_laplacian_build_rows(int64_t n, int64_t row_begin, int64_t r
   *nnz_out = nnz;
   return SPED_OK;
 }
+
+extern "C" unsigned int sped_debug_take_csr(void) { return sped::debug_take_unit(); }

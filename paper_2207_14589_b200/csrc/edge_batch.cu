@@ -44,6 +44,7 @@ __global__ void records_kernel(int64_t B, int64_t Bt, int64_t n, const int32_t* 
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int64_t e = batch[b];
+  SPED_DCHECK(e >= 0, DBG_EDGE_OOB);
   const float we = edge_w ? edge_w[e] : 1.0f;
   const int32_t p0 = epos[2 * e], p1 = epos[2 * e + 1];
 #pragma unroll
@@ -55,6 +56,7 @@ __global__ void records_kernel(int64_t B, int64_t Bt, int64_t n, const int32_t* 
       // the entry's row is the column of its partner entry (whole graph), or
       // the shard's row table
       row = erow ? erow[2 * e + s] : indices[s ? p0 : p1];
+      SPED_DCHECK(row >= 0 && row < n, DBG_EDGE_OOB);
       val = ((uint64_t)__float_as_uint(we) << 32) | (uint32_t)indices[p];
     }
     keys[2 * b + s] = row + (int32_t)((b / Bt) * (n + 1));
@@ -650,3 +652,5 @@ static int edge_batch_apply(int64_t n, int32_t k, int64_t m, const int32_t* indi
   }
   return SPED_OK;
 }
+
+extern "C" unsigned int sped_debug_take_edge_batch(void) { return sped::debug_take_unit(); }

@@ -352,6 +352,17 @@ __global__ void __launch_bounds__(PT_THREADS, 1) persistent_mueg_kernel(const PA
                 for (int j = 0; j < 8; ++j)
                   ready &= (c[j] < 0) || ((uint32_t)(q[j] >> 32) == want);
                 if (ready) break;
+                // a word already carrying a LATER generation of this buffer
+                // means its owner overwrote it before this reader consumed
+                // it: the two-buffer invariant broke (flag bit 4, raised)
+                bool ahead = false;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  ahead |= (c[j] >= 0) && ((int32_t)((uint32_t)(q[j] >> 32) - want) > 0);
+                if (ahead) {
+                  atomicOr(a.flag, 4);
+                  break;
+                }
                 if (spins > LL_SPIN_LIMIT) {
                   atomicOr(a.flag, 2);
                   break;

@@ -147,4 +147,41 @@ inline unsigned grid_for(int64_t items, int per_block, int max_blocks = 1 << 30)
   return (unsigned)g;
 }
 
+// Debug-check builds (-DSPED_DEBUG_CHECKS=1; `python -m
+// paper_2207_14589_b200.csrc.build -D SPED_DEBUG_CHECKS=1 --out ...`):
+// device-side bounds / protocol checks in the hot kernels record a bit in a
+// per-translation-unit device word instead of faulting; sped_debug_take()
+// (capi.cu) returns and clears the OR of all units.  The GPU test suite run
+// against that build asserts no bit is ever set (tests/conftest.py).  Off in
+// release builds (the checks compile away).
+#ifndef SPED_DEBUG_CHECKS
+#define SPED_DEBUG_CHECKS 0
+#endif
+enum DebugBits : unsigned {
+  DBG_GATHER_OOB = 1,      // SpMM gathered a row outside the input block
+  DBG_TICKET = 2,          // hub-chunk ticket count past the row's chunks
+  DBG_CSR_POS = 4,         // CSR build wrote outside a row's entry range
+  DBG_EDGE_OOB = 8,        // stochastic record with an edge / row out of range
+  DBG_RUN_ORDER = 16,      // stochastic sweep saw a record of another row
+};
+#if SPED_DEBUG_CHECKS
+static __device__ unsigned int g_sped_dbg = 0;
+#define SPED_DCHECK(cond, bit)                   \
+  do {                                           \
+    if (!(cond)) atomicOr(&::sped::g_sped_dbg, (bit)); \
+  } while (0)
+static inline unsigned int debug_take_unit() {
+  unsigned int v = 0, z = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&v, g_sped_dbg, sizeof(v));
+  cudaMemcpyToSymbol(g_sped_dbg, &z, sizeof(z));
+  return v;
+}
+#else
+#define SPED_DCHECK(cond, bit) \
+  do {                         \
+  } while (0)
+static inline unsigned int debug_take_unit() { return 0; }
+#endif
+
 }  // namespace sped

@@ -54,6 +54,7 @@ struct TermArgs {
   int64_t n;
   int32_t k;    // columns in this slab
   int64_t ld;   // row stride of the gathered block win (floats)
+  int64_t n_in; // rows of the gathered block (0: unknown; debug checks only)
   int64_t ldx;  // row stride of x
   int64_t ldo;  // row stride of wout (and acc_in)
   const int32_t* indptr;
@@ -252,7 +253,10 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       }
       Vf<W> gv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) gv[u] = ldg_vec<W>(wbase + (int64_t)c[u] * ldw);
+      for (int u = 0; u < U; ++u) {
+        SPED_DCHECK(c[u] >= 0 && (a.n_in == 0 || c[u] < a.n_in), DBG_GATHER_OOB);
+        gv[u] = ldg_vec<W>(wbase + (int64_t)c[u] * ldw);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) acc.fma(v[u], gv[u]);
     }
@@ -262,6 +266,7 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       if (VM == 1) v = c == row ? (float)(rowlen - 1) : -1.0f;
       else if (VM == 2) v = c == row ? 0.0f : 1.0f;
       else v = ld_csr(a.values + p);
+      SPED_DCHECK(c >= 0 && (a.n_in == 0 || c < a.n_in), DBG_GATHER_OOB);
       acc.fma(v, ldg_vec<W>(wbase + (int64_t)c * ldw));
     }
   }
@@ -377,6 +382,7 @@ __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const
   if (lane == 0) ticket = atomicAdd(a.tickets + c0, 1);
   ticket = __shfl_sync(0xffffffffu, ticket, 0);
   const int32_t nch = (re - rb + a.chunk_len - 1) / a.chunk_len;
+  SPED_DCHECK(ticket >= 0 && ticket < nch, DBG_TICKET);
   if (ticket != nch - 1) return;
   __threadfence();
   if (lsub == 0) {
@@ -780,6 +786,7 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
         a.n = n;
         a.k = kw;
         a.ld = k;
+        a.n_in = (w_init && win == w_init) ? 0 : n;  // a shard's [own | halo] input: unknown
         a.ldx = k;
         a.ldo = k;
         a.indptr = indptr;
@@ -894,6 +901,7 @@ static int shard_term(int64_t n, int32_t k, const int32_t* indptr, const int32_t
     a.n = n;
     a.k = min(128, k - c0);
     a.ld = k;
+    a.n_in = 0;  // [own | halo]: the halo length is the caller's
     a.ldx = k;
     a.ldo = k;
     a.indptr = indptr;
@@ -964,3 +972,5 @@ extern "C" int sped_csr_term_shard(int64_t n, int32_t k, const int32_t* indptr,
                     hot_begin, hot_rows, x, w, partial_in, raw_out, out, alpha, beta, gamma,
                     w0_scale, lam_f, s_final, stream);
 }
+
+extern "C" unsigned int sped_debug_take_spmm(void) { return sped::debug_take_unit(); }

@@ -592,6 +592,22 @@ class ShardedLaplacian:
             self.row_scale = torch.rsqrt(deg[:nr].double()).float().contiguous()
         return self
 
+    def lambda_upper(self, mode: str) -> float:
+        """The reference's degree bound (graph.py:351-362, transforms.py:
+        280-288) over all shards: 2.0 normalized, else 2 max_i d_i (one MAX
+        all-reduce of the shards' own fp64 degrees)."""
+        if mode == "normalized":
+            return 2.0
+        if self.m_global == 0:
+            return 0.0
+        d = getattr(self, "degrees_own", None)
+        loc = float(d.max()) if d is not None and d.numel() and self.n_own else 0.0
+        if self.world > 1:
+            t = torch.tensor([loc], dtype=torch.float64, device=_comm_device(self.group))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            loc = float(t.item())
+        return 2.0 * loc
+
     def _setup(self, offsets, rank, world, group, plan, n_global, nnz_global, m_global, indptr,
                cols_global, values, long_threshold, chunk_len, sorted_rows, eids, epos_l, edge_w):
         self.offsets = offsets

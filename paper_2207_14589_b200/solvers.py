@@ -179,6 +179,9 @@ class StepWorkspace:
         fv = int(self.flag.item())
         if fv & 2:
             raise RuntimeError("sped_persistent_mueg: a tagged term wait timed out")
+        if fv & 4:
+            raise RuntimeError("sped_persistent_mueg: tagged-term protocol violated "
+                               "(a row was overwritten before it was read)")
         f = bool(fv)
         if f:
             self.flag.zero_()

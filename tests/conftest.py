@@ -64,3 +64,23 @@ def rel_fro(a, b):
     b = np.asarray(b, dtype=np.float64)
     den = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+
+
+@pytest.fixture(autouse=True)
+def _device_debug_checks(request):
+    """With a debug-check build loaded (SPED_LIB=<lib built with
+    -DSPED_DEBUG_CHECKS=1>), every GPU test must leave the device-side
+    bounds / protocol check bits clear (the stand-in for compute-sanitizer,
+    which this pool does not allow)."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import sys as _sys
+    mod = _sys.modules.get("paper_2207_14589_b200._lib")
+    if mod is None or mod._lib is None:
+        return
+    lib = mod._lib
+    if int(lib.sped_debug_checks()) != 1:
+        return
+    bits = int(lib.sped_debug_take())
+    assert bits == 0, f"device debug checks failed: bits {bits:#x}"

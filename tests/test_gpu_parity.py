@@ -454,3 +454,27 @@ def test_bench_sped_arm_contract(cuda):
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+
+
+def test_debug_checks_detect_bad_column(cuda):
+    """The debug-check build (SPED_LIB=... built with -DSPED_DEBUG_CHECKS=1)
+    flags a gather outside the input block (bit 1) instead of reading
+    silently; the release build compiles the checks away."""
+    from paper_2207_14589_b200 import _lib
+    lib = _lib.load()
+    if int(lib.sped_debug_checks()) != 1:
+        pytest.skip("release build (checks compiled out)")
+    lib.sped_debug_take()
+    n, k = 4, 8
+    indptr = torch.tensor([0, 1, 2, 3, 4], dtype=torch.int32, device="cuda")
+    indices = torch.tensor([0, 1, 2, n], dtype=torch.int32, device="cuda")  # row 3 -> col n
+    values = torch.ones(4, dtype=torch.float32, device="cuda")
+    x = torch.zeros((2 * n, k), device="cuda")   # room behind row n: the bad read stays in bounds
+    out = torch.empty((n, k), device="cuda")
+    rc = lib.sped_csr_poly_apply(n, k, _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(values),
+                                 1 << 30, 1, None, 0, None, None, None, 0, 0, None,
+                                 _lib.ptr(x), None, None, None, _lib.ptr(out), 1,
+                                 _lib.dbl_array([0.0]), _lib.dbl_array([1.0]),
+                                 _lib.dbl_array([0.0]), 1.0, 0.0, 1.0, _lib.stream_ptr(cuda))
+    _lib.check(rc)
+    assert int(lib.sped_debug_take()) & 1
