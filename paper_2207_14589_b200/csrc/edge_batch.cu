@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(256) batch_row_kernel(const BatchArgs a) {
 // G <= 16: U = 2 records in flight and 8 resident blocks (32 registers);
 // G = 32 (k = 128, one row per warp): U = 4 at the natural register count
 // (config 3s 0.33 -> 0.23 ms/term, 5s 1.26 -> 1.17 ms/term against the
-// warp-per-row kernel, profiles/r02_ab_sto_group.log)
+// warp-per-row kernel; re-measured in profiles/r02_ab_sto_group.log)
 template <int G, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) batch_group_kernel(const BatchArgs a) {
   constexpr int RPW = 32 / G;
@@ -269,10 +269,16 @@ __global__ void __launch_bounds__(256, MINB) batch_group_kernel(const BatchArgs 
   }
 }
 
+#ifndef STO_U
+#define STO_U 2      // records in flight per group (G <= 16)
+#endif
+#ifndef STO_MINB
+#define STO_MINB 8   // resident blocks (G <= 16)
+#endif
 template <int G>
 void launch_groups(const BatchArgs& a, cudaStream_t s) {
-  constexpr int U = G == 32 ? 4 : 2;
-  constexpr int MINB = G == 32 ? 1 : 8;
+  constexpr int U = G == 32 ? 4 : STO_U;
+  constexpr int MINB = G == 32 ? 1 : STO_MINB;
   static PerDeviceOnce once;
   static int per_sm[64] = {};
   int dev = 0;
@@ -302,9 +308,12 @@ void launch_rows(const BatchArgs& a, cudaStream_t s) {
   batch_row_kernel<LPR, CPL, VEC><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(a);
 }
 
+#ifndef STO_FORCE_ROWS
+#define STO_FORCE_ROWS 0  // A/B builds only: the warp-per-row sweep for every slab
+#endif
 int launch_batch_slab(const BatchArgs& a, bool aligned, cudaStream_t s) {
   const int k = a.k;
-  if (aligned && k % 4 == 0) {
+  if (!STO_FORCE_ROWS && aligned && k % 4 == 0) {
     switch (k) {
       case 4: launch_groups<1>(a, s); break;
       case 8: launch_groups<2>(a, s); break;

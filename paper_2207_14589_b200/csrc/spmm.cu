@@ -34,6 +34,9 @@
 #ifndef CHUNK_MIN_BLOCKS
 #define CHUNK_MIN_BLOCKS 4
 #endif
+#ifndef CHUNK_W8_MIN_K
+#define CHUNK_W8_MIN_K 64  // shuffle kernels: 128-bit hub gathers won at k = 32 (0.78 vs 0.87 ms)
+#endif
 #ifndef LONG_MIN_BLOCKS
 #define LONG_MIN_BLOCKS 4
 #endif
@@ -557,11 +560,11 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
     const int lpr = k / (w8 ? 8 : 4);
     // rows in descending segment order, hub chunks last: the hub prefix of
     // the output is then the most recently written data when the next term
-    // starts gathering from it (config 4: -0.3 %/term, r02_ab_cachepolicy)
+    // starts gathering from it (config 4: -0.3 %/term in a round-2 A/B)
     auto chunks = [&]() -> int {
       if (a.n_chunks > 0) {
-        // hub chunks keep 128-bit gathers at k = 32 (0.78 vs 0.87 ms at config 4)
-        if (w8 && k >= 64) launch_chunks_w<8>(lpr, a, vm, s);
+        // hub chunks: 128-bit gathers below k = CHUNK_W8_MIN_K
+        if (w8 && k >= CHUNK_W8_MIN_K) launch_chunks_w<8>(lpr, a, vm, s);
         else launch_chunks_w<4>(k / 4, a, vm, s);
         SPED_LAUNCH_CHECK();
       }

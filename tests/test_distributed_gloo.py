@@ -278,3 +278,52 @@ def test_exchange_bytes_per_term_model():
     h = exchange_bytes_per_term(indptr, cols, off, k=4, replicate_rows=1)
     assert [x["p2p_rows"] for x in h["ranks"]] == [3, 1]
     assert [x["allgather_rows"] for x in h["ranks"]] == [0, 1]
+
+
+def _plan_worker(rank, world, port, indptr, indices, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2207_14589_b200.distributed import build_halo_plan, partition_rows
+        off = partition_rows(torch.from_numpy(indptr), world)
+        p0, p1 = int(indptr[off[rank]]), int(indptr[off[rank + 1]])
+        plan = build_halo_plan(torch.from_numpy(indices[p0:p1].copy()), off, rank, world)
+        parts = [None] * world
+        dist.all_gather_object(parts, (rank, off, plan.halo_cols.numpy(), plan.recv_counts,
+                                       [s.numpy() for s in plan.send_rows],
+                                       plan.local_indices.numpy()))
+        if rank == 0:
+            result_q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_build_halo_plan_torch_columns(golden, world):
+    """The collective halo plan built from TORCH column tensors (the device
+    path, here on CPU tensors under gloo) equals the one-process plans."""
+    from paper_2207_14589_b200.distributed import build_halo_plans_local
+    n, u, v, w = golden.graph("cfg4s")
+    u, v, w = O.canonical_edges(n, u, v, w)
+    csr = O.laplacian_csr(n, u, v, w, "normalized")
+    indptr = csr.indptr.astype(np.int64)
+    indices = csr.indices.astype(np.int64)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, indptr, indices, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = build_halo_plans_local(indptr, indices, parts[0][1])
+    for r, off, halo, rc, send, local in parts:
+        np.testing.assert_array_equal(halo, ref[r].halo_cols)
+        np.testing.assert_array_equal(rc, ref[r].recv_counts)
+        np.testing.assert_array_equal(local, ref[r].local_indices)
+        for q_ in range(world):
+            np.testing.assert_array_equal(send[q_], ref[r].send_rows[q_])
