@@ -664,11 +664,16 @@ class ShardedLaplacian:
         from .graph import HOT_FRACTION, L2_BYTES
         if not self.sorted_rows:
             return (0, 0)
-        H = int(min(self.n_global, HOT_FRACTION * L2_BYTES / (4 * max(k, 1))))
-        if self.row0 < H:
-            return (0, min(H, self.row0 + self.n_own) - self.row0)
-        halo = torch.as_tensor(self.plan.halo_cols)
-        return (self.n_own, int(torch.searchsorted(halo, torch.tensor(H, device=halo.device))))
+        cache = self.__dict__.setdefault("_hot", {})
+        if k not in cache:  # once per k: the search syncs the host
+            H = int(min(self.n_global, HOT_FRACTION * L2_BYTES / (4 * max(k, 1))))
+            if self.row0 < H:
+                cache[k] = (0, min(H, self.row0 + self.n_own) - self.row0)
+            else:
+                halo = torch.as_tensor(self.plan.halo_cols)
+                cache[k] = (self.n_own,
+                            int(torch.searchsorted(halo, torch.tensor(H, device=halo.device))))
+        return cache[k]
 
     def _plan_chunks(self):
         self.n_chunks, self.chunk_desc = _plan_chunks(
