@@ -35,7 +35,7 @@
 #define CHUNK_MIN_BLOCKS 4
 #endif
 #ifndef CHUNK_W8_MIN_K
-#define CHUNK_W8_MIN_K 64  // shuffle kernels: 128-bit hub gathers won at k = 32 (0.78 vs 0.87 ms)
+#define CHUNK_W8_MIN_K 32  // free kernels: 256-bit hub gathers at k = 32 too (config 4: 2.548 -> 2.522 ms/term, r02_ab_chunk_width_cfg4.log)
 #endif
 #ifndef LONG_MIN_BLOCKS
 #define LONG_MIN_BLOCKS 4
