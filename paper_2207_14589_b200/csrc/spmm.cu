@@ -79,7 +79,25 @@ struct TermArgs {
   int64_t hot_rows;        // hub prefix kept in L2 (persisting window)
   const float* rscale;     // d^-1/2 per row (TF_NORM_IN / TF_SCALE_OUT)
   const float* acc_in;     // VM 2/3: partial neighbour sum added before the epilogue (or NULL)
+  int pdl;                 // programmatic dependent launch role (pdl_prologue)
 };
+
+// Programmatic dependent launch (SPED_PDL=1): the launches of one term
+// (short rows, warp rows, hub chunks) read the same input and write
+// disjoint rows, so each may start as soon as the previous launch's CTAs
+// are all resident -- their tails overlap.  Completion stays ordered: the
+// first launch of a term waits (every thread) for the previous grid, which
+// is the previous term's last launch; later launches of the term chain
+// completion through one waiting thread, so a term's last launch cannot
+// complete before its first.  pdl bit 0: data dependency, bit 1: chain.
+__device__ __forceinline__ void pdl_prologue(int mode) {
+  if (mode & 1) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  } else if ((mode & 2) && blockIdx.x == 0 && threadIdx.x == 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  if (mode) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // VM 0: stored values; 1: implicit combinatorial (-1, row_len-1 on the
 // diagonal); 2: implicit normalized on the scaled block (1 off the diagonal,
@@ -282,6 +300,7 @@ template <int W, int LPR, int SUB, int VM>
 __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W * LPR >= 128 ? FREE_K128_MINB : FREE_MINB))) spmm_free_kernel(const TermArgs a) {
   constexpr int G = LPR * SUB;
   constexpr int RPW = 32 / G;
+  pdl_prologue(a.pdl);
   const int lane = threadIdx.x & 31;
   const int g = lane % G;
   const int cl = g % LPR;
@@ -321,16 +340,35 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W * LPR >= 
   st_stream_vec<W>(a.wout + offo, term_epilogue<W>(a, acc, xr, wr, row_ds(a, row)));
 }
 
+template <class Kern>
+static void launch_pdl(Kern kern, unsigned grid, cudaStream_t s, const TermArgs& a) {
+  if (a.pdl == 0) {
+    kern<<<grid, 256, 0, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 template <int W, int LPR, int SUB>
 static void launch_free(const TermArgs& a, int vm, cudaStream_t s) {
   constexpr int RPW = 32 / (LPR * SUB);
   const int64_t rows = a.row_end - a.row_begin;
   const unsigned grid = (unsigned)(((rows + RPW - 1) / RPW + 7) / 8);
   if (grid == 0) return;
-  if (vm == 1) spmm_free_kernel<W, LPR, SUB, 1><<<grid, 256, 0, s>>>(a);
-  else if (vm == 2) spmm_free_kernel<W, LPR, SUB, 2><<<grid, 256, 0, s>>>(a);
-  else if (vm == 3) spmm_free_kernel<W, LPR, SUB, 3><<<grid, 256, 0, s>>>(a);
-  else spmm_free_kernel<W, LPR, SUB, 0><<<grid, 256, 0, s>>>(a);
+  if (vm == 1) launch_pdl(spmm_free_kernel<W, LPR, SUB, 1>, grid, s, a);
+  else if (vm == 2) launch_pdl(spmm_free_kernel<W, LPR, SUB, 2>, grid, s, a);
+  else if (vm == 3) launch_pdl(spmm_free_kernel<W, LPR, SUB, 3>, grid, s, a);
+  else launch_pdl(spmm_free_kernel<W, LPR, SUB, 0>, grid, s, a);
 }
 
 template <int W, int LPR>
@@ -362,6 +400,7 @@ static void launch_free_w(int lpr, int sub, const TermArgs& a, int vm, cudaStrea
 // float atomics.
 template <int W, int LPR, int U, int VM>
 __global__ void __launch_bounds__(256, CHUNK_MIN_BLOCKS) spmm_chunk_kernel(const TermArgs a) {
+  pdl_prologue(a.pdl);
   const int lane = threadIdx.x & 31;
   const bool need_x = (a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF));
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -504,10 +543,10 @@ template <int W, int LPR>
 static void launch_chunks(const TermArgs& a, int vm, cudaStream_t s) {
   const unsigned grid = (unsigned)((a.n_chunks + 7) / 8);
   if (grid == 0) return;
-  if (vm == 1) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 1><<<grid, 256, 0, s>>>(a);
-  else if (vm == 2) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 2><<<grid, 256, 0, s>>>(a);
-  else if (vm == 3) spmm_chunk_kernel<W, LPR, FREE_LONG_U, 3><<<grid, 256, 0, s>>>(a);
-  else spmm_chunk_kernel<W, LPR, FREE_LONG_U, 0><<<grid, 256, 0, s>>>(a);
+  if (vm == 1) launch_pdl(spmm_chunk_kernel<W, LPR, FREE_LONG_U, 1>, grid, s, a);
+  else if (vm == 2) launch_pdl(spmm_chunk_kernel<W, LPR, FREE_LONG_U, 2>, grid, s, a);
+  else if (vm == 3) launch_pdl(spmm_chunk_kernel<W, LPR, FREE_LONG_U, 3>, grid, s, a);
+  else launch_pdl(spmm_chunk_kernel<W, LPR, FREE_LONG_U, 0>, grid, s, a);
 }
 
 // width dispatch: W = 8 (256-bit gathers) when k % 8 == 0 and rows are 32 B
@@ -570,10 +609,15 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       }
       return SPED_OK;
     };
+    static const bool pdl_on = [] {
+      const char* e = getenv("SPED_PDL");
+      return e && e[0] == '1';
+    }();
     for (int j = 0; j < nseg; ++j) {
       const int i = nseg - 1 - j;
       a.row_begin = segs[i].begin;
       a.row_end = segs[i].end;
+      a.pdl = pdl_on ? (j == 0 ? 1 : 2) : 0;
       int sub = segs[i].sub;
       if (sub < 1) sub = 1;
       if (sub * lpr > 32) sub = 32 / lpr;
@@ -581,9 +625,11 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       else launch_free_w<4>(lpr, sub, a, vm, s);
       SPED_LAUNCH_CHECK();
     }
+    a.pdl = pdl_on ? (nseg == 0 ? 1 : 2) : 0;
     const int rc = chunks();
     if (rc != SPED_OK) return rc;
   } else {
+    a.pdl = 0;
     a.chunk_blocks = 0;
     a.long_thresh = INT32_MAX;
     if (k <= 1) launch_generic<1, 1>(a, vm, s);
@@ -816,6 +862,7 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
         a.hot_rows = hot_rows;
         a.rscale = row_scale;
         a.acc_in = nullptr;
+        a.pdl = 0;
         const uintptr_t pbits = reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.win) |
                                 reinterpret_cast<uintptr_t>(a.wout);
         const bool aligned = (kw % 4 == 0) && (k % 4 == 0) && (pbits % 16 == 0);
@@ -931,6 +978,7 @@ static int shard_term(int64_t n, int32_t k, const int32_t* indptr, const int32_t
     a.hot_rows = hot_rows;
     a.rscale = row_scale;
     a.acc_in = partial_in ? partial_in + c0 : nullptr;
+    a.pdl = 0;
     const uintptr_t pbits = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) |
                             reinterpret_cast<uintptr_t>(out) |
                             reinterpret_cast<uintptr_t>(partial_in);
