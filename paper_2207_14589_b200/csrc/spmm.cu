@@ -82,7 +82,7 @@ struct TermArgs {
   int pdl;                 // programmatic dependent launch role (pdl_prologue)
 };
 
-// Programmatic dependent launch (SPED_PDL=1): the launches of one term
+// Programmatic dependent launch (default; SPED_PDL=0 off): the launches of one term
 // (short rows, warp rows, hub chunks) read the same input and write
 // disjoint rows, so each may start as soon as the previous launch's CTAs
 // are all resident -- their tails overlap.  Completion stays ordered: the
@@ -609,9 +609,12 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
       }
       return SPED_OK;
     };
+    // on by default (config 4: 2.528 -> 2.513 ms/term, config 3: 0.430 ->
+    // 0.428, config 5: within noise; profiles/r02_ab_pdl_cfg*.log);
+    // SPED_PDL=0 launches plainly
     static const bool pdl_on = [] {
       const char* e = getenv("SPED_PDL");
-      return e && e[0] == '1';
+      return !(e && e[0] == '0');
     }();
     for (int j = 0; j < nseg; ++j) {
       const int i = nseg - 1 - j;
