@@ -298,13 +298,19 @@ void launch_groups(const BatchArgs& a, cudaStream_t s) {
 
 template <int LPR, int CPL, bool VEC>
 void launch_rows(const BatchArgs& a, cudaStream_t s) {
-  static int per_sm = 0;  // grid = resident capacity; warps stride over rows
-  if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_row_kernel<LPR, CPL, VEC>, 256, 0);
-    if (per_sm < 1) per_sm = 1;
-  }
+  // grid = resident capacity (per device); warps stride over rows
+  static PerDeviceOnce once;
+  static int per_sm[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once([&]() -> int {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, batch_row_kernel<LPR, CPL, VEC>, 256, 0);
+    per_sm[dev & 63] = v < 1 ? 1 : v;
+    return SPED_OK;
+  });
   const int64_t blocks = std::min<int64_t>(
-      (a.n + 7) / 8, (int64_t)num_sms() * std::max(1, per_sm - a.spare_per_sm));
+      (a.n + 7) / 8, (int64_t)num_sms() * std::max(1, per_sm[dev & 63] - a.spare_per_sm));
   batch_row_kernel<LPR, CPL, VEC><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(a);
 }
 

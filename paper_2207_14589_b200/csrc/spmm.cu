@@ -587,11 +587,10 @@ static int launch_term_slab(TermArgs a, int vm, bool aligned, bool aligned32,
   const int k = a.k;
   const bool fast = aligned && (k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128);
   if (fast) {
-    static int wide = -1;  // SPED_VEC=4 forces 128-bit gathers
-    if (wide < 0) {
+    static const int wide = [] {  // SPED_VEC=4 forces 128-bit gathers
       const char* e = getenv("SPED_VEC");
-      wide = (e && e[0] == '4') ? 0 : 1;
-    }
+      return (e && e[0] == '4') ? 0 : 1;
+    }();
 #ifndef W8_MIN_K
 #define W8_MIN_K 32  // k = 32: 4 lanes x 256-bit per row (config 4: 3.53 -> 3.22 ms/term)
 #endif
