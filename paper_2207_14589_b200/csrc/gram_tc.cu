@@ -76,6 +76,18 @@ __device__ __forceinline__ int kmaj_offset2(int r, int c) {
 // Only the blocks the solvers read are kept: rows 0..k-1 of G (S and C) and
 // the Q = M^T M block (rows and columns k..2k-1).  The CTA writes its fp64
 // partial once at the end (rows 0..k-1, then Q).
+#ifndef GRAM_BIG_SPLIT
+#define GRAM_BIG_SPLIT 512
+#endif
+#ifndef GRAM_BIG_KC
+#define GRAM_BIG_KC 16
+#endif
+#ifndef GRAM_BIG_NR
+#define GRAM_BIG_NR 4
+#endif
+#ifndef GRAM_BIG_NTB
+#define GRAM_BIG_NTB 3
+#endif
 template <int K2, bool DQ = false>
 struct Cfg2 {
   // Y mode (K2 = 64): the tile is Y = [hi | lo] (128 columns) and ONE
@@ -98,10 +110,10 @@ struct Cfg2 {
   static constexpr int NACC = BIG ? 1 : 2;            // accumulators per bank
   static constexpr int NBANK = BIGQ ? 1 : 2;
   static constexpr int ACC_COLS = YM ? 2 * K2 : (BIG ? (DQ ? 256 : 384) : K2);  // TMEM columns per accumulator
-  static constexpr int SPLIT = (K2 == 64) ? 1024 : 512;  // rows per slice (drain)
-  static constexpr int KC = (K2 == 64) ? 64 : (BIG ? 16 : 32);  // rows per chunk
-  static constexpr int NR = (K2 == 64) ? 4 : (BIG ? 4 : 3);     // raw (bulk copy) stages
-  static constexpr int NTB = (K2 == 64) ? 3 : (BIG ? 3 : 2);    // converted tile buffers
+  static constexpr int SPLIT = (K2 == 64) ? 1024 : (BIG ? GRAM_BIG_SPLIT : 512);  // rows per slice (drain)
+  static constexpr int KC = (K2 == 64) ? 64 : (BIG ? GRAM_BIG_KC : 32);  // rows per chunk
+  static constexpr int NR = (K2 == 64) ? 4 : (BIG ? GRAM_BIG_NR : 3);     // raw (bulk copy) stages
+  static constexpr int NTB = (K2 == 64) ? 3 : (BIG ? GRAM_BIG_NTB : 2);    // converted tile buffers
   static constexpr int RAW_FLOATS = KC * K2;
   static constexpr int TCOLS = YM ? 2 * K2 : K2;      // columns of one K-major tile
   static constexpr int KSTEP_FLOATS = (TCOLS / 8) * (SBO_B / 4);
