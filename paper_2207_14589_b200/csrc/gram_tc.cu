@@ -347,15 +347,21 @@ __global__ void __launch_bounds__(Cfg2<K2, DQ>::NTHREADS, 1)
       const int nk = min(C::NACC, chunks * (C::KC / 8));
       if constexpr (C::BIG) {
         // TMEM lane m: row m of [S | C] (cols 0..255) and row m of Q (cols
-        // 256..383; not in DQ mode); fp64 sums accumulate in the global partial
+        // 256..383; not in DQ mode); fp64 sums accumulate in the global
+        // partial, stored COLUMN-major (element (m, c) at c*128 + m) so the
+        // 32 lanes of a drain warp read-modify-write 256 contiguous bytes per
+        // instruction instead of 32 separate lines
 #pragma unroll 1
         for (int c0 = 0; c0 < C::ACC_COLS; c0 += 16) {
           float v[16];
           tmem_ld16(tmem + (uint32_t)(bank * C::ACC_COLS + c0) + lane_base, v);
-          double* dst = (c0 < 256) ? out + row * K2 + c0
-                                   : out + C::HALF * K2 + row * C::HALF + (c0 - 256);
+          double* dst = (c0 < 256) ? out + (int64_t)c0 * C::HALF + row
+                                   : out + C::HALF * K2 + (int64_t)(c0 - 256) * C::HALF + row;
+          double cur[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) dst[i] += (double)v[i];
+          for (int i = 0; i < 16; ++i) cur[i] = dst[i * C::HALF];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) dst[i * C::HALF] = cur[i] + (double)v[i];
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(&bank_free[bank]);
@@ -421,22 +427,24 @@ __global__ void __launch_bounds__(Cfg2<K2, DQ>::NTHREADS, 1)
   }
 }
 
-// Sum the per-CTA partials (CTA order) into S / C / Q.
+// Sum the per-CTA partials (CTA order) into S / C / Q.  colmajor: the
+// partial stores element (row i, col j) at j*k + i (the k = 128 drain).
 __global__ void gram_tc2_reduce(int32_t k, int32_t nparts, const double* __restrict__ partial,
-                                double* __restrict__ G) {
+                                double* __restrict__ G, int colmajor) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int K2 = 2 * k, per = k * K2 + k * k;
   if (e >= per) return;
   double s = 0.0;
   for (int p = 0; p < nparts; ++p) s += partial[(int64_t)p * per + e];
   if (e < k * K2) {
-    const int i = e / K2, j = e % K2;
+    const int i = colmajor ? e % k : e / K2, j = colmajor ? e / k : e % K2;
     if (j < k)
       G[i * k + j] = s;  // S (full rows; symmetric by construction of the MMAs)
     else
       G[k * k + i * k + (j - k)] = s;  // C
   } else {
-    G[2 * k * k + (e - k * K2)] = s;  // Q
+    const int q = e - k * K2;
+    G[2 * k * k + (colmajor ? (q % k) * k + q / k : q)] = s;  // Q
   }
 }
 
@@ -456,7 +464,7 @@ int launch2(int64_t n, int32_t k, const float* V, const float* M, double* G, dou
   gram_tc2_kernel<K2, DQ><<<grid, C::NTHREADS, C::SMEM, s>>>(n, k, V, M, partial, nslices);
   SPED_LAUNCH_CHECK();
   const int per = k * K2 + k * k;
-  gram_tc2_reduce<<<(per + 255) / 256, 256, 0, s>>>(k, (int)grid, partial, G);
+  gram_tc2_reduce<<<(per + 255) / 256, 256, 0, s>>>(k, (int)grid, partial, G, C::BIG ? 1 : 0);
   SPED_LAUNCH_CHECK();
   return SPED_OK;
 }
