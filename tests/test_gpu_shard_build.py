@@ -254,3 +254,26 @@ def test_shard_with_no_sampled_endpoint(cuda):
     sh.local_batch_term(x, x, out, None, 10, 0.5, 1.0, 0.25, 1.0, 0.0, 1.0, 8,
                         local_batch=torch.zeros(0, dtype=torch.int32, device="cuda"))
     torch.testing.assert_close(out, 0.5 * x + 0.25 * x, rtol=1e-6, atol=0)
+
+
+def test_shard_build_zero_degree_normalized_raises(cuda):
+    """An isolated node makes the normalized Laplacian undefined: the shard
+    build raises the reference's ValueError (graph.py:187-188) on every
+    shard, from the gathered degree vector, not only on the owner."""
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200.distributed import ShardedLaplacian
+    g = sp.Graph.from_edges(6, [(0, 1), (1, 2), (3, 4)])   # node 5 isolated
+    ses = _shard_edges(g, 2, False)
+    deg = torch.zeros(6, dtype=torch.float64, device="cuda")
+    deg[:5] = torch.tensor([1, 2, 1, 1, 1], dtype=torch.float64)
+    for se in ses:
+        with pytest.raises(ValueError, match="degrees"):
+            ShardedLaplacian.from_shard_edges(se, "normalized", col_degrees=deg,
+                                              plan=None if se.world == 1 else _plan_for(g, se))
+
+
+def _plan_for(g, se):
+    import paper_2207_14589_b200 as sp
+    from paper_2207_14589_b200.distributed import build_halo_plans_local
+    L = sp.LaplacianOperator(g, "unnormalized", implicit=False)
+    return build_halo_plans_local(L.indptr.long(), L.indices[: L.nnz], se.offsets)[se.rank]
