@@ -48,6 +48,9 @@ namespace {
 using namespace ::sped::async;
 using namespace ::sped::tc;
 
+#ifndef UPD_COAL
+#define UPD_COAL 1  // coalesced converter loads: 0.881 -> 0.836 ms at n = 2e6 (r02_ab_update_tc128_transposed.log)
+#endif
 constexpr int UK = 128;                    // k
 constexpr int UTM = 128;                   // rows per tile (MMA M)
 constexpr int UKC = 32;                    // columns per chunk
@@ -141,7 +144,12 @@ __global__ void __launch_bounds__(UTHREADS, 1)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int idx = tid + 256 * i;  // 128 rows x 8 float4 per chunk
+#if UPD_COAL
+        // 8 rows x 4 consecutive float4 per instruction (64 B of each row)
+        const int m = ((idx >> 5) & 15) * 8 + (idx & 7), kq = ((idx >> 9) & 1) * 4 + ((idx >> 3) & 3);
+#else
         const int m = idx & (UTM - 1), kq = idx >> 7;  // one row per lane: conflict-free stores
+#endif
         const int64_t r = r0 + m;
         v[i] = (r < n) ? __ldg(reinterpret_cast<const float4*>(P + r * UK + c0) + kq)
                        : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -160,7 +168,12 @@ __global__ void __launch_bounds__(UTHREADS, 1)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int idx = tid + 256 * i;
+#if UPD_COAL
+        split_store(hi, lo, ukmaj(((idx >> 5) & 15) * 8 + (idx & 7),
+                                  4 * (((idx >> 9) & 1) * 4 + ((idx >> 3) & 3))), cur[i]);
+#else
         split_store(hi, lo, ukmaj(idx & (UTM - 1), 4 * (idx >> 7)), cur[i]);
+#endif
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&slot_full[slot]);
