@@ -301,10 +301,19 @@ __global__ void __launch_bounds__(256) block_update_rows(
 // is read as float4 broadcasts (one shared-memory wavefront per 4 inputs),
 // M and the output are coalesced 128-B rows.
 template <int K>
+#ifndef UPD_NSTAGE
+#define UPD_NSTAGE 4
+#endif
+#ifndef UPD_STAGE_BYTES
+#define UPD_STAGE_BYTES 16384
+#endif
+#ifndef UPD_CTAS
+#define UPD_CTAS 2
+#endif
 struct UpdCfg {
   static constexpr int KPL = K / 32;
-  static constexpr int NSTAGE = 4;
-  static constexpr int STAGE_BYTES = 16384;  // P + M rows of one stage
+  static constexpr int NSTAGE = UPD_NSTAGE;
+  static constexpr int STAGE_BYTES = UPD_STAGE_BYTES;  // P + M rows of one stage
 };
 
 template <int K, int MODE>  // MODE 0: P A; 1: P A + eta M; 2: P A + M B
@@ -455,7 +464,7 @@ int launch_v2(int64_t n, const float* P, const float* A, const float* M, const f
     if (rc_ != SPED_OK) return rc_;
   }
   const int64_t ntiles = (n + tr - 1) / tr;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * 2));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * UPD_CTAS));
   switch (mode) {
     case 0: block_update_v2<K, 0><<<grid, 288, smem, s>>>(n, P, A, M, B, eta, scale, out, tr); break;
     case 1: block_update_v2<K, 1><<<grid, 288, smem, s>>>(n, P, A, M, B, eta, scale, out, tr); break;
