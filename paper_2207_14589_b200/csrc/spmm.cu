@@ -249,7 +249,13 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
 #ifndef FREE_K128_MINB
 #define FREE_K128_MINB 5
 #endif
-template <int W, int LPR, int SUB, int U, int VM>
+// DIAG_EPI=1 (default): implicit combinatorial rows (VM 1) skip the diagonal
+// gather too and add (len-1) * w_i from the epilogue's coalesced own-row
+// read (changes the fp32 summation order of the diagonal term)
+#ifndef DIAG_EPI
+#define DIAG_EPI 1  // config 3: 0.431 -> 0.424 ms/term (r02_ab_diag_skip_cfg3.log)
+#endif
+template <int W, int LPR, int SUB, int U, int VM, bool SKIPD = (VM == 2)>
 __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row, bool valid,
                                                  int32_t b, int32_t e, int32_t rowlen, int lane) {
   constexpr int G = LPR * SUB;
@@ -276,7 +282,10 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         SPED_DCHECK(c[u] >= 0 && (a.n_in == 0 || c[u] < a.n_in), DBG_GATHER_OOB);
-        gv[u] = ldg_vec<W>(wbase + (int64_t)c[u] * ldw);
+        // VM 2: the diagonal's weight is 0 (the epilogue reads the own row
+        // itself) -- no gather for it; the sum is unchanged bit for bit
+        if (SKIPD && c[u] == row) gv[u].zero();
+        else gv[u] = ldg_vec<W>(wbase + (int64_t)c[u] * ldw);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) acc.fma(v[u], gv[u]);
@@ -288,7 +297,7 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       else if (VM == 2) v = c == row ? 0.0f : 1.0f;
       else v = ld_csr(a.values + p);
       SPED_DCHECK(c >= 0 && (a.n_in == 0 || c < a.n_in), DBG_GATHER_OOB);
-      acc.fma(v, ldg_vec<W>(wbase + (int64_t)c * ldw));
+      if (!(SKIPD && c == row)) acc.fma(v, ldg_vec<W>(wbase + (int64_t)c * ldw));
     }
   }
 #pragma unroll
@@ -318,12 +327,15 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W * LPR >= 
   } else if (!valid) {
     return;
   }
+  constexpr bool SKIPD = (VM == 2) || (DIAG_EPI && VM == 1);
   Vf<W> acc = free_accumulate<W, LPR, SUB,
-                              (SUB > 1 ? FREE_LONG_U : (W * LPR >= 128 ? FREE_K128_U : FREE_U)), VM>(
-      a, row, valid, b, e, e - b, lane);
+                              (SUB > 1 ? FREE_LONG_U : (W * LPR >= 128 ? FREE_K128_U : FREE_U)), VM,
+                              SKIPD>(a, row, valid, b, e, e - b, lane);
   if (!valid || g >= LPR) return;
   const int64_t off = (int64_t)row * a.ld + cl * W;
   const int64_t offo = (int64_t)row * a.ldo + cl * W;
+  if (DIAG_EPI && VM == 1 && e > b)  // the diagonal, from the own row (coalesced)
+    acc.fma((float)(e - b - 1), ldg_vec<W>(a.win + off));
   if (VM == 3 || VM == 2) {
     if (a.acc_in) acc.add(ldg_vec<W>(a.acc_in + offo));
     if (a.flags & TF_RAW_OUT) {
