@@ -225,6 +225,29 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+L2_BYTES = 126 * 1024 * 1024
+
+
+def l2_capacity_bound(rowlen, k, algorithmic_bytes):
+    """What a perfect static cache of the whole L2 would leave: gathers of row
+    j happen (len_j - 1) times per term (once per neighbour); with the N =
+    L2 / 4k most-gathered rows resident, the others cost one 4k-byte DRAM
+    access each.  ``max_frac`` = algorithmic / (algorithmic + miss bytes): the
+    roofline fraction a kernel running at 100 % of DRAM peak would report."""
+    deg = np.sort(np.asarray(rowlen, dtype=np.int64) - 1)[::-1]
+    deg = np.maximum(deg, 0)
+    total = int(deg.sum())
+    if total == 0:
+        return None
+    rows = int(min(deg.size, L2_BYTES // (4 * k)))
+    hit = float(deg[:rows].sum()) / total
+    miss_bytes = (1.0 - hit) * total * 4 * k
+    return {"l2_bytes": L2_BYTES, "rows_resident": rows, "gathers_per_term": total,
+            "hit_share": hit, "miss_bytes_per_term": miss_bytes,
+            "min_traffic_per_term": algorithmic_bytes + miss_bytes,
+            "max_frac": algorithmic_bytes / (algorithmic_bytes + miss_bytes)}
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -672,6 +695,12 @@ def run_sped(args):
         if traffic is None and traffic_ncu:
             traffic, traffic_src = ncu_bytes, (ncu_src + " (in-run meter unavailable: %s)"
                                                % meter.err)
+    # lower bound on a term's DRAM traffic under a PERFECT static L2 (the whole
+    # 126 MB holding the most-gathered rows, no streaming pollution): every
+    # gather of a row outside that set is a DRAM access of 4k bytes
+    l2_bound = None
+    if not sharded:
+        l2_bound = l2_capacity_bound(lap.rowlen, k, bpt)
     # our kernels per step: per term one launch per row segment (+ the hub
     # chunk launch); Gram (tcgen05 partials + fp64 reduce), coefficients,
     # update.  Sharded: + the halo pack per term (NCCL's own kernels excluded).
@@ -767,7 +796,8 @@ def run_sped(args):
                          "peak_source": peak_src,
                          "traffic_source": traffic_src,
                          "traffic_ncu": traffic_ncu,
-                         "dram_frac_actual": (traffic / t_term_s / 1e9 / peak) if traffic else None},
+                         "dram_frac_actual": (traffic / t_term_s / 1e9 / peak) if traffic else None,
+                         "l2_capacity_bound": l2_bound},
             "cpu_baseline": cpu,
             "time_to_angle": conv,
             "stochastic": sto,
