@@ -32,13 +32,13 @@
 #include "sped_common.cuh"
 
 #ifndef CHUNK_MIN_BLOCKS
-#define CHUNK_MIN_BLOCKS 4
+#define CHUNK_MIN_BLOCKS 5  // with LONG_MIN_BLOCKS 5 / FREE_LONG_U 3: config 4 2.520 -> 2.481 ms/term (r02_ab_long_occupancy_cfg4.log)
 #endif
 #ifndef CHUNK_W8_MIN_K
 #define CHUNK_W8_MIN_K 32  // free kernels: 256-bit hub gathers at k = 32 too (config 4: 2.548 -> 2.522 ms/term, r02_ab_chunk_width_cfg4.log)
 #endif
 #ifndef LONG_MIN_BLOCKS
-#define LONG_MIN_BLOCKS 4
+#define LONG_MIN_BLOCKS 5
 #endif
 
 namespace sped {
@@ -241,7 +241,7 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
 #define FREE_MINB 6
 #endif
 #ifndef FREE_LONG_U
-#define FREE_LONG_U 4
+#define FREE_LONG_U 3
 #endif
 #ifndef FREE_K128_U
 #define FREE_K128_U 3  // k = 128 rows (16 lanes): config 5 2.41 -> 2.36 ms/term
@@ -252,9 +252,6 @@ __device__ __forceinline__ float4 term_epilogue(const TermArgs& a, float4 y, flo
 // DIAG_EPI=1 (default): implicit combinatorial rows (VM 1) skip the diagonal
 // gather too and add (len-1) * w_i from the epilogue's coalesced own-row
 // read (changes the fp32 summation order of the diagonal term)
-#ifndef EPI_PREFETCH
-#define EPI_PREFETCH 0
-#endif
 #ifndef DIAG_EPI
 #define DIAG_EPI 1  // config 3: 0.431 -> 0.424 ms/term (r02_ab_diag_skip_cfg3.log)
 #endif
@@ -331,18 +328,6 @@ __global__ void __launch_bounds__(256, (SUB > 1 ? LONG_MIN_BLOCKS : (W * LPR >= 
     return;
   }
   constexpr bool SKIPD = (VM == 2) || (DIAG_EPI && VM == 1);
-#if EPI_PREFETCH
-  // the epilogue's own-row / x reads are DRAM streams issued after the row
-  // sum; pull their sectors towards the L2 while the gathers are in flight
-  if (valid && g < LPR) {
-    if ((a.flags & TF_ALPHA) || ((a.flags & TF_FINAL) && (a.flags & TF_LAMF)))
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.x + (int64_t)row * a.ldx + cl * W));
-#if EPI_PREFETCH >= 2
-    if (a.flags & (TF_GAMMA | TF_NORM_IN))
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.win + (int64_t)row * a.ld + cl * W));
-#endif
-  }
-#endif
   Vf<W> acc = free_accumulate<W, LPR, SUB,
                               (SUB > 1 ? FREE_LONG_U : (W * LPR >= 128 ? FREE_K128_U : FREE_U)), VM,
                               SKIPD>(a, row, valid, b, e, e - b, lane);
