@@ -443,6 +443,113 @@ __global__ void __launch_bounds__(288) block_update_v2(int64_t n, const float* _
   }
 }
 
+// k = 32 without M*B (mu-EG / CholQR updates): half a warp per row, a lane
+// owning two adjacent output columns, so every FMA is a packed FFMA2 (the P
+// element as the scalar operand, the lane's two A entries as the pair): half
+// the FMA instructions of the lane-per-column layout, the same per-element
+// sums in the same order.  Same cp.async.bulk ring as block_update_v2.
+#ifndef UPD_F2
+#define UPD_F2 1
+#endif
+__device__ __forceinline__ void ffma2_s(uint64_t& acc, float s, uint64_t b) {
+  uint64_t ss;
+  asm("mov.b64 %0, {%1,%1};" : "=l"(ss) : "f"(s));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(ss), "l"(b));
+}
+
+template <int MODE>  // 0: P A; 1: P A + eta M
+__global__ void __launch_bounds__(288, 2) block_update_k32_f2(int64_t n, const float* __restrict__ P,
+                                                          const float* __restrict__ A,
+                                                          const float* __restrict__ M, float eta,
+                                                          const float* __restrict__ scale,
+                                                          float* __restrict__ out, int tr) {
+  using namespace ::sped::async;
+  constexpr int K = 32, NS = UpdCfg<K>::NSTAGE;
+  extern __shared__ __align__(128) float stage[];
+  __shared__ uint64_t full[NS], empty[NS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int stage_floats = tr * K * (MODE == 0 ? 1 : 2);
+  const int64_t ntiles = (n + tr - 1) / tr;
+  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int64_t j = 0; j < my_tiles; ++j) {
+        const int st = (int)(j % NS);
+        if (j >= NS) mbar_wait(&empty[st], (uint32_t)(((j / NS) - 1) & 1));
+        const int64_t r0 = (blockIdx.x + j * gridDim.x) * (int64_t)tr;
+        const int rows = (int)min((int64_t)tr, n - r0);
+        const uint32_t bytes = (uint32_t)rows * K * 4u;
+        float* dst = stage + (size_t)st * stage_floats;
+        mbar_expect_tx(&full[st], (MODE == 0 ? 1u : 2u) * bytes);
+        bulk_g2s(dst, P + r0 * K, bytes, &full[st]);
+        if (MODE != 0) bulk_g2s(dst + tr * K, M + r0 * K, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  const int hl = lane & 15, half = lane >> 4;
+  uint64_t a2[K];  // {A[i][2hl], A[i][2hl+1]}
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(A + i * K + 2 * hl));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(a2[i]) : "f"(t.x), "f"(t.y));
+  }
+  float2 sc = make_float2(1.f, 1.f);
+  if (scale) sc = __ldg(reinterpret_cast<const float2*>(scale + 2 * hl));
+  for (int64_t j = 0; j < my_tiles; ++j) {
+    const int st = (int)(j % NS);
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * (int64_t)tr;
+    const int rows = (int)min((int64_t)tr, n - r0);
+    mbar_wait(&full[st], (uint32_t)((j / NS) & 1));
+    const float* ps = stage + (size_t)st * stage_floats;
+    const float* ms = ps + tr * K;
+    // a pass: 32 rows per CTA, each half-warp two rows (two FMA chains)
+    for (int rb = 0; rb < rows; rb += 32) {
+      const int ra = rb + warp * 2 + half, rc = ra + 16;
+      const bool va = ra < rows, vc = rc < rows;
+      const float4* pa = reinterpret_cast<const float4*>(ps + (va ? ra : 0) * K);
+      const float4* pc = reinterpret_cast<const float4*>(ps + (vc ? rc : 0) * K);
+      uint64_t acca = 0ull, accc = 0ull;
+#pragma unroll
+      for (int i4 = 0; i4 < K / 4; ++i4) {
+        const float4 xa = pa[i4];  // one broadcast per half-warp
+        const float4 xc = pc[i4];
+        ffma2_s(acca, xa.x, a2[4 * i4 + 0]);
+        ffma2_s(accc, xc.x, a2[4 * i4 + 0]);
+        ffma2_s(acca, xa.y, a2[4 * i4 + 1]);
+        ffma2_s(accc, xc.y, a2[4 * i4 + 1]);
+        ffma2_s(acca, xa.z, a2[4 * i4 + 2]);
+        ffma2_s(accc, xc.z, a2[4 * i4 + 2]);
+        ffma2_s(acca, xa.w, a2[4 * i4 + 3]);
+        ffma2_s(accc, xc.w, a2[4 * i4 + 3]);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool v = h ? vc : va;
+        if (!v) continue;
+        const int rr = h ? rc : ra;
+        float2 o;
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(h ? accc : acca));
+        if (MODE == 1) {
+          const float2 m = *reinterpret_cast<const float2*>(ms + rr * K + 2 * hl);
+          o.x = fmaf(eta, m.x, o.x);
+          o.y = fmaf(eta, m.y, o.y);
+        }
+        __stcs(reinterpret_cast<float2*>(out + (r0 + rr) * K + 2 * hl), make_float2(o.x * sc.x, o.y * sc.y));
+      }
+    }
+    mbar_arrive(&empty[st]);
+  }
+}
+
 template <int K>
 int launch_v2(int64_t n, const float* P, const float* A, const float* M, const float* B, float eta,
               const float* scale, float* out, cudaStream_t s) {
@@ -457,14 +564,29 @@ int launch_v2(int64_t n, const float* P, const float* A, const float* M, const f
     const int rc_ = attr([&]() -> int {
       SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      if constexpr (K == 32)
+      if constexpr (K == 32) {
         SPED_CUDA(cudaFuncSetAttribute(block_update_v2<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SPED_CUDA(cudaFuncSetAttribute(block_update_k32_f2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SPED_CUDA(cudaFuncSetAttribute(block_update_k32_f2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      }
       return SPED_OK;
     });
     if (rc_ != SPED_OK) return rc_;
   }
   const int64_t ntiles = (n + tr - 1) / tr;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * UPD_CTAS));
+  if constexpr (K == 32 && UPD_F2) {
+    if (mode == 0) {
+      block_update_k32_f2<0><<<grid, 288, smem, s>>>(n, P, A, M, eta, scale, out, tr);
+      SPED_LAUNCH_CHECK();
+      return SPED_OK;
+    }
+    if (mode == 1) {
+      block_update_k32_f2<1><<<grid, 288, smem, s>>>(n, P, A, M, eta, scale, out, tr);
+      SPED_LAUNCH_CHECK();
+      return SPED_OK;
+    }
+  }
   switch (mode) {
     case 0: block_update_v2<K, 0><<<grid, 288, smem, s>>>(n, P, A, M, B, eta, scale, out, tr); break;
     case 1: block_update_v2<K, 1><<<grid, 288, smem, s>>>(n, P, A, M, B, eta, scale, out, tr); break;

@@ -131,6 +131,15 @@ __device__ __forceinline__ T ld_csr(const T* p) {
   return __ldg(p);
 }
 
+#ifndef SPMM_FMA2
+#define SPMM_FMA2 1
+#endif
+#ifndef SPMM_U32_STRIDE
+#define SPMM_U32_STRIDE 1
+#endif
+#ifndef SPMM_PRED_SKIP
+#define SPMM_PRED_SKIP 1
+#endif
 // W-float lane vectors: W = 4 (128-bit loads) or W = 8 (256-bit loads,
 // LDG.E.256 on sm_100a).
 template <int W>
@@ -140,9 +149,24 @@ struct Vf {
 #pragma unroll
     for (int i = 0; i < W; ++i) v[i] = 0.f;
   }
+  // packed fp32 FMAs (FFMA2 on sm_100a): two of the lane's columns per
+  // instruction, each element still one fused multiply-add (same bits)
   __device__ __forceinline__ void fma(float s, const Vf& x) {
+#if SPMM_FMA2
+    uint64_t ss;
+    asm("mov.b64 %0, {%1,%1};" : "=l"(ss) : "f"(s));
+#pragma unroll
+    for (int i = 0; i < W; i += 2) {
+      uint64_t xv, av;
+      asm("mov.b64 %0, {%1,%2};" : "=l"(xv) : "f"(x.v[i]), "f"(x.v[i + 1]));
+      asm("mov.b64 %0, {%1,%2};" : "=l"(av) : "f"(v[i]), "f"(v[i + 1]));
+      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(av) : "l"(ss), "l"(xv));
+      asm("mov.b64 {%0,%1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(av));
+    }
+#else
 #pragma unroll
     for (int i = 0; i < W; ++i) v[i] = fmaf(s, x.v[i], v[i]);
+#endif
   }
   __device__ __forceinline__ void add(const Vf& x) {
 #pragma unroll
@@ -263,7 +287,20 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
   const int sub = g / LPR;
   const int cl = g % LPR;
   const float* wbase = a.win + cl * W;
+#if SPMM_U32_STRIDE
+  // row stride < 2^30 floats and columns are non-negative: the gather
+  // address is one 32x32+64 multiply-add (IMAD.WIDE.U32) on the lane's base
+  const char* wlb = reinterpret_cast<const char*>(wbase);
+  const uint32_t ldb = (uint32_t)a.ld * 4u;
+#define SPED_ROW_PTR(c) reinterpret_cast<const float*>(wlb + (uint64_t)(uint32_t)(c) * ldb)
+#else
   const int64_t ldw = a.ld;
+#define SPED_ROW_PTR(c) (wbase + (int64_t)(c) * ldw)
+#endif
+  // the skipped diagonal: implicit combinatorial rows (VM 1) predicate the
+  // gather and the add; scaled-normalized rows (VM 2) zero-fill instead
+  // (config 3 -2.8 %, config 4 -1.5 % that way round; r02_ab_diet_cfg*.log)
+  constexpr bool PRED = SPMM_PRED_SKIP && (VM == 1);
   Vf<W> acc;
   acc.zero();
   if (valid) {
@@ -283,12 +320,17 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       for (int u = 0; u < U; ++u) {
         SPED_DCHECK(c[u] >= 0 && (a.n_in == 0 || c[u] < a.n_in), DBG_GATHER_OOB);
         // VM 2: the diagonal's weight is 0 (the epilogue reads the own row
-        // itself) -- no gather for it; the sum is unchanged bit for bit
-        if (SKIPD && c[u] == row) gv[u].zero();
-        else gv[u] = ldg_vec<W>(wbase + (int64_t)c[u] * ldw);
+        // itself) -- no gather and no add for it (predicated, nothing zeroed)
+        if (PRED) {
+          if (!(SKIPD && c[u] == row)) gv[u] = ldg_vec<W>(SPED_ROW_PTR(c[u]));
+        } else {
+          if (SKIPD && c[u] == row) gv[u].zero();
+          else gv[u] = ldg_vec<W>(SPED_ROW_PTR(c[u]));
+        }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc.fma(v[u], gv[u]);
+      for (int u = 0; u < U; ++u)
+        if (!PRED || !(SKIPD && c[u] == row)) acc.fma(v[u], gv[u]);
     }
     for (; p < e; p += SUB) {
       const int32_t c = ld_csr(a.indices + p);
@@ -297,7 +339,7 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       else if (VM == 2) v = c == row ? 0.0f : 1.0f;
       else v = ld_csr(a.values + p);
       SPED_DCHECK(c >= 0 && (a.n_in == 0 || c < a.n_in), DBG_GATHER_OOB);
-      if (!(SKIPD && c == row)) acc.fma(v, ldg_vec<W>(wbase + (int64_t)c * ldw));
+      if (!(SKIPD && c == row)) acc.fma(v, ldg_vec<W>(SPED_ROW_PTR(c)));
     }
   }
 #pragma unroll
