@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(256, MINB) batch_group_kernel(const BatchArgs 
   const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x >> 5) * RPW;
   const bool need_x = (a.flags & 1) || ((a.flags & 4) && (a.flags & 8));
   const unsigned long long* rec = reinterpret_cast<const unsigned long long*>(a.rec);
+  const char* wlb = reinterpret_cast<const char*>(a.win + c);  // the lane's column slice
+  const uint32_t ldb = (uint32_t)a.ld * 4u;                    // row stride in bytes (< 2^32)
   for (int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW + lane / G;
        row < a.n; row += ngroups) {
     const int32_t b = __ldg(a.start + row), e = __ldg(a.start + row + 1);
@@ -242,7 +244,8 @@ __global__ void __launch_bounds__(256, MINB) batch_group_kernel(const BatchArgs 
       float4 g[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        g[u] = (p + u < e) ? ld_gather_f4(a.win + (int64_t)(int32_t)(uint32_t)r[u] * a.ld + c)
+        g[u] = (p + u < e) ? ld_gather_f4(reinterpret_cast<const float*>(
+                                 wlb + (uint64_t)(uint32_t)r[u] * ldb))  // one IMAD.WIDE.U32
                            : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int u = 0; u < U; ++u) {

@@ -316,6 +316,21 @@ struct UpdCfg {
   static constexpr int STAGE_BYTES = UPD_STAGE_BYTES;  // P + M rows of one stage
 };
 
+// packed fp32 FMA (FFMA2 on sm_100a): acc.{lo,hi} += s * b.{lo,hi}
+#ifndef UPD_F2
+#define UPD_F2 1
+#endif
+__device__ __forceinline__ void ffma2_s(uint64_t& acc, float s, uint64_t b) {
+  uint64_t ss;
+  asm("mov.b64 %0, {%1,%1};" : "=l"(ss) : "f"(s));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(ss), "l"(b));
+}
+__device__ __forceinline__ uint64_t pack_f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
 template <int K, int MODE>  // MODE 0: P A; 1: P A + eta M; 2: P A + M B
 __global__ void __launch_bounds__(288) block_update_v2(int64_t n, const float* __restrict__ P,
                                                       const float* __restrict__ A,
@@ -386,6 +401,19 @@ __global__ void __launch_bounds__(288) block_update_v2(int64_t n, const float* _
       for (int q = 0; q < KPL; ++q) acc[0][q] = acc[1][q] = 0.f;
       const float4* prow0 = reinterpret_cast<const float4*>(ps + r * K);
       const float4* prow1 = reinterpret_cast<const float4*>(ps + r2 * K);
+      if constexpr (KPL == 2 && RB == 1 && MODE != 2 && UPD_F2) {
+        // k = 64: the lane's two columns (lane, lane + 32) as one packed FMA
+        uint64_t accp = 0ull;
+#pragma unroll
+        for (int i4 = 0; i4 < K / 4; ++i4) {
+          const float4 p0 = prow0[i4];
+          ffma2_s(accp, p0.x, pack_f2(a[4 * i4 + 0][0], a[4 * i4 + 0][1]));
+          ffma2_s(accp, p0.y, pack_f2(a[4 * i4 + 1][0], a[4 * i4 + 1][1]));
+          ffma2_s(accp, p0.z, pack_f2(a[4 * i4 + 2][0], a[4 * i4 + 2][1]));
+          ffma2_s(accp, p0.w, pack_f2(a[4 * i4 + 3][0], a[4 * i4 + 3][1]));
+        }
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(acc[0][0]), "=f"(acc[0][1]) : "l"(accp));
+      } else
 #pragma unroll
       for (int i4 = 0; i4 < K / 4; ++i4) {
         const float4 p0 = prow0[i4];  // broadcasts
@@ -448,14 +476,6 @@ __global__ void __launch_bounds__(288) block_update_v2(int64_t n, const float* _
 // element as the scalar operand, the lane's two A entries as the pair): half
 // the FMA instructions of the lane-per-column layout, the same per-element
 // sums in the same order.  Same cp.async.bulk ring as block_update_v2.
-#ifndef UPD_F2
-#define UPD_F2 1
-#endif
-__device__ __forceinline__ void ffma2_s(uint64_t& acc, float s, uint64_t b) {
-  uint64_t ss;
-  asm("mov.b64 %0, {%1,%1};" : "=l"(ss) : "f"(s));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(ss), "l"(b));
-}
 
 template <int MODE>  // 0: P A; 1: P A + eta M
 __global__ void __launch_bounds__(288, 2) block_update_k32_f2(int64_t n, const float* __restrict__ P,

@@ -123,8 +123,21 @@ __device__ __forceinline__ void st_stream_f4(float* p, float4 v) {
                :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
+// a*x + y on four floats as two packed FMAs (FFMA2 on sm_100a; each element
+// is still one fused multiply-add, so the bits are those of four fmaf)
 __device__ __forceinline__ float4 f4_fma(float a, float4 x, float4 y) {
-  return make_float4(fmaf(a, x.x, y.x), fmaf(a, x.y, y.y), fmaf(a, x.z, y.z), fmaf(a, x.w, y.w));
+  uint64_t aa, x0, x1, y0, y1;
+  asm("mov.b64 %0, {%1,%1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(x0) : "f"(x.x), "f"(x.y));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(x1) : "f"(x.z), "f"(x.w));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(y0) : "f"(y.x), "f"(y.y));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(y1) : "f"(y.z), "f"(y.w));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(y0) : "l"(aa), "l"(x0));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(y1) : "l"(aa), "l"(x1));
+  float4 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(y0));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.z), "=f"(r.w) : "l"(y1));
+  return r;
 }
 __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
