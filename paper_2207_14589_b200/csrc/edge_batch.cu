@@ -443,7 +443,7 @@ extern "C" int sped_edge_batch_poly_apply(int64_t n, int32_t k, int64_t m, const
                                           const double* alpha, const double* beta,
                                           const double* gamma, double w0_scale, double lam_f,
                                           double s_final, sped_stream_t stream) {
-  SPED_CHECK_ARG(n >= 0 && k >= 1 && m >= 0 && B >= 1, "bad sizes");
+  SPED_CHECK_ARG(n >= 0 && k >= 1 && k < (1 << 30) && m >= 0 && B >= 1, "bad sizes");
   return edge_batch_apply(n, k, m, indices, edge_w, epos, erow, batch, B, (double)m / (double)B,
                           workspace, workspace_bytes, x, w_init, w_a, w_b, out, n_terms, alpha,
                           beta, gamma, w0_scale, lam_f, s_final, stream);
@@ -455,7 +455,7 @@ extern "C" int sped_edge_batch_poly_apply_scaled(
     void* workspace, int64_t workspace_bytes, const float* x, const float* w_init, float* w_a,
     float* w_b, float* out, int32_t n_terms, const double* alpha, const double* beta,
     const double* gamma, double w0_scale, double lam_f, double s_final, sped_stream_t stream) {
-  SPED_CHECK_ARG(n >= 0 && k >= 1 && m >= 0 && B >= 0, "bad sizes");
+  SPED_CHECK_ARG(n >= 0 && k >= 1 && k < (1 << 30) && m >= 0 && B >= 0, "bad sizes");
   SPED_CHECK_ARG(B == 0 || n_terms <= 1, "a compacted shard batch carries one term");
   return edge_batch_apply(n, k, m, indices, edge_w, epos, erow, batch, B, scale, workspace,
                           workspace_bytes, x, w_init, w_a, w_b, out, n_terms, alpha, beta, gamma,

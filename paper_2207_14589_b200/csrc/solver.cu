@@ -317,9 +317,6 @@ struct UpdCfg {
 };
 
 // packed fp32 FMA (FFMA2 on sm_100a): acc.{lo,hi} += s * b.{lo,hi}
-#ifndef UPD_F2
-#define UPD_F2 1
-#endif
 __device__ __forceinline__ void ffma2_s(uint64_t& acc, float s, uint64_t b) {
   uint64_t ss;
   asm("mov.b64 %0, {%1,%1};" : "=l"(ss) : "f"(s));
@@ -401,7 +398,7 @@ __global__ void __launch_bounds__(288) block_update_v2(int64_t n, const float* _
       for (int q = 0; q < KPL; ++q) acc[0][q] = acc[1][q] = 0.f;
       const float4* prow0 = reinterpret_cast<const float4*>(ps + r * K);
       const float4* prow1 = reinterpret_cast<const float4*>(ps + r2 * K);
-      if constexpr (KPL == 2 && RB == 1 && MODE != 2 && UPD_F2) {
+      if constexpr (KPL == 2 && RB == 1 && MODE != 2) {
         // k = 64: the lane's two columns (lane, lane + 32) as one packed FMA
         uint64_t accp = 0ull;
 #pragma unroll
@@ -595,7 +592,7 @@ int launch_v2(int64_t n, const float* P, const float* A, const float* M, const f
   }
   const int64_t ntiles = (n + tr - 1) / tr;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * UPD_CTAS));
-  if constexpr (K == 32 && UPD_F2) {
+  if constexpr (K == 32) {
     if (mode == 0) {
       block_update_k32_f2<0><<<grid, 288, smem, s>>>(n, P, A, M, eta, scale, out, tr);
       SPED_LAUNCH_CHECK();

@@ -131,15 +131,6 @@ __device__ __forceinline__ T ld_csr(const T* p) {
   return __ldg(p);
 }
 
-#ifndef SPMM_FMA2
-#define SPMM_FMA2 1
-#endif
-#ifndef SPMM_U32_STRIDE
-#define SPMM_U32_STRIDE 1
-#endif
-#ifndef SPMM_PRED_SKIP
-#define SPMM_PRED_SKIP 1
-#endif
 // W-float lane vectors: W = 4 (128-bit loads) or W = 8 (256-bit loads,
 // LDG.E.256 on sm_100a).
 template <int W>
@@ -152,7 +143,6 @@ struct Vf {
   // packed fp32 FMAs (FFMA2 on sm_100a): two of the lane's columns per
   // instruction, each element still one fused multiply-add (same bits)
   __device__ __forceinline__ void fma(float s, const Vf& x) {
-#if SPMM_FMA2
     uint64_t ss;
     asm("mov.b64 %0, {%1,%1};" : "=l"(ss) : "f"(s));
 #pragma unroll
@@ -163,10 +153,6 @@ struct Vf {
       asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(av) : "l"(ss), "l"(xv));
       asm("mov.b64 {%0,%1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(av));
     }
-#else
-#pragma unroll
-    for (int i = 0; i < W; ++i) v[i] = fmaf(s, x.v[i], v[i]);
-#endif
   }
   __device__ __forceinline__ void add(const Vf& x) {
 #pragma unroll
@@ -287,20 +273,15 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
   const int sub = g / LPR;
   const int cl = g % LPR;
   const float* wbase = a.win + cl * W;
-#if SPMM_U32_STRIDE
   // row stride < 2^30 floats and columns are non-negative: the gather
   // address is one 32x32+64 multiply-add (IMAD.WIDE.U32) on the lane's base
   const char* wlb = reinterpret_cast<const char*>(wbase);
   const uint32_t ldb = (uint32_t)a.ld * 4u;
 #define SPED_ROW_PTR(c) reinterpret_cast<const float*>(wlb + (uint64_t)(uint32_t)(c) * ldb)
-#else
-  const int64_t ldw = a.ld;
-#define SPED_ROW_PTR(c) (wbase + (int64_t)(c) * ldw)
-#endif
   // the skipped diagonal: implicit combinatorial rows (VM 1) predicate the
   // gather and the add; scaled-normalized rows (VM 2) zero-fill instead
   // (config 3 -2.8 %, config 4 -1.5 % that way round; r02_ab_diet_cfg*.log)
-  constexpr bool PRED = SPMM_PRED_SKIP && (VM == 1);
+  constexpr bool PRED = (VM == 1);
   Vf<W> acc;
   acc.zero();
   if (valid) {
@@ -839,7 +820,7 @@ extern "C" int sped_csr_poly_apply(int64_t n, int32_t k, const int32_t* indptr,
   SPED_CHECK_ARG(n_chunks == 0 || (chunk_desc && partials && tickets && chunk_len > 0 &&
                                    long_threshold > 0),
                  "null or inconsistent long-row plan");
-  SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX, "problem too large");
+  SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX && k < (1 << 30), "problem too large");
   SPED_CHECK_ARG(n_segments >= 0 && n_segments <= 8 && (n_segments == 0 || segments),
                  "bad segment table");
   if (n == 0) return SPED_OK;
@@ -963,7 +944,7 @@ static int shard_term(int64_t n, int32_t k, const int32_t* indptr, const int32_t
   SPED_CHECK_ARG(n_chunks == 0 || (chunk_desc && partials && tickets && chunk_len > 0 &&
                                    long_threshold > 0),
                  "null or inconsistent long-row plan");
-  SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX, "problem too large");
+  SPED_CHECK_ARG(n_chunks < INT32_MAX && n < INT32_MAX && k < (1 << 30), "problem too large");
   SPED_CHECK_ARG(n_segments >= 0 && n_segments <= 8 && (n_segments == 0 || segments),
                  "bad segment table");
   SPED_CHECK_ARG(!(scaled_in || scaled_out) || row_scale, "scaled terms need row_scale");
