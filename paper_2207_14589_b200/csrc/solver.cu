@@ -592,7 +592,10 @@ int launch_v2(int64_t n, const float* P, const float* A, const float* M, const f
   }
   const int64_t ntiles = (n + tr - 1) / tr;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * UPD_CTAS));
-  if constexpr (K == 32) {
+  // the packed kernel reads A / scale and writes out as float2
+  const bool pair_ok = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(scale) |
+                         reinterpret_cast<uintptr_t>(out)) % 8) == 0;
+  if constexpr (K == 32) if (pair_ok) {
     if (mode == 0) {
       block_update_k32_f2<0><<<grid, 288, smem, s>>>(n, P, A, M, eta, scale, out, tr);
       SPED_LAUNCH_CHECK();
