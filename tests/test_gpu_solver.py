@@ -439,6 +439,32 @@ def test_block_update_vs_fp64(cuda, k):
     assert rel_fro(out.cpu().numpy(), (Pd @ Ad).cpu().numpy()) <= tol
 
 
+def test_block_update_k32_unaligned_coefficients(cuda):
+    """The packed-FMA k = 32 update reads A / scale as float2; pointers that
+    are only 4-B aligned take the lane-per-column kernel -- same result, and
+    the packed kernel's output is bit-identical to it (same per-element sums
+    in the same order)."""
+    from paper_2207_14589_b200.solvers import StepWorkspace
+    n, k = 20011, 32
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    P = torch.randn((n, k), device="cuda", generator=gen)
+    M = torch.randn((n, k), device="cuda", generator=gen)
+    A = torch.triu(torch.randn((k, k), device="cuda", generator=gen)).contiguous()
+    sc = torch.rand(k, device="cuda", generator=gen) + 0.5
+    ws = StepWorkspace(n, k, torch.device("cuda"))
+    out = torch.empty_like(P)
+    ws.update(P, A, M, None, 0.3, sc, out, upper=True)
+    buf = torch.empty(k * k + 1, device="cuda")
+    A_odd = buf[1:]                       # 4-B aligned view of the same coefficients
+    A_odd.copy_(A.flatten())
+    assert A_odd.data_ptr() % 8 == 4
+    out2 = torch.empty_like(P)
+    ws.update(P, A_odd, M, None, 0.3, sc, out2, upper=True)
+    assert torch.equal(out, out2)
+    ref = (P.double() @ A.double() + 0.3 * M.double()) * sc.double()
+    assert rel_fro(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
+
+
 @pytest.mark.parametrize("name,mode,kind,ell,k", [("cfg1", "unnormalized", "negexp-limit", 13, 10),
                                                   ("er0", "unnormalized", "negexp-limit", 9, 3),
                                                   ("er1", "normalized", "negexp-taylor", 8, 4)])
