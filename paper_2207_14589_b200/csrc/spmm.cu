@@ -285,7 +285,9 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
     asm("" : "+l"(wlb));
     asm("" : "+r"(ldb));
   }
-#define SPED_ROW_PTR(c) reinterpret_cast<const float*>(wlb + (uint64_t)(uint32_t)(c) * ldb)
+  auto row_ptr = [&](int32_t c) {
+    return reinterpret_cast<const float*>(wlb + (uint64_t)(uint32_t)c * ldb);
+  };
   // the skipped diagonal: implicit combinatorial rows (VM 1) predicate the
   // gather and the add; scaled-normalized rows (VM 2) zero-fill instead
   // (config 3 -2.8 %, config 4 -1.5 % that way round; r02_ab_diet_cfg*.log)
@@ -311,10 +313,10 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
         // VM 2: the diagonal's weight is 0 (the epilogue reads the own row
         // itself) -- no gather and no add for it (predicated, nothing zeroed)
         if (PRED) {
-          if (!(SKIPD && c[u] == row)) gv[u] = ldg_vec<W>(SPED_ROW_PTR(c[u]));
+          if (!(SKIPD && c[u] == row)) gv[u] = ldg_vec<W>(row_ptr(c[u]));
         } else {
           if (SKIPD && c[u] == row) gv[u].zero();
-          else gv[u] = ldg_vec<W>(SPED_ROW_PTR(c[u]));
+          else gv[u] = ldg_vec<W>(row_ptr(c[u]));
         }
       }
 #pragma unroll
@@ -328,7 +330,7 @@ __device__ __forceinline__ Vf<W> free_accumulate(const TermArgs& a, int32_t row,
       else if (VM == 2) v = c == row ? 0.0f : 1.0f;
       else v = ld_csr(a.values + p);
       SPED_DCHECK(c >= 0 && (a.n_in == 0 || c < a.n_in), DBG_GATHER_OOB);
-      if (!(SKIPD && c == row)) acc.fma(v, ldg_vec<W>(SPED_ROW_PTR(c)));
+      if (!(SKIPD && c == row)) acc.fma(v, ldg_vec<W>(row_ptr(c)));
     }
   }
 #pragma unroll
