@@ -254,7 +254,10 @@ def segment_table(rowlen: np.ndarray, k: int, sorted_desc: bool, long_threshold)
         r_64 = max(int(np.searchsorted(-L, -64, side="left")), r_long)
         seg = []
         if r_64 > r_long:
-            seg.append((r_long, r_64, smax))      # long rows: warp per row
+            # long rows: several lane slices per row.  At k = 32 two slices
+            # (8 lanes per row, four rows per warp) beat four: config 4
+            # 2.457 -> 2.424 ms/term (profiles/r02_ab_long_sub_cfg4.log)
+            seg.append((r_long, r_64, max(1, smax // 2) if k <= 32 else smax))
         if n > r_64:
             seg.append((r_64, n, 1))              # medium/short rows: LPR lanes per row
     else:
