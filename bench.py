@@ -674,24 +674,28 @@ def run_sped(args):
     if not sharded:
         ncu_bytes, ncu_src = measured_traffic(spec["name"])
         traffic_ncu = {"bytes_per_term": ncu_bytes, "source": ncu_src} if ncu_bytes else None
-        meter = DramMeter(torch.cuda.current_device())
-        if meter.ok:
+        reps = 4
+        xb = torch.randn((n, k), device=dev)
+        ob = torch.empty_like(xb)
+        op.apply_internal(xb, out=ob)
+        for attempt in range(2):  # the range profiler's Stop fails now and then: one retry
+            meter = DramMeter(torch.cuda.current_device())
+            if not meter.ok:
+                break
             try:
-                reps = 4
-                xb = torch.randn((n, k), device=dev)
-                ob = torch.empty_like(xb)
-                op.apply_internal(xb, out=ob)
                 rd, wr = meter.bytes(lambda: [op.apply_internal(xb, out=ob) for _ in range(reps)])
                 traffic = (rd + wr) / (reps * n_terms)
                 traffic_src = ("in-run CUPTI range profiler (bench_support/libdram_meter.so): "
                                "dram__bytes_read.sum + dram__bytes_write.sum over %d whole "
                                "applies (%.2f + %.2f GB), per term = bytes / (%d x %d terms)"
                                % (reps, rd / 1e9, wr / 1e9, reps, n_terms))
-                del xb, ob
             except RuntimeError as exc:
                 meter.err = str(exc)
                 traffic = None
             meter.lib.dm_close()
+            if traffic is not None:
+                break
+        del xb, ob
         if traffic is None and traffic_ncu:
             traffic, traffic_src = ncu_bytes, (ncu_src + " (in-run meter unavailable: %s)"
                                                % meter.err)
